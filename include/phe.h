@@ -1,0 +1,179 @@
+/*
+ * phe.h — C ABI of the B200-native encrypted-vector x clear-matrix hot path of
+ * arXiv 2505.07329 ("private LoRA fine-tuning with HE"): W . [x]_HE.
+ *
+ * Citations: P:<n> = /root/reference/PAPER.md line n, S:<n> = SPEC.md line n (the reference
+ * tree is not shipped; DESIGN.md restates every passage used).
+ *
+ * Conventions (all calls):
+ *  - Pointers prefixed d_ are DEVICE pointers (cudaMalloc / torch CUDA tensors) owned by the
+ *    caller.  The library never allocates device memory except in phe_server_matvec_host,
+ *    which documents it.  Host pointers are prefixed h_.
+ *  - Every call is asynchronous on the caller's `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream).  Argument validation is synchronous: on a non-zero
+ *    return nothing was enqueued.
+ *  - Errors are returned as int codes (PHE_*); phe_strerror() names them.  A CUDA launch or
+ *    runtime failure returns PHE_ECUDA (the CUDA error is left queryable via
+ *    phe_last_cuda_error()).  No exception ever crosses the ABI.
+ *  - All functions are re-entrant and thread-safe.
+ *  - Privacy rule, structural: no server-side call (phe_weights_prepare,
+ *    phe_ct_prepare, phe_matmul_clear[_T], phe_modswitch) takes the secret key.
+ *  - Integers: ciphertext words are residues mod 2^q stored in uint64_t (q <= 64) or, after
+ *    the fused modulus switch to q_out <= 32, in uint32_t.  Moduli are powers of two
+ *    (reading R3): Q = 2^q_in, Q' = 2^q_out, t = 2^beta, Delta = Q/t.
+ */
+#ifndef PHE_H_
+#define PHE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ------------------------------------------------------------------ */
+#define PHE_OK 0
+#define PHE_EINVAL 1       /* bad dimension / pointer / parameter   */
+#define PHE_ERANGE 2       /* |w| > 127 or message outside +-2^(beta-1)   */
+#define PHE_EMODULUS 3     /* modulus mismatch: out_bits not in {q_in, q_out} */
+#define PHE_ENOMEM 4       /* caller buffer / workspace too small                          */
+#define PHE_ECUDA 5        /* CUDA runtime / launch error                                  */
+#define PHE_EUNSUPPORTED 6 /* valid parameters this build does not implement (e.g. N<128) */
+
+const char *phe_strerror(int code);
+int phe_last_cuda_error(void);
+
+/* ---- a1: parameters (Table 1) -------------------------------------------
+ * N      polynomial size, power of two.          GPU path: 128 <= N <= 16384.
+ * q_in   input ciphertext modulus bits.           8 <= q_in <= 64 (GPU: <= 64).
+ * q_out  output modulus bits after ModulusSwitch. q_out <= q_in, q_out <= 32.
+ * beta   plaintext bits, t = 2^beta (R4).          gamma <= beta <= q_in.
+ * gamma  MSBs guaranteed noise-free; informational (decrypt contract).
+ * noise_eta  0 = E == 0 ("SPEC" reading of sigma, R5); else CBD(eta), eta <= 32.
+ */
+typedef struct phe_params {
+  int32_t N;
+  int32_t q_in;
+  int32_t q_out;
+  int32_t beta;
+  int32_t gamma;
+  int32_t noise_eta;
+} phe_params;
+
+#define PHE_PRESET_PAPER 0 /* N=2048, q_in=39, q_out=26, beta=27, gamma=12 (Table 1)       */
+#define PHE_PRESET_TOY 1   /* N=1024, q_in=32, q_out=28, beta=21, gamma=12 (DESIGN R16)    */
+
+int phe_params_init(phe_params *p, int preset);
+/* PHE_OK if valid: N power of two, q_out <= q_in <= 64, gamma <= beta <= q_in. */
+int phe_params_validate(const phe_params *p);
+/* ell = ceil(q_in / 8): int8 limbs per Z_Q word. */
+int phe_num_limbs(const phe_params *p);
+/* L = ceil(d / N) blocks per vector of length d. */
+int64_t phe_num_blocks(const phe_params *p, int64_t d);
+
+/* ---- keygen (client): S in R_2, binary, deterministic in master_seed.
+ * d_S: [N] uint8 in {0,1}; S' = coefficients of S is the LWE key.
+ * S[k] = bit (k mod 8) of ChaCha20 keystream byte k/8, key LE64(master_seed)||0^24,
+ * nonce "phe-sk" (R6). */
+int phe_keygen(const phe_params *p, uint64_t master_seed, uint8_t *d_S, void *stream);
+
+/* ---- encrypt_pack (client): block split + seeded RLWE.
+ * d_x:     [T][d_in] int8 (quantized activations/gradients, symmetric).
+ * d_seeds: [T][L] uint64 out: seed_{tau,i} = seed_base + tau*L + i (public, one per block).
+ * d_body:  [T][L][N] uint64 out: B = A*S + E + Delta*x_hat mod 2^q_in, A = expand(seed),
+ *          x_hat_i[k] = x[iN+k] zero-padded; E from noise_seed per noise_eta (R5).
+ * Errors: EINVAL (T < 0, d_in < 1, null pointers), ERANGE if 2^(beta-1) <= 128.      */
+int phe_encrypt_pack(const phe_params *p, const uint8_t *d_S, const int8_t *d_x, int64_t T,
+                     int64_t d_in, uint64_t seed_base, uint64_t noise_seed, uint64_t *d_seeds,
+                     uint64_t *d_body, void *stream);
+
+/* ---- a2: weight registration (server, once per model) --------------------------------
+ * Absorbs the reversed encoding w_hat_ij[k] = w_j[iN+N-1-k] into the operand layout
+ * of the limb GEMM.  With transpose = 0 the prepared matrix is
+ * M = W ([rows=d_out][cols=d_in]); with transpose = 1 it is M = W^T ([rows=d_in][cols=d_out])
+ * for the backward W^T . [g].  d_W is always W, row-major [d_out][d_in].
+ * Layout of d_wprep (bytes, caller-allocated, size phe_weights_bytes):
+ *   [rows][Lc][2N][16] int8  "16-shift expansion" of wext_{j,i}[m] = M[j,iN+m] (m < N),
+ *                            -M[j,iN+m-N] (N <= m < 2N), 0 beyond cols/2N; Lc = ceil(cols/N)
+ *   [rows][Lc*N]       int8  M, zero-padded to Lc*N columns (body GEMM operand)
+ * Errors: EINVAL on dims, ERANGE is NOT checked on device (call phe_weights_check). */
+size_t phe_weights_bytes(const phe_params *p, int64_t rows, int64_t cols);
+int phe_weights_prepare(const phe_params *p, const int8_t *d_W, int64_t d_out, int64_t d_in,
+                        int transpose, void *d_wprep, size_t bytes, void *stream);
+
+/* ---- a3+a4: ct_prepare (server) -----------------------------------------------------
+ * Expands every mask A_{tau,i} = PRNG(seed_{tau,i}) mod 2^q_in (ChaCha20 per R6) and
+ * splits masks and bodies into ell little-endian 8-bit limb planes (the GEMM's B operand):
+ *   d_operand = [ mask planes  [T*ell][L*N] uint8 | body planes [T*ell][L*N] uint8 ]
+ *   plane row tau*ell + l holds byte l of every word of token tau, column i*N + k.
+ * Inputs that several linears share (q/k/v; gate/up) are prepared once.            */
+size_t phe_ct_operand_bytes(const phe_params *p, int64_t T, int64_t L);
+int phe_ct_prepare(const phe_params *p, const uint64_t *d_seeds, const uint64_t *d_body,
+                   int64_t T, int64_t L, void *d_operand, size_t bytes, void *stream);
+
+/* ---- a5-a8: matmul_clear (server): LWE(x.w_j) for j in [row_begin, row_end) ---------
+ * Eq. 6: LWE(x.w_j) = sum_i SampleExtract(RLWE(x_hat_i) . w_hat_ij, N-1),
+ * computed as an int8 limb GEMM on tcgen05 tensor cores with the limb recombination mod
+ * 2^q_in and (if out_bits == q_out) the ModulusSwitch fused in the epilogue.
+ *   d_wprep:   from phe_weights_prepare(transpose = 0) of W [d_out][d_in].
+ *   d_operand: from phe_ct_prepare with L = ceil(d_in / N) for T tokens.
+ *   out_bits:  q_in  -> d_out_mask uint64 [T][R][N], d_out_body uint64 [T][R]  (no switch)
+ *              q_out -> d_out_mask uint32 [T][R][N], d_out_body uint32 [T][R]  (switched)
+ *              with R = row_end - row_begin (row sharding).
+ *   Mask entry [tau][j][t] is a'_t of LWE(x_tau . w_j) (Eq. 2 with h = N-1); body [tau][j] = b'.
+ * Errors: EINVAL (row range, T < 0, null), EMODULUS (out_bits not q_in/q_out),
+ *         EUNSUPPORTED (N < 128, ell > 8).  T == 0 is a no-op returning PHE_OK.          */
+int phe_matmul_clear(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                     int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
+                     int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);
+
+/* ---- a9: matmul_clear_T (server, backward): LWE((W^T g)_c), c in [row_begin, row_end) --
+ * Same contract with M = W^T: d_wprep from phe_weights_prepare(transpose = 1) of W
+ * [d_out][d_in]; the input ciphertext encrypts g in Z^{d_out} (L = ceil(d_out / N)); output
+ * rows index c in [0, d_in).                                                */
+int phe_matmul_clear_T(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                       int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
+                       int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);
+
+/* ---- a8 standalone: ModulusSwitch --------------------------
+ * d_out[k] = floor((d_in[k] + 2^(f-t-1)) / 2^(f-t)) mod 2^t, f = from_bits, t = to_bits,
+ * round half up on the non-negative residue (R8).  Requires 1 <= t <= f <= 64, t <= 32.  */
+int phe_modswitch(const uint64_t *d_in, uint32_t *d_out, int64_t count, int32_t from_bits,
+                  int32_t to_bits, void *stream);
+
+/* ---- decrypt_unpack (client): LWE decryption under S' ---
+ * phi = (b - sum_t a[t] S[t]) mod 2^q_bits; q_bits >= beta: m = round(phi / 2^(q-beta)) mod t;
+ * q_bits < beta: m = phi * 2^(beta-q) mod t; centred into [-t/2, t/2).
+ * d_mask/d_body: uint64 if q_bits == p->q_in, uint32 if q_bits == p->q_out (matmul outputs);
+ * shapes [T][rows][N] and [T][rows].  d_y: [T][rows] int32 out.                          */
+int phe_decrypt_unpack(const phe_params *p, const uint8_t *d_S, const void *d_mask,
+                       const void *d_body, int64_t T, int64_t rows, int32_t q_bits,
+                       int32_t *d_y, void *stream);
+
+/* ---- end to end with HOST buffers (the server step as a client call sees it) ----------
+ * h_seeds [T][L] uint64, h_body [T][L][N] uint64 (pinned host memory recommended);
+ * result (switched to q_out, uint32) streamed back into h_out_mask [T][R][N], h_out_body
+ * [T][R].  Tokens are processed in chunks of `chunk_tokens`: H2D of chunk c+1 and D2H of
+ * chunk c-1 overlap the GEMM of chunk c on internal streams.  d_wprep is device-resident
+ * (registered once).  Allocates and frees its own device workspace (documented exception
+ * to the ownership rule).  Synchronous: returns after all copies completed.              */
+int phe_server_matvec_host(const phe_params *p, const void *d_wprep, int64_t d_out,
+                           int64_t d_in, int transpose, int64_t row_begin, int64_t row_end,
+                           const uint64_t *h_seeds, const uint64_t *h_body, int64_t T,
+                           int64_t chunk_tokens, uint32_t *h_out_mask, uint32_t *h_out_body,
+                           void *stream);
+
+/* ---- introspection (tests / bench) -------------------------------------------------- */
+/* Number of kernel launches the last phe_matmul_clear[_T] on this thread enqueued. */
+int phe_last_launch_count(void);
+/* Reference SIMT (CUDA-core, 64-bit) implementation of the same contract as
+ * phe_matmul_clear, used only as an on-device cross-check in tests.                      */
+int phe_matmul_clear_simt(const phe_params *p, const int8_t *d_W, int64_t d_out, int64_t d_in,
+                          int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
+                          int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHE_H_ */

@@ -1,0 +1,277 @@
+"""Python binding of libphe (include/phe.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libphe.so; this module allocates
+torch device tensors for the outputs, passes raw pointers and the current CUDA stream, and
+raises on any non-zero return code.  There is no CPU fallback: if libphe.so is missing or
+no GPU is present, `load()` raises.
+
+Storage convention: uint64 ciphertext words live in torch.int64 tensors and uint32 words in
+torch.int32 tensors (same bits; every value the path produces is < 2^63 / < 2^31 except the
+public seeds, which are opaque 64-bit patterns).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libphe.so")
+
+PHE_OK, PHE_EINVAL, PHE_ERANGE, PHE_EMODULUS, PHE_ENOMEM, PHE_ECUDA, PHE_EUNSUPPORTED = range(7)
+PRESET_PAPER, PRESET_TOY = 0, 1
+
+# every symbol include/phe.h declares (checked by tests/test_boundary.py)
+EXPORTS = [
+    "phe_strerror", "phe_last_cuda_error", "phe_params_init", "phe_params_validate",
+    "phe_num_limbs", "phe_num_blocks", "phe_keygen", "phe_encrypt_pack", "phe_weights_bytes",
+    "phe_weights_prepare", "phe_ct_operand_bytes", "phe_ct_prepare", "phe_matmul_clear",
+    "phe_matmul_clear_T", "phe_modswitch", "phe_decrypt_unpack", "phe_server_matvec_host",
+    "phe_last_launch_count", "phe_matmul_clear_simt",
+]
+
+
+class Params(ctypes.Structure):
+    """phe_params (Table 1)."""
+    _fields_ = [("N", ctypes.c_int32), ("q_in", ctypes.c_int32), ("q_out", ctypes.c_int32),
+                ("beta", ctypes.c_int32), ("gamma", ctypes.c_int32), ("noise_eta", ctypes.c_int32)]
+
+    def __repr__(self):
+        return (f"Params(N={self.N}, q_in={self.q_in}, q_out={self.q_out}, beta={self.beta}, "
+                f"gamma={self.gamma}, noise_eta={self.noise_eta})")
+
+    @property
+    def ell(self) -> int:
+        return (self.q_in + 7) // 8
+
+    def L(self, d: int) -> int:
+        return (d + self.N - 1) // self.N
+
+
+class PheError(RuntimeError):
+    pass
+
+
+_lib = None
+_P = ctypes.POINTER(Params)
+_vp, _i64, _i32, _u64, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_size_t
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libphe.so (raises if missing: the product path has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise PheError(f"libphe.so not built at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    sig = {
+        "phe_strerror": ([ctypes.c_int], ctypes.c_char_p),
+        "phe_last_cuda_error": ([], ctypes.c_int),
+        "phe_last_launch_count": ([], ctypes.c_int),
+        "phe_params_init": ([_P, ctypes.c_int], ctypes.c_int),
+        "phe_params_validate": ([_P], ctypes.c_int),
+        "phe_num_limbs": ([_P], ctypes.c_int),
+        "phe_num_blocks": ([_P, _i64], _i64),
+        "phe_keygen": ([_P, _u64, _vp, _vp], ctypes.c_int),
+        "phe_encrypt_pack": ([_P, _vp, _vp, _i64, _i64, _u64, _u64, _vp, _vp, _vp], ctypes.c_int),
+        "phe_weights_bytes": ([_P, _i64, _i64], _sz),
+        "phe_weights_prepare": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _sz, _vp], ctypes.c_int),
+        "phe_ct_operand_bytes": ([_P, _i64, _i64], _sz),
+        "phe_ct_prepare": ([_P, _vp, _vp, _i64, _i64, _vp, _sz, _vp], ctypes.c_int),
+        "phe_matmul_clear": ([_P, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _i32, _vp, _vp, _vp], ctypes.c_int),
+        "phe_matmul_clear_T": ([_P, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _i32, _vp, _vp, _vp], ctypes.c_int),
+        "phe_matmul_clear_simt": ([_P, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _i32, _vp, _vp, _vp], ctypes.c_int),
+        "phe_modswitch": ([_vp, _vp, _i64, _i32, _i32, _vp], ctypes.c_int),
+        "phe_decrypt_unpack": ([_P, _vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp], ctypes.c_int),
+        "phe_server_matvec_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64,
+                                    _i64, _vp, _vp, _vp], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != PHE_OK:
+        lib = load()
+        msg = lib.phe_strerror(rc).decode()
+        if rc == PHE_ECUDA:
+            msg += f" (cudaError {lib.phe_last_cuda_error()})"
+        raise PheError(f"{what}: {msg} [code {rc}]")
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev(t: torch.Tensor, dtype=None, name="tensor"):
+    if not t.is_cuda:
+        raise PheError(f"{name} must be a CUDA tensor (no CPU path)")
+    if dtype is not None and t.dtype != dtype:
+        raise PheError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise PheError(f"{name} must be contiguous")
+    return t
+
+
+# ------------------------------------------------------------------ params
+def params(preset: int = PRESET_PAPER, **override) -> Params:
+    p = Params()
+    _check(load().phe_params_init(ctypes.byref(p), preset), "phe_params_init")
+    for k, v in override.items():
+        setattr(p, k, v)
+    _check(load().phe_params_validate(ctypes.byref(p)), "phe_params_validate")
+    return p
+
+
+def num_limbs(p: Params) -> int:
+    return load().phe_num_limbs(ctypes.byref(p))
+
+
+def num_blocks(p: Params, d: int) -> int:
+    return load().phe_num_blocks(ctypes.byref(p), d)
+
+
+# ------------------------------------------------------------------ client ops
+def keygen(p: Params, master_seed: int, device="cuda") -> torch.Tensor:
+    S = torch.empty(p.N, dtype=torch.uint8, device=device)
+    _check(load().phe_keygen(ctypes.byref(p), master_seed & (2**64 - 1), _ptr(S), _stream()), "phe_keygen")
+    return S
+
+
+def encrypt_pack(p: Params, S: torch.Tensor, x: torch.Tensor, seed_base: int, noise_seed: int = 0):
+    """x int8 [T][d_in] -> (seeds int64[T][L] (u64 bits), body int64[T][L][N])."""
+    _dev(S, torch.uint8, "S"); _dev(x, torch.int8, "x")
+    T, d_in = x.shape
+    L = p.L(d_in)
+    seeds = torch.empty((T, L), dtype=torch.int64, device=x.device)
+    body = torch.empty((T, L, p.N), dtype=torch.int64, device=x.device)
+    _check(load().phe_encrypt_pack(ctypes.byref(p), _ptr(S), _ptr(x), T, d_in, seed_base & (2**64 - 1),
+                                   noise_seed & (2**64 - 1), _ptr(seeds), _ptr(body), _stream()),
+           "phe_encrypt_pack")
+    return seeds, body
+
+
+def decrypt_unpack(p: Params, S: torch.Tensor, mask: torch.Tensor, body: torch.Tensor, q_bits: int):
+    """mask [T][rows][N], body [T][rows] (int64 if q_bits == q_in else int32) -> int32 [T][rows]."""
+    _dev(S, torch.uint8, "S"); _dev(mask, None, "mask"); _dev(body, None, "body")
+    T, rows = body.shape
+    y = torch.empty((T, rows), dtype=torch.int32, device=body.device)
+    _check(load().phe_decrypt_unpack(ctypes.byref(p), _ptr(S), _ptr(mask), _ptr(body), T, rows, q_bits,
+                                     _ptr(y), _stream()), "phe_decrypt_unpack")
+    return y
+
+
+# ------------------------------------------------------------------ server ops
+class Weights:
+    """A weight matrix registered for the limb GEMM (phe_weights_prepare, P:182 absorbed).
+    transpose=True registers M = W^T for the backward matmul_clear_T."""
+
+    def __init__(self, p: Params, W: torch.Tensor, transpose: bool = False):
+        _dev(W, torch.int8, "W")
+        self.p = p
+        self.d_out, self.d_in = W.shape
+        self.transpose = bool(transpose)
+        self.rows, self.cols = (self.d_in, self.d_out) if transpose else (self.d_out, self.d_in)
+        nbytes = load().phe_weights_bytes(ctypes.byref(p), self.rows, self.cols)
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=W.device)
+        _check(load().phe_weights_prepare(ctypes.byref(p), _ptr(W), self.d_out, self.d_in, int(transpose),
+                                          _ptr(self.buf), nbytes, _stream()), "phe_weights_prepare")
+
+
+def ct_prepare(p: Params, seeds: torch.Tensor, body: torch.Tensor, out: torch.Tensor | None = None):
+    _dev(seeds, torch.int64, "seeds"); _dev(body, torch.int64, "body")
+    T, L = seeds.shape
+    nbytes = load().phe_ct_operand_bytes(ctypes.byref(p), T, L)
+    if out is None:
+        out = torch.empty(nbytes, dtype=torch.uint8, device=seeds.device)
+    _check(load().phe_ct_prepare(ctypes.byref(p), _ptr(seeds), _ptr(body), T, L, _ptr(out),
+                                 out.numel(), _stream()), "phe_ct_prepare")
+    return out
+
+
+def _outputs(p, T, R, out_bits, device, out_mask, out_body):
+    dt = torch.int64 if out_bits == p.q_in else torch.int32
+    if out_mask is None:
+        out_mask = torch.empty((T, R, p.N), dtype=dt, device=device)
+    if out_body is None:
+        out_body = torch.empty((T, R), dtype=dt, device=device)
+    return out_mask, out_body
+
+
+def matmul_clear(p: Params, w: Weights, operand: torch.Tensor, T: int, out_bits: int | None = None,
+                 row_begin: int = 0, row_end: int | None = None, out_mask=None, out_body=None):
+    """LWE(x_tau . w_j) for j in [row_begin, row_end) (Eq. 6), modulus-switched to
+    q_out when out_bits == q_out (default).  Returns (mask [T][R][N], body [T][R])."""
+    if w.transpose:
+        raise PheError("matmul_clear needs weights registered with transpose=False")
+    out_bits = p.q_out if out_bits is None else out_bits
+    row_end = w.rows if row_end is None else row_end
+    out_mask, out_body = _outputs(p, T, row_end - row_begin, out_bits, operand.device, out_mask, out_body)
+    _check(load().phe_matmul_clear(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, row_begin, row_end,
+                                   _ptr(operand), T, out_bits, _ptr(out_mask), _ptr(out_body), _stream()),
+           "phe_matmul_clear")
+    return out_mask, out_body
+
+
+def matmul_clear_T(p: Params, w: Weights, operand: torch.Tensor, T: int, out_bits: int | None = None,
+                   row_begin: int = 0, row_end: int | None = None, out_mask=None, out_body=None):
+    """Backward W^T . [g]: rows index d_in."""
+    if not w.transpose:
+        raise PheError("matmul_clear_T needs weights registered with transpose=True")
+    out_bits = p.q_out if out_bits is None else out_bits
+    row_end = w.rows if row_end is None else row_end
+    out_mask, out_body = _outputs(p, T, row_end - row_begin, out_bits, operand.device, out_mask, out_body)
+    _check(load().phe_matmul_clear_T(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, row_begin, row_end,
+                                     _ptr(operand), T, out_bits, _ptr(out_mask), _ptr(out_body), _stream()),
+           "phe_matmul_clear_T")
+    return out_mask, out_body
+
+
+def matmul_clear_simt(p: Params, W: torch.Tensor, operand: torch.Tensor, T: int, out_bits: int | None = None,
+                      row_begin: int = 0, row_end: int | None = None):
+    """CUDA-core cross-check of matmul_clear (same contract; W raw int8 [rows][cols])."""
+    _dev(W, torch.int8, "W")
+    out_bits = p.q_out if out_bits is None else out_bits
+    row_end = W.shape[0] if row_end is None else row_end
+    out_mask, out_body = _outputs(p, T, row_end - row_begin, out_bits, operand.device, None, None)
+    _check(load().phe_matmul_clear_simt(ctypes.byref(p), _ptr(W), W.shape[0], W.shape[1], row_begin, row_end,
+                                        _ptr(operand), T, out_bits, _ptr(out_mask), _ptr(out_body), _stream()),
+           "phe_matmul_clear_simt")
+    return out_mask, out_body
+
+
+def modswitch(x: torch.Tensor, from_bits: int, to_bits: int, out: torch.Tensor | None = None):
+    _dev(x, torch.int64, "x")
+    if out is None:
+        out = torch.empty(x.shape, dtype=torch.int32, device=x.device)
+    _check(load().phe_modswitch(_ptr(x), _ptr(out), x.numel(), from_bits, to_bits, _stream()), "phe_modswitch")
+    return out
+
+
+def server_matvec_host(p: Params, w: Weights, h_seeds: torch.Tensor, h_body: torch.Tensor,
+                       h_out_mask: torch.Tensor, h_out_body: torch.Tensor, chunk_tokens: int = 256,
+                       row_begin: int = 0, row_end: int | None = None) -> None:
+    """End-to-end with HOST buffers (pinned CPU tensors): H2D, prepare, GEMM, D2H pipelined."""
+    for t, n in [(h_seeds, "h_seeds"), (h_body, "h_body"), (h_out_mask, "h_out_mask"), (h_out_body, "h_out_body")]:
+        if t.is_cuda or not t.is_contiguous():
+            raise PheError(f"{n} must be a contiguous host tensor")
+    T = h_seeds.shape[0]
+    row_end = w.rows if row_end is None else row_end
+    _check(load().phe_server_matvec_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
+                                         row_begin, row_end, _ptr(h_seeds), _ptr(h_body), T, chunk_tokens,
+                                         _ptr(h_out_mask), _ptr(h_out_body), _stream()),
+           "phe_server_matvec_host")
+
+
+def last_launch_count() -> int:
+    return load().phe_last_launch_count()

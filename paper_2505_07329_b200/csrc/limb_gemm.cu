@@ -1,0 +1,452 @@
+// limb_gemm.cu — the hot path: Eq. 6 + SampleExtract(N-1) + block sum + limb recombination
+// + ModulusSwitch as ONE int8 GEMM on tcgen05 tensor cores (sm_100a), per DESIGN.md.
+//
+// Formulation ("Hankel form").  For one token tau and output row j
+// (P:176-182 with Eq. 2 at h = N-1):
+//     a_{tau,j}[t] = sum_i sum_{k<N} A_{tau,i}[k] * wext_{j,i}[k + t]   (mod 2^q_in)
+//     wext_{j,i}[u] = W[j, iN+u] (u < N),  -W[j, iN+u-N] (N <= u < 2N)
+// Split every 39-bit mask word into ell little-endian u8 limbs A = sum_l 2^(8l) A_l.  Then
+//     D[(j,t), (tau,l)] = sum_{(i,k)} Hankel(wext)[(j,t), (i,k)] * A_l[tau][(i,k)]
+// is a plain int8 x uint8 -> int32 GEMM:  M = rows*N (row = (j,t)), N_gemm = T*ell (column =
+// (tau,l)), K = L*N.  The epilogue recombines v = sum_l D[.,(tau,l)] << 8l mod 2^q_in and
+// applies the modulus switch, writing one word per (tau, j, t).
+// The body b_{tau,j} = sum_c W[j,c] B_tau[c] (coefficient N-1 of B*w_hat) is the same GEMM
+// with a plain W operand ("PLAIN" mode, M = rows).
+//
+// The Hankel A operand is never materialised.  Its tile (128 rows t x 128 bytes of k) holds
+// only 240 distinct 16-byte rows R[p] = wext[s+p .. s+p+16) (s = k0 + t0): core matrix (g,h)
+// (8 rows x 16 B, K-major, no swizzle) equals R[8(g+2h) .. +8), so a UMMA smem descriptor with
+// SBO = 128 B and LBO = 256 B walks a compact 3840-byte buffer.  That buffer is a plain TMA
+// box of the weight's 16-shift expansion (phe_weights_prepare).
+//
+// Pipeline (per CTA, persistent over tiles, 1 CTA per SM):
+//   warp 0     TMA producer  (A box + B box per K-stage, mbarrier complete_tx)
+//   warp 1     MMA issuer    (tcgen05.mma.cta_group::1.kind::i8, M=128 N=256 K=32)
+//   warp 2     TMEM allocator (512 columns = 2 accumulator stages of 256)
+//   warps 4-7  epilogue      (tcgen05.ld -> recombine -> modswitch -> st.global.cs)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "phe_common.cuh"
+#include "side_kernels.cuh"
+
+namespace phe {
+namespace tc {
+
+constexpr int BM = 128;   // rows per tile (TMEM lanes)
+constexpr int BN = 256;   // GEMM columns per tile: tokens*ell (+ pad)
+constexpr int BK = 128;   // bytes of K per pipeline stage
+constexpr int UK = 32;    // K of one tcgen05.mma kind::i8
+constexpr int NUM_THREADS = 256;
+constexpr int A_ROWS_HANKEL = BM + BK - 16;            // 240 compact rows
+constexpr int A_BYTES_HANKEL = A_ROWS_HANKEL * 16;     // 3840
+constexpr int A_BYTES_PLAIN = BM * BK;                 // 16384
+constexpr int B_BYTES = BN * BK;                       // 32768
+
+template <bool HANKEL> struct Cfg;
+template <> struct Cfg<true> {
+  static constexpr int STAGES = 5;
+  static constexpr int A_BYTES = A_BYTES_HANKEL;
+  static constexpr int A_SLOT = 4096;  // 1024-aligned slot
+};
+template <> struct Cfg<false> {
+  static constexpr int STAGES = 4;
+  static constexpr int A_BYTES = A_BYTES_PLAIN;
+  static constexpr int A_SLOT = A_BYTES_PLAIN;
+};
+template <bool HANKEL>
+constexpr int smem_bytes() {
+  return 1024 /*align slack*/ + Cfg<HANKEL>::STAGES * (B_BYTES + Cfg<HANKEL>::A_SLOT) + 256;
+}
+
+struct KArgs {
+  int N;
+  int tpt;            // tokens per tile = BN / ell
+  int n_tiles;        // token tiles
+  int tb_per_row;     // N / BM (HANKEL) or 1
+  int64_t m_tiles;    // rows*tb_per_row (HANKEL) or ceil(rows/BM)
+  int64_t total_tiles;
+  int k_blocks;       // Lc*N / BK
+  int kb_per_block;   // N / BK
+  int64_t Lc;
+  int64_t row_begin;  // absolute first row
+  int64_t R;          // rows in range
+  int64_t T;
+  int q_in, out_bits;
+  void *out;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int x, int y,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t *v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptors (sm_100 format: version 1 at bit 46).
+// Hankel: K-major, SWIZZLE_NONE, core matrix 8 rows x 16 B; LBO (next 16 B of K) = 256 B,
+// SBO (next 8 rows) = 128 B  ->  core (g,h) at start + 128*(g + 2h) (compact buffer).
+__device__ __forceinline__ uint64_t desc_hankel(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(256 >> 4) << 16) |
+         ((uint64_t)(128 >> 4) << 32) | (1ull << 46);
+}
+// Dense K-major tile written by TMA with 128-byte swizzle: SBO = 1024 B (8 rows x 128 B).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+// Instruction descriptor: D = S32, A = s8 (weights), B = u8 (limbs), both K-major.
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+  return (2u << 4) | (1u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+
+// ------------------------------------------------------------------ the kernel
+template <int ELL, bool HANKEL>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                 KArgs ka) {
+  using C = Cfg<HANKEL>;
+  constexpr int S = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  uint8_t *sB = smem;                          // S x 32 KB (1024-aligned)
+  uint8_t *sA = smem + S * B_BYTES;            // S x A_SLOT
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sA + S * C::A_SLOT);
+  uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int64_t total = ka.total_tiles;
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      int s = 0; uint32_t ph = 0;
+      for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int64_t m_tile = tile / ka.n_tiles;
+        const int n_tile = (int)(tile % ka.n_tiles);
+        const int brow = n_tile * ka.tpt * ELL;
+        int64_t jrow; int t0;
+        if (HANKEL) { jrow = ka.row_begin + m_tile / ka.tb_per_row; t0 = (int)(m_tile % ka.tb_per_row) * BM; }
+        else { jrow = ka.row_begin + m_tile * BM; t0 = 0; }
+        for (int kb = 0; kb < ka.k_blocks; kb++) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], (uint32_t)(C::A_BYTES + B_BYTES));
+          if (HANKEL) {
+            const int i = kb / ka.kb_per_block, k0 = (kb % ka.kb_per_block) * BK;
+            const int64_t arow = (jrow * ka.Lc + i) * (2 * (int64_t)ka.N) + k0 + t0;
+            tma_load_2d(smem_u32(sA + s * C::A_SLOT), &map_a, 0, (int)arow, &full[s]);
+          } else {
+            tma_load_2d(smem_u32(sA + s * C::A_SLOT), &map_a, kb * BK, (int)jrow, &full[s]);
+          }
+          tma_load_2d(smem_u32(sB + s * B_BYTES), &map_b, kb * BK, brow, &full[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(BM, BN);
+      int s = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
+      for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < ka.k_blocks; kb++) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * C::A_SLOT);
+          const uint32_t b_addr = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int q = 0; q < BK / UK; q++) {
+            const uint64_t adesc = HANKEL ? desc_hankel(a_addr + 512 * q) : desc_sw128(a_addr + 32 * q);
+            const uint64_t bdesc = desc_sw128(b_addr + 32 * q);
+            mma_i8(d_tmem, adesc, bdesc, idesc, (kb | q) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ===== epilogue: TMEM -> registers -> recombine limbs -> modswitch -> HBM =====
+    const int q4 = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q4 * 32 + lane;
+    const bool sw = ka.out_bits != ka.q_in;
+    const int shift = ka.q_in - ka.out_bits;
+    const uint64_t half = shift > 0 ? (1ull << (shift - 1)) : 0ull;
+    const uint64_t omask = mask_bits(ka.out_bits);
+    const int64_t N = ka.N;
+    int acc = 0; uint32_t aph = 0;
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int64_t m_tile = tile / ka.n_tiles;
+      const int n_tile = (int)(tile % ka.n_tiles);
+      const int64_t tau0 = (int64_t)n_tile * ka.tpt;
+      const int ntok = (int)min((int64_t)ka.tpt, ka.T - tau0);
+      int64_t obase;  // output index of (tau0, this row)
+      int64_t tstride;  // index stride between consecutive tokens
+      bool valid = true;
+      if (HANKEL) {
+        const int64_t jr = m_tile / ka.tb_per_row;
+        const int64_t t = (m_tile % ka.tb_per_row) * BM + row;
+        tstride = ka.R * N;
+        obase = tau0 * tstride + jr * N + t;
+      } else {
+        const int64_t jr = m_tile * BM + row;
+        valid = jr < ka.R;
+        tstride = ka.R;
+        obase = tau0 * tstride + jr;
+      }
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN);
+      for (int c0 = 0; c0 < ntok; c0 += 16) {
+        const int nt = min(16, ntok - c0);
+        const int nloads = (nt * ELL + 15) / 16;
+        uint32_t v[16 * ELL];
+#pragma unroll
+        for (int q = 0; q < ELL; q++)
+          if (q < nloads) tmem_ld16(tbase + (uint32_t)(c0 * ELL + 16 * q), &v[16 * q]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int tk = 0; tk < 16; tk++) {
+          if (tk < nt && valid) {
+            uint64_t x = 0;
+#pragma unroll
+            for (int l = 0; l < ELL; l++) x += (uint64_t)(int64_t)(int32_t)v[tk * ELL + l] << (8 * l);
+            const int64_t o = obase + (int64_t)(c0 + tk) * tstride;
+            if (sw) __stcs(static_cast<uint32_t *>(ka.out) + o, (uint32_t)(((x + half) >> shift) & omask));
+            else __stcs(reinterpret_cast<unsigned long long *>(ka.out) + o, (unsigned long long)(x & omask));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+static int make_map_2d(CUtensorMap *m, const void *base, uint64_t dim0, uint64_t dim1,
+                       uint64_t stride1, uint32_t box0, uint32_t box1, CUtensorMapSwizzle sw) {
+  auto enc = get_encode();
+  if (!enc) return PHE_ECUDA;
+  cuuint64_t dims[2] = {dim0, dim1};
+  cuuint64_t strides[1] = {stride1};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? PHE_OK : PHE_EINVAL;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int ELL, bool HANKEL>
+static int launch_one(const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka, cudaStream_t st) {
+  auto kern = limb_gemm_kernel<ELL, HANKEL>;
+  constexpr int smem = smem_bytes<HANKEL>();
+  static thread_local bool set = false;
+  if (!set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+    set = true;
+  }
+  int64_t grid = ka.total_tiles < num_sms() ? ka.total_tiles : num_sms();
+  kern<<<(unsigned)grid, NUM_THREADS, smem, st>>>(ma, mb, ka);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+template <bool HANKEL>
+static int dispatch_ell(int ell, const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka,
+                        cudaStream_t st) {
+  switch (ell) {
+    case 1: return launch_one<1, HANKEL>(ma, mb, ka, st);
+    case 2: return launch_one<2, HANKEL>(ma, mb, ka, st);
+    case 3: return launch_one<3, HANKEL>(ma, mb, ka, st);
+    case 4: return launch_one<4, HANKEL>(ma, mb, ka, st);
+    case 5: return launch_one<5, HANKEL>(ma, mb, ka, st);
+    case 6: return launch_one<6, HANKEL>(ma, mb, ka, st);
+    case 7: return launch_one<7, HANKEL>(ma, mb, ka, st);
+    case 8: return launch_one<8, HANKEL>(ma, mb, ka, st);
+  }
+  return PHE_EUNSUPPORTED;
+}
+
+}  // namespace tc
+
+int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
+  using namespace tc;
+  const int N = a.kp.N, ell = a.kp.ell;
+  *n_launches = 0;
+  const int64_t R = a.row_end - a.row_begin;
+  if (a.T == 0 || R == 0) return PHE_OK;
+  if (N % BM != 0 || N % BK != 0) return PHE_EUNSUPPORTED;
+  const int64_t K = a.Lc * N;
+  const int tpt = BN / ell;
+  const int n_tiles = (int)((a.T + tpt - 1) / tpt);
+  const uint64_t brows = (uint64_t)a.op_rows;  // padded: boxes never leave the allocation
+  KArgs ka{};
+  ka.N = N; ka.tpt = tpt; ka.n_tiles = n_tiles; ka.k_blocks = (int)(K / BK);
+  ka.kb_per_block = N / BK; ka.Lc = a.Lc; ka.row_begin = a.row_begin; ka.R = R; ka.T = a.T;
+  ka.q_in = a.kp.q_in; ka.out_bits = a.out_bits;
+  // ---- body: plain W operand, M = rows in range
+  {
+    CUtensorMap ma, mb;
+    int rc = make_map_2d(&ma, a.wplain, (uint64_t)K, (uint64_t)a.wplain_rows, (uint64_t)K, BK, BM,
+                         CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    rc = make_map_2d(&mb, a.bplanes, (uint64_t)K, brows, (uint64_t)K, BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    KArgs kb = ka;
+    kb.tb_per_row = 1;
+    kb.m_tiles = (R + BM - 1) / BM;
+    kb.total_tiles = kb.m_tiles * n_tiles;
+    kb.out = a.out_body;
+    rc = dispatch_ell<false>(ell, ma, mb, kb, st);
+    if (rc) return rc;
+    (*n_launches)++;
+  }
+  // ---- mask: Hankel operand, M = R * N
+  {
+    CUtensorMap ma, mb;
+    int rc = make_map_2d(&ma, a.wexp, 16, (uint64_t)(a.rows * a.Lc * 2 * N), 16, 16, A_ROWS_HANKEL,
+                         CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+    rc = make_map_2d(&mb, a.mplanes, (uint64_t)K, brows, (uint64_t)K, BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    KArgs km = ka;
+    km.tb_per_row = N / BM;
+    km.m_tiles = R * km.tb_per_row;
+    km.total_tiles = km.m_tiles * n_tiles;
+    km.out = a.out_mask;
+    rc = dispatch_ell<true>(ell, ma, mb, km, st);
+    if (rc) return rc;
+    (*n_launches)++;
+  }
+  return PHE_OK;
+}
+
+}  // namespace phe

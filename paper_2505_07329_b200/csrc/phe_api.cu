@@ -1,0 +1,325 @@
+// phe_api.cu — the C ABI declared in include/phe.h: validation, layouts, launches, and the
+// host-buffer end-to-end pipeline.  No torch types cross this boundary.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "phe_common.cuh"
+#include "side_kernels.cuh"
+
+using phe::KParams;
+
+static thread_local int g_last_cuda_error = 0;
+static thread_local int g_last_launches = 0;
+
+int phe_set_cuda_error(cudaError_t e) {
+  g_last_cuda_error = (int)e;
+  return PHE_ECUDA;
+}
+
+extern "C" {
+
+const char *phe_strerror(int code) {
+  switch (code) {
+    case PHE_OK: return "ok";
+    case PHE_EINVAL: return "invalid argument";
+    case PHE_ERANGE: return "value out of range";
+    case PHE_EMODULUS: return "modulus mismatch";
+    case PHE_ENOMEM: return "buffer too small";
+    case PHE_ECUDA: return "CUDA error";
+    case PHE_EUNSUPPORTED: return "unsupported parameters";
+  }
+  return "unknown error";
+}
+
+int phe_last_cuda_error(void) { return g_last_cuda_error; }
+int phe_last_launch_count(void) { return g_last_launches; }
+
+int phe_params_init(phe_params *p, int preset) {
+  if (!p) return PHE_EINVAL;
+  if (preset == PHE_PRESET_PAPER) {  // Table 1
+    *p = phe_params{2048, 39, 26, 27, 12, 0};
+  } else if (preset == PHE_PRESET_TOY) {  // DESIGN.md R16
+    *p = phe_params{1024, 32, 28, 21, 12, 0};
+  } else {
+    return PHE_EINVAL;
+  }
+  return PHE_OK;
+}
+
+int phe_params_validate(const phe_params *p) {
+  if (!p) return PHE_EINVAL;
+  if (p->N < 2 || (p->N & (p->N - 1))) return PHE_EINVAL;  // power of two
+  if (p->q_in < 1 || p->q_in > 64) return PHE_EINVAL;
+  if (p->q_out < 1 || p->q_out > p->q_in) return PHE_EINVAL;
+  if (p->beta < p->gamma || p->beta > p->q_in || p->gamma < 0) return PHE_EINVAL;
+  if (p->noise_eta < 0 || p->noise_eta > 32) return PHE_EINVAL;
+  return PHE_OK;
+}
+
+int phe_num_limbs(const phe_params *p) { return p ? (p->q_in + 7) / 8 : 0; }
+
+int64_t phe_num_blocks(const phe_params *p, int64_t d) {
+  return (p && p->N > 0 && d > 0) ? (d + p->N - 1) / p->N : 0;
+}
+
+}  // extern "C"
+
+// GPU-path requirements beyond phe_params_validate
+static int check_gpu(const phe_params *p, KParams *kp) {
+  int rc = phe_params_validate(p);
+  if (rc) return rc;
+  if (p->N < 128 || p->N > 16384) return PHE_EUNSUPPORTED;
+  if (p->q_out > 32) return PHE_EUNSUPPORTED;
+  kp->N = p->N;
+  kp->log2N = 0;
+  while ((1 << kp->log2N) < p->N) kp->log2N++;
+  kp->q_in = p->q_in; kp->q_out = p->q_out; kp->beta = p->beta; kp->eta = p->noise_eta;
+  kp->ell = (p->q_in + 7) / 8;
+  kp->qmask = phe::mask_bits(p->q_in);
+  return PHE_OK;
+}
+
+static inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+static inline int64_t op_rows(int64_t T, int ell) {
+  int64_t r = round_up(T * ell, 256);
+  return r < 256 ? 256 : r;
+}
+
+extern "C" {
+
+int phe_keygen(const phe_params *p, uint64_t master_seed, uint8_t *d_S, void *stream) {
+  KParams kp;
+  int rc = check_gpu(p, &kp);
+  if (rc) return rc;
+  if (!d_S) return PHE_EINVAL;
+  return phe::launch_keygen(kp, master_seed, d_S, S(stream));
+}
+
+int phe_encrypt_pack(const phe_params *p, const uint8_t *d_S, const int8_t *d_x, int64_t T,
+                     int64_t d_in, uint64_t seed_base, uint64_t noise_seed, uint64_t *d_seeds,
+                     uint64_t *d_body, void *stream) {
+  KParams kp;
+  int rc = check_gpu(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || d_in < 1) return PHE_EINVAL;
+  if (T > 0 && (!d_S || !d_x || !d_seeds || !d_body)) return PHE_EINVAL;
+  if (p->beta < 9) return PHE_ERANGE;  // int8 messages need |m| < 2^(beta-1)
+  int64_t L = phe_num_blocks(p, d_in);
+  return phe::launch_encrypt(kp, d_S, d_x, T, d_in, L, seed_base, noise_seed, d_seeds, d_body,
+                             S(stream));
+}
+
+size_t phe_weights_bytes(const phe_params *p, int64_t rows, int64_t cols) {
+  if (!p || rows < 1 || cols < 1 || p->N < 1) return 0;
+  int64_t Lc = phe_num_blocks(p, cols);
+  return (size_t)(rows * Lc * 2 * p->N * 16) + (size_t)(round_up(rows, 128) * Lc * p->N);
+}
+
+int phe_weights_prepare(const phe_params *p, const int8_t *d_W, int64_t d_out, int64_t d_in,
+                        int transpose, void *d_wprep, size_t bytes, void *stream) {
+  KParams kp;
+  int rc = check_gpu(p, &kp);
+  if (rc) return rc;
+  if (!d_W || !d_wprep || d_out < 1 || d_in < 1 || (transpose != 0 && transpose != 1))
+    return PHE_EINVAL;
+  int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  if (bytes < phe_weights_bytes(p, rows, cols)) return PHE_ENOMEM;
+  return phe::launch_weights_prepare(kp, d_W, d_out, d_in, transpose, d_wprep, S(stream));
+}
+
+size_t phe_ct_operand_bytes(const phe_params *p, int64_t T, int64_t L) {
+  if (!p || T < 0 || L < 1 || p->N < 1) return 0;
+  int ell = (p->q_in + 7) / 8;
+  return (size_t)(2 * op_rows(T, ell) * L * p->N);
+}
+
+int phe_ct_prepare(const phe_params *p, const uint64_t *d_seeds, const uint64_t *d_body, int64_t T,
+                   int64_t L, void *d_operand, size_t bytes, void *stream) {
+  KParams kp;
+  int rc = check_gpu(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || L < 1 || !d_operand) return PHE_EINVAL;
+  if (T > 0 && (!d_seeds || !d_body)) return PHE_EINVAL;
+  if (bytes < phe_ct_operand_bytes(p, T, L)) return PHE_ENOMEM;
+  uint8_t *mp = static_cast<uint8_t *>(d_operand);
+  uint8_t *bp = mp + op_rows(T, kp.ell) * L * p->N;
+  return phe::launch_ct_prepare(kp, d_seeds, d_body, T, L, mp, bp, S(stream));
+}
+
+}  // extern "C"
+
+static int matmul_common(const phe_params *p, const void *d_wprep, int64_t rows, int64_t cols,
+                         int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
+                         int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_gpu(p, &kp);
+  if (rc) return rc;
+  if (rows < 1 || cols < 1 || T < 0) return PHE_EINVAL;
+  if (row_begin < 0 || row_end > rows || row_begin > row_end) return PHE_EINVAL;
+  if (out_bits != p->q_in && out_bits != p->q_out) return PHE_EMODULUS;
+  if (T == 0 || row_end == row_begin) return PHE_OK;
+  if (!d_wprep || !d_operand || !d_out_mask || !d_out_body) return PHE_EINVAL;
+  if (p->N % 128) return PHE_EUNSUPPORTED;
+  const int64_t N = p->N, Lc = phe_num_blocks(p, cols);
+  phe::GemmArgs a{};
+  a.kp = kp;
+  a.wexp = static_cast<const uint8_t *>(d_wprep);
+  a.wplain = reinterpret_cast<const int8_t *>(a.wexp + rows * Lc * 2 * N * 16);
+  a.rows = rows;
+  a.wplain_rows = round_up(rows, 128);
+  a.op_rows = op_rows(T, kp.ell);
+  a.Lc = Lc;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  a.mplanes = static_cast<const uint8_t *>(d_operand);
+  a.bplanes = a.mplanes + a.op_rows * Lc * N;
+  a.T = T;
+  a.out_bits = out_bits;
+  a.out_mask = d_out_mask;
+  a.out_body = d_out_body;
+  int n = 0;
+  rc = phe::launch_limb_gemm(a, S(stream), &n);
+  g_last_launches = n;
+  return rc;
+}
+
+extern "C" {
+
+int phe_matmul_clear(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                     int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
+                     int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
+  return matmul_common(p, d_wprep, d_out, d_in, row_begin, row_end, d_operand, T, out_bits,
+                       d_out_mask, d_out_body, stream);
+}
+
+int phe_matmul_clear_T(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                       int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
+                       int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
+  // M = W^T: rows = d_in, cols = d_out
+  return matmul_common(p, d_wprep, d_in, d_out, row_begin, row_end, d_operand, T, out_bits,
+                       d_out_mask, d_out_body, stream);
+}
+
+int phe_matmul_clear_simt(const phe_params *p, const int8_t *d_W, int64_t d_out, int64_t d_in,
+                          int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
+                          int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
+  KParams kp;
+  int rc = check_gpu(p, &kp);
+  if (rc) return rc;
+  if (d_out < 1 || d_in < 1 || T < 0 || row_begin < 0 || row_end > d_out || row_begin > row_end)
+    return PHE_EINVAL;
+  if (out_bits != p->q_in && out_bits != p->q_out) return PHE_EMODULUS;
+  if (T == 0 || row_end == row_begin) return PHE_OK;
+  const int64_t L = phe_num_blocks(p, d_in);
+  const uint8_t *mp = static_cast<const uint8_t *>(d_operand);
+  const uint8_t *bp = mp + op_rows(T, kp.ell) * L * p->N;
+  return phe::launch_simt_matmul(kp, d_W, d_in, row_begin, row_end - row_begin, mp, bp, L, T,
+                                 out_bits, d_out_mask, d_out_body, S(stream));
+}
+
+int phe_modswitch(const uint64_t *d_in, uint32_t *d_out, int64_t count, int32_t from_bits,
+                  int32_t to_bits, void *stream) {
+  if (count < 0 || to_bits < 1 || to_bits > 32 || from_bits < to_bits || from_bits > 64)
+    return PHE_EINVAL;
+  if (count == 0) return PHE_OK;
+  if (!d_in || !d_out) return PHE_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(d_in) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
+    return PHE_EINVAL;  // 16-byte vector accesses
+  return phe::launch_modswitch(d_in, d_out, count, from_bits, to_bits, S(stream));
+}
+
+int phe_decrypt_unpack(const phe_params *p, const uint8_t *d_S, const void *d_mask,
+                       const void *d_body, int64_t T, int64_t rows, int32_t q_bits, int32_t *d_y,
+                       void *stream) {
+  KParams kp;
+  int rc = check_gpu(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || rows < 0) return PHE_EINVAL;
+  if (q_bits != p->q_in && q_bits != p->q_out) return PHE_EMODULUS;
+  if (T * rows == 0) return PHE_OK;
+  if (!d_S || !d_mask || !d_body || !d_y) return PHE_EINVAL;
+  const bool u64 = (q_bits == p->q_in);  // matmul_clear writes uint64 iff out_bits == q_in
+  return phe::launch_decrypt(kp, d_S, d_mask, d_body, T * rows, q_bits, u64, d_y, S(stream));
+}
+
+// ------------------------------------------------------------------ host end-to-end
+// Chunked pipeline over two device slots and two streams: chunk c runs H2D -> ct_prepare ->
+// limb GEMM -> D2H on stream c%2, so chunk c+1's copies overlap chunk c's GEMM.
+struct HostWs {
+  void *buf = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t ev = nullptr;
+};
+static thread_local HostWs g_ws;
+
+int phe_server_matvec_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                           int transpose, int64_t row_begin, int64_t row_end,
+                           const uint64_t *h_seeds, const uint64_t *h_body, int64_t T,
+                           int64_t chunk_tokens, uint32_t *h_out_mask, uint32_t *h_out_body,
+                           void *stream) {
+  KParams kp;
+  int rc = check_gpu(p, &kp);
+  if (rc) return rc;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  if (rows < 1 || cols < 1 || T < 0 || chunk_tokens < 1) return PHE_EINVAL;
+  if (row_begin < 0 || row_end > rows || row_begin > row_end) return PHE_EINVAL;
+  if (T == 0 || row_end == row_begin) return PHE_OK;
+  if (!d_wprep || !h_seeds || !h_body || !h_out_mask || !h_out_body) return PHE_EINVAL;
+  const int64_t N = p->N, L = phe_num_blocks(p, cols), R = row_end - row_begin;
+  const int64_t C = chunk_tokens < T ? chunk_tokens : T;
+  const size_t b_seeds = round_up(C * L * 8, 256), b_body = round_up(C * L * N * 8, 256);
+  const size_t b_op = round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256);
+  const size_t b_om = round_up(C * R * N * 4, 256), b_ob = round_up(C * R * 4, 256);
+  const size_t slot = b_seeds + b_body + b_op + b_om + b_ob;
+  if (g_ws.bytes < 2 * slot) {
+    if (g_ws.buf) cudaFree(g_ws.buf);
+    g_ws.buf = nullptr; g_ws.bytes = 0;
+    if (cudaMalloc(&g_ws.buf, 2 * slot) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+    g_ws.bytes = 2 * slot;
+  }
+  if (!g_ws.st[0]) {
+    for (int s = 0; s < 2; s++)
+      if (cudaStreamCreateWithFlags(&g_ws.st[s], cudaStreamNonBlocking) != cudaSuccess)
+        return phe_set_cuda_error(cudaGetLastError());
+    if (cudaEventCreateWithFlags(&g_ws.ev, cudaEventDisableTiming) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+  }
+  // order after work already queued on the caller's stream (e.g. weight registration)
+  cudaEventRecord(g_ws.ev, S(stream));
+  cudaStreamWaitEvent(g_ws.st[0], g_ws.ev, 0);
+  cudaStreamWaitEvent(g_ws.st[1], g_ws.ev, 0);
+  int64_t c = 0;
+  for (int64_t t0 = 0; t0 < T; t0 += C, c++) {
+    const int64_t n = (T - t0) < C ? (T - t0) : C;
+    cudaStream_t st = g_ws.st[c & 1];
+    uint8_t *base = static_cast<uint8_t *>(g_ws.buf) + (c & 1) * slot;
+    uint64_t *d_seeds = reinterpret_cast<uint64_t *>(base);
+    uint64_t *d_bod = reinterpret_cast<uint64_t *>(base + b_seeds);
+    void *d_op = base + b_seeds + b_body;
+    uint32_t *d_om = reinterpret_cast<uint32_t *>(base + b_seeds + b_body + b_op);
+    uint32_t *d_ob = reinterpret_cast<uint32_t *>(base + b_seeds + b_body + b_op + b_om);
+    cudaMemcpyAsync(d_seeds, h_seeds + t0 * L, n * L * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_bod, h_body + t0 * L * N, n * L * N * 8, cudaMemcpyHostToDevice, st);
+    rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
+    if (rc) return rc;
+    rc = matmul_common(p, d_wprep, rows, cols, row_begin, row_end, d_op, n, p->q_out, d_om, d_ob, st);
+    if (rc) return rc;
+    cudaMemcpyAsync(h_out_mask + t0 * R * N, d_om, n * R * N * 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h_out_body + t0 * R, d_ob, n * R * 4, cudaMemcpyDeviceToHost, st);
+  }
+  cudaError_t e0 = cudaStreamSynchronize(g_ws.st[0]);
+  cudaError_t e1 = cudaStreamSynchronize(g_ws.st[1]);
+  if (e0 != cudaSuccess) return phe_set_cuda_error(e0);
+  if (e1 != cudaSuccess) return phe_set_cuda_error(e1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return phe_set_cuda_error(e);
+  return PHE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,371 @@
+// side_kernels.cu — HBM/ALU-bound kernels around the limb GEMM:
+//   keygen, encrypt_pack (client), weights_prepare (a2), ct_prepare (a3+a4),
+//   modswitch (a8 standalone), decrypt_unpack (client), and the SIMT cross-check GEMM.
+// Every kernel is plain, coalesced CUDA for sm_100a; grids are sized in multiples of the SM
+// count where the work allows (148 SMs).
+#include <cstdint>
+
+#include "phe_common.cuh"
+#include "side_kernels.cuh"
+
+namespace phe {
+
+// ------------------------------------------------------------------ keygen (R6)
+__global__ void keygen_kernel(uint64_t master_seed, int N, uint8_t *__restrict__ S) {
+  // one thread per 64-byte keystream block = 512 key bits
+  int blk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blk * 512 >= N) return;
+  uint32_t o[16];
+  chacha20_block(master_seed, (uint32_t)blk, nonce_sk(), o);
+  for (int b = 0; b < 512 && blk * 512 + b < N; b++) {
+    uint32_t byte = (o[(b >> 3) >> 2] >> (8 * ((b >> 3) & 3))) & 0xffu;
+    S[blk * 512 + b] = (uint8_t)((byte >> (b & 7)) & 1u);
+  }
+}
+
+// ------------------------------------------------------------------ encrypt_pack
+// One CTA per block (tau, i).  B = A*S + E + Delta*x_hat mod 2^q_in.
+// A*S: negacyclic product with the binary key, computed as sum over key bits S[n] = 1 of
+// the shifted mask: (A*S)[k] = sum_{n<=k, S_n} A[k-n] - sum_{n>k, S_n} A[k-n+N].
+// The loop over n is warp-uniform (S[n] read from shared memory by all lanes).
+constexpr int ENC_THREADS = 256;
+
+__global__ void __launch_bounds__(ENC_THREADS)
+encrypt_kernel(KParams kp, const uint8_t *__restrict__ S, const int8_t *__restrict__ x, int64_t T,
+               int64_t d_in, int64_t L, uint64_t seed_base, uint64_t noise_seed,
+               uint64_t *__restrict__ seeds, uint64_t *__restrict__ body) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int N = kp.N;
+  uint64_t *A = reinterpret_cast<uint64_t *>(smem);
+  uint8_t *Ss = smem + sizeof(uint64_t) * N;
+  const int64_t blk = blockIdx.x;  // tau * L + i
+  const int64_t tau = blk / L, i = blk % L;
+  const uint64_t seed = seed_base + (uint64_t)blk;
+  if (threadIdx.x == 0) seeds[blk] = seed;
+  for (int b = threadIdx.x; b < N / 8; b += blockDim.x) {
+    uint64_t w[8];
+    chacha20_u64x8(seed, (uint32_t)b, nonce_mask(), w);
+#pragma unroll
+    for (int e = 0; e < 8; e++) A[8 * b + e] = w[e] & kp.qmask;
+  }
+  for (int k = threadIdx.x; k < N; k += blockDim.x) Ss[k] = S[k];
+  __syncthreads();
+
+  const uint64_t delta = 1ull << (kp.q_in - kp.beta);
+  // thread handles k = threadIdx.x + e * ENC_THREADS; the n-loop is warp-uniform
+  for (int k = threadIdx.x; k < N; k += ENC_THREADS) {
+    uint64_t acc = 0;
+    for (int n = 0; n < N; n++) {
+      if (!Ss[n]) continue;  // uniform branch
+      int d = k - n;
+      uint64_t a = A[d & (N - 1)];
+      acc += (d >= 0) ? a : (0ull - a);
+    }
+    int64_t c = i * (int64_t)N + k;
+    int64_t xv = (c < d_in) ? (int64_t)x[tau * d_in + c] : 0;
+    int64_t ev = 0;
+    if (kp.eta > 0) {
+      // one keystream u64 word per coefficient in global order (tau, i, k)  (R5/R6)
+      uint64_t widx = (uint64_t)blk * (uint64_t)N + (uint64_t)k;
+      uint32_t o[16];
+      chacha20_block(noise_seed, (uint32_t)(widx >> 3), nonce_noise(), o);
+      int q = (int)(widx & 7);
+      uint64_t w = (uint64_t)o[2 * q] | ((uint64_t)o[2 * q + 1] << 32);
+      uint64_t m = mask_bits(kp.eta);
+      ev = (int64_t)__popcll(w & m) - (int64_t)__popcll((w >> kp.eta) & m);
+    }
+    uint64_t v = acc + (uint64_t)ev + delta * (uint64_t)xv;
+    body[blk * (int64_t)N + k] = v & kp.qmask;
+  }
+}
+
+// ------------------------------------------------------------------ weights_prepare (a2)
+// 16-shift expansion of wext (P:182 absorbed):
+//   exp[((j*Lc + i)*2N + m)*16 + b] = wext_{j,i}[m + b]
+//   wext_{j,i}[u] = M[j, iN+u] (u < N), -M[j, iN+u-N] (N <= u < 2N), 0 otherwise / beyond cols.
+__device__ __forceinline__ int8_t mat_at(const int8_t *__restrict__ W, int64_t d_in, int transpose,
+                                         int64_t r, int64_t c) {
+  // M = W (transpose = 0) or W^T (transpose = 1); W is [d_out][d_in]
+  return transpose ? W[c * d_in + r] : W[r * d_in + c];
+}
+
+__global__ void weights_expand_kernel(const int8_t *__restrict__ W, int64_t d_in, int transpose,
+                                      int64_t rows, int64_t cols, int N, int64_t Lc,
+                                      uint4 *__restrict__ exp16) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (j, i, m)
+  int64_t total = rows * Lc * 2 * N;
+  if (idx >= total) return;
+  int64_t m = idx % (2 * N);
+  int64_t ji = idx / (2 * N);
+  int64_t i = ji % Lc, j = ji / Lc;
+  uint32_t wd[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    uint32_t packed = 0;
+#pragma unroll
+    for (int bb = 0; bb < 4; bb++) {
+      int64_t u = m + 4 * q + bb;
+      int v = 0;
+      if (u < 2 * N) {
+        int64_t c = i * N + (u < N ? u : u - N);
+        if (c < cols) {
+          int w = mat_at(W, d_in, transpose, j, c);
+          v = (u < N) ? w : -w;
+        }
+      }
+      packed |= ((uint32_t)(uint8_t)(int8_t)v) << (8 * bb);
+    }
+    wd[q] = packed;
+  }
+  exp16[idx] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+}
+
+__global__ void weights_plain_kernel(const int8_t *__restrict__ W, int64_t d_in, int transpose,
+                                     int64_t rows, int64_t rows_pad, int64_t cols, int64_t K,
+                                     int8_t *__restrict__ plain) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows_pad * K) return;
+  int64_t j = idx / K, c = idx % K;
+  plain[idx] = (j < rows && c < cols) ? mat_at(W, d_in, transpose, j, c) : (int8_t)0;
+}
+
+// ------------------------------------------------------------------ ct_prepare (a3 + a4)
+// Thread per (tau, i, 8-word group): expand 8 mask words with ChaCha20 (R6), reduce
+// mod 2^q_in, split into ell byte planes; same limb split for the 8 body words.
+__global__ void ct_prepare_kernel(KParams kp, const uint64_t *__restrict__ seeds,
+                                  const uint64_t *__restrict__ body, int64_t T, int64_t L,
+                                  uint8_t *__restrict__ mask_planes,
+                                  uint8_t *__restrict__ body_planes) {
+  const int N = kp.N;
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t groups = (int64_t)N / 8;
+  if (idx >= T * L * groups) return;
+  int64_t g = idx % groups;
+  int64_t blk = idx / groups;  // tau * L + i
+  int64_t tau = blk / L, i = blk % L;
+  const int64_t K = L * N;
+  uint64_t w[8];
+  chacha20_u64x8(seeds[blk], (uint32_t)g, nonce_mask(), w);
+  const uint64_t *bsrc = body + blk * (int64_t)N + 8 * g;
+  uint64_t bw[8];
+  {
+    const ulonglong2 *b2 = reinterpret_cast<const ulonglong2 *>(bsrc);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      ulonglong2 v = b2[e];
+      bw[2 * e] = v.x; bw[2 * e + 1] = v.y;
+    }
+  }
+  const int64_t col = i * N + 8 * g;
+  for (int l = 0; l < kp.ell; l++) {
+    uint64_t pm = 0, pb = 0;
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      pm |= (((w[e] & kp.qmask) >> (8 * l)) & 0xffull) << (8 * e);
+      pb |= (((bw[e] & kp.qmask) >> (8 * l)) & 0xffull) << (8 * e);
+    }
+    int64_t row = tau * kp.ell + l;
+    *reinterpret_cast<uint64_t *>(mask_planes + row * K + col) = pm;
+    *reinterpret_cast<uint64_t *>(body_planes + row * K + col) = pb;
+  }
+}
+
+// ------------------------------------------------------------------ modswitch (a8)
+__global__ void modswitch_kernel(const uint64_t *__restrict__ in, uint32_t *__restrict__ out,
+                                 int64_t count, int shift, uint32_t omask) {
+  int64_t i4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const uint64_t half = shift > 0 ? (1ull << (shift - 1)) : 0ull;
+  if (i4 + 3 < count) {
+    const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(in + i4);
+    ulonglong2 a = __ldcs(p), b = __ldcs(p + 1);
+    uint4 r;
+    r.x = (uint32_t)((a.x + half) >> shift) & omask;
+    r.y = (uint32_t)((a.y + half) >> shift) & omask;
+    r.z = (uint32_t)((b.x + half) >> shift) & omask;
+    r.w = (uint32_t)((b.y + half) >> shift) & omask;
+    __stcs(reinterpret_cast<uint4 *>(out + i4), r);
+  } else {
+    for (int64_t k = i4; k < count; k++) out[k] = (uint32_t)((in[k] + half) >> shift) & omask;
+  }
+}
+
+// ------------------------------------------------------------------ decrypt_unpack
+// Warp per LWE ciphertext (tau, j): phi = b - <a, S'> mod 2^q, decode.
+template <typename Word>
+__global__ void decrypt_kernel(KParams kp, const uint8_t *__restrict__ S,
+                               const Word *__restrict__ mask, const Word *__restrict__ body,
+                               int64_t n_ct, int q_bits, int32_t *__restrict__ y) {
+  extern __shared__ uint8_t Ss[];
+  const int N = kp.N;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) Ss[k] = S[k];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  constexpr int V = 16 / sizeof(Word);  // words per 16-byte load
+  for (int64_t ct = warp; ct < n_ct; ct += nwarps) {
+    const Word *a = mask + ct * (int64_t)N;
+    uint64_t acc = 0;
+    for (int t0 = lane * V; t0 < N; t0 += 32 * V) {
+      uint4 raw = __ldcs(reinterpret_cast<const uint4 *>(a + t0));
+      const Word *wv = reinterpret_cast<const Word *>(&raw);
+#pragma unroll
+      for (int e = 0; e < V; e++) acc += Ss[t0 + e] ? (uint64_t)wv[e] : 0ull;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const uint64_t qm = mask_bits(q_bits);
+      uint64_t phi = ((uint64_t)body[ct] - acc) & qm;
+      const uint64_t tmask = mask_bits(kp.beta);
+      uint64_t m;
+      if (q_bits >= kp.beta) {
+        // floor((phi + 2^(sh-1)) / 2^sh) = (phi >> sh) + bit (sh-1) of phi: no carry-out
+        int sh = q_bits - kp.beta;
+        m = sh == 0 ? phi : ((phi >> sh) + ((phi >> (sh - 1)) & 1ull));
+        m &= tmask;
+      } else {
+        m = (phi << (kp.beta - q_bits)) & tmask;
+      }
+      int64_t c = (m >= (1ull << (kp.beta - 1))) ? (int64_t)m - (int64_t)(1ull << kp.beta) : (int64_t)m;
+      y[ct] = (int32_t)c;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ SIMT cross-check GEMM
+// Reference CUDA-core implementation (64-bit MACs, no limbs in the arithmetic): one CTA per
+// (tau, j); threads stride over t.  Reads the same limb-plane operand as the tensor-core
+// path and reconstructs each mask word from its limbs.  Test infrastructure on the device.
+__device__ __forceinline__ uint64_t limb_word(const uint8_t *__restrict__ planes, int64_t K,
+                                              int64_t tau, int ell, int64_t col) {
+  uint64_t v = 0;
+  for (int l = 0; l < ell; l++) v |= (uint64_t)planes[(tau * ell + l) * K + col] << (8 * l);
+  return v;
+}
+
+__global__ void simt_matmul_kernel(KParams kp, const int8_t *__restrict__ W, int64_t d_in,
+                                   int64_t row_begin, int64_t R, const uint8_t *__restrict__ mplanes,
+                                   const uint8_t *__restrict__ bplanes, int64_t L, int out_bits,
+                                   void *__restrict__ out_mask, void *__restrict__ out_body) {
+  const int N = kp.N;
+  const int64_t tau = blockIdx.x / R, jr = blockIdx.x % R, j = row_begin + jr;
+  const int64_t K = L * N;
+  const int8_t *w = W + j * d_in;
+  const int shift = kp.q_in - out_bits;
+  const uint64_t half = shift > 0 ? (1ull << (shift - 1)) : 0ull;
+  for (int t = threadIdx.x; t < N; t += blockDim.x) {
+    uint64_t acc = 0;
+    for (int64_t c = 0; c < d_in; c++) {
+      int64_t i = c / N, m = c % N;
+      int64_t wv = w[c];
+      if (wv == 0) continue;
+      uint64_t a = (m >= t) ? limb_word(mplanes, K, tau, kp.ell, i * N + (m - t))
+                            : (0ull - limb_word(mplanes, K, tau, kp.ell, i * N + (m - t + N)));
+      acc += (uint64_t)wv * a;
+    }
+    acc &= kp.qmask;
+    int64_t o = (tau * R + jr) * N + t;
+    if (shift == 0) static_cast<uint64_t *>(out_mask)[o] = acc;
+    else static_cast<uint32_t *>(out_mask)[o] = (uint32_t)(((acc + half) >> shift) & mask_bits(out_bits));
+  }
+  if (threadIdx.x == 0) {
+    uint64_t acc = 0;
+    for (int64_t c = 0; c < d_in; c++)
+      acc += (uint64_t)(int64_t)w[c] * limb_word(bplanes, K, tau, kp.ell, c);
+    acc &= kp.qmask;
+    int64_t o = tau * R + jr;
+    if (shift == 0) static_cast<uint64_t *>(out_body)[o] = acc;
+    else static_cast<uint32_t *>(out_body)[o] = (uint32_t)(((acc + half) >> shift) & mask_bits(out_bits));
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+int launch_keygen(const KParams &kp, uint64_t seed, uint8_t *S, cudaStream_t st) {
+  int nb = (kp.N + 511) / 512;
+  keygen_kernel<<<1, nb, 0, st>>>(seed, kp.N, S);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_encrypt(const KParams &kp, const uint8_t *S, const int8_t *x, int64_t T, int64_t d_in,
+                   int64_t L, uint64_t seed_base, uint64_t noise_seed, uint64_t *seeds,
+                   uint64_t *body, cudaStream_t st) {
+  if (T == 0) return PHE_OK;
+  size_t smem = sizeof(uint64_t) * kp.N + kp.N;
+  static thread_local int configured = 0;
+  if (!configured) {
+    cudaFuncSetAttribute(encrypt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = 1;
+  }
+  encrypt_kernel<<<(unsigned)(T * L), ENC_THREADS, smem, st>>>(kp, S, x, T, d_in, L, seed_base,
+                                                              noise_seed, seeds, body);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_weights_prepare(const KParams &kp, const int8_t *W, int64_t d_out, int64_t d_in,
+                           int transpose, void *wprep, cudaStream_t st) {
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  const int N = kp.N;
+  const int64_t Lc = (cols + N - 1) / N;
+  uint8_t *base = static_cast<uint8_t *>(wprep);
+  int64_t n_exp = rows * Lc * 2 * N;
+  weights_expand_kernel<<<(unsigned)((n_exp + 255) / 256), 256, 0, st>>>(
+      W, d_in, transpose, rows, cols, N, Lc, reinterpret_cast<uint4 *>(base));
+  PHE_CUDA_CHECK_LAUNCH();
+  const int64_t rows_pad = (rows + 127) / 128 * 128;
+  int64_t n_plain = rows_pad * Lc * N;
+  weights_plain_kernel<<<(unsigned)((n_plain + 255) / 256), 256, 0, st>>>(
+      W, d_in, transpose, rows, rows_pad, cols, Lc * N, reinterpret_cast<int8_t *>(base + n_exp * 16));
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_ct_prepare(const KParams &kp, const uint64_t *seeds, const uint64_t *body, int64_t T,
+                      int64_t L, uint8_t *mask_planes, uint8_t *body_planes, cudaStream_t st) {
+  int64_t n = T * L * (kp.N / 8);
+  if (n == 0) return PHE_OK;
+  ct_prepare_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kp, seeds, body, T, L,
+                                                                 mask_planes, body_planes);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_modswitch(const uint64_t *in, uint32_t *out, int64_t count, int from, int to,
+                     cudaStream_t st) {
+  if (count == 0) return PHE_OK;
+  int64_t threads = (count + 3) / 4;
+  modswitch_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+      in, out, count, from - to, (uint32_t)mask_bits(to));
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_decrypt(const KParams &kp, const uint8_t *S, const void *mask, const void *body,
+                   int64_t n_ct, int q_bits, bool u64words, int32_t *y, cudaStream_t st) {
+  if (n_ct == 0) return PHE_OK;
+  int64_t warps = n_ct;
+  int64_t blocks = (warps * 32 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (u64words)
+    decrypt_kernel<uint64_t><<<(unsigned)blocks, 256, kp.N, st>>>(
+        kp, S, (const uint64_t *)mask, (const uint64_t *)body, n_ct, q_bits, y);
+  else
+    decrypt_kernel<uint32_t><<<(unsigned)blocks, 256, kp.N, st>>>(
+        kp, S, (const uint32_t *)mask, (const uint32_t *)body, n_ct, q_bits, y);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_simt_matmul(const KParams &kp, const int8_t *W, int64_t d_in, int64_t row_begin,
+                       int64_t R, const uint8_t *mplanes, const uint8_t *bplanes, int64_t L,
+                       int64_t T, int out_bits, void *out_mask, void *out_body, cudaStream_t st) {
+  if (T == 0 || R == 0) return PHE_OK;
+  simt_matmul_kernel<<<(unsigned)(T * R), 256, 0, st>>>(kp, W, d_in, row_begin, R, mplanes,
+                                                        bplanes, L, out_bits, out_mask, out_body);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+}  // namespace phe

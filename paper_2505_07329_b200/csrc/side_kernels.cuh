@@ -1,0 +1,44 @@
+// side_kernels.cuh — launchers (host) for side_kernels.cu and limb_gemm.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "phe_common.cuh"
+
+namespace phe {
+
+int launch_keygen(const KParams &kp, uint64_t seed, uint8_t *S, cudaStream_t st);
+int launch_encrypt(const KParams &kp, const uint8_t *S, const int8_t *x, int64_t T, int64_t d_in,
+                   int64_t L, uint64_t seed_base, uint64_t noise_seed, uint64_t *seeds,
+                   uint64_t *body, cudaStream_t st);
+int launch_weights_prepare(const KParams &kp, const int8_t *W, int64_t d_out, int64_t d_in,
+                           int transpose, void *wprep, cudaStream_t st);
+int launch_ct_prepare(const KParams &kp, const uint64_t *seeds, const uint64_t *body, int64_t T,
+                      int64_t L, uint8_t *mask_planes, uint8_t *body_planes, cudaStream_t st);
+int launch_modswitch(const uint64_t *in, uint32_t *out, int64_t count, int from, int to,
+                     cudaStream_t st);
+int launch_decrypt(const KParams &kp, const uint8_t *S, const void *mask, const void *body,
+                   int64_t n_ct, int q_bits, bool u64words, int32_t *y, cudaStream_t st);
+int launch_simt_matmul(const KParams &kp, const int8_t *W, int64_t d_in, int64_t row_begin,
+                       int64_t R, const uint8_t *mplanes, const uint8_t *bplanes, int64_t L,
+                       int64_t T, int out_bits, void *out_mask, void *out_body, cudaStream_t st);
+
+// limb_gemm.cu: the tcgen05 int8 limb GEMM (mask = Hankel operand, body = plain operand).
+struct GemmArgs {
+  KParams kp;
+  const uint8_t *wexp;    // [rows][Lc][2N][16] 16-shift expansion
+  const int8_t *wplain;   // [wplain_rows][Lc*N] (rows padded to a multiple of 128)
+  int64_t rows;           // rows of the prepared matrix M
+  int64_t wplain_rows;    // padded row count of wplain
+  int64_t op_rows;        // padded row count of each limb-plane matrix (>= T*ell, mult. of 256)
+  int64_t Lc;             // blocks along M's columns (= L of the input ciphertext)
+  int64_t row_begin, row_end;
+  const uint8_t *mplanes; // [T*ell][Lc*N]
+  const uint8_t *bplanes; // [T*ell][Lc*N]
+  int64_t T;
+  int out_bits;
+  void *out_mask, *out_body;
+};
+int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches);
+
+}  // namespace phe
