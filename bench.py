@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""bench.py — encrypted tokens/s through the W.[x]_HE hot path on B200 (BASELINE.json metric).
+
+Default workload = BASELINE configs[1]: Llama-3.2-1B q_proj 2048x2048 forward, B=8 x C=256 =
+2048 tokens per GPU, Table 1 parameters (N=2048, q 2^39 -> 2^26).  One step = one pass of the
+whole server hot path over one batch:
+    ct_prepare   seed expansion (ChaCha20) + limb split of masks and bodies      (a3, a4)
+    body GEMM    b = W . B  (tcgen05 limb GEMM, plain operand)                    (a6-a8)
+    mask GEMM    a = Hankel(W) . A-limbs (tcgen05 limb GEMM) + recombine + switch (a5, a7, a8)
+Inputs are resident in HBM when the timed region starts (client-side keygen/encrypt_pack run
+untimed); L2 is flushed (256 MiB write) between timed steps, outside the per-step events.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload q_proj|ffn]
+Multi-GPU (torchrun, one rank per GPU): tokens are sharded (each rank its own 2048-token
+batch, "scaling": "weak"); no collective on the data path; the NCCL all-reduce only takes
+the max step time over ranks.  --impl reference times the CPU oracle (oracle/) on host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "encrypted tokens/sec through all Llama-3.2-1B linears; % int8 TC peak"
+NOMINAL_INT8_TOPS = 4500.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["q_proj", "ffn"], default="q_proj")
+    ap.add_argument("--tokens", type=int, default=2048, help="tokens per rank (B*C = 8*256)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e/cpu/clocks)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- environment
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return mp, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(gpu_index)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.count(",") >= 8]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- workloads
+def linears(workload: str):
+    """(name, d_out, d_in, transpose) of each linear one step runs (Llama-3.2-1B)."""
+    if workload == "q_proj":
+        return [("q_proj", 2048, 2048, False)]
+    # configs[2]: FFN gate/up 8192x2048 and down 2048x8192, forward + backward W^T
+    return [("gate", 8192, 2048, False), ("up", 8192, 2048, False), ("down", 2048, 8192, False),
+            ("gate_T", 8192, 2048, True), ("up_T", 8192, 2048, True), ("down_T", 2048, 8192, True)]
+
+
+def alg_int8_ops(p, rows, cols, T, part):
+    """per token per linear d_out*d_in*(N+1) Z_Q-MACs = N mask + 1 body; each costs
+    ell int8 MACs; 2 ops per MAC.  K is the unpadded d_in."""
+    macs = rows * cols * (p.N if part == "mask" else 1)
+    return 2.0 * p.ell * macs * T
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_07329_b200 as phe
+    import synth
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(dev))
+    phe.load()
+    p = phe.params(phe.PRESET_PAPER)
+    T = args.tokens
+    lins = linears(args.workload)
+    # ---------------- untimed setup: weights (server registration) and client encryption
+    regs = []
+    for name, d_out, d_in, tr in lins:
+        W = torch.from_numpy(synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED + len(regs))).to(dev)
+        regs.append((name, phe.Weights(p, W, transpose=tr)))
+        del W
+    S = phe.keygen(p, synth.MASTER_SEED + 17)
+    inputs = {}
+    for name, w in regs:
+        d = w.cols
+        if d not in inputs:
+            gen = synth.activations_int8 if not w.transpose else synth.gradients_int8
+            x = torch.from_numpy(gen(T, d, seed=synth.MASTER_SEED + 1000 * rank + d)).to(dev)
+            seeds, body = phe.encrypt_pack(p, S, x, synth.seed_base(rank * 131 + d))
+            inputs[d] = (seeds, body)
+    chunk = T if args.workload == "q_proj" else 256  # FFN outputs are 137 GB/T=2048: chunk tokens
+    max_rows = max(w.rows for _, w in regs)
+    out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
+    out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)
+    operands = {d: torch.empty(phe.load().phe_ct_operand_bytes(__import__("ctypes").byref(p), chunk, p.L(d)),
+                               dtype=torch.uint8, device=dev) for d in inputs}
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    parts_ms = {"ct_prepare": [], "body_gemm": [], "mask_gemm": []}
+    launches = [0]
+
+    def step(record):
+        evs = []
+        for t0 in range(0, T, chunk):
+            n = min(chunk, T - t0)
+            prepared = set()
+            for name, w in regs:
+                d = w.cols
+                seeds, body = inputs[d]
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                e[0].record(stream)
+                if d not in prepared:
+                    phe.ct_prepare(p, seeds[t0:t0 + n], body[t0:t0 + n], out=operands[d])
+                    prepared.add(d)
+                    launches[0] += 1
+                e[1].record(stream)
+                f = phe.matmul_clear_T if w.transpose else phe.matmul_clear
+                mview = out_mask.view(-1)[: n * w.rows * p.N].view(n, w.rows, p.N)
+                bview = out_body.view(-1)[: n * w.rows].view(n, w.rows)
+                f(p, w, operands[d], n, out_mask=phe.SKIP, out_body=bview)   # a6 body GEMM
+                launches[0] += phe.last_launch_count()
+                e[2].record(stream)
+                f(p, w, operands[d], n, out_mask=mview, out_body=phe.SKIP)   # a5 mask GEMM
+                launches[0] += phe.last_launch_count()
+                e[3].record(stream)
+                evs.append(e)
+        return evs
+
+    # ---------------- warmup
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    launches[0] = 0
+    # ---------------- timed region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = None if args.profile else ClockSampler(local)
+    step_ms = []
+    for _ in range(args.steps):
+        evs = step(True)
+        torch.cuda.synchronize()
+        step_ms.append(sum(e[0].elapsed_time(e[3]) for e in evs))
+        parts_ms["ct_prepare"].append(sum(e[0].elapsed_time(e[1]) for e in evs))
+        parts_ms["body_gemm"].append(sum(e[1].elapsed_time(e[2]) for e in evs))
+        parts_ms["mask_gemm"].append(sum(e[2].elapsed_time(e[3]) for e in evs))
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+    torch.cuda.synchronize()
+    clocks = clk.stop() if clk else None
+    if world > 1:
+        dist.barrier()
+    ms = statistics.mean(step_ms)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * T / (ms_max / 1e3)
+
+    # ---------------- roofline of the dominant kernel (mask limb GEMM)
+    mp, src = measured_peaks()
+    peak = 2.0 * float(mp["bf16_tflops"])  # int8 dense = 2x bf16 (guide's nominal ratio)
+    mask_ops = sum(alg_int8_ops(p, w.rows, w.cols, T, "mask") for _, w in regs)
+    mask_ms = statistics.mean(parts_ms["mask_gemm"])
+    achieved = mask_ops / (mask_ms / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.workload)
+        except Exception:
+            traffic = None
+    total_ops = sum(alg_int8_ops(p, w.rows, w.cols, T, "mask") + alg_int8_ops(p, w.rows, w.cols, T, "body")
+                    for _, w in regs)
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "limb_gemm_kernel<5,HANKEL> (mask contraction)",
+                "ops": "int8 tensor ops (2 per MAC), algorithmic: 2*ell*d_out*d_in*N per token",
+                "peak_source": f"{src}: 2 x bf16_tflops (burst) of MEASURED_PEAKS.json",
+                "frac_of_nominal_4500": round(achieved / NOMINAL_INT8_TOPS, 4),
+                "step_frac": round(total_ops / (ms_max / 1e3) / 1e12 / peak, 4)}
+
+    # ---------------- e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e and not args.profile and args.workload == "q_proj":
+        name, w = regs[0]
+        seeds, body = inputs[w.cols]
+        hs = seeds.cpu().pin_memory()
+        hb = body.cpu().pin_memory()
+        hm = torch.empty((T, w.rows, p.N), dtype=torch.int32, pin_memory=True)
+        hbo = torch.empty((T, w.rows), dtype=torch.int32, pin_memory=True)
+        phe.server_matvec_host(p, w, hs, hb, hm, hbo, chunk_tokens=256)  # warm
+        if world > 1:
+            dist.barrier()
+        wall = []
+        for _ in range(max(2, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            phe.server_matvec_host(p, w, hs, hb, hm, hbo, chunk_tokens=256)
+            wall.append(time.perf_counter() - t0)
+        e2e_s = statistics.mean(wall)
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * T / float(te.item()), 2), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(hs.numel() * 8 + hb.numel() * 8),
+               "d2h_bytes_per_step": int(hm.numel() * 4 + hbo.numel() * 4),
+               "ms_per_step": round(float(te.item()) * 1e3, 2),
+               "api": "phe_server_matvec_host (pinned host buffers, 256-token chunks, 2 streams)"}
+        del hm, hbo
+
+    # ---------------- CPU baseline: the oracle on host cores, bounded sample (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        cpu = cpu_baseline(args, lins[0], budget_s=12.0)
+
+    launches_total = launches[0]
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic (seeded int8 Llama-like W, DTok int8 activations, ChaCha20 masks)",
+            "config": config_dict(args, world, T),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
+            "clocks": clocks,
+            "breakdown_ms": {k: round(statistics.mean(v), 3) for k, v in parts_ms.items()},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def config_dict(args, world, T):
+    wl = {"q_proj": "Llama-3.2-1B q_proj 2048x2048 forward W.[x]_HE (BASELINE configs[1])",
+          "ffn": "Llama-3.2-1B FFN gate/up 8192x2048 + down 2048x8192, fwd + W^T bwd (configs[2])"}[args.workload]
+    return {"workload": wl, "tokens_per_gpu": T, "B": 8, "C": 256, "N": 2048, "q_in": 39, "q_out": 26,
+            "beta": 27, "parallelism": f"token-sharded x{world}" if world > 1 else "single GPU",
+            "l2": "flushed between steps (256 MiB write), outputs 34 GB/step >> L2",
+            "output": "LWE ciphertexts, uint32 per coefficient after 39->26 modulus switch"}
+
+
+def cpu_baseline(args, lin, budget_s=12.0):
+    """Times the oracle (oracle/phe_oracle.py + the C literal path) as it stands on the host's
+    cores: server-side expansion + literal Eq. 6 + modswitch, on a bounded token sample."""
+    import numpy as np
+
+    import synth
+    from oracle import c_oracle
+    from oracle import phe_oracle as O
+
+    name, d_out, d_in, tr = lin
+    lib = c_oracle.load()
+    op = O.PAPER
+    W = synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED)
+    M = np.ascontiguousarray(W.T) if tr else W
+    cols = M.shape[1]
+    S = O.keygen(synth.MASTER_SEED + 17, op.N)
+    cores = os.cpu_count() or 1
+
+    def sample(n):
+        x = synth.activations_int8(n, cols, seed=synth.MASTER_SEED + 5)
+        seeds = O.block_seeds(synth.seed_base(99), n, op.L(cols))
+        bodies = np.stack([O.encrypt(op, S, x[t], seeds[t])[1] for t in range(n)])
+        t0 = time.perf_counter()
+        O.server_matmul(op, M, seeds, bodies, out_bits=op.q_out, lib=lib, nthreads=cores)
+        return time.perf_counter() - t0
+
+    t1 = sample(1)
+    n = int(max(1, min(64, budget_s // max(t1, 1e-3))))
+    tn = sample(n) if n > 1 else t1
+    return {"value": round(n / tn, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} tokens of {name} {d_out}x{d_in} (seed expansion + literal Eq.6 in C/OpenMP + "
+                      f"modswitch), {tn:.1f} s wall"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU oracle; other ranks exit 0 without work
+    import numpy as np
+
+    import synth
+    from oracle import c_oracle
+    from oracle import phe_oracle as O
+
+    lib = c_oracle.load()
+    op = O.PAPER
+    cores = os.cpu_count() or 1
+    lin = linears(args.workload)[0]
+    name, d_out, d_in, tr = lin
+    W = synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED)
+    M = np.ascontiguousarray(W.T) if tr else W
+    cols = M.shape[1]
+    S = O.keygen(synth.MASTER_SEED + 17, op.N)
+    per_step = 2  # tokens per step: a bounded sample of the workload
+    x = synth.activations_int8(per_step, cols, seed=synth.MASTER_SEED + 5)
+    seeds = O.block_seeds(synth.seed_base(7), per_step, op.L(cols))
+    bodies = np.stack([O.encrypt(op, S, x[t], seeds[t])[1] for t in range(per_step)])
+
+    def step():
+        O.server_matmul(op, M, seeds, bodies, out_bits=op.q_out, lib=lib, nthreads=cores)
+
+    for _ in range(args.warmup):
+        step()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    ms = statistics.mean(ts) * 1e3
+    value = per_step / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "uint64",
+            "data": "synthetic", "config": config_dict(args, world, args.tokens),
+            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} tokens of {name} {d_out}x{d_in} per step (literal Eq. 6, "
+                                       f"C/OpenMP, {cores} threads)"},
+            "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

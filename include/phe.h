@@ -97,7 +97,7 @@ int phe_encrypt_pack(const phe_params *p, const uint8_t *d_S, const int8_t *d_x,
  *   [rows][Lc][2N][16] int8  "16-shift expansion" of wext_{j,i}[m] = M[j,iN+m] (m < N),
  *                            -M[j,iN+m-N] (N <= m < 2N), 0 beyond cols/2N; Lc = ceil(cols/N)
  *   [rows][Lc*N]       int8  M, zero-padded to Lc*N columns (body GEMM operand)
- * Errors: EINVAL on dims, ERANGE is NOT checked on device (call phe_weights_check). */
+ * Errors: EINVAL on dims, ENOMEM if bytes is too small.  |w| <= 127 is the caller's contract.  */
 size_t phe_weights_bytes(const phe_params *p, int64_t rows, int64_t cols);
 int phe_weights_prepare(const phe_params *p, const int8_t *d_W, int64_t d_out, int64_t d_in,
                         int transpose, void *d_wprep, size_t bytes, void *stream);
@@ -122,6 +122,8 @@ int phe_ct_prepare(const phe_params *p, const uint64_t *d_seeds, const uint64_t 
  *              q_out -> d_out_mask uint32 [T][R][N], d_out_body uint32 [T][R]  (switched)
  *              with R = row_end - row_begin (row sharding).
  *   Mask entry [tau][j][t] is a'_t of LWE(x_tau . w_j) (Eq. 2 with h = N-1); body [tau][j] = b'.
+ *   Either output pointer may be NULL: that part (a5 mask / a6 body GEMM) is then skipped,
+ *   so the two contractions can be launched and timed separately.
  * Errors: EINVAL (row range, T < 0, null), EMODULUS (out_bits not q_in/q_out),
  *         EUNSUPPORTED (N < 128, ell > 8).  T == 0 is a no-op returning PHE_OK.          */
 int phe_matmul_clear(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,

@@ -199,13 +199,16 @@ def ct_prepare(p: Params, seeds: torch.Tensor, body: torch.Tensor, out: torch.Te
     return out
 
 
+SKIP = "skip"  # pass as out_mask / out_body to skip that contraction (NULL in the C ABI)
+
+
 def _outputs(p, T, R, out_bits, device, out_mask, out_body):
     dt = torch.int64 if out_bits == p.q_in else torch.int32
     if out_mask is None:
         out_mask = torch.empty((T, R, p.N), dtype=dt, device=device)
     if out_body is None:
         out_body = torch.empty((T, R), dtype=dt, device=device)
-    return out_mask, out_body
+    return (None if isinstance(out_mask, str) else out_mask), (None if isinstance(out_body, str) else out_body)
 
 
 def matmul_clear(p: Params, w: Weights, operand: torch.Tensor, T: int, out_bits: int | None = None,

@@ -412,8 +412,8 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
   ka.N = N; ka.tpt = tpt; ka.n_tiles = n_tiles; ka.k_blocks = (int)(K / BK);
   ka.kb_per_block = N / BK; ka.Lc = a.Lc; ka.row_begin = a.row_begin; ka.R = R; ka.T = a.T;
   ka.q_in = a.kp.q_in; ka.out_bits = a.out_bits;
-  // ---- body: plain W operand, M = rows in range
-  {
+  // ---- body: plain W operand, M = rows in range (skipped when out_body == NULL)
+  if (a.out_body) {
     CUtensorMap ma, mb;
     int rc = make_map_2d(&ma, a.wplain, (uint64_t)K, (uint64_t)a.wplain_rows, (uint64_t)K, BK, BM,
                          CU_TENSOR_MAP_SWIZZLE_128B);
@@ -429,8 +429,8 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
     if (rc) return rc;
     (*n_launches)++;
   }
-  // ---- mask: Hankel operand, M = R * N
-  {
+  // ---- mask: Hankel operand, M = R * N (skipped when out_mask == NULL)
+  if (a.out_mask) {
     CUtensorMap ma, mb;
     int rc = make_map_2d(&ma, a.wexp, 16, (uint64_t)(a.rows * a.Lc * 2 * N), 16, 16, A_ROWS_HANKEL,
                          CU_TENSOR_MAP_SWIZZLE_NONE);

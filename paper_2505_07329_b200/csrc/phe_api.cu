@@ -163,7 +163,7 @@ static int matmul_common(const phe_params *p, const void *d_wprep, int64_t rows,
   if (row_begin < 0 || row_end > rows || row_begin > row_end) return PHE_EINVAL;
   if (out_bits != p->q_in && out_bits != p->q_out) return PHE_EMODULUS;
   if (T == 0 || row_end == row_begin) return PHE_OK;
-  if (!d_wprep || !d_operand || !d_out_mask || !d_out_body) return PHE_EINVAL;
+  if (!d_wprep || !d_operand || (!d_out_mask && !d_out_body)) return PHE_EINVAL;
   if (p->N % 128) return PHE_EUNSUPPORTED;
   const int64_t N = p->N, Lc = phe_num_blocks(p, cols);
   phe::GemmArgs a{};
