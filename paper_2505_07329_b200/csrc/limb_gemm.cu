@@ -29,7 +29,9 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "phe_common.cuh"
 #include "side_kernels.cuh"
@@ -41,7 +43,8 @@ constexpr int BM = 128;   // rows per tile (TMEM lanes)
 constexpr int BN = 256;   // GEMM columns per tile: tokens*ell (+ pad)
 constexpr int BK = 128;   // bytes of K per pipeline stage
 constexpr int UK = 32;    // K of one tcgen05.mma kind::i8
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 384;  // 4 role warps + 8 epilogue warps
+constexpr int NUM_EPI = 256;
 constexpr int A_ROWS_HANKEL = BM + BK - 16;            // 240 compact rows
 constexpr int A_BYTES_HANKEL = A_ROWS_HANKEL * 16;     // 3840
 constexpr int A_BYTES_PLAIN = BM * BK;                 // 16384
@@ -165,12 +168,30 @@ __host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
          ((uint32_t)(m >> 4) << 24);
 }
 
+// Limb recombination mod 2^q_in (a7) + ModulusSwitch (a8), one output word:
+//   x = half + sum_l acc_l * 2^(8l)  (two's complement in 64 bits; 2^q_in | 2^64)
+//   SW:  r = (x >> (q_in - q_out)) mod 2^q_out   (round half up: half = 2^(q_in-q_out-1))
+//   !SW: r = x mod 2^q_in
+// acc_l * 2^(8l) for 8l < 32 is one IMAD.WIDE; for 8l >= 32 only the high word moves.
+template <int ELL, bool SW, typename OutT>
+__device__ __forceinline__ OutT finish(const uint32_t *acc, int64_t half, int shift, uint64_t omask) {
+  int64_t x = half + (int64_t)(int32_t)acc[0];
+#pragma unroll
+  for (int l = 1; l < ELL; l++) {
+    if (8 * l < 32) x += (int64_t)(int32_t)acc[l] * (int64_t)(1ll << (8 * l));
+    else x += (int64_t)((uint64_t)(uint32_t)acc[l] << (8 * l));
+  }
+  if (SW) return (OutT)(((uint64_t)x >> shift) & omask);
+  return (OutT)((uint64_t)x & omask);
+}
+
 // ------------------------------------------------------------------ the kernel
-template <int ELL, bool HANKEL>
+template <int ELL, bool HANKEL, bool SW>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  KArgs ka) {
   using C = Cfg<HANKEL>;
+  using OutT = typename std::conditional<SW, uint32_t, unsigned long long>::type;
   constexpr int S = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -185,7 +206,7 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], NUM_EPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -261,20 +282,22 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     __syncwarp();
   } else if (warp >= 4) {
     // ===== epilogue: TMEM -> registers -> recombine limbs -> modswitch -> HBM =====
+    // 8 warps: two per TMEM lane quarter; group g = 0/1 takes the even/odd 16-token chunks.
     const int q4 = warp & 3;  // TMEM lane quarter this warp may access
+    const int grp = (warp - 4) >> 2;
     const int row = q4 * 32 + lane;
-    const bool sw = ka.out_bits != ka.q_in;
     const int shift = ka.q_in - ka.out_bits;
-    const uint64_t half = shift > 0 ? (1ull << (shift - 1)) : 0ull;
+    const int64_t half = SW ? (1ll << (shift - 1)) : 0;
     const uint64_t omask = mask_bits(ka.out_bits);
     const int64_t N = ka.N;
+    OutT *const out = static_cast<OutT *>(ka.out);
     int acc = 0; uint32_t aph = 0;
     for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int64_t m_tile = tile / ka.n_tiles;
       const int n_tile = (int)(tile % ka.n_tiles);
       const int64_t tau0 = (int64_t)n_tile * ka.tpt;
       const int ntok = (int)min((int64_t)ka.tpt, ka.T - tau0);
-      int64_t obase;  // output index of (tau0, this row)
+      int64_t obase;    // output index of (tau0, this row)
       int64_t tstride;  // index stride between consecutive tokens
       bool valid = true;
       if (HANKEL) {
@@ -291,7 +314,7 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN);
-      for (int c0 = 0; c0 < ntok; c0 += 16) {
+      for (int c0 = 16 * grp; c0 < ntok; c0 += 32) {
         const int nt = min(16, ntok - c0);
         const int nloads = (nt * ELL + 15) / 16;
         uint32_t v[16 * ELL];
@@ -299,15 +322,18 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         for (int q = 0; q < ELL; q++)
           if (q < nloads) tmem_ld16(tbase + (uint32_t)(c0 * ELL + 16 * q), &v[16 * q]);
         tmem_wait_ld();
+        OutT *o = out + obase + (int64_t)c0 * tstride;
+        if (nt == 16 && valid) {
 #pragma unroll
-        for (int tk = 0; tk < 16; tk++) {
-          if (tk < nt && valid) {
-            uint64_t x = 0;
+          for (int tk = 0; tk < 16; tk++) {
+            __stcs(o, finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask));
+            o += tstride;
+          }
+        } else if (valid) {
 #pragma unroll
-            for (int l = 0; l < ELL; l++) x += (uint64_t)(int64_t)(int32_t)v[tk * ELL + l] << (8 * l);
-            const int64_t o = obase + (int64_t)(c0 + tk) * tstride;
-            if (sw) __stcs(static_cast<uint32_t *>(ka.out) + o, (uint32_t)(((x + half) >> shift) & omask));
-            else __stcs(reinterpret_cast<unsigned long long *>(ka.out) + o, (unsigned long long)(x & omask));
+          for (int tk = 0; tk < 16; tk++) {
+            if (tk < nt) __stcs(o, finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask));
+            o += tstride;
           }
         }
       }
@@ -321,6 +347,207 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ 2-CTA (CTA pair) kernel
+// Same contraction on a CTA pair (cluster of 2 on one TPC): tcgen05.mma.cta_group::2 with
+// M = 256 (CTA r holds Hankel rows t0 + 128r .. +128 of the same j) and N = 256 (CTA r holds
+// B rows 128r .. +128).  Per SM this halves the B (limb-plane) bytes moved through TMA, L2 and
+// shared memory per MAC.  Only the leader CTA issues MMAs; both CTAs run TMA and epilogue.
+constexpr int S2_STAGES = 8;
+constexpr int B_HALF_BYTES = (BN / 2) * BK;   // 16 KB
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;   // clears the peer bit: addresses CTA 0's barrier
+__host__ __device__ constexpr int smem_bytes_2sm() {
+  return 1024 + S2_STAGES * (B_HALF_BYTES + 4096) + 256;
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap *map, int x, int y,
+                                                uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc2(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+template <int ELL, bool SW>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                     KArgs ka) {
+  using OutT = typename std::conditional<SW, uint32_t, unsigned long long>::type;
+  constexpr int S = S2_STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  uint8_t *sB = smem;                       // S x 16 KB (1024-aligned)
+  uint8_t *sA = smem + S * B_HALF_BYTES;    // S x 4 KB
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sA + S * 4096);
+  uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * NUM_EPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int64_t total = ka.total_tiles;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs): own Hankel rows + own half of B, bytes land on CTA 0 =====
+    if (lane == 0) {
+      int s = 0; uint32_t ph = 0;
+      for (int64_t tile = cid; tile < total; tile += ncl) {
+        const int64_t m_tile = tile / ka.n_tiles;
+        const int n_tile = (int)(tile % ka.n_tiles);
+        const int brow = n_tile * ka.tpt * ELL + (int)crank * (BN / 2);
+        const int64_t jrow = ka.row_begin + m_tile / ka.tb_per_row;
+        const int t0 = (int)(m_tile % ka.tb_per_row) * (2 * BM) + (int)crank * BM;
+        for (int kb = 0; kb < ka.k_blocks; kb++) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_expect_tx(&full[s], (uint32_t)(2 * (A_BYTES_HANKEL + B_HALF_BYTES)));
+          const uint32_t fb = smem_u32(&full[s]) & PEER_MASK;
+          const int i = kb / ka.kb_per_block, k0 = (kb % ka.kb_per_block) * BK;
+          const int64_t arow = (jrow * ka.Lc + i) * (2 * (int64_t)ka.N) + k0 + t0;
+          tma_load_2d_2sm(smem_u32(sA + s * 4096), &map_a, 0, (int)arow, fb);
+          tma_load_2d_2sm(smem_u32(sB + s * B_HALF_BYTES), &map_b, kb * BK, brow, fb);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader CTA only) =====
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
+      int s = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
+      for (int64_t tile = cid; tile < total; tile += ncl) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < ka.k_blocks; kb++) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * 4096);
+          const uint32_t b_addr = smem_u32(sB + s * B_HALF_BYTES);
+#pragma unroll
+          for (int q = 0; q < BK / UK; q++)
+            mma_i8_2sm(d_tmem, desc_hankel(a_addr + 512 * q), desc_sw128(b_addr + 32 * q), idesc,
+                       (kb | q) != 0 ? 1u : 0u);
+          tc_commit_mc2(&empty[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        tc_commit_mc2(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ===== epilogue (both CTAs): own 128 TMEM lanes = own 128 rows t =====
+    const int q4 = warp & 3;
+    const int grp = (warp - 4) >> 2;
+    const int row = q4 * 32 + lane;
+    const int shift = ka.q_in - ka.out_bits;
+    const int64_t half = SW ? (1ll << (shift - 1)) : 0;
+    const uint64_t omask = mask_bits(ka.out_bits);
+    const int64_t N = ka.N;
+    OutT *const out = static_cast<OutT *>(ka.out);
+    const uint32_t tempty_c0 = smem_u32(&tempty[0]) & PEER_MASK;
+    int acc = 0; uint32_t aph = 0;
+    for (int64_t tile = cid; tile < total; tile += ncl) {
+      const int64_t m_tile = tile / ka.n_tiles;
+      const int n_tile = (int)(tile % ka.n_tiles);
+      const int64_t tau0 = (int64_t)n_tile * ka.tpt;
+      const int ntok = (int)min((int64_t)ka.tpt, ka.T - tau0);
+      const int64_t jr = m_tile / ka.tb_per_row;
+      const int64_t t = (m_tile % ka.tb_per_row) * (2 * BM) + (int64_t)crank * BM + row;
+      const int64_t tstride = ka.R * N;
+      const int64_t obase = tau0 * tstride + jr * N + t;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN);
+      for (int c0 = 16 * grp; c0 < ntok; c0 += 32) {
+        const int nt = min(16, ntok - c0);
+        const int nloads = (nt * ELL + 15) / 16;
+        uint32_t v[16 * ELL];
+#pragma unroll
+        for (int q = 0; q < ELL; q++)
+          if (q < nloads) tmem_ld16(tbase + (uint32_t)(c0 * ELL + 16 * q), &v[16 * q]);
+        tmem_wait_ld();
+        OutT *o = out + obase + (int64_t)c0 * tstride;
+        if (nt == 16) {
+#pragma unroll
+          for (int tk = 0; tk < 16; tk++) {
+            __stcs(o, finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask));
+            o += tstride;
+          }
+        } else {
+#pragma unroll
+          for (int tk = 0; tk < 16; tk++) {
+            if (tk < nt) __stcs(o, finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask));
+            o += tstride;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)acc);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
 }
 
@@ -363,9 +590,9 @@ static int num_sms() {
   return n;
 }
 
-template <int ELL, bool HANKEL>
+template <int ELL, bool HANKEL, bool SW>
 static int launch_one(const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka, cudaStream_t st) {
-  auto kern = limb_gemm_kernel<ELL, HANKEL>;
+  auto kern = limb_gemm_kernel<ELL, HANKEL, SW>;
   constexpr int smem = smem_bytes<HANKEL>();
   static thread_local bool set = false;
   if (!set) {
@@ -379,20 +606,63 @@ static int launch_one(const CUtensorMap &ma, const CUtensorMap &mb, const KArgs 
   return PHE_OK;
 }
 
-template <bool HANKEL>
+template <bool HANKEL, bool SW>
 static int dispatch_ell(int ell, const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka,
                         cudaStream_t st) {
   switch (ell) {
-    case 1: return launch_one<1, HANKEL>(ma, mb, ka, st);
-    case 2: return launch_one<2, HANKEL>(ma, mb, ka, st);
-    case 3: return launch_one<3, HANKEL>(ma, mb, ka, st);
-    case 4: return launch_one<4, HANKEL>(ma, mb, ka, st);
-    case 5: return launch_one<5, HANKEL>(ma, mb, ka, st);
-    case 6: return launch_one<6, HANKEL>(ma, mb, ka, st);
-    case 7: return launch_one<7, HANKEL>(ma, mb, ka, st);
-    case 8: return launch_one<8, HANKEL>(ma, mb, ka, st);
+    case 1: return launch_one<1, HANKEL, SW>(ma, mb, ka, st);
+    case 2: return launch_one<2, HANKEL, SW>(ma, mb, ka, st);
+    case 3: return launch_one<3, HANKEL, SW>(ma, mb, ka, st);
+    case 4: return launch_one<4, HANKEL, SW>(ma, mb, ka, st);
+    case 5: return launch_one<5, HANKEL, SW>(ma, mb, ka, st);
+    case 6: return launch_one<6, HANKEL, SW>(ma, mb, ka, st);
+    case 7: return launch_one<7, HANKEL, SW>(ma, mb, ka, st);
+    case 8: return launch_one<8, HANKEL, SW>(ma, mb, ka, st);
   }
   return PHE_EUNSUPPORTED;
+}
+
+
+template <int ELL, bool SW>
+static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka, cudaStream_t st) {
+  auto kern = limb_gemm_2sm_kernel<ELL, SW>;
+  constexpr int smem = smem_bytes_2sm();
+  static thread_local bool set = false;
+  if (!set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+    set = true;
+  }
+  int64_t pairs = num_sms() / 2;
+  if (ka.total_tiles < pairs) pairs = ka.total_tiles;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, ka) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+template <bool SW>
+static int dispatch_2sm(int ell, const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka, cudaStream_t st) {
+  switch (ell) {
+    case 4: return launch_2sm<4, SW>(ma, mb, ka, st);
+    case 5: return launch_2sm<5, SW>(ma, mb, ka, st);
+  }
+  return PHE_EUNSUPPORTED;
+}
+
+template <bool HANKEL>
+static int dispatch(int ell, bool sw, const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka,
+                    cudaStream_t st) {
+  return sw ? dispatch_ell<HANKEL, true>(ell, ma, mb, ka, st) : dispatch_ell<HANKEL, false>(ell, ma, mb, ka, st);
 }
 
 }  // namespace tc
@@ -425,24 +695,28 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
     kb.m_tiles = (R + BM - 1) / BM;
     kb.total_tiles = kb.m_tiles * n_tiles;
     kb.out = a.out_body;
-    rc = dispatch_ell<false>(ell, ma, mb, kb, st);
+    rc = dispatch<false>(ell, a.out_bits != a.kp.q_in, ma, mb, kb, st);
     if (rc) return rc;
     (*n_launches)++;
   }
   // ---- mask: Hankel operand, M = R * N (skipped when out_mask == NULL)
   if (a.out_mask) {
+    const bool two_sm = (ell == 4 || ell == 5) && (N % (2 * BM) == 0) && !getenv("PHE_FORCE_1SM");
     CUtensorMap ma, mb;
     int rc = make_map_2d(&ma, a.wexp, 16, (uint64_t)(a.rows * a.Lc * 2 * N), 16, 16, A_ROWS_HANKEL,
                          CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
-    rc = make_map_2d(&mb, a.mplanes, (uint64_t)K, brows, (uint64_t)K, BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    rc = make_map_2d(&mb, a.mplanes, (uint64_t)K, brows, (uint64_t)K, BK, two_sm ? BN / 2 : BN,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
     KArgs km = ka;
-    km.tb_per_row = N / BM;
+    km.tb_per_row = N / (two_sm ? 2 * BM : BM);
     km.m_tiles = R * km.tb_per_row;
     km.total_tiles = km.m_tiles * n_tiles;
     km.out = a.out_mask;
-    rc = dispatch_ell<true>(ell, ma, mb, km, st);
+    const bool sw = a.out_bits != a.kp.q_in;
+    if (two_sm) rc = sw ? dispatch_2sm<true>(ell, ma, mb, km, st) : dispatch_2sm<false>(ell, ma, mb, km, st);
+    else rc = dispatch<true>(ell, sw, ma, mb, km, st);
     if (rc) return rc;
     (*n_launches)++;
   }
