@@ -238,7 +238,7 @@ def run_ours(args):
                     for _, w in regs)
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "limb_gemm_kernel<5,HANKEL> (mask contraction)",
+                "kernel": "limb_gemm_2sm_kernel<5,SW,13> (mask contraction, tcgen05 cta_group::2)",
                 "ops": "int8 tensor ops (2 per MAC), algorithmic: 2*ell*d_out*d_in*N per token",
                 "peak_source": f"{src}: 2 x bf16_tflops (burst) of MEASURED_PEAKS.json",
                 "frac_of_nominal_4500": round(achieved / NOMINAL_INT8_TOPS, 4),

@@ -20,10 +20,14 @@
 // box of the weight's 16-shift expansion (phe_weights_prepare).
 //
 // Pipeline (per CTA, persistent over tiles, 1 CTA per SM):
-//   warp 0     TMA producer  (A box + B box per K-stage, mbarrier complete_tx)
-//   warp 1     MMA issuer    (tcgen05.mma.cta_group::1.kind::i8, M=128 N=256 K=32)
-//   warp 2     TMEM allocator (512 columns = 2 accumulator stages of 256)
-//   warps 4-7  epilogue      (tcgen05.ld -> recombine -> modswitch -> st.global.cs)
+//   warps 0-7  epilogue      (tcgen05.ld -> recombine -> modswitch -> HBM); warp w reads TMEM
+//                            lane quarter w % 4 (= its SM sub-partition)
+//   warp 8     TMA producer  (A box + B box per K-stage, mbarrier complete_tx)
+//   warp 9     MMA issuer    (tcgen05.mma kind::i8: M=128 N=256 K=32, or the CTA-pair M=256)
+//   warp 10    TMEM allocator (512 columns = 2 accumulator stages of 256)
+// The role warps have the HIGHEST warp ids on purpose: the sub-partition scheduler picks the
+// highest eligible warp id first, so the single MMA-issuing thread is never starved by the
+// epilogue warps that share its sub-partition (measured: ~10% of tensor-pipe cycles).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -43,7 +47,8 @@ constexpr int BM = 128;   // rows per tile (TMEM lanes)
 constexpr int BN = 256;   // GEMM columns per tile: tokens*ell (+ pad)
 constexpr int BK = 128;   // bytes of K per pipeline stage
 constexpr int UK = 32;    // K of one tcgen05.mma kind::i8
-constexpr int NUM_THREADS = 384;  // 4 role warps + 8 epilogue warps
+constexpr int NUM_THREADS = 384;  // 8 epilogue warps (0-7) + producer 8, MMA 9, TMEM 10, spare 11
+constexpr int W_PROD = 8, W_MMA = 9, W_TMEM = 10;
 constexpr int NUM_EPI = 256;
 constexpr int A_ROWS_HANKEL = BM + BK - 16;            // 240 compact rows
 constexpr int A_BYTES_HANKEL = A_ROWS_HANKEL * 16;     // 3840
@@ -68,7 +73,8 @@ constexpr int smem_bytes() {
 
 struct KArgs {
   int N;
-  int tpt;            // tokens per tile = BN / ell
+  int tpt;            // tokens per tile
+  int n_mma;          // MMA N = round16(tpt * ell) (2-CTA kernel)
   int n_tiles;        // token tiles
   int tb_per_row;     // N / BM (HANKEL) or 1
   int64_t m_tiles;    // rows*tb_per_row (HANKEL) or ceil(rows/BM)
@@ -80,6 +86,7 @@ struct KArgs {
   int64_t R;          // rows in range
   int64_t T;
   int q_in, out_bits;
+  int dbg;            // experiments only (PHE_DEBUG_EPI): 1 = no TMEM loads/stores, 2 = no stores
   void *out;
 };
 
@@ -185,6 +192,26 @@ __device__ __forceinline__ OutT finish(const uint32_t *acc, int64_t half, int sh
   return (OutT)((uint64_t)x & omask);
 }
 
+// Same result for SW with s = q_in - q_out known at compile time, in 32-bit integer ALU ops
+// only (no wide multiplies).  With M = floor(s/8):
+//   c_0 = acc_0 + 2^(s-1);  c_l = acc_l + (c_(l-1) >> 8)  (l = 1..M, arithmetic shifts)
+//   r   = (c_M >> (s - 8M)) + sum_{l > M} acc_l << (8l - s)   (mod 2^q_out)
+// Exact: floor((sum_l acc_l 2^(8l) + 2^(s-1)) / 2^s) splits into the exact multiples of 2^s
+// (limbs l > M) plus a floor over the low limbs, and floor((2^8 Y + r)/2^s) = floor(Y / 2^(s-8))
+// for 0 <= r < 2^8 <= 2^s.  |c_l| < 2^29 for K <= 8192 (|acc| <= 8192*127*255 < 2^28).
+template <int ELL, int SH>
+__device__ __forceinline__ uint32_t finish_sw(const uint32_t *acc, uint32_t omask) {
+  constexpr int M = SH / 8;
+  int32_t c = (int32_t)acc[0] + (1 << (SH - 1));
+#pragma unroll
+  for (int l = 1; l <= M && l < ELL; l++) c = (int32_t)acc[l] + (c >> 8);
+  uint32_t r = (uint32_t)(c >> (SH - 8 * M));
+#pragma unroll
+  for (int l = M + 1; l < ELL; l++)
+    if (8 * l - SH < 32) r += acc[l] << (8 * l - SH);
+  return r & omask;
+}
+
 // ------------------------------------------------------------------ the kernel
 template <int ELL, bool HANKEL, bool SW>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -209,11 +236,11 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], NUM_EPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == W_PROD && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
   }
-  if (warp == 2) {
+  if (warp == W_TMEM) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_holder))
                  : "memory");
@@ -225,7 +252,7 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   const uint32_t tmem_base = *tmem_holder;
 
   const int64_t total = ka.total_tiles;
-  if (warp == 0) {
+  if (warp == W_PROD) {
     // ===== TMA producer =====
     if (lane == 0) {
       int s = 0; uint32_t ph = 0;
@@ -252,7 +279,7 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == W_MMA) {
     // ===== MMA issuer =====
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_i8(BM, BN);
@@ -280,11 +307,11 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp < 8) {
     // ===== epilogue: TMEM -> registers -> recombine limbs -> modswitch -> HBM =====
-    // 8 warps: two per TMEM lane quarter; group g = 0/1 takes the even/odd 16-token chunks.
+    // 8 warps (0-7): two per TMEM lane quarter; group g = 0/1 takes the even/odd 16-token chunks.
     const int q4 = warp & 3;  // TMEM lane quarter this warp may access
-    const int grp = (warp - 4) >> 2;
+    const int grp = warp >> 2;
     const int row = q4 * 32 + lane;
     const int shift = ka.q_in - ka.out_bits;
     const int64_t half = SW ? (1ll << (shift - 1)) : 0;
@@ -344,23 +371,32 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == W_TMEM) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
 }
 
+// Experiment-only pipeline counters (PHE_DEBUG_EPI=4): cycles spent in each wait, summed over CTAs.
+__device__ unsigned long long g_dbg_cnt[8];
+__device__ __forceinline__ void dbg_add(int i, long long v) { atomicAdd(&g_dbg_cnt[i], (unsigned long long)v); }
+
 // ------------------------------------------------------------------ 2-CTA (CTA pair) kernel
 // Same contraction on a CTA pair (cluster of 2 on one TPC): tcgen05.mma.cta_group::2 with
-// M = 256 (CTA r holds Hankel rows t0 + 128r .. +128 of the same j) and N = 256 (CTA r holds
-// B rows 128r .. +128).  Per SM this halves the B (limb-plane) bytes moved through TMA, L2 and
-// shared memory per MAC.  Only the leader CTA issues MMAs; both CTAs run TMA and epilogue.
-constexpr int S2_STAGES = 8;
-constexpr int B_HALF_BYTES = (BN / 2) * BK;   // 16 KB
+// M = 256 (CTA r holds Hankel rows t0 + 128r .. +128 of the same j) and N = n_mma <= 256
+// (CTA r holds B rows n_mma/2 * r .. +n_mma/2).  Per SM this halves the B (limb-plane) bytes
+// moved through TMA, L2 and shared memory per MAC.  Only the leader CTA issues MMAs; both
+// CTAs run TMA and the epilogue.  Epilogue: TMEM -> registers (recombine + switch) -> shared
+// memory -> TMA bulk-tensor store of a [16 tokens][1 row j][128 t] box, double-buffered.
+constexpr int B_HALF_MAX = (BN / 2) * BK;     // 16 KB per stage per CTA
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;   // clears the peer bit: addresses CTA 0's barrier
-__host__ __device__ constexpr int smem_bytes_2sm() {
-  return 1024 + S2_STAGES * (B_HALF_BYTES + 4096) + 256;
-}
+constexpr int EPI_TOK = 16;                   // tokens per epilogue chunk
+template <bool SW> struct Cfg2 {
+  using OutT = typename std::conditional<SW, uint32_t, unsigned long long>::type;
+  static constexpr int STAGES = SW ? 8 : 6;
+  static constexpr int OUT_BUF = EPI_TOK * BM * (int)sizeof(OutT);  // 8 KB (u32) / 16 KB (u64)
+  static constexpr int SMEM = 1024 + STAGES * (B_HALF_MAX + 4096) + 4 * OUT_BUF + 256;
+};
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -377,6 +413,23 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap 
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster)
       : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y), "r"(z)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void tc_commit_mc2(uint64_t *bar) {
   asm volatile(
@@ -396,39 +449,47 @@ __device__ __forceinline__ void mma_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Epilogue -> MMA "accumulator drained" signal.  Relaxed: what must be ordered before it is
+// only the TMEM reads, which tcgen05.wait::ld + tcgen05.fence::before_thread_sync completed.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
-template <int ELL, bool SW>
+template <int ELL, bool SW, int SH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                     KArgs ka) {
-  using OutT = typename std::conditional<SW, uint32_t, unsigned long long>::type;
-  constexpr int S = S2_STAGES;
+                     const __grid_constant__ CUtensorMap map_out,
+                     const __grid_constant__ CUtensorMap map_out_tail, KArgs ka) {
+  using C2 = Cfg2<SW>;
+  using OutT = typename C2::OutT;
+  constexpr int S = C2::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
-  uint8_t *sB = smem;                       // S x 16 KB (1024-aligned)
-  uint8_t *sA = smem + S * B_HALF_BYTES;    // S x 4 KB
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sA + S * 4096);
+  uint8_t *sB = smem;                                // S x 16 KB (1024-aligned)
+  uint8_t *sA = smem + S * B_HALF_MAX;               // S x 4 KB
+  uint8_t *sO = sA + S * 4096;                       // 2 groups x 2 buffers x OUT_BUF
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sO + 4 * C2::OUT_BUF);
   uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
+  const int n_mma = ka.n_mma;                 // MMA N = round16(tpt * ELL)
+  const int b_half = (n_mma / 2) * BK;        // B bytes per CTA per stage
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * NUM_EPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == W_PROD && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_out)) : "memory");
   }
-  if (warp == 2) {
+  if (warp == W_TMEM) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_holder))
                  : "memory");
@@ -441,43 +502,53 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
 
   const int64_t total = ka.total_tiles;
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  if (warp == 0) {
+  if (warp == W_PROD) {
     // ===== TMA producer (both CTAs): own Hankel rows + own half of B, bytes land on CTA 0 =====
     if (lane == 0) {
       int s = 0; uint32_t ph = 0;
+      long long pw = 0;
+      const uint32_t tx = (uint32_t)(2 * ((ka.dbg == 5 ? 0 : A_BYTES_HANKEL) + (ka.dbg == 6 ? 0 : b_half)));
       for (int64_t tile = cid; tile < total; tile += ncl) {
         const int64_t m_tile = tile / ka.n_tiles;
         const int n_tile = (int)(tile % ka.n_tiles);
-        const int brow = n_tile * ka.tpt * ELL + (int)crank * (BN / 2);
+        const int brow = n_tile * ka.tpt * ELL + (int)crank * (n_mma / 2);
         const int64_t jrow = ka.row_begin + m_tile / ka.tb_per_row;
         const int t0 = (int)(m_tile % ka.tb_per_row) * (2 * BM) + (int)crank * BM;
         for (int kb = 0; kb < ka.k_blocks; kb++) {
+          long long w0 = ka.dbg == 4 ? clock64() : 0;
           mbar_wait(&empty[s], ph ^ 1);
-          if (leader) mbar_expect_tx(&full[s], (uint32_t)(2 * (A_BYTES_HANKEL + B_HALF_BYTES)));
+          if (ka.dbg == 4) pw += clock64() - w0;
+          if (leader) mbar_expect_tx(&full[s], tx);
           const uint32_t fb = smem_u32(&full[s]) & PEER_MASK;
           const int i = kb / ka.kb_per_block, k0 = (kb % ka.kb_per_block) * BK;
           const int64_t arow = (jrow * ka.Lc + i) * (2 * (int64_t)ka.N) + k0 + t0;
-          tma_load_2d_2sm(smem_u32(sA + s * 4096), &map_a, 0, (int)arow, fb);
-          tma_load_2d_2sm(smem_u32(sB + s * B_HALF_BYTES), &map_b, kb * BK, brow, fb);
+          if (ka.dbg != 5) tma_load_2d_2sm(smem_u32(sA + s * 4096), &map_a, 0, (int)arow, fb);
+          if (ka.dbg != 6) tma_load_2d_2sm(smem_u32(sB + s * B_HALF_MAX), &map_b, kb * BK, brow, fb);
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
+      if (ka.dbg == 4) dbg_add(5, pw);
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == W_MMA) {
     // ===== MMA issuer (leader CTA only) =====
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
+      const uint32_t idesc = idesc_i8(2 * BM, n_mma);
       int s = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
+      long long t_start = clock64(), wt = 0, wf = 0;
       for (int64_t tile = cid; tile < total; tile += ncl) {
+        long long w0 = ka.dbg == 4 ? clock64() : 0;
         mbar_wait(&tempty[acc], aph ^ 1);
+        if (ka.dbg == 4) wt += clock64() - w0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < ka.k_blocks; kb++) {
+          long long w1 = ka.dbg == 4 ? clock64() : 0;
           mbar_wait(&full[s], ph);
+          if (ka.dbg == 4) wf += clock64() - w1;
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + s * 4096);
-          const uint32_t b_addr = smem_u32(sB + s * B_HALF_BYTES);
+          const uint32_t b_addr = smem_u32(sB + s * B_HALF_MAX);
 #pragma unroll
           for (int q = 0; q < BK / UK; q++)
             mma_i8_2sm(d_tmem, desc_hankel(a_addr + 512 * q), desc_sw128(b_addr + 32 * q), idesc,
@@ -488,64 +559,92 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         tc_commit_mc2(&tfull[acc]);
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
+      if (ka.dbg == 4) { dbg_add(0, wt); dbg_add(1, wf); dbg_add(2, clock64() - t_start); }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp < 8) {
     // ===== epilogue (both CTAs): own 128 TMEM lanes = own 128 rows t =====
+    // Group g (warps 0-3 / 4-7) takes every other 16-token chunk (alternating per tile).
     const int q4 = warp & 3;
-    const int grp = (warp - 4) >> 2;
+    const int grp = warp >> 2;
     const int row = q4 * 32 + lane;
+    const bool issuer = (warp & 3) == 0 && lane == 0;
     const int shift = ka.q_in - ka.out_bits;
     const int64_t half = SW ? (1ll << (shift - 1)) : 0;
     const uint64_t omask = mask_bits(ka.out_bits);
-    const int64_t N = ka.N;
-    OutT *const out = static_cast<OutT *>(ka.out);
     const uint32_t tempty_c0 = smem_u32(&tempty[0]) & PEER_MASK;
-    int acc = 0; uint32_t aph = 0;
-    for (int64_t tile = cid; tile < total; tile += ncl) {
+    OutT *const obuf = reinterpret_cast<OutT *>(sO + grp * 2 * C2::OUT_BUF);
+    int acc = 0; uint32_t aph = 0; int nbuf = 0; int64_t iter = 0;
+    for (int64_t tile = cid; tile < total; tile += ncl, iter++) {
       const int64_t m_tile = tile / ka.n_tiles;
       const int n_tile = (int)(tile % ka.n_tiles);
-      const int64_t tau0 = (int64_t)n_tile * ka.tpt;
+      const int tau0 = n_tile * ka.tpt;
       const int ntok = (int)min((int64_t)ka.tpt, ka.T - tau0);
-      const int64_t jr = m_tile / ka.tb_per_row;
-      const int64_t t = (m_tile % ka.tb_per_row) * (2 * BM) + (int64_t)crank * BM + row;
-      const int64_t tstride = ka.R * N;
-      const int64_t obase = tau0 * tstride + jr * N + t;
+      const int jr = (int)(m_tile / ka.tb_per_row);
+      const int tb = (int)(m_tile % ka.tb_per_row) * (2 * BM) + (int)crank * BM;
+      const int nchunks = (ntok + EPI_TOK - 1) / EPI_TOK;
+      const int first = (grp + (int)(iter & 1)) & 1;
+      long long e0 = (ka.dbg == 4 && warp == 0 && lane == 0) ? clock64() : 0;
       mbar_wait(&tfull[acc], aph);
+      long long e1 = (ka.dbg == 4 && warp == 0 && lane == 0) ? clock64() : 0;
+      if (ka.dbg == 4 && warp == 0 && lane == 0) dbg_add(4, e1 - e0);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN);
-      for (int c0 = 16 * grp; c0 < ntok; c0 += 32) {
-        const int nt = min(16, ntok - c0);
+      bool arrived = false;
+      for (int c = first; c < nchunks; c += 2) {
+        const int c0 = c * EPI_TOK;
+        const int nt = min(EPI_TOK, ntok - c0);
         const int nloads = (nt * ELL + 15) / 16;
-        uint32_t v[16 * ELL];
+        uint32_t v[EPI_TOK * ELL];
 #pragma unroll
         for (int q = 0; q < ELL; q++)
           if (q < nloads) tmem_ld16(tbase + (uint32_t)(c0 * ELL + 16 * q), &v[16 * q]);
         tmem_wait_ld();
-        OutT *o = out + obase + (int64_t)c0 * tstride;
-        if (nt == 16) {
+        if (c + 2 >= nchunks) {  // last TMEM read of this tile by this thread: release the buffer
+          tc_fence_before();
+          mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)acc);
+          arrived = true;
+        }
+        OutT *ob = obuf + nbuf * (EPI_TOK * BM);
+        named_bar(1 + grp, 128);  // the store that last read buffer nbuf has drained
+        if (ka.dbg == 7) {  // experiment: compute only
+          OutT x = 0;
 #pragma unroll
-          for (int tk = 0; tk < 16; tk++) {
-            __stcs(o, finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask));
-            o += tstride;
-          }
-        } else {
+          for (int tk = 0; tk < EPI_TOK; tk++) x ^= finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask);
+          if (x == (OutT)0x9e3779b9u) ob[row] = x;
+        } else if (ka.dbg == 8) {  // experiment: stores of raw limbs, no compute
 #pragma unroll
-          for (int tk = 0; tk < 16; tk++) {
-            if (tk < nt) __stcs(o, finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask));
-            o += tstride;
+          for (int tk = 0; tk < EPI_TOK; tk++) ob[tk * BM + row] = (OutT)v[tk * ELL];
+        } else if (ka.dbg != 1) {
+#pragma unroll
+          for (int tk = 0; tk < EPI_TOK; tk++) {
+            if constexpr (SW && SH > 0) ob[tk * BM + row] = (OutT)finish_sw<ELL, SH>(&v[tk * ELL], (uint32_t)omask);
+            else ob[tk * BM + row] = finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask);
           }
         }
+        fence_proxy_async_smem();
+        named_bar(1 + grp, 128);  // chunk staged
+        if (issuer) {
+          // a full 16-token box, or the tpt % 16 tail box of this tile (never past the tile)
+          const CUtensorMap *mo = (c0 + EPI_TOK <= ka.tpt) ? &map_out : &map_out_tail;
+          if (ka.dbg == 0 || ka.dbg == 4) tma_store_3d(mo, smem_u32(ob), tb, jr, tau0 + c0);
+          bulk_wait_read_1();
+        }
+        nbuf ^= 1;
       }
-      tc_fence_before();
-      mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)acc);
+      if (!arrived) {
+        tc_fence_before();
+        mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)acc);
+      }
+      if (ka.dbg == 4 && warp == 0 && lane == 0) { dbg_add(3, clock64() - e1); dbg_add(6, 1); }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
+    if (issuer) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
   cluster_sync();
-  if (warp == 2) {
+  if (warp == W_TMEM) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
@@ -623,10 +722,11 @@ static int dispatch_ell(int ell, const CUtensorMap &ma, const CUtensorMap &mb, c
 }
 
 
-template <int ELL, bool SW>
-static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka, cudaStream_t st) {
-  auto kern = limb_gemm_2sm_kernel<ELL, SW>;
-  constexpr int smem = smem_bytes_2sm();
+template <int ELL, bool SW, int SH>
+static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo,
+                      const CUtensorMap &mot, const KArgs &ka, cudaStream_t st) {
+  auto kern = limb_gemm_2sm_kernel<ELL, SW, SH>;
+  constexpr int smem = Cfg2<SW>::SMEM;
   static thread_local bool set = false;
   if (!set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -645,18 +745,47 @@ static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const KArgs 
   attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, ka) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mo, mot, ka) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
 }
 
 template <bool SW>
-static int dispatch_2sm(int ell, const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka, cudaStream_t st) {
+static int dispatch_2sm(int ell, const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo,
+                        const CUtensorMap &mot, const KArgs &ka, cudaStream_t st) {
+  const int sh = ka.q_in - ka.out_bits;
+  if (SW && ell == 5 && sh == 13) return launch_2sm<5, SW, 13>(ma, mb, mo, mot, ka, st);  // Table 1
+  if (SW && ell == 4 && sh == 4) return launch_2sm<4, SW, 4>(ma, mb, mo, mot, ka, st);    // toy
   switch (ell) {
-    case 4: return launch_2sm<4, SW>(ma, mb, ka, st);
-    case 5: return launch_2sm<5, SW>(ma, mb, ka, st);
+    case 4: return launch_2sm<4, SW, 0>(ma, mb, mo, mot, ka, st);
+    case 5: return launch_2sm<5, SW, 0>(ma, mb, mo, mot, ka, st);
   }
   return PHE_EUNSUPPORTED;
+}
+
+// Tokens per tile for the 2-CTA kernel: floor(256/ell) (MMA N = 256: N = 240 runs at the
+// N = 256 rate on the tensor core, so fewer, fuller tiles win), fewer when T is small.
+static int choose_tpt(int64_t T, int ell, int *n_mma) {
+  int tpt = BN / ell;
+  if (T < tpt) tpt = (int)T;
+  int n = ((tpt * ell + 15) / 16) * 16;
+  if (n < 32) n = 32;
+  *n_mma = n;
+  return tpt;
+}
+
+static int make_map_out(CUtensorMap *m, void *base, bool sw, int64_t N, int64_t R, int64_t T, int box_tok) {
+  auto enc = get_encode();
+  if (!enc) return PHE_ECUDA;
+  const uint64_t es = sw ? 4 : 8;
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)R, (cuuint64_t)T};
+  cuuint64_t strides[2] = {(cuuint64_t)(N * es), (cuuint64_t)(R * N * es)};
+  cuuint32_t box[3] = {(cuuint32_t)BM, 1, (cuuint32_t)box_tok};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, sw ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? PHE_OK : PHE_EINVAL;
 }
 
 template <bool HANKEL>
@@ -682,6 +811,7 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
   ka.N = N; ka.tpt = tpt; ka.n_tiles = n_tiles; ka.k_blocks = (int)(K / BK);
   ka.kb_per_block = N / BK; ka.Lc = a.Lc; ka.row_begin = a.row_begin; ka.R = R; ka.T = a.T;
   ka.q_in = a.kp.q_in; ka.out_bits = a.out_bits;
+  ka.dbg = getenv("PHE_DEBUG_EPI") ? atoi(getenv("PHE_DEBUG_EPI")) : 0;
   // ---- body: plain W operand, M = rows in range (skipped when out_body == NULL)
   if (a.out_body) {
     CUtensorMap ma, mb;
@@ -702,21 +832,43 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
   // ---- mask: Hankel operand, M = R * N (skipped when out_mask == NULL)
   if (a.out_mask) {
     const bool two_sm = (ell == 4 || ell == 5) && (N % (2 * BM) == 0) && !getenv("PHE_FORCE_1SM");
-    CUtensorMap ma, mb;
+    const bool sw = a.out_bits != a.kp.q_in;
+    KArgs km = ka;
+    if (two_sm) km.tpt = choose_tpt(a.T, ell, &km.n_mma);
+    km.n_tiles = (int)((a.T + km.tpt - 1) / km.tpt);
+    CUtensorMap ma, mb, mo;
     int rc = make_map_2d(&ma, a.wexp, 16, (uint64_t)(a.rows * a.Lc * 2 * N), 16, 16, A_ROWS_HANKEL,
                          CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
-    rc = make_map_2d(&mb, a.mplanes, (uint64_t)K, brows, (uint64_t)K, BK, two_sm ? BN / 2 : BN,
+    rc = make_map_2d(&mb, a.mplanes, (uint64_t)K, brows, (uint64_t)K, BK, two_sm ? km.n_mma / 2 : BN,
                      CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
-    KArgs km = ka;
     km.tb_per_row = N / (two_sm ? 2 * BM : BM);
     km.m_tiles = R * km.tb_per_row;
-    km.total_tiles = km.m_tiles * n_tiles;
+    km.total_tiles = km.m_tiles * km.n_tiles;
     km.out = a.out_mask;
-    const bool sw = a.out_bits != a.kp.q_in;
-    if (two_sm) rc = sw ? dispatch_2sm<true>(ell, ma, mb, km, st) : dispatch_2sm<false>(ell, ma, mb, km, st);
-    else rc = dispatch<true>(ell, sw, ma, mb, km, st);
+    if (two_sm) {
+      rc = make_map_out(&mo, a.out_mask, sw, N, R, a.T, EPI_TOK);
+      if (rc) return rc;
+      CUtensorMap mot;
+      rc = make_map_out(&mot, a.out_mask, sw, N, R, a.T, km.tpt % EPI_TOK ? km.tpt % EPI_TOK : EPI_TOK);
+      if (rc) return rc;
+      unsigned long long zero[8] = {0};
+      if (km.dbg == 4) cudaMemcpyToSymbolAsync(g_dbg_cnt, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+      rc = sw ? dispatch_2sm<true>(ell, ma, mb, mo, mot, km, st) : dispatch_2sm<false>(ell, ma, mb, mo, mot, km, st);
+      if (km.dbg == 4) {
+        unsigned long long c[8];
+        cudaMemcpyFromSymbolAsync(c, g_dbg_cnt, sizeof(c), 0, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        const double pairs = (double)(num_sms() / 2), ntiles = (double)c[6] / (2.0 * pairs);
+        fprintf(stderr, "[phe dbg] per leader: mma_total %.1fM wait_tempty %.1fM wait_full %.1fM | "
+                "per CTA: producer_wait_empty %.1fM | epi(warp4): busy/tile %.0f wait/tile %.0f tiles %.0f\n",
+                c[2] / pairs / 1e6, c[0] / pairs / 1e6, c[1] / pairs / 1e6, c[5] / (2 * pairs) / 1e6,
+                (double)c[3] / c[6], (double)c[4] / c[6], ntiles);
+      }
+    } else {
+      rc = dispatch<true>(ell, sw, ma, mb, km, st);
+    }
     if (rc) return rc;
     (*n_launches)++;
   }
