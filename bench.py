@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e/cpu/clocks)")
+    ap.add_argument("--shard", choices=["tokens", "rows"], default="tokens",
+                    help="N>1: tokens = each rank its own batch (weak); rows = W rows split (strong)")
+    ap.add_argument("--gather", action="store_true", help="rows mode: also time the NCCL gather to rank 0")
     return ap.parse_args()
 
 
@@ -137,22 +140,27 @@ def run_ours(args):
     T = args.tokens
     lins = linears(args.workload)
     # ---------------- untimed setup: weights (server registration) and client encryption
+    from paper_2505_07329_b200.dist import gather_rows, shard_range
+    rows_mode = args.shard == "rows" and world > 1
     regs = []
     for name, d_out, d_in, tr in lins:
         W = torch.from_numpy(synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED + len(regs))).to(dev)
         regs.append((name, phe.Weights(p, W, transpose=tr)))
         del W
+    # this rank's output rows of each linear (all rows unless row-sharded)
+    rr = {name: (shard_range(w.rows, world, rank) if rows_mode else (0, w.rows)) for name, w in regs}
     S = phe.keygen(p, synth.MASTER_SEED + 17)
     inputs = {}
     for name, w in regs:
         d = w.cols
         if d not in inputs:
             gen = synth.activations_int8 if not w.transpose else synth.gradients_int8
-            x = torch.from_numpy(gen(T, d, seed=synth.MASTER_SEED + 1000 * rank + d)).to(dev)
-            seeds, body = phe.encrypt_pack(p, S, x, synth.seed_base(rank * 131 + d))
+            xr = 0 if rows_mode else rank  # row sharding: every rank sees the same tokens
+            x = torch.from_numpy(gen(T, d, seed=synth.MASTER_SEED + 1000 * xr + d)).to(dev)
+            seeds, body = phe.encrypt_pack(p, S, x, synth.seed_base(xr * 131 + d))
             inputs[d] = (seeds, body)
     chunk = T if args.workload == "q_proj" else 256  # FFN outputs are 137 GB/T=2048: chunk tokens
-    max_rows = max(w.rows for _, w in regs)
+    max_rows = max(rr[name][1] - rr[name][0] for name, _ in regs)
     out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
     out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)
     operands = {d: torch.empty(phe.load().phe_ct_operand_bytes(__import__("ctypes").byref(p), chunk, p.L(d)),
@@ -180,12 +188,14 @@ def run_ours(args):
                     launches[0] += 1
                 e[1].record(stream)
                 f = phe.matmul_clear_T if w.transpose else phe.matmul_clear
-                mview = out_mask.view(-1)[: n * w.rows * p.N].view(n, w.rows, p.N)
-                bview = out_body.view(-1)[: n * w.rows].view(n, w.rows)
-                f(p, w, operands[d], n, out_mask=phe.SKIP, out_body=bview)   # a6 body GEMM
+                r0, r1 = rr[name]
+                nr = r1 - r0
+                mview = out_mask.view(-1)[: n * nr * p.N].view(n, nr, p.N)
+                bview = out_body.view(-1)[: n * nr].view(n, nr)
+                f(p, w, operands[d], n, out_mask=phe.SKIP, out_body=bview, row_begin=r0, row_end=r1)  # a6
                 launches[0] += phe.last_launch_count()
                 e[2].record(stream)
-                f(p, w, operands[d], n, out_mask=mview, out_body=phe.SKIP)   # a5 mask GEMM
+                f(p, w, operands[d], n, out_mask=mview, out_body=phe.SKIP, row_begin=r0, row_end=r1)  # a5
                 launches[0] += phe.last_launch_count()
                 e[3].record(stream)
                 evs.append(e)
@@ -219,12 +229,30 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * T / (ms_max / 1e3)
+    value = (T if rows_mode else world * T) / (ms_max / 1e3)
+
+    # ---------------- optional: NCCL gather of the row-sharded output ciphertexts to rank 0
+    gather = None
+    if rows_mode and args.gather and args.workload == "q_proj":
+        name, w = regs[0]
+        r0, r1 = rr[name]
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        nr = r1 - r0
+        gather_rows(out_mask.view(-1)[: T * nr * p.N].view(T, nr, p.N), out_body.view(-1)[: T * nr].view(T, nr),
+                    w.rows, world, rank)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        gather = {"ms": round(float(tg.item()), 2), "bytes": int(T * w.rows * (p.N + 1) * 4),
+                  "api": "paper_2505_07329_b200.dist.gather_rows (NCCL send/recv to rank 0)"}
 
     # ---------------- roofline of the dominant kernel (mask limb GEMM)
     mp, src = measured_peaks()
     peak = 2.0 * float(mp["bf16_tflops"])  # int8 dense = 2x bf16 (guide's nominal ratio)
-    mask_ops = sum(alg_int8_ops(p, w.rows, w.cols, T, "mask") for _, w in regs)
+    mask_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") for n_, w in regs)
     mask_ms = statistics.mean(parts_ms["mask_gemm"])
     achieved = mask_ops / (mask_ms / 1e3) / 1e12
     traffic = None
@@ -234,8 +262,8 @@ def run_ours(args):
             traffic = json.load(open(tp)).get(args.workload)
         except Exception:
             traffic = None
-    total_ops = sum(alg_int8_ops(p, w.rows, w.cols, T, "mask") + alg_int8_ops(p, w.rows, w.cols, T, "body")
-                    for _, w in regs)
+    total_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") +
+                    alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "body") for n_, w in regs)
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": "limb_gemm_2sm_kernel<5,SW,13> (mask contraction, tcgen05 cta_group::2)",
@@ -246,7 +274,7 @@ def run_ours(args):
 
     # ---------------- e2e through the C ABI with host buffers
     e2e = None
-    if not args.no_e2e and not args.profile and args.workload == "q_proj":
+    if not args.no_e2e and not args.profile and args.workload == "q_proj" and not rows_mode:
         name, w = regs[0]
         seeds, body = inputs[w.cols]
         hs = seeds.cpu().pin_memory()
@@ -282,23 +310,28 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "higher_is_better": True, "scaling": "strong" if rows_mode else "weak", "vs_baseline": None,
+            "dtype": "int8",
             "data": "synthetic (seeded int8 Llama-like W, DTok int8 activations, ChaCha20 masks)",
-            "config": config_dict(args, world, T),
+            "config": config_dict(args, world, T, rows_mode),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
             "clocks": clocks,
             "breakdown_ms": {k: round(statistics.mean(v), 3) for k, v in parts_ms.items()},
         }
+        if gather is not None:
+            line["gather"] = gather
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def config_dict(args, world, T):
+def config_dict(args, world, T, rows_mode=False):
     wl = {"q_proj": "Llama-3.2-1B q_proj 2048x2048 forward W.[x]_HE (BASELINE configs[1])",
           "ffn": "Llama-3.2-1B FFN gate/up 8192x2048 + down 2048x8192, fwd + W^T bwd (configs[2])"}[args.workload]
-    return {"workload": wl, "tokens_per_gpu": T, "B": 8, "C": 256, "N": 2048, "q_in": 39, "q_out": 26,
-            "beta": 27, "parallelism": f"token-sharded x{world}" if world > 1 else "single GPU",
+    return {"workload": wl, "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": 8, "C": 256, "N": 2048, "q_in": 39, "q_out": 26,
+            "beta": 27,
+            "parallelism": (f"row-sharded x{world}" if rows_mode else f"token-sharded x{world}") if world > 1
+            else "single GPU",
             "l2": "flushed between steps (256 MiB write), outputs 34 GB/step >> L2",
             "output": "LWE ciphertexts, uint32 per coefficient after 39->26 modulus switch"}
 
