@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["q_proj", "ffn"], default="q_proj")
+    ap.add_argument("--workload", choices=["q_proj", "ffn", "stack"], default="q_proj")
     ap.add_argument("--tokens", type=int, default=2048, help="tokens per rank (B*C = 8*256)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -106,12 +106,26 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- workloads
 def linears(workload: str):
-    """(name, d_out, d_in, transpose) of each linear one step runs (Llama-3.2-1B)."""
-    if workload == "q_proj":
-        return [("q_proj", 2048, 2048, False)]
-    # configs[2]: FFN gate/up 8192x2048 and down 2048x8192, forward + backward W^T
-    return [("gate", 8192, 2048, False), ("up", 8192, 2048, False), ("down", 2048, 8192, False),
-            ("gate_T", 8192, 2048, True), ("up_T", 8192, 2048, True), ("down_T", 2048, 8192, True)]
+    """Calls one step makes: (name, d_out, d_in, transpose, input_key).  Llama-3.2-1B:
+    d = 2048, m = 8192, GQA k/v 512x2048, 16 layers.  Linears that share an input ciphertext
+    are registered fused (qkv 3072x2048, gate_up 16384x2048), so the input is expanded once and
+    read by one GEMM.  Backward W^T takes each output's own gradient."""
+    if workload == "q_proj":  # configs[1]
+        return [("q_proj", 2048, 2048, False, "x")]
+    if workload == "ffn":     # configs[2]: gate/up 8192x2048, down 2048x8192, fwd + W^T bwd
+        return [("gate", 8192, 2048, False, "h"), ("up", 8192, 2048, False, "h"),
+                ("down", 2048, 8192, False, "m"),
+                ("gate_T", 8192, 2048, True, "g_gate"), ("up_T", 8192, 2048, True, "g_up"),
+                ("down_T", 2048, 8192, True, "g_down")]
+    calls = []                # configs[3]: the full 16-layer stack, forward + backward
+    for l in range(16):
+        calls += [(f"L{l}.qkv", 3072, 2048, False, f"L{l}.x"), (f"L{l}.o", 2048, 2048, False, f"L{l}.a"),
+                  (f"L{l}.gate_up", 16384, 2048, False, f"L{l}.h"), (f"L{l}.down", 2048, 8192, False, f"L{l}.m"),
+                  (f"L{l}.q_T", 2048, 2048, True, f"L{l}.gq"), (f"L{l}.k_T", 512, 2048, True, f"L{l}.gk"),
+                  (f"L{l}.v_T", 512, 2048, True, f"L{l}.gv"), (f"L{l}.o_T", 2048, 2048, True, f"L{l}.go"),
+                  (f"L{l}.gate_T", 8192, 2048, True, f"L{l}.gg"), (f"L{l}.up_T", 8192, 2048, True, f"L{l}.gu"),
+                  (f"L{l}.down_T", 2048, 8192, True, f"L{l}.gd")]
+    return calls
 
 
 def alg_int8_ops(p, rows, cols, T, part):
@@ -142,29 +156,32 @@ def run_ours(args):
     # ---------------- untimed setup: weights (server registration) and client encryption
     from paper_2505_07329_b200.dist import gather_rows, shard_range
     rows_mode = args.shard == "rows" and world > 1
-    regs = []
-    for name, d_out, d_in, tr in lins:
-        W = torch.from_numpy(synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED + len(regs))).to(dev)
-        regs.append((name, phe.Weights(p, W, transpose=tr)))
+    regs = []   # (name, Weights, input_key)
+    for name, d_out, d_in, tr, ikey in lins:
+        W = synth.weights_int8_torch(d_out, d_in, seed=synth.MASTER_SEED + len(regs), device=dev)
+        regs.append((name, phe.Weights(p, W, transpose=tr), ikey))
         del W
     # this rank's output rows of each linear (all rows unless row-sharded)
-    rr = {name: (shard_range(w.rows, world, rank) if rows_mode else (0, w.rows)) for name, w in regs}
+    rr = {name: (shard_range(w.rows, world, rank) if rows_mode else (0, w.rows)) for name, w, _ in regs}
     S = phe.keygen(p, synth.MASTER_SEED + 17)
+    # input ciphertexts: one per distinct (shape, role) -- layers reuse the resident synthetic
+    # ciphertexts of the same shape, but every call still expands (ct_prepare) and contracts its own
     inputs = {}
-    for name, w in regs:
-        d = w.cols
-        if d not in inputs:
+    for name, w, ikey in regs:
+        base = (w.cols, w.transpose)
+        if base not in inputs:
             gen = synth.activations_int8 if not w.transpose else synth.gradients_int8
             xr = 0 if rows_mode else rank  # row sharding: every rank sees the same tokens
-            x = torch.from_numpy(gen(T, d, seed=synth.MASTER_SEED + 1000 * xr + d)).to(dev)
-            seeds, body = phe.encrypt_pack(p, S, x, synth.seed_base(xr * 131 + d))
-            inputs[d] = (seeds, body)
+            x = torch.from_numpy(gen(T, w.cols, seed=synth.MASTER_SEED + 1000 * xr + w.cols + 7 * w.transpose)).to(dev)
+            seeds, body = phe.encrypt_pack(p, S, x, synth.seed_base(xr * 131 + w.cols + 7 * w.transpose))
+            inputs[base] = (seeds, body)
     chunk = T if args.workload == "q_proj" else 256  # FFN outputs are 137 GB/T=2048: chunk tokens
-    max_rows = max(rr[name][1] - rr[name][0] for name, _ in regs)
+    max_rows = max(rr[name][1] - rr[name][0] for name, _, _ in regs)
     out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
     out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)
-    operands = {d: torch.empty(phe.load().phe_ct_operand_bytes(__import__("ctypes").byref(p), chunk, p.L(d)),
-                               dtype=torch.uint8, device=dev) for d in inputs}
+    max_L = max(p.L(w.cols) for _, w, _ in regs)
+    operand = torch.empty(phe.load().phe_ct_operand_bytes(__import__("ctypes").byref(p), chunk, max_L),
+                          dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
@@ -176,29 +193,25 @@ def run_ours(args):
         evs = []
         for t0 in range(0, T, chunk):
             n = min(chunk, T - t0)
-            prepared = set()
-            for name, w in regs:
-                d = w.cols
-                seeds, body = inputs[d]
+            for name, w, ikey in regs:
+                seeds, body = inputs[(w.cols, w.transpose)]
                 e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                 e[0].record(stream)
-                if d not in prepared:
-                    phe.ct_prepare(p, seeds[t0:t0 + n], body[t0:t0 + n], out=operands[d])
-                    prepared.add(d)
-                    launches[0] += 1
+                phe.ct_prepare(p, seeds[t0:t0 + n], body[t0:t0 + n], out=operand)  # a3, a4
+                launches[0] += 1
                 e[1].record(stream)
                 f = phe.matmul_clear_T if w.transpose else phe.matmul_clear
                 r0, r1 = rr[name]
                 nr = r1 - r0
                 mview = out_mask.view(-1)[: n * nr * p.N].view(n, nr, p.N)
                 bview = out_body.view(-1)[: n * nr].view(n, nr)
-                f(p, w, operands[d], n, out_mask=phe.SKIP, out_body=bview, row_begin=r0, row_end=r1)  # a6
+                f(p, w, operand, n, out_mask=phe.SKIP, out_body=bview, row_begin=r0, row_end=r1)  # a6
                 launches[0] += phe.last_launch_count()
                 e[2].record(stream)
-                f(p, w, operands[d], n, out_mask=mview, out_body=phe.SKIP, row_begin=r0, row_end=r1)  # a5
+                f(p, w, operand, n, out_mask=mview, out_body=phe.SKIP, row_begin=r0, row_end=r1)  # a5
                 launches[0] += phe.last_launch_count()
                 e[3].record(stream)
-                evs.append(e)
+                evs.append((name, e))
         return evs
 
     # ---------------- warmup
@@ -212,13 +225,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     clk = None if args.profile else ClockSampler(local)
     step_ms = []
+    per_kind = {}
     for _ in range(args.steps):
         evs = step(True)
         torch.cuda.synchronize()
-        step_ms.append(sum(e[0].elapsed_time(e[3]) for e in evs))
-        parts_ms["ct_prepare"].append(sum(e[0].elapsed_time(e[1]) for e in evs))
-        parts_ms["body_gemm"].append(sum(e[1].elapsed_time(e[2]) for e in evs))
-        parts_ms["mask_gemm"].append(sum(e[2].elapsed_time(e[3]) for e in evs))
+        step_ms.append(sum(e[0].elapsed_time(e[3]) for _, e in evs))
+        parts_ms["ct_prepare"].append(sum(e[0].elapsed_time(e[1]) for _, e in evs))
+        parts_ms["body_gemm"].append(sum(e[1].elapsed_time(e[2]) for _, e in evs))
+        parts_ms["mask_gemm"].append(sum(e[2].elapsed_time(e[3]) for _, e in evs))
+        for name, e in evs:
+            kind = name.split(".")[-1]
+            per_kind.setdefault(kind, []).append(e[0].elapsed_time(e[3]))
         flush.zero_()  # L2 flush between timed steps (outside the events)
     torch.cuda.synchronize()
     clocks = clk.stop() if clk else None
@@ -234,7 +251,7 @@ def run_ours(args):
     # ---------------- optional: NCCL gather of the row-sharded output ciphertexts to rank 0
     gather = None
     if rows_mode and args.gather and args.workload == "q_proj":
-        name, w = regs[0]
+        name, w, _ = regs[0]
         r0, r1 = rr[name]
         dist.barrier()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -252,7 +269,7 @@ def run_ours(args):
     # ---------------- roofline of the dominant kernel (mask limb GEMM)
     mp, src = measured_peaks()
     peak = 2.0 * float(mp["bf16_tflops"])  # int8 dense = 2x bf16 (guide's nominal ratio)
-    mask_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") for n_, w in regs)
+    mask_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") for n_, w, _ in regs)
     mask_ms = statistics.mean(parts_ms["mask_gemm"])
     achieved = mask_ops / (mask_ms / 1e3) / 1e12
     traffic = None
@@ -263,7 +280,7 @@ def run_ours(args):
         except Exception:
             traffic = None
     total_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") +
-                    alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "body") for n_, w in regs)
+                    alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "body") for n_, w, _ in regs)
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": "limb_gemm_2sm_kernel<5,SW,13> (mask contraction, tcgen05 cta_group::2)",
@@ -275,8 +292,8 @@ def run_ours(args):
     # ---------------- e2e through the C ABI with host buffers
     e2e = None
     if not args.no_e2e and not args.profile and args.workload == "q_proj" and not rows_mode:
-        name, w = regs[0]
-        seeds, body = inputs[w.cols]
+        name, w, _ = regs[0]
+        seeds, body = inputs[(w.cols, w.transpose)]
         hs = seeds.cpu().pin_memory()
         hb = body.cpu().pin_memory()
         hm = torch.empty((T, w.rows, p.N), dtype=torch.int32, pin_memory=True)
@@ -318,6 +335,8 @@ def run_ours(args):
             "clocks": clocks,
             "breakdown_ms": {k: round(statistics.mean(v), 3) for k, v in parts_ms.items()},
         }
+        if len(regs) > 1:
+            line["per_linear_ms"] = {k: round(sum(v) / args.steps, 3) for k, v in per_kind.items()}
         if gather is not None:
             line["gather"] = gather
         print(json.dumps(line), flush=True)
@@ -327,7 +346,9 @@ def run_ours(args):
 
 def config_dict(args, world, T, rows_mode=False):
     wl = {"q_proj": "Llama-3.2-1B q_proj 2048x2048 forward W.[x]_HE (BASELINE configs[1])",
-          "ffn": "Llama-3.2-1B FFN gate/up 8192x2048 + down 2048x8192, fwd + W^T bwd (configs[2])"}[args.workload]
+          "ffn": "Llama-3.2-1B FFN gate/up 8192x2048 + down 2048x8192, fwd + W^T bwd (configs[2])",
+          "stack": "Llama-3.2-1B all linears x 16 layers (qkv fused 3072x2048, o, gate_up fused 16384x2048, "
+                   "down; bwd W^T incl. GQA k/v 512x2048), fwd + bwd (configs[3])"}[args.workload]
     return {"workload": wl, "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": 8, "C": 256, "N": 2048, "q_in": 39, "q_out": 26,
             "beta": 27,
             "parallelism": (f"row-sharded x{world}" if rows_mode else f"token-sharded x{world}") if world > 1
@@ -345,7 +366,7 @@ def cpu_baseline(args, lin, budget_s=12.0):
     from oracle import c_oracle
     from oracle import phe_oracle as O
 
-    name, d_out, d_in, tr = lin
+    name, d_out, d_in, tr, _ = lin
     lib = c_oracle.load()
     op = O.PAPER
     W = synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED)
@@ -385,7 +406,7 @@ def run_reference(args):
     op = O.PAPER
     cores = os.cpu_count() or 1
     lin = linears(args.workload)[0]
-    name, d_out, d_in, tr = lin
+    name, d_out, d_in, tr, _ = lin
     W = synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED)
     M = np.ascontiguousarray(W.T) if tr else W
     cols = M.shape[1]

@@ -77,3 +77,15 @@ def uniform_u64(shape, seed: int, bits: int) -> np.ndarray:
 def seed_base(tag: int = 0) -> int:
     """Public per-call seed base (an integer; the expansion is each side's own)."""
     return (MASTER_SEED * 1000003 + tag * 7919) & ((1 << 63) - 1)
+
+
+def weights_int8_torch(d_out: int, d_in: int, seed: int = MASTER_SEED, device="cuda"):
+    """Same recipe as weights_int8 (N(0, 0.02^2), per-row symmetric int8), drawn with torch on
+    `device` so the 16-layer stack (973M weights) is generated in seconds.  Not bitwise equal
+    to weights_int8 (different RNG); used only where no oracle comparison is made."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed ^ 0x5757)
+    f = torch.randn((d_out, d_in), generator=g, device=device, dtype=torch.float32) * 0.02
+    amax = f.abs().amax(dim=1, keepdim=True).clamp_min(1e-30)
+    return torch.clamp(torch.round(f / amax * 127.0), -127, 127).to(torch.int8)

@@ -259,3 +259,24 @@ def test_full_size_q_proj_bench_config(phe, coracle):
     m26, b26 = phe.matmul_clear(p, w, opnd, T)
     y26 = phe.decrypt_unpack(p, S, m26, b26, 26).double()
     assert (y26 - wx).abs().max().item() <= 1 + int(S.sum().item())
+
+
+# ----------------------------------------------------------------------------- other parameter sets
+@pytest.mark.parametrize("over,d_out,d_in,T", [
+    (dict(N=512, q_in=39, q_out=26, beta=27), 40, 1100, 9),     # P1-like ring, L = 3, 2-CTA path
+    (dict(N=4096, q_in=39, q_out=26, beta=27), 5, 4096, 3),     # P3 ring
+    (dict(N=2048, q_in=32, q_out=24, beta=27), 33, 2048, 70),   # P2: ell = 4, s = 8 (generic epilogue)
+    (dict(N=256, q_in=48, q_out=30, beta=27), 17, 300, 11),     # ell = 6: 1-CTA fallback kernel
+    (dict(N=256, q_in=20, q_out=16, beta=12, gamma=8), 9, 256, 100),  # ell = 3, 1-CTA kernel
+])
+def test_parameter_sets_bit_exact(phe, coracle, over, d_out, d_in, T):
+    p = phe.params(phe.PRESET_PAPER, **over)
+    W = synth.uniform_int8((d_out, d_in), d_in + T, -127, 127)
+    x = synth.uniform_int8((T, d_in), d_out + T, -7, 7)
+    S, seeds, body, w, opnd, (mq, bq) = run_gpu(phe, p, W, x, out_bits=p.q_in)
+    _, _, B_o, mask_o, body_o = oracle_expect(coracle, p, W, x, 7, 12345)
+    assert np.array_equal(u64(body), B_o)
+    assert np.array_equal(u64(mq), mask_o) and np.array_equal(u64(bq), body_o)
+    ms, bs = phe.matmul_clear(p, w, opnd, T)
+    assert np.array_equal(ms.cpu().numpy().astype(np.uint32).astype(np.uint64), O.modswitch(mask_o, p.q_in, p.q_out))
+    assert np.array_equal(bs.cpu().numpy().astype(np.uint32).astype(np.uint64), O.modswitch(body_o, p.q_in, p.q_out))
