@@ -175,8 +175,11 @@ def run_ours(args):
             x = torch.from_numpy(gen(T, w.cols, seed=synth.MASTER_SEED + 1000 * xr + w.cols + 7 * w.transpose)).to(dev)
             seeds, body = phe.encrypt_pack(p, S, x, synth.seed_base(xr * 131 + w.cols + 7 * w.transpose))
             inputs[base] = (seeds, body)
-    chunk = T if args.workload == "q_proj" else 256  # FFN outputs are 137 GB/T=2048: chunk tokens
     max_rows = max(rr[name][1] - rr[name][0] for name, _, _ in regs)
+    # token chunks: outputs stay <= ~34 GB (gate_up: 275 GB at T=2048) and a chunk is a whole
+    # number of 51-token tiles (no extra tile-padding waste)
+    tpt = 256 // p.ell
+    chunk = min(T, max(tpt, (34_400_000_000 // (max_rows * p.N * 4)) // tpt * tpt))
     out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
     out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)
     max_L = max(p.L(w.cols) for _, w, _ in regs)

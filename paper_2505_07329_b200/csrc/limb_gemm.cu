@@ -82,6 +82,8 @@ struct KArgs {
   int k_blocks;       // Lc*N / BK
   int kb_per_block;   // N / BK
   int64_t Lc;
+  int64_t cols;       // columns of the prepared matrix (d_in of the contraction)
+  int full_k;         // no zero-padded K-blocks (or more than 64): no skipping
   int64_t row_begin;  // absolute first row
   int64_t R;          // rows in range
   int64_t T;
@@ -455,6 +457,63 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
+// K-block skipping for zero-padded blocks: the pair tile (rows tp .. tp+255) reads
+// wext[u], u in [k0 + tp, k0 + tp + 383) for K-block k0 of block i; wext is zero outside
+// [0, V) U [N, N+V), V = min(N, cols - iN).  Full blocks are never skipped; the tile's mask
+// (bit kb = issue) is computed once per tile, identically by the producer and MMA warps, so
+// the smem ring stays in step.  Never empty for V >= 1.  Blocks kb >= 64 are never skipped.
+__device__ __forceinline__ uint64_t kblock_mask(const KArgs &ka, int tp) {
+  if (ka.full_k || ka.dbg == 9) return ~0ull;
+  // Closed form (checked against the per-block definition above for N in 256..4096, all
+  // cols, all tp): only the last block il = Lc-1 can be partial (V < N); its needed kk are
+  // [0, lo_end) U [hi_start, hi_end) with a = kk*BK + tp:
+  //   a < V               <=> kk < ceil((V - tp) / BK)
+  //   a + 383 > N         <=> kk >= floor((N - tp - 383) / BK) + 1   (all kk if N - tp - 383 < 0)
+  //   a < N + V           <=> kk < ceil((N + V - tp) / BK)
+  const int kbpb = ka.kb_per_block, N = ka.N, il = (int)ka.Lc - 1;
+  const int V = (int)(ka.cols - (int64_t)il * N);
+  auto cl = [kbpb](int v) { return v < 0 ? 0 : (v > kbpb ? kbpb : v); };
+  auto rng = [](int a, int b) -> uint64_t { return b > a ? (((1ull << b) - 1ull) & ~((1ull << a) - 1ull)) : 0ull; };
+  const int lo_end = V - tp > 0 ? cl((V - tp + BK - 1) / BK) : 0;
+  const int x = N - tp - (2 * BM + BK - 1);
+  const int hi_start = x >= 0 ? cl(x / BK + 1) : 0;
+  const int hi_end = cl((N + V - tp + BK - 1) / BK);
+  const uint64_t full_bits = il * kbpb >= 64 ? ~0ull : ((1ull << (il * kbpb)) - 1ull);
+  return full_bits | ((rng(0, lo_end) | rng(hi_start, hi_end)) << (il * kbpb));
+}
+__device__ __forceinline__ bool kb_issue(uint64_t m, int kb) { return kb >= 64 || ((m >> kb) & 1ull); }
+
+// Persistent tile walk: tile = cid, cid + ncl, ... decoded incrementally (no 64-bit divides
+// per tile): tile = m * n_tiles + n.
+struct TileIter {
+  int64_t tile, m;
+  int n;
+  int64_t step_m;
+  int step_n;
+  __device__ __forceinline__ TileIter(int64_t cid, int64_t ncl, int n_tiles) {
+    tile = cid; m = cid / n_tiles; n = (int)(cid % n_tiles);
+    step_m = ncl / n_tiles; step_n = (int)(ncl % n_tiles);
+  }
+  __device__ __forceinline__ void next(int64_t ncl, int n_tiles) {
+    tile += ncl; m += step_m; n += step_n;
+    if (n >= n_tiles) { n -= n_tiles; m++; }
+  }
+};
+
+// One lane of a fully active warp (the issuing loops run warp-wide so that descriptors and
+// loop state stay warp-uniform, i.e. in uniform registers; only the elected lane issues).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "elect.sync _|p, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 template <int ELL, bool SW, int SH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -503,65 +562,80 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
   const int64_t total = ka.total_tiles;
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   if (warp == W_PROD) {
-    // ===== TMA producer (both CTAs): own Hankel rows + own half of B, bytes land on CTA 0 =====
-    if (lane == 0) {
-      int s = 0; uint32_t ph = 0;
-      long long pw = 0;
-      const uint32_t tx = (uint32_t)(2 * ((ka.dbg == 5 ? 0 : A_BYTES_HANKEL) + (ka.dbg == 6 ? 0 : b_half)));
-      for (int64_t tile = cid; tile < total; tile += ncl) {
-        const int64_t m_tile = tile / ka.n_tiles;
-        const int n_tile = (int)(tile % ka.n_tiles);
-        const int brow = n_tile * ka.tpt * ELL + (int)crank * (n_mma / 2);
-        const int64_t jrow = ka.row_begin + m_tile / ka.tb_per_row;
-        const int t0 = (int)(m_tile % ka.tb_per_row) * (2 * BM) + (int)crank * BM;
-        for (int kb = 0; kb < ka.k_blocks; kb++) {
+    // ===== TMA producer (both CTAs, warp-wide loop, elected lane issues): own Hankel rows +
+    // own half of B, bytes land on CTA 0's barrier =====
+    int s = 0; uint32_t ph = 0;
+    long long pw = 0;
+    const uint32_t tx = (uint32_t)(2 * ((ka.dbg == 5 ? 0 : A_BYTES_HANKEL) + (ka.dbg == 6 ? 0 : b_half)));
+    for (TileIter it(cid, ncl, ka.n_tiles); it.tile < total; it.next(ncl, ka.n_tiles)) {
+      const int64_t m_tile = it.m;
+      const int n_tile = it.n;
+      const int brow = n_tile * ka.tpt * ELL + (int)crank * (n_mma / 2);
+      const int jr_ = (int)((uint32_t)m_tile / (uint32_t)ka.tb_per_row);
+      const int64_t jrow = ka.row_begin + jr_;
+      const int tp = ((int)m_tile - jr_ * ka.tb_per_row) * (2 * BM);  // pair's first row t
+      const int64_t abase = jrow * ka.Lc * (2 * (int64_t)ka.N) + tp + (int)crank * BM;
+      const uint64_t km = kblock_mask(ka, tp);
+      int i = 0, kk = 0;
+      for (int kb = 0; kb < ka.k_blocks; kb++) {
+        if (kb_issue(km, kb)) {
           long long w0 = ka.dbg == 4 ? clock64() : 0;
           mbar_wait(&empty[s], ph ^ 1);
           if (ka.dbg == 4) pw += clock64() - w0;
-          if (leader) mbar_expect_tx(&full[s], tx);
-          const uint32_t fb = smem_u32(&full[s]) & PEER_MASK;
-          const int i = kb / ka.kb_per_block, k0 = (kb % ka.kb_per_block) * BK;
-          const int64_t arow = (jrow * ka.Lc + i) * (2 * (int64_t)ka.N) + k0 + t0;
-          if (ka.dbg != 5) tma_load_2d_2sm(smem_u32(sA + s * 4096), &map_a, 0, (int)arow, fb);
-          if (ka.dbg != 6) tma_load_2d_2sm(smem_u32(sB + s * B_HALF_MAX), &map_b, kb * BK, brow, fb);
+          if (elect_one()) {
+            if (leader) mbar_expect_tx(&full[s], tx);
+            const uint32_t fb = smem_u32(&full[s]) & PEER_MASK;
+            const int64_t arow = abase + (int64_t)i * (2 * (int64_t)ka.N) + kk * BK;
+            if (ka.dbg != 5) tma_load_2d_2sm(smem_u32(sA + s * 4096), &map_a, 0, (int)arow, fb);
+            if (ka.dbg != 6) tma_load_2d_2sm(smem_u32(sB + s * B_HALF_MAX), &map_b, kb * BK, brow, fb);
+          }
+          __syncwarp();
           if (++s == S) { s = 0; ph ^= 1; }
         }
+        if (++kk == ka.kb_per_block) { kk = 0; i++; }
       }
-      if (ka.dbg == 4) dbg_add(5, pw);
     }
-    __syncwarp();
+    if (ka.dbg == 4 && lane == 0) dbg_add(5, pw);
   } else if (warp == W_MMA) {
-    // ===== MMA issuer (leader CTA only) =====
-    if (leader && lane == 0) {
+    // ===== MMA issuer (leader CTA only; warp-wide loop, elected lane issues + commits) =====
+    if (leader) {
       const uint32_t idesc = idesc_i8(2 * BM, n_mma);
       int s = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
       long long t_start = clock64(), wt = 0, wf = 0;
-      for (int64_t tile = cid; tile < total; tile += ncl) {
+      for (TileIter it(cid, ncl, ka.n_tiles); it.tile < total; it.next(ncl, ka.n_tiles)) {
         long long w0 = ka.dbg == 4 ? clock64() : 0;
         mbar_wait(&tempty[acc], aph ^ 1);
         if (ka.dbg == 4) wt += clock64() - w0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        const int tp = (int)((uint32_t)it.m % (uint32_t)ka.tb_per_row) * (2 * BM);
+        const uint64_t km = kblock_mask(ka, tp);
+        uint32_t acc_flag = 0;  // first issued MMA of the tile overwrites the accumulator
         for (int kb = 0; kb < ka.k_blocks; kb++) {
+          if (!kb_issue(km, kb)) continue;
           long long w1 = ka.dbg == 4 ? clock64() : 0;
           mbar_wait(&full[s], ph);
           if (ka.dbg == 4) wf += clock64() - w1;
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + s * 4096);
           const uint32_t b_addr = smem_u32(sB + s * B_HALF_MAX);
+          if (elect_one()) {
 #pragma unroll
-          for (int q = 0; q < BK / UK; q++)
-            mma_i8_2sm(d_tmem, desc_hankel(a_addr + 512 * q), desc_sw128(b_addr + 32 * q), idesc,
-                       (kb | q) != 0 ? 1u : 0u);
-          tc_commit_mc2(&empty[s]);
+            for (int q = 0; q < BK / UK; q++)
+              mma_i8_2sm(d_tmem, desc_hankel(a_addr + 512 * q), desc_sw128(b_addr + 32 * q), idesc,
+                         (acc_flag | (uint32_t)q) ? 1u : 0u);
+            tc_commit_mc2(&empty[s]);
+          }
+          __syncwarp();
+          acc_flag = 1u;
           if (++s == S) { s = 0; ph ^= 1; }
         }
-        tc_commit_mc2(&tfull[acc]);
+        if (elect_one()) tc_commit_mc2(&tfull[acc]);
+        __syncwarp();
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
-      if (ka.dbg == 4) { dbg_add(0, wt); dbg_add(1, wf); dbg_add(2, clock64() - t_start); }
+      if (ka.dbg == 4 && lane == 0) { dbg_add(0, wt); dbg_add(1, wf); dbg_add(2, clock64() - t_start); }
     }
-    __syncwarp();
   } else if (warp < 8) {
     // ===== epilogue (both CTAs): own 128 TMEM lanes = own 128 rows t =====
     // Group g (warps 0-3 / 4-7) takes every other 16-token chunk (alternating per tile).
@@ -575,13 +649,12 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     const uint32_t tempty_c0 = smem_u32(&tempty[0]) & PEER_MASK;
     OutT *const obuf = reinterpret_cast<OutT *>(sO + grp * 2 * C2::OUT_BUF);
     int acc = 0; uint32_t aph = 0; int nbuf = 0; int64_t iter = 0;
-    for (int64_t tile = cid; tile < total; tile += ncl, iter++) {
-      const int64_t m_tile = tile / ka.n_tiles;
-      const int n_tile = (int)(tile % ka.n_tiles);
+    for (TileIter it(cid, ncl, ka.n_tiles); it.tile < total; it.next(ncl, ka.n_tiles), iter++) {
+      const int n_tile = it.n;
       const int tau0 = n_tile * ka.tpt;
       const int ntok = (int)min((int64_t)ka.tpt, ka.T - tau0);
-      const int jr = (int)(m_tile / ka.tb_per_row);
-      const int tb = (int)(m_tile % ka.tb_per_row) * (2 * BM) + (int)crank * BM;
+      const int jr = (int)((uint32_t)it.m / (uint32_t)ka.tb_per_row);
+      const int tb = ((int)it.m - jr * ka.tb_per_row) * (2 * BM) + (int)crank * BM;
       const int nchunks = (ntok + EPI_TOK - 1) / EPI_TOK;
       const int first = (grp + (int)(iter & 1)) & 1;
       long long e0 = (ka.dbg == 4 && warp == 0 && lane == 0) ? clock64() : 0;
@@ -809,7 +882,8 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
   const uint64_t brows = (uint64_t)a.op_rows;  // padded: boxes never leave the allocation
   KArgs ka{};
   ka.N = N; ka.tpt = tpt; ka.n_tiles = n_tiles; ka.k_blocks = (int)(K / BK);
-  ka.kb_per_block = N / BK; ka.Lc = a.Lc; ka.row_begin = a.row_begin; ka.R = R; ka.T = a.T;
+  ka.kb_per_block = N / BK; ka.Lc = a.Lc; ka.cols = a.cols; ka.row_begin = a.row_begin; ka.R = R; ka.T = a.T;
+  ka.full_k = (a.cols == a.Lc * N) || (K / BK > 64);
   ka.q_in = a.kp.q_in; ka.out_bits = a.out_bits;
   ka.dbg = getenv("PHE_DEBUG_EPI") ? atoi(getenv("PHE_DEBUG_EPI")) : 0;
   // ---- body: plain W operand, M = rows in range (skipped when out_body == NULL)

@@ -174,6 +174,7 @@ static int matmul_common(const phe_params *p, const void *d_wprep, int64_t rows,
   a.wplain_rows = round_up(rows, 128);
   a.op_rows = op_rows(T, kp.ell);
   a.Lc = Lc;
+  a.cols = cols;
   a.row_begin = row_begin;
   a.row_end = row_end;
   a.mplanes = static_cast<const uint8_t *>(d_operand);

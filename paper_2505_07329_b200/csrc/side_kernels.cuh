@@ -32,6 +32,7 @@ struct GemmArgs {
   int64_t wplain_rows;    // padded row count of wplain
   int64_t op_rows;        // padded row count of each limb-plane matrix (>= T*ell, mult. of 256)
   int64_t Lc;             // blocks along M's columns (= L of the input ciphertext)
+  int64_t cols;           // columns of M (the contraction length, unpadded)
   int64_t row_begin, row_end;
   const uint8_t *mplanes; // [T*ell][Lc*N]
   const uint8_t *bplanes; // [T*ell][Lc*N]
