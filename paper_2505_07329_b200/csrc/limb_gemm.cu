@@ -177,6 +177,37 @@ __host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
          ((uint32_t)(m >> 4) << 24);
 }
 
+// Persistent tile walk: tile = cid, cid + ncl, ... decoded incrementally (no 64-bit divides
+// per tile): tile = m * n_tiles + n.
+struct TileIter {
+  int64_t tile, m;
+  int n;
+  int64_t step_m;
+  int step_n;
+  __device__ __forceinline__ TileIter(int64_t cid, int64_t ncl, int n_tiles) {
+    tile = cid; m = cid / n_tiles; n = (int)(cid % n_tiles);
+    step_m = ncl / n_tiles; step_n = (int)(ncl % n_tiles);
+  }
+  __device__ __forceinline__ void next(int64_t ncl, int n_tiles) {
+    tile += ncl; m += step_m; n += step_n;
+    if (n >= n_tiles) { n -= n_tiles; m++; }
+  }
+};
+
+// One lane of a fully active warp (the issuing loops run warp-wide so that descriptors and
+// loop state stay warp-uniform, i.e. in uniform registers; only the elected lane issues).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "elect.sync _|p, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // Limb recombination mod 2^q_in (a7) + ModulusSwitch (a8), one output word:
 //   x = half + sum_l acc_l * 2^(8l)  (two's complement in 64 bits; 2^q_in | 2^64)
 //   SW:  r = (x >> (q_in - q_out)) mod 2^q_out   (round half up: half = 2^(q_in-q_out-1))
@@ -255,60 +286,60 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 
   const int64_t total = ka.total_tiles;
   if (warp == W_PROD) {
-    // ===== TMA producer =====
-    if (lane == 0) {
-      int s = 0; uint32_t ph = 0;
-      for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const int64_t m_tile = tile / ka.n_tiles;
-        const int n_tile = (int)(tile % ka.n_tiles);
-        const int brow = n_tile * ka.tpt * ELL;
-        int64_t jrow; int t0;
-        if (HANKEL) { jrow = ka.row_begin + m_tile / ka.tb_per_row; t0 = (int)(m_tile % ka.tb_per_row) * BM; }
-        else { jrow = ka.row_begin + m_tile * BM; t0 = 0; }
-        for (int kb = 0; kb < ka.k_blocks; kb++) {
-          mbar_wait(&empty[s], ph ^ 1);
+    // ===== TMA producer (warp-wide loop, elected lane issues) =====
+    int s = 0; uint32_t ph = 0;
+    for (TileIter it(blockIdx.x, gridDim.x, ka.n_tiles); it.tile < total; it.next(gridDim.x, ka.n_tiles)) {
+      const int64_t m_tile = it.m;
+      const int brow = it.n * ka.tpt * ELL;
+      int64_t jrow; int t0;
+      if (HANKEL) { jrow = ka.row_begin + m_tile / ka.tb_per_row; t0 = (int)(m_tile % ka.tb_per_row) * BM; }
+      else { jrow = ka.row_begin + m_tile * BM; t0 = 0; }
+      int i = 0, kk = 0;
+      for (int kb = 0; kb < ka.k_blocks; kb++) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (elect_one()) {
           mbar_expect_tx(&full[s], (uint32_t)(C::A_BYTES + B_BYTES));
           if (HANKEL) {
-            const int i = kb / ka.kb_per_block, k0 = (kb % ka.kb_per_block) * BK;
-            const int64_t arow = (jrow * ka.Lc + i) * (2 * (int64_t)ka.N) + k0 + t0;
+            const int64_t arow = (jrow * ka.Lc + i) * (2 * (int64_t)ka.N) + kk * BK + t0;
             tma_load_2d(smem_u32(sA + s * C::A_SLOT), &map_a, 0, (int)arow, &full[s]);
           } else {
             tma_load_2d(smem_u32(sA + s * C::A_SLOT), &map_a, kb * BK, (int)jrow, &full[s]);
           }
           tma_load_2d(smem_u32(sB + s * B_BYTES), &map_b, kb * BK, brow, &full[s]);
-          if (++s == S) { s = 0; ph ^= 1; }
         }
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
+        if (++kk == ka.kb_per_block) { kk = 0; i++; }
       }
     }
-    __syncwarp();
   } else if (warp == W_MMA) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8(BM, BN);
-      int s = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
-      for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        mbar_wait(&tempty[acc], aph ^ 1);
+    // ===== MMA issuer (warp-wide loop, elected lane issues + commits) =====
+    constexpr uint32_t idesc = idesc_i8(BM, BN);
+    int s = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < ka.k_blocks; kb++) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < ka.k_blocks; kb++) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + s * C::A_SLOT);
-          const uint32_t b_addr = smem_u32(sB + s * B_BYTES);
+        const uint32_t a_addr = smem_u32(sA + s * C::A_SLOT);
+        const uint32_t b_addr = smem_u32(sB + s * B_BYTES);
+        if (elect_one()) {
 #pragma unroll
           for (int q = 0; q < BK / UK; q++) {
             const uint64_t adesc = HANKEL ? desc_hankel(a_addr + 512 * q) : desc_sw128(a_addr + 32 * q);
-            const uint64_t bdesc = desc_sw128(b_addr + 32 * q);
-            mma_i8(d_tmem, adesc, bdesc, idesc, (kb | q) != 0 ? 1u : 0u);
+            mma_i8(d_tmem, adesc, desc_sw128(b_addr + 32 * q), idesc, (kb | q) != 0 ? 1u : 0u);
           }
           tc_commit(&empty[s]);
-          if (++s == S) { s = 0; ph ^= 1; }
         }
-        tc_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; aph ^= 1; }
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
       }
+      if (elect_one()) tc_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aph ^= 1; }
     }
-    __syncwarp();
   } else if (warp < 8) {
     // ===== epilogue: TMEM -> registers -> recombine limbs -> modswitch -> HBM =====
     // 8 warps (0-7): two per TMEM lane quarter; group g = 0/1 takes the even/odd 16-token chunks.
@@ -482,37 +513,6 @@ __device__ __forceinline__ uint64_t kblock_mask(const KArgs &ka, int tp) {
   return full_bits | ((rng(0, lo_end) | rng(hi_start, hi_end)) << (il * kbpb));
 }
 __device__ __forceinline__ bool kb_issue(uint64_t m, int kb) { return kb >= 64 || ((m >> kb) & 1ull); }
-
-// Persistent tile walk: tile = cid, cid + ncl, ... decoded incrementally (no 64-bit divides
-// per tile): tile = m * n_tiles + n.
-struct TileIter {
-  int64_t tile, m;
-  int n;
-  int64_t step_m;
-  int step_n;
-  __device__ __forceinline__ TileIter(int64_t cid, int64_t ncl, int n_tiles) {
-    tile = cid; m = cid / n_tiles; n = (int)(cid % n_tiles);
-    step_m = ncl / n_tiles; step_n = (int)(ncl % n_tiles);
-  }
-  __device__ __forceinline__ void next(int64_t ncl, int n_tiles) {
-    tile += ncl; m += step_m; n += step_n;
-    if (n >= n_tiles) { n -= n_tiles; m++; }
-  }
-};
-
-// One lane of a fully active warp (the issuing loops run warp-wide so that descriptors and
-// loop state stay warp-uniform, i.e. in uniform registers; only the elected lane issues).
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "elect.sync _|p, 0xffffffff;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(pred));
-  return pred != 0;
-}
 
 template <int ELL, bool SW, int SH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)

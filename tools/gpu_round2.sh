@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 100 python __graft_entry__.py smoke 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | cut -c1-200
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1b.csv python bench.py --profile --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:limb_gemm_2sm -c 1 -o gpurun_out/prof_mask_r1b python bench.py --profile --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+ls gpurun_out
