@@ -45,6 +45,12 @@ class COracle:
         L.oracle_mask_entries.argtypes = [ctypes.c_int, ctypes.c_int, _i8p, ctypes.c_int64,
                                           _u64p, _i64p, _i64p, ctypes.c_int64, _u64p]
         L.oracle_modswitch.argtypes = [_u64p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _u64p]
+        L.oracle_ksk_gen.argtypes = [ctypes.c_int, ctypes.c_int, _u8p, ctypes.c_uint64, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, _u64p, _u64p, ctypes.c_int]
+        L.oracle_decompose.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_int32)]
+        L.oracle_pack.argtypes = [ctypes.c_int, ctypes.c_int, _u64p, _u64p, ctypes.c_int64, _u64p, _u64p,
+                                  ctypes.c_int, ctypes.c_int, _u64p, _u64p, ctypes.c_int]
 
     def chacha20_block(self, key: bytes, counter: int, nonce: bytes) -> bytes:
         k = np.frombuffer(key, np.uint8).copy()
@@ -87,6 +93,30 @@ class COracle:
         out = np.zeros_like(v)
         self.lib.oracle_modswitch(_p(v, _u64p), v.size, q_from, q_to, _p(out, _u64p))
         return out
+
+
+    def ksk_gen(self, params, S, ksk_seed: int, eta: int = 0, base_log: int = 8, levels: int = 3,
+                nthreads: int = 1):
+        N = params.N
+        S = np.ascontiguousarray(S, dtype=np.uint8)
+        KA = np.zeros((levels * N, N), np.uint64)
+        KB = np.zeros((levels * N, N), np.uint64)
+        self.lib.oracle_ksk_gen(N, params.q_in, _p(S, _u8p), ksk_seed, eta, base_log, levels,
+                                _p(KA, _u64p), _p(KB, _u64p), nthreads)
+        return KA, KB
+
+    def pack(self, params, A_lwe, b_lwe, KA, KB, base_log: int = 8, levels: int = 3, nthreads: int = 1):
+        N = params.N
+        A_lwe = np.ascontiguousarray(A_lwe, dtype=np.uint64)
+        b_lwe = np.ascontiguousarray(b_lwe, dtype=np.uint64)
+        d_out = A_lwe.shape[0]
+        G = (d_out + N - 1) // N
+        PA = np.zeros((G, N), np.uint64)
+        PB = np.zeros((G, N), np.uint64)
+        self.lib.oracle_pack(N, params.q_in, _p(A_lwe, _u64p), _p(b_lwe, _u64p), d_out,
+                             _p(np.ascontiguousarray(KA), _u64p), _p(np.ascontiguousarray(KB), _u64p),
+                             base_log, levels, _p(PA, _u64p), _p(PB, _u64p), nthreads)
+        return PA, PB
 
 
 _cached = None

@@ -148,3 +148,124 @@ void oracle_modswitch(const uint64_t *v, int64_t n, int q_from, int q_to, uint64
   for (int64_t k = 0; k < n; k++)
     out[k] = (s == 0) ? v[k] : (((v[k] + (1ull << (s - 1))) >> s) & m);
 }
+
+/* ================= NEXT #1: KeySwitch packing (Eq. 7; Eq. 4; Eq. 8) ========= */
+static void keystream_words(uint64_t seed, const uint8_t nonce[12], uint64_t word0, int64_t n,
+                            uint64_t *out) {
+  uint8_t key[32] = {0}, blk[64];
+  for (int i = 0; i < 8; i++) key[i] = (uint8_t)(seed >> (8 * i));
+  int64_t cur = -1;
+  for (int64_t k = 0; k < n; k++) {
+    uint64_t w = word0 + (uint64_t)k;
+    if ((int64_t)(w / 8) != cur) { cur = (int64_t)(w / 8); oracle_chacha20_block(key, (uint32_t)cur, nonce, blk); }
+    uint64_t v = 0;
+    for (int b = 0; b < 8; b++) v |= (uint64_t)blk[8 * (w % 8) + b] << (8 * b);
+    out[k] = v;
+  }
+}
+
+/* KSK_{i,l} = RLWE_S(S'_i 2^(q-(l+1)B)), row l*N+i; A from nonce "phe-ksk", noise CBD(eta)
+ * from "phe-ksknoise", both in word order (l, i, k) (R18-R20). */
+void oracle_ksk_gen(int N, int q, const uint8_t *S, uint64_t ksk_seed, int eta, int base_log,
+                    int levels, uint64_t *KA, uint64_t *KB, int nthreads) {
+  static const uint8_t n_ksk[12] = {'p', 'h', 'e', '-', 'k', 's', 'k', 0, 0, 0, 0, 0};
+  static const uint8_t n_kno[12] = {'p', 'h', 'e', '-', 'k', 's', 'k', 'n', 'o', 'i', 's', 'e'};
+  uint64_t qm = (q >= 64) ? ~0ull : ((1ull << q) - 1);
+  int64_t rows = (int64_t)levels * N;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 4)
+#endif
+  for (int64_t r = 0; r < rows; r++) {
+    uint64_t *A = KA + r * N, *B = KB + r * N;
+    keystream_words(ksk_seed, n_ksk, (uint64_t)r * N, N, A);
+    for (int k = 0; k < N; k++) A[k] &= qm;
+    for (int k = 0; k < N; k++) { /* (A*S)[k] = sum_n S_n (A[k-n] or -A[k-n+N]) */
+      uint64_t acc = 0;
+      for (int n = 0; n < N; n++)
+        if (S[n]) acc += (k >= n) ? A[k - n] : (0ull - A[k - n + N]);
+      B[k] = acc;
+    }
+    if (eta > 0) {
+      uint64_t *w = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)N);
+      keystream_words(ksk_seed, n_kno, (uint64_t)r * N, N, w);
+      uint64_t m = (1ull << eta) - 1;
+      for (int k = 0; k < N; k++)
+        B[k] += (uint64_t)((int64_t)__builtin_popcountll(w[k] & m) - (int64_t)__builtin_popcountll((w[k] >> eta) & m));
+      free(w);
+    }
+    int l = (int)(r / N), i = (int)(r % N);
+    B[0] += (uint64_t)S[i] << (q - (l + 1) * base_log);
+    for (int k = 0; k < N; k++) B[k] &= qm;
+  }
+}
+
+/* Decomp (Eq. 4): signed balanced digits of the top base_log*levels bits, tail rounded half up. */
+void oracle_decompose(uint64_t v, int q, int base_log, int levels, int32_t *digits) {
+  int tail = q - base_log * levels;
+  uint64_t vr = (v + (tail > 0 ? (1ull << (tail - 1)) : 0)) >> tail;
+  int bits = base_log * levels;
+  if (bits < 64) vr &= (1ull << bits) - 1;
+  for (int l = levels - 1; l >= 0; l--) {
+    int64_t d = (int64_t)(vr & ((1ull << base_log) - 1));
+    vr >>= base_log;
+    if (d >= (1ll << (base_log - 1))) { d -= (1ll << base_log); vr += 1; }
+    digits[l] = (int32_t)d;
+  }
+}
+
+/* Eq. 7 literally for one token: every LWE j is keyswitched (Eq. 4), rotated by j mod N
+ * (X^N = -1), summed into group j / N.  A_lwe [d_out][N], b_lwe [d_out]; PA, PB [G][N]. */
+void oracle_pack(int N, int q, const uint64_t *A_lwe, const uint64_t *b_lwe, int64_t d_out,
+                 const uint64_t *KA, const uint64_t *KB, int base_log, int levels, uint64_t *PA,
+                 uint64_t *PB, int nthreads) {
+  uint64_t qm = (q >= 64) ? ~0ull : ((1ull << q) - 1);
+  int64_t G = (d_out + N - 1) / N;
+  memset(PA, 0, sizeof(uint64_t) * (size_t)(G * N));
+  memset(PB, 0, sizeof(uint64_t) * (size_t)(G * N));
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  for (int64_t g = 0; g < G; g++) {
+    const int64_t jend = ((g + 1) * N < d_out) ? (g + 1) * N : d_out;
+#ifdef _OPENMP
+#pragma omp parallel
+#endif
+    {
+      uint64_t *Ap = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)N);
+      uint64_t *Bp = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)N);
+      uint64_t *accA = (uint64_t *)calloc((size_t)N, sizeof(uint64_t));
+      uint64_t *accB = (uint64_t *)calloc((size_t)N, sizeof(uint64_t));
+      int32_t dg[64];
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+      for (int64_t j = g * N; j < jend; j++) {
+        memset(Ap, 0, sizeof(uint64_t) * (size_t)N);
+        memset(Bp, 0, sizeof(uint64_t) * (size_t)N);
+        Bp[0] = b_lwe[j];
+        for (int i = 0; i < N; i++) {
+          oracle_decompose(A_lwe[j * N + i], q, base_log, levels, dg);
+          for (int l = 0; l < levels; l++) {
+            if (!dg[l]) continue;
+            uint64_t d = (uint64_t)(int64_t)dg[l];
+            const uint64_t *ka = KA + ((int64_t)l * N + i) * N, *kb = KB + ((int64_t)l * N + i) * N;
+            for (int k = 0; k < N; k++) { Ap[k] -= d * ka[k]; Bp[k] -= d * kb[k]; }
+          }
+        }
+        int r = (int)(j - g * N); /* Rotate by X^r and accumulate */
+        for (int k = 0; k < N; k++) {
+          int p = k + r;
+          if (p < N) { accA[p] += Ap[k]; accB[p] += Bp[k]; }
+          else { accA[p - N] -= Ap[k]; accB[p - N] -= Bp[k]; }
+        }
+      }
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+      for (int k = 0; k < N; k++) { PA[g * N + k] += accA[k]; PB[g * N + k] += accB[k]; }
+      free(Ap); free(Bp); free(accA); free(accB);
+    }
+    for (int k = 0; k < N; k++) { PA[g * N + k] &= qm; PB[g * N + k] &= qm; }
+  }
+}

@@ -15,7 +15,10 @@ cross-check against the `cryptography` package; brute-force schoolbook vs numpy
 polynomial convolution folded mod X^N+1; SPEC worked examples; Eq. 2 special cases;
 W = I reduces Eq. 6 to textbook SampleExtract; A = 0 reduces it to a plain integer
 matvec; the E = 0 decryption invariant b - <a,S> = Delta*(W x) mod Q exactly; modulus
-switch worked examples and the 1/2-ULP bound; hand-derived golden vectors.
+switch worked examples and the 1/2-ULP bound; hand-derived golden vectors.  NEXT #1
+(KeySwitch packing): SPEC decomposition examples + exhaustive recomposition; with an exact
+decomposition (B*levels = q) and E = 0 the keyswitch / pack decrypt EXACTLY (algebraic
+identity, independent of the implementation); batched (Eq. 8) == sequential (Eq. 4).
 No function here is "parity unpinned".
 """
 from __future__ import annotations
@@ -400,3 +403,149 @@ def server_matmul(params: Params, W: np.ndarray, seeds: np.ndarray, bodies: np.n
         mask = modswitch(mask, params.q_in, params.q_out)
         body = modswitch(body, params.q_in, params.q_out)
     return mask, body
+
+
+# ======================================================================================
+# NEXT #1: KeySwitch packing of the LWE outputs into RLWE (Eq. 7; Eq. 8)
+# Readings (R18-R21): Decomp = signed balanced base-2^B digits of the top B*levels
+# bits after rounding (TFHE), B = 8, levels = 3; KSK_{i,l} = RLWE_S(S'_i *
+# 2^(q - (l+1)B)); K-index of the batched form = l*N + i (planar).
+# ======================================================================================
+KS_BASE_LOG = 8
+KS_LEVELS = 3
+NONCE_KSK = b"phe-ksk".ljust(12, b"\0")
+NONCE_KSK_NOISE = b"phe-ksknoise"  # exactly 12 bytes
+
+
+def decompose(v: int, q_bits: int, base_log: int = KS_BASE_LOG, levels: int = KS_LEVELS) -> list:
+    """Decomp (Eq. 4): signed digits d_0..d_{levels-1} in [-2^(B-1), 2^(B-1)) with
+    v ~= sum_l d_l 2^(q - (l+1)B) mod 2^q, |error| <= 2^(q - levels*B - 1).
+    Round the discarded tail half up (R8), then peel digits from the least significant one,
+    moving d >= 2^(B-1) to d - 2^B with a carry into the next digit; the last carry is mod q."""
+    tail = q_bits - base_log * levels
+    assert tail >= 0
+    vr = (v + ((1 << (tail - 1)) if tail > 0 else 0)) >> tail
+    vr %= 1 << (base_log * levels)
+    digits = [0] * levels
+    for l in range(levels - 1, -1, -1):
+        d = vr & ((1 << base_log) - 1)
+        vr >>= base_log
+        if d >= 1 << (base_log - 1):
+            d -= 1 << base_log
+            vr += 1
+        digits[l] = d
+    return digits
+
+
+def recompose(digits: list, q_bits: int, base_log: int = KS_BASE_LOG) -> int:
+    return sum(d << (q_bits - (l + 1) * base_log) for l, d in enumerate(digits)) % (1 << q_bits)
+
+
+def ksk_gen(params: Params, S: np.ndarray, ksk_seed: int, eta: int = 0,
+            base_log: int = KS_BASE_LOG, levels: int = KS_LEVELS):
+    """KSK_{i,l} = RLWE_S(S'_i * 2^(q - (l+1)B)) for i in [0,N), l in [0,levels) (P:78-86).
+    A_{i,l} = ChaCha20 words (nonce "phe-ksk") in order (l, i, k) mod 2^q; E_{i,l} = CBD(eta)
+    (nonce "phe-ksk-noise", same order) or 0.  Returns KSK_A, KSK_B as [levels*N][N] uint64
+    with row l*N + i (the batched matrices of Eq. 8)."""
+    N, q = params.N, params.q_in
+    rows = levels * N
+    Aall = keystream_u64(ksk_seed, NONCE_KSK, rows * N).reshape(rows, N) & U64(params.Q - 1)
+    if eta:
+        w = keystream_u64(ksk_seed, NONCE_KSK_NOISE, rows * N)
+        m = (1 << eta) - 1
+        Eall = np.array([bin(int(x) & m).count("1") - bin((int(x) >> eta) & m).count("1") for x in w],
+                        dtype=np.int64).reshape(rows, N)
+    else:
+        Eall = np.zeros((rows, N), np.int64)
+    Ball = np.zeros((rows, N), U64)
+    for l in range(levels):
+        g = 1 << (q - (l + 1) * base_log)
+        for i in range(N):
+            r = l * N + i
+            AS = negacyclic_mul(Aall[r], S.astype(np.int64), q)
+            with np.errstate(over="ignore"):
+                Br = AS + Eall[r].astype(U64)
+                Br[0] += U64(int(S[i]) * g)
+            Ball[r] = Br & U64(params.Q - 1)
+    return Aall, Ball
+
+
+def keyswitch(params: Params, a: np.ndarray, b: int, KA: np.ndarray, KB: np.ndarray,
+              base_log: int = KS_BASE_LOG, levels: int = KS_LEVELS):
+    """Eq. 4 literally: (A', B') = (0, b) - sum_i Decomp(a_i) . KSK_i."""
+    N, q = params.N, params.q_in
+    Ap = [0] * N
+    Bp = [0] * N
+    Bp[0] = int(b)
+    for i in range(N):
+        ds = decompose(int(a[i]), q, base_log, levels)
+        for l, d in enumerate(ds):
+            if d == 0:
+                continue
+            r = l * N + i
+            for k in range(N):
+                Ap[k] -= d * int(KA[r, k])
+                Bp[k] -= d * int(KB[r, k])
+    Q = params.Q
+    return np.array([x % Q for x in Ap], U64), np.array([x % Q for x in Bp], U64)
+
+
+def decomp_matrix(params: Params, A_lwe: np.ndarray, base_log: int = KS_BASE_LOG,
+                  levels: int = KS_LEVELS) -> np.ndarray:
+    """Decomp(A_LWE) of Eq. 8: [d_out][levels*N] int64, column l*N + i = digit l of a_j[i]."""
+    d_out, N = A_lwe.shape
+    D = np.zeros((d_out, levels * N), np.int64)
+    for j in range(d_out):
+        for i in range(N):
+            ds = decompose(int(A_lwe[j, i]), params.q_in, base_log, levels)
+            for l, d in enumerate(ds):
+                D[j, l * N + i] = d
+    return D
+
+
+def keyswitch_batched(params: Params, A_lwe: np.ndarray, b_lwe: np.ndarray, KA: np.ndarray,
+                      KB: np.ndarray, base_log: int = KS_BASE_LOG, levels: int = KS_LEVELS):
+    """Eq. 8: A_RLWE = 0 - Decomp(A_LWE) KSK_A, B_RLWE = b - Decomp(A_LWE) KSK_B (P:240-246).
+    Row j of the result is the RLWE ciphertext of keyswitch(LWE_j) with b_j in coefficient 0."""
+    D = decomp_matrix(params, A_lwe, base_log, levels).astype(object)
+    Q = params.Q
+    PA = (D @ KA.astype(object)) % Q
+    PB = (D @ KB.astype(object)) % Q
+    A_r = np.array((-PA) % Q, dtype=U64)
+    B_r = (-PB) % Q
+    B_r[:, 0] = (B_r[:, 0] + b_lwe.astype(object)) % Q
+    return A_r, np.array(B_r, dtype=U64)
+
+
+def pack_lwes(params: Params, A_lwe: np.ndarray, b_lwe: np.ndarray, KA: np.ndarray, KB: np.ndarray,
+              out_bits: int | None = None, batched: bool = True):
+    """Eq. 7: for each group g of up to N consecutive outputs,
+    RLWE_g = sum_j Rotate(KeySwitch(LWE_j), j - gN); then ModulusSwitch to q_out.
+    Returns (A [G][N], B [G][N]) uint64."""
+    d_out, N = A_lwe.shape
+    q = params.q_in
+    G = (d_out + N - 1) // N
+    if batched:
+        Ar, Br = keyswitch_batched(params, A_lwe, b_lwe, KA, KB)
+    else:
+        pairs = [keyswitch(params, A_lwe[j], int(b_lwe[j]), KA, KB) for j in range(d_out)]
+        Ar = np.stack([p[0] for p in pairs])
+        Br = np.stack([p[1] for p in pairs])
+    PA = np.zeros((G, N), U64)
+    PB = np.zeros((G, N), U64)
+    with np.errstate(over="ignore"):
+        for j in range(d_out):
+            g, r = divmod(j, N)
+            PA[g] = (PA[g] + rotate(Ar[j], r, q)) & U64(params.Q - 1)
+            PB[g] = (PB[g] + rotate(Br[j], r, q)) & U64(params.Q - 1)
+    if out_bits is not None and out_bits != q:
+        PA, PB = modswitch(PA, q, out_bits), modswitch(PB, q, out_bits)
+    return PA, PB
+
+
+def decrypt_packed(params: Params, A: np.ndarray, B: np.ndarray, S: np.ndarray, q_bits: int) -> np.ndarray:
+    """RLWE decryption of a packed output: phase = B - A*S, decode per coefficient."""
+    AS = negacyclic_mul(A, S.astype(np.int64), q_bits)
+    with np.errstate(over="ignore"):
+        phi = (B.astype(U64) - AS) & U64((1 << q_bits) - 1)
+    return np.array([decode(int(p), q_bits, params.beta) for p in phi], dtype=np.int64)
