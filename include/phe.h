@@ -166,6 +166,37 @@ int phe_server_matvec_host(const phe_params *p, const void *d_wprep, int64_t d_o
                            int64_t chunk_tokens, uint32_t *h_out_mask, uint32_t *h_out_body,
                            void *stream);
 
+/* ---- NEXT #1: KeySwitch packing of the LWE outputs into RLWE (Eq. 7; Eq. 8,
+ * P:233-249) --------------------------------------------------------------------------------
+ * Gadget: Decomp = signed balanced base-2^8 digits of the top 24 bits (3 levels) after rounding
+ * the q_in - 24 bit tail half up (R18).  Requires q_in > 24.
+ * KSK_{i,l} = RLWE_S(S'_i * 2^(q_in - 8(l+1))) for i < N, l < 3.
+ *
+ * phe_ksk_gen (client): d_ksk = uint64 [2][3N][N]: part 0 = KSK_A, part 1 = KSK_B, row l*N + i
+ *   (the batched matrices of Eq. 8).  Masks from ChaCha20(ksk_seed, "phe-ksk"), noise CBD(eta)
+ *   from "phe-ksknoise" (R19).  Public key material: the server may hold it.            */
+size_t phe_ksk_bytes(const phe_params *p);
+int phe_ksk_gen(const phe_params *p, const uint8_t *d_S, uint64_t ksk_seed, void *d_ksk,
+                size_t bytes, void *stream);
+/* phe_ksk_prepare (server, once per key): KSK limb planes, the B operand of the packing GEMM
+ * (uint8 [rows][3N], rows = phe_ksk_prep_bytes / 3N).                                      */
+size_t phe_ksk_prep_bytes(const phe_params *p);
+int phe_ksk_prepare(const phe_params *p, const void *d_ksk, void *d_kprep, size_t bytes, void *stream);
+/* phe_matmul_clear_packed (server): the paper's whole primitive RLWE(Wx) for T tokens:
+ *   LWE outputs of Eq. 6 (mask GEMM writing Decomp digits, body GEMM at q_in), then Eq. 8 +
+ *   Eq. 7 (packing GEMM: KeySwitch, Rotate by j mod N, sum), then ModulusSwitch to q_out.
+ *   d_out_packed: uint32 [T][G][2][N], G = ceil(R / N), R = rows of M (d_out, or d_in with
+ *   transpose = 1); [..][0][..] = A', [..][1][..] = B'; output j sits in coefficient j mod N
+ *   of ciphertext j / N.  d_ws: workspace of phe_packed_ws_bytes(p, R, T) bytes.
+ *   Errors: EUNSUPPORTED unless ell in {4,5}, N % 256 == 0, q_in > 24.                       */
+size_t phe_packed_ws_bytes(const phe_params *p, int64_t rows, int64_t T);
+int phe_matmul_clear_packed(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                            int transpose, const void *d_operand, int64_t T, const void *d_kprep,
+                            void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream);
+/* phe_decrypt_packed (client): d_y int32 [T][rows] = decode(B' - A'S) coefficient-wise. */
+int phe_decrypt_packed(const phe_params *p, const uint8_t *d_S, const uint32_t *d_packed, int64_t T,
+                       int64_t rows, int32_t q_bits, int32_t *d_y, void *stream);
+
 /* ---- introspection (tests / bench) -------------------------------------------------- */
 /* Number of kernel launches the last phe_matmul_clear[_T] on this thread enqueued. */
 int phe_last_launch_count(void);

@@ -29,6 +29,8 @@ EXPORTS = [
     "phe_weights_prepare", "phe_ct_operand_bytes", "phe_ct_prepare", "phe_matmul_clear",
     "phe_matmul_clear_T", "phe_modswitch", "phe_decrypt_unpack", "phe_server_matvec_host",
     "phe_last_launch_count", "phe_matmul_clear_simt",
+    "phe_ksk_bytes", "phe_ksk_gen", "phe_ksk_prep_bytes", "phe_ksk_prepare", "phe_packed_ws_bytes",
+    "phe_matmul_clear_packed", "phe_decrypt_packed",
 ]
 
 
@@ -87,6 +89,14 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_decrypt_unpack": ([_P, _vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp], ctypes.c_int),
         "phe_server_matvec_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64,
                                     _i64, _vp, _vp, _vp], ctypes.c_int),
+        "phe_ksk_bytes": ([_P], _sz),
+        "phe_ksk_gen": ([_P, _vp, _u64, _vp, _sz, _vp], ctypes.c_int),
+        "phe_ksk_prep_bytes": ([_P], _sz),
+        "phe_ksk_prepare": ([_P, _vp, _vp, _sz, _vp], ctypes.c_int),
+        "phe_packed_ws_bytes": ([_P, _i64, _i64], _sz),
+        "phe_matmul_clear_packed": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp, _vp, _sz, _vp, _vp],
+                                    ctypes.c_int),
+        "phe_decrypt_packed": ([_P, _vp, _vp, _i64, _i64, _i32, _vp, _vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -278,3 +288,56 @@ def server_matvec_host(p: Params, w: Weights, h_seeds: torch.Tensor, h_body: tor
 
 def last_launch_count() -> int:
     return load().phe_last_launch_count()
+
+
+# ------------------------------------------------------------------ NEXT #1: KeySwitch packing
+def ksk_gen(p: Params, S: torch.Tensor, ksk_seed: int) -> torch.Tensor:
+    """Client: KSK_A, KSK_B as int64 [2][3N][N] (u64 bits), row l*N + i (Eq. 8's matrices)."""
+    _dev(S, torch.uint8, "S")
+    ksk = torch.empty((2, 3 * p.N, p.N), dtype=torch.int64, device=S.device)
+    _check(load().phe_ksk_gen(ctypes.byref(p), _ptr(S), ksk_seed & (2**64 - 1), _ptr(ksk), ksk.numel() * 8,
+                              _stream()), "phe_ksk_gen")
+    return ksk
+
+
+class KeySwitchKey:
+    """Server-side registration of a KSK (limb planes for the packing GEMM)."""
+
+    def __init__(self, p: Params, ksk: torch.Tensor):
+        _dev(ksk, torch.int64, "ksk")
+        self.p = p
+        nbytes = load().phe_ksk_prep_bytes(ctypes.byref(p))
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=ksk.device)
+        _check(load().phe_ksk_prepare(ctypes.byref(p), _ptr(ksk), _ptr(self.buf), nbytes, _stream()),
+               "phe_ksk_prepare")
+
+
+_ws_cache = {}
+
+
+def matmul_clear_packed(p: Params, w: Weights, operand: torch.Tensor, T: int, ksk: KeySwitchKey,
+                        out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """RLWE(Wx) (Eq. 7 + Eq. 8): int32 [T][G][2][N] (A', B' at q_out), G = ceil(rows / N)."""
+    G = (w.rows + p.N - 1) // p.N
+    if out is None:
+        out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=operand.device)
+    nbytes = load().phe_packed_ws_bytes(ctypes.byref(p), w.rows, T)
+    if ws is None:
+        ws = _ws_cache.get(operand.device)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=operand.device)
+            _ws_cache[operand.device] = ws
+    _check(load().phe_matmul_clear_packed(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
+                                          _ptr(operand), T, _ptr(ksk.buf), _ptr(ws), ws.numel(), _ptr(out),
+                                          _stream()), "phe_matmul_clear_packed")
+    return out
+
+
+def decrypt_packed(p: Params, S: torch.Tensor, packed: torch.Tensor, rows: int, q_bits: int | None = None):
+    _dev(S, torch.uint8, "S"); _dev(packed, torch.int32, "packed")
+    q_bits = p.q_out if q_bits is None else q_bits
+    T = packed.shape[0]
+    y = torch.empty((T, rows), dtype=torch.int32, device=packed.device)
+    _check(load().phe_decrypt_packed(ctypes.byref(p), _ptr(S), _ptr(packed), T, rows, q_bits, _ptr(y), _stream()),
+           "phe_decrypt_packed")
+    return y

@@ -424,10 +424,15 @@ __device__ __forceinline__ void dbg_add(int i, long long v) { atomicAdd(&g_dbg_c
 constexpr int B_HALF_MAX = (BN / 2) * BK;     // 16 KB per stage per CTA
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;   // clears the peer bit: addresses CTA 0's barrier
 constexpr int EPI_TOK = 16;                   // tokens per epilogue chunk
-template <bool SW> struct Cfg2 {
-  using OutT = typename std::conditional<SW, uint32_t, unsigned long long>::type;
-  static constexpr int STAGES = SW ? 8 : 6;
-  static constexpr int OUT_BUF = EPI_TOK * BM * (int)sizeof(OutT);  // 8 KB (u32) / 16 KB (u64)
+// Output modes of the 2-CTA mask kernel.
+constexpr int OUT_U64 = 0;  // raw LWE masks mod 2^q_in (uint64)
+constexpr int OUT_U32 = 1;  // modulus-switched to q_out (uint32), the hot-path product
+constexpr int OUT_DIG = 2;  // Decomp(A_LWE) digits for KeySwitch packing (Eq. 8): 3 int8 planes
+template <int MODE> struct Cfg2 {
+  using OutT = typename std::conditional<MODE == OUT_U64, unsigned long long,
+               typename std::conditional<MODE == OUT_U32, uint32_t, uint8_t>::type>::type;
+  static constexpr int STAGES = MODE == OUT_U64 ? 6 : 8;
+  static constexpr int OUT_BUF = EPI_TOK * BM * (MODE == OUT_DIG ? 3 : (int)sizeof(OutT));  // 8/16/6 KB
   static constexpr int SMEM = 1024 + STAGES * (B_HALF_MAX + 4096) + 4 * OUT_BUF + 256;
 };
 
@@ -451,6 +456,13 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t sr
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(src), "r"(x), "r"(y), "r"(z)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, uint32_t src, int x, int y, int z, int w) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y), "r"(z), "r"(w)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -514,13 +526,14 @@ __device__ __forceinline__ uint64_t kblock_mask(const KArgs &ka, int tp) {
 }
 __device__ __forceinline__ bool kb_issue(uint64_t m, int kb) { return kb >= 64 || ((m >> kb) & 1ull); }
 
-template <int ELL, bool SW, int SH>
+template <int ELL, int MODE, int SH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const __grid_constant__ CUtensorMap map_out,
                      const __grid_constant__ CUtensorMap map_out_tail, KArgs ka) {
-  using C2 = Cfg2<SW>;
+  using C2 = Cfg2<MODE>;
   using OutT = typename C2::OutT;
+  constexpr bool SW = MODE != OUT_U64;  // OUT_DIG shifts by q_in - 24 (ka.out_bits = 24)
   constexpr int S = C2::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -648,6 +661,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     const uint64_t omask = mask_bits(ka.out_bits);
     const uint32_t tempty_c0 = smem_u32(&tempty[0]) & PEER_MASK;
     OutT *const obuf = reinterpret_cast<OutT *>(sO + grp * 2 * C2::OUT_BUF);
+    constexpr int OB_ELEMS = C2::OUT_BUF / (int)sizeof(OutT);
     int acc = 0; uint32_t aph = 0; int nbuf = 0; int64_t iter = 0;
     for (TileIter it(cid, ncl, ka.n_tiles); it.tile < total; it.next(ncl, ka.n_tiles), iter++) {
       const int n_tile = it.n;
@@ -678,21 +692,31 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
           mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)acc);
           arrived = true;
         }
-        OutT *ob = obuf + nbuf * (EPI_TOK * BM);
+        OutT *ob = obuf + nbuf * OB_ELEMS;
         named_bar(1 + grp, 128);  // the store that last read buffer nbuf has drained
-        if (ka.dbg == 7) {  // experiment: compute only
-          OutT x = 0;
+        if (ka.dbg != 1) {
+          if constexpr (MODE == OUT_DIG) {
+            // r = top 24 bits of v after rounding (tail q_in - 24); signed base-2^8 digits, least
+            // significant first with carry (Decomp, Eq. 4 / S:59-67); planes [tk][l][t]
+            uint8_t *od = reinterpret_cast<uint8_t *>(ob);
 #pragma unroll
-          for (int tk = 0; tk < EPI_TOK; tk++) x ^= finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask);
-          if (x == (OutT)0x9e3779b9u) ob[row] = x;
-        } else if (ka.dbg == 8) {  // experiment: stores of raw limbs, no compute
+            for (int tk = 0; tk < EPI_TOK; tk++) {
+              uint32_t r;
+              if constexpr (SH > 0) r = finish_sw<ELL, SH>(&v[tk * ELL], 0xFFFFFFu);
+              else r = (uint32_t)finish<ELL, true, uint32_t>(&v[tk * ELL], half, shift, 0xFFFFFFull);
+              int d2 = (int)(r & 255u); r >>= 8; if (d2 >= 128) { d2 -= 256; r += 1; }
+              int d1 = (int)(r & 255u); r >>= 8; if (d1 >= 128) { d1 -= 256; r += 1; }
+              int d0 = (int)(r & 255u);
+              od[(tk * 3 + 0) * BM + row] = (uint8_t)d0;
+              od[(tk * 3 + 1) * BM + row] = (uint8_t)d1;
+              od[(tk * 3 + 2) * BM + row] = (uint8_t)d2;
+            }
+          } else {
 #pragma unroll
-          for (int tk = 0; tk < EPI_TOK; tk++) ob[tk * BM + row] = (OutT)v[tk * ELL];
-        } else if (ka.dbg != 1) {
-#pragma unroll
-          for (int tk = 0; tk < EPI_TOK; tk++) {
-            if constexpr (SW && SH > 0) ob[tk * BM + row] = (OutT)finish_sw<ELL, SH>(&v[tk * ELL], (uint32_t)omask);
-            else ob[tk * BM + row] = finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask);
+            for (int tk = 0; tk < EPI_TOK; tk++) {
+              if constexpr (SW && SH > 0) ob[tk * BM + row] = (OutT)finish_sw<ELL, SH>(&v[tk * ELL], (uint32_t)omask);
+              else ob[tk * BM + row] = finish<ELL, SW, OutT>(&v[tk * ELL], half, shift, omask);
+            }
           }
         }
         fence_proxy_async_smem();
@@ -700,7 +724,10 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         if (issuer) {
           // a full 16-token box, or the tpt % 16 tail box of this tile (never past the tile)
           const CUtensorMap *mo = (c0 + EPI_TOK <= ka.tpt) ? &map_out : &map_out_tail;
-          if (ka.dbg == 0 || ka.dbg == 4) tma_store_3d(mo, smem_u32(ob), tb, jr, tau0 + c0);
+          if (ka.dbg == 0 || ka.dbg == 4) {
+            if constexpr (MODE == OUT_DIG) tma_store_4d(mo, smem_u32(ob), tb, 0, jr, tau0 + c0);
+            else tma_store_3d(mo, smem_u32(ob), tb, jr, tau0 + c0);
+          }
           bulk_wait_read_1();
         }
         nbuf ^= 1;
@@ -713,6 +740,195 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
     if (issuer) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == W_TMEM) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ KeySwitch packing GEMM (NEXT #1)
+// Eq. 8 + the rotate-and-sum of Eq. 7 for T tokens at once:
+//   C[(tau,j), (part,k)] = sum_{(l,i)} Decomp(a_{tau,j})[l*N+i] * KSK_part[l*N+i][k]   (mod 2^q)
+// as an int8 (digits) x u8 (KSK limbs) GEMM on tcgen05 cta_group::2: M = rows (tau, j) (256
+// per pair), N = 51 coefficient slots x 5 limbs, K = 3N.  The epilogue recombines limbs and
+// applies Rotate(., j mod N) + the sum over j of Eq. 7 in shared-memory bins (a CTA's 128 rows
+// and 51 slots land on 178 consecutive output coefficients), then reduces the bins into the
+// packed accumulator [T][G][part][N] (uint64, mod 2^64) with global atomics.
+struct PArgs {
+  int N;
+  int kpad;           // coefficient slots per part = ceil(N / spt) * spt
+  int spt;            // slots per tile = floor(256 / ell)
+  int n_tiles;        // 2 * kpad / spt
+  int tpt_rows;       // 256-row tiles per token = rows_pad / 256
+  int64_t rows_pad;   // digit rows per token (multiple of 256)
+  int G;              // output RLWE groups per token = ceil(R / N)
+  int64_t total_tiles;
+  int k_blocks;       // 3N / BK
+  unsigned long long *acc;
+};
+constexpr int PK_STAGES = 6;
+constexpr int PK_A_BYTES = BM * BK;            // 16 KB per CTA per stage (digit rows)
+constexpr int PK_B_BYTES = (BN / 2) * BK;      // 16 KB per CTA per stage (KSK limb rows)
+constexpr int PK_BINS = 184;                   // >= spt + BM - 1
+constexpr int PK_SMEM = 1024 + PK_STAGES * (PK_A_BYTES + PK_B_BYTES) + 2 * PK_BINS * 8 + 256;
+
+template <int ELL>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+pack_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                     PArgs pa) {
+  constexpr int S = PK_STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  uint8_t *sB = smem;
+  uint8_t *sA = smem + S * PK_B_BYTES;
+  unsigned long long *bins = reinterpret_cast<unsigned long long *>(sA + S * PK_A_BYTES);  // [2][PK_BINS]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(bins + 2 * PK_BINS);
+  uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+
+  for (int i = threadIdx.x; i < 2 * PK_BINS; i += blockDim.x) bins[i] = 0ull;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * NUM_EPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == W_PROD && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == W_TMEM) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int64_t total = pa.total_tiles;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == W_PROD) {
+    int s = 0; uint32_t ph = 0;
+    const uint32_t tx = (uint32_t)(2 * (PK_A_BYTES + PK_B_BYTES));
+    for (TileIter it(cid, ncl, pa.n_tiles); it.tile < total; it.next(ncl, pa.n_tiles)) {
+      const int tau = (int)((uint64_t)it.m / (uint64_t)pa.tpt_rows);
+      const int64_t j0 = (it.m - (int64_t)tau * pa.tpt_rows) * (2 * BM);
+      const int64_t arow = (int64_t)tau * pa.rows_pad + j0 + (int)crank * BM;
+      const int brow = it.n * pa.spt * ELL + (int)crank * (BN / 2);
+      for (int kb = 0; kb < pa.k_blocks; kb++) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (elect_one()) {
+          if (leader) mbar_expect_tx(&full[s], tx);
+          const uint32_t fb = smem_u32(&full[s]) & PEER_MASK;
+          tma_load_2d_2sm(smem_u32(sA + s * PK_A_BYTES), &map_a, kb * BK, (int)arow, fb);
+          tma_load_2d_2sm(smem_u32(sB + s * PK_B_BYTES), &map_b, kb * BK, brow, fb);
+        }
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == W_MMA) {
+    if (leader) {
+      const uint32_t idesc = idesc_i8(2 * BM, BN);
+      int s = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
+      for (int64_t tile = cid; tile < total; tile += ncl) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < pa.k_blocks; kb++) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * PK_A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + s * PK_B_BYTES);
+          if (elect_one()) {
+#pragma unroll
+            for (int q = 0; q < BK / UK; q++)
+              mma_i8_2sm(d_tmem, desc_sw128(a_addr + 32 * q), desc_sw128(b_addr + 32 * q), idesc,
+                         (kb | q) != 0 ? 1u : 0u);
+            tc_commit_mc2(&empty[s]);
+          }
+          __syncwarp();
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        if (elect_one()) tc_commit_mc2(&tfull[acc]);
+        __syncwarp();
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp < 8) {
+    // ===== epilogue: recombine limbs, Rotate(., j mod N) + sum over j into bins, reduce =====
+    const int q4 = warp & 3, grp = warp >> 2;
+    const int row = q4 * 32 + lane;  // this CTA's row = TMEM lane
+    const int etid = threadIdx.x;    // 0..255 (epilogue warps are 0-7)
+    const uint32_t tempty_c0 = smem_u32(&tempty[0]) & PEER_MASK;
+    const int nchunks = (pa.spt + EPI_TOK - 1) / EPI_TOK;
+    int acc = 0; uint32_t aph = 0; int64_t iter = 0;
+    for (TileIter it(cid, ncl, pa.n_tiles); it.tile < total; it.next(ncl, pa.n_tiles), iter++) {
+      const int tau = (int)((uint64_t)it.m / (uint64_t)pa.tpt_rows);
+      const int64_t jc = (it.m - (int64_t)tau * pa.tpt_rows) * (2 * BM) + (int)crank * BM;
+      const int g = (int)(jc / pa.N);
+      const int r_c0 = (int)(jc - (int64_t)g * pa.N);  // rotation of this CTA's first row
+      const int slot0 = it.n * pa.spt;
+      const int part = slot0 / pa.kpad;
+      const int k0 = slot0 - part * pa.kpad;
+      unsigned long long *bn = bins + acc * PK_BINS;
+      const int first = (grp + (int)(iter & 1)) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN);
+      bool arrived = false;
+      for (int c = first; c < nchunks; c += 2) {
+        const int c0 = c * EPI_TOK;
+        const int nt = min(EPI_TOK, pa.spt - c0);
+        const int nloads = (nt * ELL + 15) / 16;
+        uint32_t v[EPI_TOK * ELL];
+#pragma unroll
+        for (int q = 0; q < ELL; q++)
+          if (q < nloads) tmem_ld16(tbase + (uint32_t)(c0 * ELL + 16 * q), &v[16 * q]);
+        tmem_wait_ld();
+        if (c + 2 >= nchunks) {
+          tc_fence_before();
+          mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)acc);
+          arrived = true;
+        }
+#pragma unroll
+        for (int tk = 0; tk < EPI_TOK; tk++) {
+          if (tk < nt && k0 + c0 + tk < pa.N) {
+            uint64_t x = 0;
+#pragma unroll
+            for (int l = 0; l < ELL; l++) x += (uint64_t)(int64_t)(int32_t)v[tk * ELL + l] << (8 * l);
+            if (x) atomicAdd(&bn[c0 + tk + row], (unsigned long long)x);  // p = k + r, unwrapped
+          }
+        }
+      }
+      if (!arrived) {
+        tc_fence_before();
+        mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)acc);
+      }
+      named_bar(1, NUM_EPI);  // all slots of this tile are in the bins
+      for (int t = etid; t < pa.spt + BM - 1; t += NUM_EPI) {
+        unsigned long long val = bn[t];
+        if (val) {
+          bn[t] = 0ull;
+          int p = k0 + r_c0 + t;                 // X^N = -1: p >= N wraps with a sign flip
+          if (p >= pa.N) { p -= pa.N; val = 0ull - val; }
+          atomicAdd(pa.acc + (((int64_t)tau * pa.G + g) * 2 + part) * pa.N + p, val);
+        }
+      }
+      // bins[acc] is reused two tiles later, after the next tile's named barrier
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -795,11 +1011,11 @@ static int dispatch_ell(int ell, const CUtensorMap &ma, const CUtensorMap &mb, c
 }
 
 
-template <int ELL, bool SW, int SH>
+template <int ELL, int MODE, int SH>
 static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo,
                       const CUtensorMap &mot, const KArgs &ka, cudaStream_t st) {
-  auto kern = limb_gemm_2sm_kernel<ELL, SW, SH>;
-  constexpr int smem = Cfg2<SW>::SMEM;
+  auto kern = limb_gemm_2sm_kernel<ELL, MODE, SH>;
+  constexpr int smem = Cfg2<MODE>::SMEM;
   static thread_local bool set = false;
   if (!set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -823,15 +1039,16 @@ static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtens
   return PHE_OK;
 }
 
-template <bool SW>
+template <int MODE>
 static int dispatch_2sm(int ell, const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo,
                         const CUtensorMap &mot, const KArgs &ka, cudaStream_t st) {
   const int sh = ka.q_in - ka.out_bits;
-  if (SW && ell == 5 && sh == 13) return launch_2sm<5, SW, 13>(ma, mb, mo, mot, ka, st);  // Table 1
-  if (SW && ell == 4 && sh == 4) return launch_2sm<4, SW, 4>(ma, mb, mo, mot, ka, st);    // toy
+  if (MODE != OUT_U64 && ell == 5 && sh == 13) return launch_2sm<5, MODE, 13>(ma, mb, mo, mot, ka, st);  // Table 1
+  if (MODE != OUT_U64 && ell == 5 && sh == 15) return launch_2sm<5, MODE, 15>(ma, mb, mo, mot, ka, st);  // digits, q=39
+  if (MODE != OUT_U64 && ell == 4 && sh == 4) return launch_2sm<4, MODE, 4>(ma, mb, mo, mot, ka, st);    // toy
   switch (ell) {
-    case 4: return launch_2sm<4, SW, 0>(ma, mb, mo, mot, ka, st);
-    case 5: return launch_2sm<5, SW, 0>(ma, mb, mo, mot, ka, st);
+    case 4: return launch_2sm<4, MODE, 0>(ma, mb, mo, mot, ka, st);
+    case 5: return launch_2sm<5, MODE, 0>(ma, mb, mo, mot, ka, st);
   }
   return PHE_EUNSUPPORTED;
 }
@@ -845,6 +1062,19 @@ static int choose_tpt(int64_t T, int ell, int *n_mma) {
   if (n < 32) n = 32;
   *n_mma = n;
   return tpt;
+}
+
+static int make_map_digits(CUtensorMap *m, void *base, int64_t N, int64_t Rpad, int64_t T, int box_tok) {
+  auto enc = get_encode();
+  if (!enc) return PHE_ECUDA;
+  cuuint64_t dims[4] = {(cuuint64_t)N, 3, (cuuint64_t)Rpad, (cuuint64_t)T};
+  cuuint64_t strides[3] = {(cuuint64_t)N, (cuuint64_t)(3 * N), (cuuint64_t)(3 * N * Rpad)};
+  cuuint32_t box[4] = {(cuuint32_t)BM, 3, 1, (cuuint32_t)box_tok};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? PHE_OK : PHE_EINVAL;
 }
 
 static int make_map_out(CUtensorMap *m, void *base, bool sw, int64_t N, int64_t R, int64_t T, int box_tok) {
@@ -921,15 +1151,26 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
     km.m_tiles = R * km.tb_per_row;
     km.total_tiles = km.m_tiles * km.n_tiles;
     km.out = a.out_mask;
+    if (a.digits && !two_sm) return PHE_EUNSUPPORTED;
     if (two_sm) {
-      rc = make_map_out(&mo, a.out_mask, sw, N, R, a.T, EPI_TOK);
-      if (rc) return rc;
+      const int tail = km.tpt % EPI_TOK ? km.tpt % EPI_TOK : EPI_TOK;
       CUtensorMap mot;
-      rc = make_map_out(&mot, a.out_mask, sw, N, R, a.T, km.tpt % EPI_TOK ? km.tpt % EPI_TOK : EPI_TOK);
+      if (a.digits) {
+        rc = make_map_digits(&mo, a.out_mask, N, a.digit_rows, a.T, EPI_TOK);
+        if (!rc) rc = make_map_digits(&mot, a.out_mask, N, a.digit_rows, a.T, tail);
+      } else {
+        rc = make_map_out(&mo, a.out_mask, sw, N, R, a.T, EPI_TOK);
+        if (!rc) rc = make_map_out(&mot, a.out_mask, sw, N, R, a.T, tail);
+      }
       if (rc) return rc;
       unsigned long long zero[8] = {0};
       if (km.dbg == 4) cudaMemcpyToSymbolAsync(g_dbg_cnt, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
-      rc = sw ? dispatch_2sm<true>(ell, ma, mb, mo, mot, km, st) : dispatch_2sm<false>(ell, ma, mb, mo, mot, km, st);
+      if (a.digits) {
+        km.out_bits = a.kp.q_in - 24 >= 1 ? 24 : a.kp.q_in;  // digits keep the top 24 bits
+        rc = dispatch_2sm<OUT_DIG>(ell, ma, mb, mo, mot, km, st);
+      } else {
+        rc = sw ? dispatch_2sm<OUT_U32>(ell, ma, mb, mo, mot, km, st) : dispatch_2sm<OUT_U64>(ell, ma, mb, mo, mot, km, st);
+      }
       if (km.dbg == 4) {
         unsigned long long c[8];
         cudaMemcpyFromSymbolAsync(c, g_dbg_cnt, sizeof(c), 0, cudaMemcpyDeviceToHost, st);
@@ -946,6 +1187,56 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
     if (rc) return rc;
     (*n_launches)++;
   }
+  return PHE_OK;
+}
+
+// ------------------------------------------------------------------ packing GEMM launcher
+int launch_pack_gemm(const PackArgs &a, cudaStream_t st) {
+  using namespace tc;
+  const int N = a.N, ell = a.ell;
+  if (a.T == 0) return PHE_OK;
+  if (ell != 5 && ell != 4) return PHE_EUNSUPPORTED;
+  if (N % (2 * BM) != 0 || a.rows_pad % (2 * BM) != 0) return PHE_EUNSUPPORTED;
+  PArgs pa{};
+  pa.N = N;
+  pa.spt = BN / ell;
+  pa.kpad = (N + pa.spt - 1) / pa.spt * pa.spt;
+  pa.n_tiles = 2 * pa.kpad / pa.spt;
+  pa.rows_pad = a.rows_pad;
+  pa.tpt_rows = (int)(a.rows_pad / (2 * BM));
+  pa.G = a.G;
+  pa.total_tiles = (int64_t)a.T * pa.tpt_rows * pa.n_tiles;
+  pa.k_blocks = 3 * N / BK;
+  pa.acc = static_cast<unsigned long long *>(a.acc);
+  CUtensorMap ma, mb;
+  int rc = make_map_2d(&ma, a.digits, (uint64_t)(3 * N), (uint64_t)(a.T * a.rows_pad), (uint64_t)(3 * N), BK, BM,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  rc = make_map_2d(&mb, a.kplanes, (uint64_t)(3 * N), (uint64_t)a.kplane_rows, (uint64_t)(3 * N), BK, BN / 2,
+                   CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  auto kern = ell == 5 ? pack_gemm_2sm_kernel<5> : pack_gemm_2sm_kernel<4>;
+  static thread_local bool set5 = false, set4 = false;
+  bool &set = ell == 5 ? set5 : set4;
+  if (!set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PK_SMEM) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+    set = true;
+  }
+  int64_t pairs = num_sms() / 2;
+  if (pa.total_tiles < pairs) pairs = pa.total_tiles;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = PK_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, pa) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+  PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
 }
 

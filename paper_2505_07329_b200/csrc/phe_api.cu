@@ -324,3 +324,133 @@ int phe_server_matvec_host(const phe_params *p, const void *d_wprep, int64_t d_o
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ NEXT #1: packing
+static inline int ks_spt(int ell) { return 256 / ell; }
+static inline int64_t ks_kpad(const phe_params *p) {
+  int spt = ks_spt((p->q_in + 7) / 8);
+  return (p->N + spt - 1) / spt * spt;
+}
+static inline int64_t ks_plane_rows(const phe_params *p) {
+  int ell = (p->q_in + 7) / 8, spt = ks_spt(ell);
+  int64_t n_tiles = 2 * ks_kpad(p) / spt;
+  return round_up(n_tiles * spt * ell + 1, 256);
+}
+static int check_pack(const phe_params *p, KParams *kp) {
+  int rc = check_gpu(p, kp);
+  if (rc) return rc;
+  if (p->q_in <= 24 || (kp->ell != 4 && kp->ell != 5) || p->N % 256) return PHE_EUNSUPPORTED;
+  return PHE_OK;
+}
+
+extern "C" {
+
+size_t phe_ksk_bytes(const phe_params *p) {
+  return p ? (size_t)2 * 3 * p->N * (size_t)p->N * 8 : 0;
+}
+
+int phe_ksk_gen(const phe_params *p, const uint8_t *d_S, uint64_t ksk_seed, void *d_ksk, size_t bytes,
+                void *stream) {
+  KParams kp;
+  int rc = check_pack(p, &kp);
+  if (rc) return rc;
+  if (!d_S || !d_ksk) return PHE_EINVAL;
+  if (bytes < phe_ksk_bytes(p)) return PHE_ENOMEM;
+  uint64_t *KA = static_cast<uint64_t *>(d_ksk), *KB = KA + (int64_t)3 * p->N * p->N;
+  return phe::launch_ksk_gen(kp, d_S, ksk_seed, KA, KB, S(stream));
+}
+
+size_t phe_ksk_prep_bytes(const phe_params *p) {
+  return p ? (size_t)ks_plane_rows(p) * 3 * (size_t)p->N : 0;
+}
+
+int phe_ksk_prepare(const phe_params *p, const void *d_ksk, void *d_kprep, size_t bytes, void *stream) {
+  KParams kp;
+  int rc = check_pack(p, &kp);
+  if (rc) return rc;
+  if (!d_ksk || !d_kprep) return PHE_EINVAL;
+  if (bytes < phe_ksk_prep_bytes(p)) return PHE_ENOMEM;
+  return phe::launch_ksk_planes(kp, static_cast<const uint64_t *>(d_ksk), (int)ks_kpad(p), ks_plane_rows(p),
+                                static_cast<uint8_t *>(d_kprep), S(stream));
+}
+
+size_t phe_packed_ws_bytes(const phe_params *p, int64_t rows, int64_t T) {
+  if (!p || rows < 1 || T < 0) return 0;
+  const int64_t N = p->N, rp = round_up(rows, 256), G = (rows + N - 1) / N;
+  return (size_t)(round_up(T * rp * 3 * N, 256) + round_up(T * rows * 8, 256) + round_up(T * G * 2 * N * 8, 256));
+}
+
+int phe_matmul_clear_packed(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                            int transpose, const void *d_operand, int64_t T, const void *d_kprep,
+                            void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_pack(p, &kp);
+  if (rc) return rc;
+  if (d_out < 1 || d_in < 1 || T < 0 || (transpose != 0 && transpose != 1)) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_wprep || !d_operand || !d_kprep || !d_ws || !d_out_packed) return PHE_EINVAL;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  if (ws_bytes < phe_packed_ws_bytes(p, rows, T)) return PHE_ENOMEM;
+  const int64_t N = p->N, rp = round_up(rows, 256), G = (rows + N - 1) / N;
+  uint8_t *digits = static_cast<uint8_t *>(d_ws);
+  uint64_t *body = reinterpret_cast<uint64_t *>(digits + round_up(T * rp * 3 * N, 256));
+  void *acc = reinterpret_cast<uint8_t *>(body) + round_up(T * rows * 8, 256);
+  cudaStream_t st = S(stream);
+  int launches = 0;
+  // (1) LWE outputs of Eq. 6: body at q_in, masks as Decomp digits (Eq. 8's left operand)
+  rc = matmul_common(p, d_wprep, rows, cols, 0, rows, d_operand, T, p->q_in, nullptr, body, stream);
+  if (rc) return rc;
+  launches += g_last_launches;
+  if (rp > rows) {  // zero digit rows of the 256-row padding (they contribute nothing)
+    if (cudaMemset2DAsync(digits + rows * 3 * N, (size_t)(rp * 3 * N), 0, (size_t)((rp - rows) * 3 * N),
+                          (size_t)T, st) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+  }
+  {
+    const int64_t Lc = phe_num_blocks(p, cols);
+    phe::GemmArgs a{};
+    a.kp = kp;
+    a.wexp = static_cast<const uint8_t *>(d_wprep);
+    a.wplain = reinterpret_cast<const int8_t *>(a.wexp + rows * Lc * 2 * N * 16);
+    a.rows = rows; a.wplain_rows = round_up(rows, 128); a.op_rows = op_rows(T, kp.ell);
+    a.Lc = Lc; a.cols = cols; a.row_begin = 0; a.row_end = rows;
+    a.mplanes = static_cast<const uint8_t *>(d_operand);
+    a.bplanes = a.mplanes + a.op_rows * Lc * N;
+    a.T = T; a.out_bits = p->q_in; a.out_mask = digits; a.out_body = nullptr;
+    a.digits = 1; a.digit_rows = rp;
+    int n = 0;
+    rc = phe::launch_limb_gemm(a, st, &n);
+    if (rc) return rc;
+    launches += n;
+  }
+  // (2) Eq. 8 + Eq. 7: KeySwitch GEMM with Rotate-and-sum into the packed accumulator
+  if (cudaMemsetAsync(acc, 0, (size_t)(T * G * 2 * N * 8), st) != cudaSuccess)
+    return phe_set_cuda_error(cudaGetLastError());
+  phe::PackArgs pa{};
+  pa.N = (int)N; pa.ell = kp.ell; pa.T = T; pa.rows_pad = rp; pa.G = (int)G;
+  pa.digits = digits; pa.kplanes = static_cast<const uint8_t *>(d_kprep); pa.kplane_rows = ks_plane_rows(p);
+  pa.acc = acc;
+  rc = phe::launch_pack_gemm(pa, st);
+  if (rc) return rc;
+  launches++;
+  // (3) (0, b) - ..., reduce mod 2^q_in, ModulusSwitch to q_out
+  rc = phe::launch_pack_finalize(kp, acc, body, T, rows, (int)G, d_out_packed, st);
+  if (rc) return rc;
+  g_last_launches = launches + 1;
+  return PHE_OK;
+}
+
+int phe_decrypt_packed(const phe_params *p, const uint8_t *d_S, const uint32_t *d_packed, int64_t T,
+                       int64_t rows, int32_t q_bits, int32_t *d_y, void *stream) {
+  KParams kp;
+  int rc = check_gpu(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || rows < 0 || q_bits < 1 || q_bits > 32) return PHE_EINVAL;
+  if (T * rows == 0) return PHE_OK;
+  if (!d_S || !d_packed || !d_y) return PHE_EINVAL;
+  const int64_t G = (rows + p->N - 1) / p->N;
+  return phe::launch_decrypt_packed(kp, d_S, d_packed, T, rows, (int)G, q_bits, d_y, S(stream));
+}
+
+}  // extern "C"

@@ -29,6 +29,13 @@ struct Nonce { uint32_t w0, w1, w2; };
 __host__ __device__ constexpr Nonce nonce_mask() { return {0u, 0u, 0u}; }
 __host__ __device__ constexpr Nonce nonce_sk() { return {0x2d656870u, 0x00006b73u, 0u}; }
 __host__ __device__ constexpr Nonce nonce_noise() { return {0x2d656870u, 0x73696f6eu, 0x00000065u}; }
+// NEXT #1 (R18-R20): "phe-ksk" (KSK masks), "phe-ksknoise" (KSK noise)
+__host__ __device__ constexpr Nonce nonce_ksk() { return {0x2d656870u, 0x006b736bu, 0u}; }
+__host__ __device__ constexpr Nonce nonce_ksk_noise() { return {0x2d656870u, 0x6e6b736bu, 0x6573696fu}; }
+
+// KeySwitch gadget (Decomp) parameters: base 2^8, 3 levels (R18)
+constexpr int KS_BASE_LOG = 8;
+constexpr int KS_LEVELS = 3;
 
 __device__ __forceinline__ uint32_t rotl(uint32_t v, int c) { return __funnelshift_l(v, v, c); }
 

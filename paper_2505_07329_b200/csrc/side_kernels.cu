@@ -368,4 +368,172 @@ int launch_simt_matmul(const KParams &kp, const int8_t *W, int64_t d_in, int64_t
   return PHE_OK;
 }
 
+// ================================================================== NEXT #1: KeySwitch packing
+// KSK generation (client): row r = l*N + i is RLWE_S(S'_i * 2^(q - (l+1)*8)):
+// A_r = ChaCha20 words (nonce "phe-ksk") r*N + k, B_r = A_r*S + E_r + S'_i 2^(q-(l+1)8) X^0.
+__global__ void __launch_bounds__(ENC_THREADS)
+ksk_gen_kernel(KParams kp, const uint8_t *__restrict__ S, uint64_t seed, uint64_t *__restrict__ KA,
+               uint64_t *__restrict__ KB) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int N = kp.N;
+  uint64_t *A = reinterpret_cast<uint64_t *>(smem);
+  uint8_t *Ss = smem + sizeof(uint64_t) * N;
+  const int64_t r = blockIdx.x;
+  const int l = (int)(r / N), i = (int)(r % N);
+  for (int b = threadIdx.x; b < N / 8; b += blockDim.x) {
+    uint64_t w[8];
+    chacha20_u64x8(seed, (uint32_t)(r * (N / 8) + b), nonce_ksk(), w);
+#pragma unroll
+    for (int e = 0; e < 8; e++) A[8 * b + e] = w[e] & kp.qmask;
+  }
+  for (int k = threadIdx.x; k < N; k += blockDim.x) Ss[k] = S[k];
+  __syncthreads();
+  for (int k = threadIdx.x; k < N; k += ENC_THREADS) {
+    uint64_t acc = 0;
+    for (int n = 0; n < N; n++) {
+      if (!Ss[n]) continue;
+      int d = k - n;
+      uint64_t a = A[d & (N - 1)];
+      acc += (d >= 0) ? a : (0ull - a);
+    }
+    if (kp.eta > 0) {
+      uint64_t widx = (uint64_t)r * (uint64_t)N + (uint64_t)k;
+      uint32_t o[16];
+      chacha20_block(seed, (uint32_t)(widx >> 3), nonce_ksk_noise(), o);
+      int q = (int)(widx & 7);
+      uint64_t w = (uint64_t)o[2 * q] | ((uint64_t)o[2 * q + 1] << 32);
+      uint64_t m = mask_bits(kp.eta);
+      acc += (uint64_t)((int64_t)__popcll(w & m) - (int64_t)__popcll((w >> kp.eta) & m));
+    }
+    if (k == 0) acc += (uint64_t)Ss[i] << (kp.q_in - (l + 1) * KS_BASE_LOG);
+    KA[r * N + k] = A[k];
+    KB[r * N + k] = acc & kp.qmask;
+  }
+}
+
+// KSK registration (server): limb planes of the packing GEMM's B operand.  Plane row
+// slot*ell + l (slot = part*kpad + k, k < N; zero for padding), column c = l'*N + i holds
+// byte l of KSK_part[c][k].  32x32 transpose tiles through shared memory.
+__global__ void ksk_planes_kernel(const uint64_t *__restrict__ ksk, int N, int ell, int kpad,
+                                  int64_t rows, uint8_t *__restrict__ planes) {
+  __shared__ uint64_t tile[32][33];
+  const int64_t K3 = 3 * (int64_t)N;
+  const int part = blockIdx.z;
+  const int64_t c0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+  const uint64_t *src = ksk + (int64_t)part * K3 * N;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + y, k = k0 + threadIdx.x;
+    tile[y][threadIdx.x] = (c < K3 && k < N) ? src[c * N + k] : 0ull;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t k = k0 + y, c = c0 + threadIdx.x;
+    if (k >= kpad || c >= K3) continue;
+    const uint64_t v = tile[threadIdx.x][y];
+    const int64_t slot = (int64_t)part * kpad + k;
+    for (int l = 0; l < ell; l++) planes[(slot * ell + l) * K3 + c] = (uint8_t)(v >> (8 * l));
+  }
+}
+
+// Finalize (Eq. 7/8): A = -acc_A, B = b_j - acc_B at coefficient p = j mod N of group j / N,
+// reduce mod 2^q_in, ModulusSwitch to q_out.  out: uint32 [T][G][2][N].
+__global__ void pack_finalize_kernel(KParams kp, const unsigned long long *__restrict__ acc,
+                                     const uint64_t *__restrict__ body, int64_t T, int64_t R, int G,
+                                     uint32_t *__restrict__ out) {
+  const int N = kp.N;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= T * G * N) return;
+  const int p = (int)(idx % N);
+  const int64_t tg = idx / N;
+  const int g = (int)(tg % G);
+  const int64_t tau = tg / G;
+  const int64_t j = (int64_t)g * N + p;
+  const uint64_t a = (0ull - acc[(tg * 2 + 0) * N + p]) & kp.qmask;
+  const uint64_t b = ((j < R ? body[tau * R + j] : 0ull) - acc[(tg * 2 + 1) * N + p]) & kp.qmask;
+  const int s = kp.q_in - kp.q_out;
+  const uint64_t half = s > 0 ? (1ull << (s - 1)) : 0ull, om = mask_bits(kp.q_out);
+  out[(tg * 2 + 0) * N + p] = (uint32_t)(((a + half) >> s) & om);
+  out[(tg * 2 + 1) * N + p] = (uint32_t)(((b + half) >> s) & om);
+}
+
+// Decryption of packed RLWE outputs (client): phase = B - A*S, decode per coefficient.
+__global__ void __launch_bounds__(ENC_THREADS)
+decrypt_packed_kernel(KParams kp, const uint8_t *__restrict__ S, const uint32_t *__restrict__ packed,
+                      int64_t R, int G, int q_bits, int32_t *__restrict__ y) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int N = kp.N;
+  uint32_t *A = reinterpret_cast<uint32_t *>(smem);
+  uint8_t *Ss = smem + sizeof(uint32_t) * N;
+  const int64_t tg = blockIdx.x;  // tau * G + g
+  const int g = (int)(tg % G);
+  const int64_t tau = tg / G;
+  const uint32_t *pa = packed + tg * 2 * N, *pb = pa + N;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) { A[k] = pa[k]; Ss[k] = S[k]; }
+  __syncthreads();
+  const uint64_t qm = mask_bits(q_bits), tmask = mask_bits(kp.beta);
+  for (int k = threadIdx.x; k < N; k += ENC_THREADS) {
+    const int64_t j = (int64_t)g * N + k;
+    if (j >= R) continue;
+    uint64_t acc = 0;
+    for (int n = 0; n < N; n++) {
+      if (!Ss[n]) continue;
+      int d = k - n;
+      uint64_t a = A[d & (N - 1)];
+      acc += (d >= 0) ? a : (0ull - a);
+    }
+    const uint64_t phi = ((uint64_t)pb[k] - acc) & qm;
+    uint64_t m;
+    if (q_bits >= kp.beta) {
+      int sh = q_bits - kp.beta;
+      m = sh == 0 ? phi : ((phi >> sh) + ((phi >> (sh - 1)) & 1ull));
+      m &= tmask;
+    } else {
+      m = (phi << (kp.beta - q_bits)) & tmask;
+    }
+    y[tau * R + j] = (int32_t)((m >= (1ull << (kp.beta - 1))) ? (int64_t)m - (int64_t)(1ull << kp.beta) : (int64_t)m);
+  }
+}
+
+int launch_ksk_gen(const KParams &kp, const uint8_t *S, uint64_t seed, uint64_t *KA, uint64_t *KB,
+                   cudaStream_t st) {
+  size_t smem = sizeof(uint64_t) * kp.N + kp.N;
+  static thread_local int configured = 0;
+  if (!configured) {
+    cudaFuncSetAttribute(ksk_gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = 1;
+  }
+  ksk_gen_kernel<<<(unsigned)(KS_LEVELS * kp.N), ENC_THREADS, smem, st>>>(kp, S, seed, KA, KB);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_ksk_planes(const KParams &kp, const uint64_t *ksk, int kpad, int64_t rows, uint8_t *planes,
+                      cudaStream_t st) {
+  if (cudaMemsetAsync(planes, 0, (size_t)rows * 3 * kp.N, st) != cudaSuccess)
+    return phe_set_cuda_error(cudaGetLastError());
+  dim3 grid((unsigned)((kpad + 31) / 32), (unsigned)((3 * kp.N + 31) / 32), 2);
+  ksk_planes_kernel<<<grid, dim3(32, 8), 0, st>>>(ksk, kp.N, kp.ell, kpad, rows, planes);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_pack_finalize(const KParams &kp, const void *acc, const uint64_t *body, int64_t T, int64_t R,
+                         int G, uint32_t *out, cudaStream_t st) {
+  int64_t n = T * G * kp.N;
+  if (n == 0) return PHE_OK;
+  pack_finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      kp, static_cast<const unsigned long long *>(acc), body, T, R, G, out);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_decrypt_packed(const KParams &kp, const uint8_t *S, const uint32_t *packed, int64_t T, int64_t R,
+                          int G, int q_bits, int32_t *y, cudaStream_t st) {
+  if (T * G == 0) return PHE_OK;
+  size_t smem = sizeof(uint32_t) * kp.N + kp.N;
+  decrypt_packed_kernel<<<(unsigned)(T * G), ENC_THREADS, smem, st>>>(kp, S, packed, R, G, q_bits, y);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
 }  // namespace phe

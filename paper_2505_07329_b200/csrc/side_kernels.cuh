@@ -23,6 +23,15 @@ int launch_simt_matmul(const KParams &kp, const int8_t *W, int64_t d_in, int64_t
                        int64_t R, const uint8_t *mplanes, const uint8_t *bplanes, int64_t L,
                        int64_t T, int out_bits, void *out_mask, void *out_body, cudaStream_t st);
 
+int launch_ksk_gen(const KParams &kp, const uint8_t *S, uint64_t seed, uint64_t *KA, uint64_t *KB,
+                   cudaStream_t st);
+int launch_ksk_planes(const KParams &kp, const uint64_t *ksk, int kpad, int64_t rows, uint8_t *planes,
+                      cudaStream_t st);
+int launch_pack_finalize(const KParams &kp, const void *acc, const uint64_t *body, int64_t T, int64_t R,
+                         int G, uint32_t *out, cudaStream_t st);
+int launch_decrypt_packed(const KParams &kp, const uint8_t *S, const uint32_t *packed, int64_t T, int64_t R,
+                          int G, int q_bits, int32_t *y, cudaStream_t st);
+
 // limb_gemm.cu: the tcgen05 int8 limb GEMM (mask = Hankel operand, body = plain operand).
 struct GemmArgs {
   KParams kp;
@@ -39,7 +48,21 @@ struct GemmArgs {
   int64_t T;
   int out_bits;
   void *out_mask, *out_body;
+  int digits;             // 1: out_mask receives Decomp digits int8 [T][digit_rows][3][N] (Eq. 8)
+  int64_t digit_rows;     // row stride of the digit tensor (>= row_end - row_begin)
 };
 int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches);
+
+// KeySwitch packing GEMM (NEXT #1): digits [T*rows_pad][3N] int8 x KSK limb planes.
+struct PackArgs {
+  int N, ell;
+  int64_t T, rows_pad;
+  int G;
+  const uint8_t *digits;
+  const uint8_t *kplanes;
+  int64_t kplane_rows;
+  void *acc;  // uint64 [T][G][2][N], zeroed by the caller
+};
+int launch_pack_gemm(const PackArgs &a, cudaStream_t st);
 
 }  // namespace phe
