@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["q_proj", "ffn", "stack"], default="q_proj")
+    ap.add_argument("--workload", choices=["q_proj", "ffn", "stack", "q_proj_packed"], default="q_proj")
     ap.add_argument("--tokens", type=int, default=2048, help="tokens per rank (B*C = 8*256)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -110,7 +110,7 @@ def linears(workload: str):
     d = 2048, m = 8192, GQA k/v 512x2048, 16 layers.  Linears that share an input ciphertext
     are registered fused (qkv 3072x2048, gate_up 16384x2048), so the input is expanded once and
     read by one GEMM.  Backward W^T takes each output's own gradient."""
-    if workload == "q_proj":  # configs[1]
+    if workload in ("q_proj", "q_proj_packed"):  # configs[1] (LWE outputs / + Eq. 7 packing)
         return [("q_proj", 2048, 2048, False, "x")]
     if workload == "ffn":     # configs[2]: gate/up 8192x2048, down 2048x8192, fwd + W^T bwd
         return [("gate", 8192, 2048, False, "h"), ("up", 8192, 2048, False, "h"),
@@ -164,6 +164,9 @@ def run_ours(args):
     # this rank's output rows of each linear (all rows unless row-sharded)
     rr = {name: (shard_range(w.rows, world, rank) if rows_mode else (0, w.rows)) for name, w, _ in regs}
     S = phe.keygen(p, synth.MASTER_SEED + 17)
+    packed = args.workload.endswith("_packed")
+    if packed:  # NEXT #1: KeySwitch key (client keygen, server registration), untimed setup
+        K = phe.KeySwitchKey(p, phe.ksk_gen(p, S, synth.MASTER_SEED + 23))
     # input ciphertexts: one per distinct (shape, role) -- layers reuse the resident synthetic
     # ciphertexts of the same shape, but every call still expands (ct_prepare) and contracts its own
     inputs = {}
@@ -176,12 +179,25 @@ def run_ours(args):
             seeds, body = phe.encrypt_pack(p, S, x, synth.seed_base(xr * 131 + w.cols + 7 * w.transpose))
             inputs[base] = (seeds, body)
     max_rows = max(rr[name][1] - rr[name][0] for name, _, _ in regs)
+    if args.workload.endswith("_packed"):
+        max_rows = 1  # outputs are packed RLWE (16 KB per token per 2048 rows): no chunking needed
     # token chunks: outputs stay <= ~34 GB (gate_up: 275 GB at T=2048) and a chunk is a whole
     # number of 51-token tiles (no extra tile-padding waste)
     tpt = 256 // p.ell
     chunk = min(T, max(tpt, (34_400_000_000 // (max_rows * p.N * 4)) // tpt * tpt))
-    out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
-    out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)
+    if not args.workload.endswith("_packed"):
+        out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
+        out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)
+    if packed:
+        name0, w0, _ = regs[0]
+        r256 = (w0.rows + 255) // 256 * 256
+        G0 = (w0.rows + p.N - 1) // p.N
+        dig_buf = torch.empty((chunk, r256, 3, p.N), dtype=torch.int8, device=dev)
+        bod_buf = torch.empty((chunk, w0.rows), dtype=torch.int64, device=dev)
+        acc_buf = torch.empty(phe.load().phe_pack_acc_bytes(__import__("ctypes").byref(p), w0.rows, chunk),
+                              dtype=torch.uint8, device=dev)
+        pk_buf = torch.empty((chunk, G0, 2, p.N), dtype=torch.int32, device=dev)
+        out_mask = torch.empty(1, dtype=torch.int32, device=dev)  # unused: no LWE-form outputs
     max_L = max(p.L(w.cols) for _, w, _ in regs)
     operand = torch.empty(phe.load().phe_ct_operand_bytes(__import__("ctypes").byref(p), chunk, max_L),
                           dtype=torch.uint8, device=dev)
@@ -203,6 +219,15 @@ def run_ours(args):
                 phe.ct_prepare(p, seeds[t0:t0 + n], body[t0:t0 + n], out=operand)  # a3, a4
                 launches[0] += 1
                 e[1].record(stream)
+                if packed:  # Eq. 6 -> digits + bodies, then Eq. 8 + Eq. 7 + switch
+                    phe.matmul_clear_digits(p, w, operand, n, digits=dig_buf[:n], body=bod_buf[:n])
+                    launches[0] += phe.last_launch_count()
+                    e[2].record(stream)
+                    phe.pack(p, dig_buf[:n], bod_buf[:n], K, out=pk_buf[:n], acc=acc_buf)
+                    launches[0] += phe.last_launch_count()
+                    e[3].record(stream)
+                    evs.append((name, e))
+                    continue
                 f = phe.matmul_clear_T if w.transpose else phe.matmul_clear
                 r0, r1 = rr[name]
                 nr = r1 - r0
@@ -290,6 +315,10 @@ def run_ours(args):
     peak = 2.0 * float(mp["bf16_tflops"])  # int8 dense = 2x bf16 (guide's nominal ratio)
     mask_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") for n_, w, _ in regs)
     mask_ms = statistics.mean(parts_ms["mask_gemm"])
+    pack_ops = 0.0
+    if packed:  # Eq. 8: 2 parts x Decomp(A_LWE) [rows x 3N] x KSK [3N x N], ell int8 MACs each
+        pack_ops = sum(2.0 * 2 * p.ell * 3 * p.N * p.N * w.rows * T for _, w, _ in regs)
+        mask_ops, mask_ms = pack_ops, statistics.mean(parts_ms["mask_gemm"])
     achieved = mask_ops / (mask_ms / 1e3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -299,10 +328,11 @@ def run_ours(args):
         except Exception:
             traffic = None
     total_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") +
-                    alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "body") for n_, w, _ in regs)
+                    alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "body") for n_, w, _ in regs) + pack_ops
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "limb_gemm_2sm_kernel<5,SW,13> (mask contraction, tcgen05 cta_group::2)",
+                "kernel": ("pack_gemm_2sm_kernel<5> (KeySwitch GEMM Eq. 8 + rotate-sum Eq. 7)" if packed else
+                           "limb_gemm_2sm_kernel<5,SW,13> (mask contraction, tcgen05 cta_group::2)"),
                 "ops": "int8 tensor ops (2 per MAC), algorithmic: 2*ell*d_out*d_in*N per token",
                 "peak_source": f"{src}: 2 x bf16_tflops (burst) of MEASURED_PEAKS.json",
                 "frac_of_nominal_4500": round(achieved / NOMINAL_INT8_TOPS, 4),
@@ -310,6 +340,26 @@ def run_ours(args):
 
     # ---------------- e2e through the C ABI with host buffers
     e2e = None
+    if not args.no_e2e and not args.profile and packed and not rows_mode:
+        name, w, _ = regs[0]
+        seeds, body = inputs[(w.cols, w.transpose)]
+        hs = seeds.cpu().pin_memory()
+        hb = body.cpu().pin_memory()
+        ho = torch.empty((T, (w.rows + p.N - 1) // p.N, 2, p.N), dtype=torch.int32, pin_memory=True)
+        phe.server_matvec_packed_host(p, w, K, hs, hb, ho, chunk_tokens=255)
+        wall = []
+        for _ in range(max(2, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            phe.server_matvec_packed_host(p, w, K, hs, hb, ho, chunk_tokens=255)
+            wall.append(time.perf_counter() - t0)
+        e2e_s = statistics.mean(wall)
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * T / float(te.item()), 2), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(hs.numel() * 8 + hb.numel() * 8), "d2h_bytes_per_step": int(ho.numel() * 4),
+               "ms_per_step": round(float(te.item()) * 1e3, 2),
+               "api": "phe_server_matvec_packed_host (pinned host buffers, 255-token chunks, 2 streams)"}
     if not args.no_e2e and not args.profile and args.workload == "q_proj" and not rows_mode:
         name, w, _ = regs[0]
         seeds, body = inputs[(w.cols, w.transpose)]
@@ -352,7 +402,10 @@ def run_ours(args):
             "config": config_dict(args, world, T, rows_mode),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
             "clocks": clocks,
-            "breakdown_ms": {k: round(statistics.mean(v), 3) for k, v in parts_ms.items()},
+            "breakdown_ms": ({"ct_prepare": round(statistics.mean(parts_ms["ct_prepare"]), 3),
+                              "lwe_digits_gemms": round(statistics.mean(parts_ms["body_gemm"]), 3),
+                              "pack_gemm_finalize": round(statistics.mean(parts_ms["mask_gemm"]), 3)} if packed else
+                             {k: round(statistics.mean(v), 3) for k, v in parts_ms.items()}),
         }
         if len(regs) > 1:
             line["per_linear_ms"] = {k: round(sum(v) / args.steps, 3) for k, v in per_kind.items()}
@@ -366,6 +419,8 @@ def run_ours(args):
 def config_dict(args, world, T, rows_mode=False):
     wl = {"q_proj": "Llama-3.2-1B q_proj 2048x2048 forward W.[x]_HE (BASELINE configs[1])",
           "ffn": "Llama-3.2-1B FFN gate/up 8192x2048 + down 2048x8192, fwd + W^T bwd (configs[2])",
+          "q_proj_packed": "Llama-3.2-1B q_proj 2048x2048 forward, full primitive: Eq. 6 + KeySwitch packing "
+                           "Eq. 7/8 -> RLWE(Wx), 39->26 switch (configs[1] + SURVEY NEXT #1)",
           "stack": "Llama-3.2-1B all linears x 16 layers (qkv fused 3072x2048, o, gate_up fused 16384x2048, "
                    "down; bwd W^T incl. GQA k/v 512x2048), fwd + bwd (configs[3])"}[args.workload]
     return {"workload": wl, "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": 8, "C": 256, "N": 2048, "q_in": 39, "q_out": 26,

@@ -190,9 +190,28 @@ int phe_ksk_prepare(const phe_params *p, const void *d_ksk, void *d_kprep, size_
  *   of ciphertext j / N.  d_ws: workspace of phe_packed_ws_bytes(p, R, T) bytes.
  *   Errors: EUNSUPPORTED unless ell in {4,5}, N % 256 == 0, q_in > 24.                       */
 size_t phe_packed_ws_bytes(const phe_params *p, int64_t rows, int64_t T);
+/* The two stages of phe_matmul_clear_packed, callable separately:
+ * phe_matmul_clear_digits: Eq. 6 with the LWE masks written as Decomp digits, int8
+ *   d_digits [T][R256][3][N] (R256 = R rounded up to 256; pad rows zeroed; plane l = digit of
+ *   weight 2^(q_in - 8(l+1))) and bodies d_body uint64 [T][R] at q_in.
+ * phe_pack: Eq. 8 + Eq. 7 from those digits/bodies; d_acc: uint64 scratch of
+ *   phe_pack_acc_bytes(p, R, T) bytes; output as phe_matmul_clear_packed.                    */
+int phe_matmul_clear_digits(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                            int transpose, const void *d_operand, int64_t T, void *d_digits,
+                            uint64_t *d_body, void *stream);
+size_t phe_pack_acc_bytes(const phe_params *p, int64_t rows, int64_t T);
+int phe_pack(const phe_params *p, const void *d_digits, const uint64_t *d_body, int64_t T, int64_t rows,
+             const void *d_kprep, void *d_acc, size_t acc_bytes, uint32_t *d_out_packed, void *stream);
 int phe_matmul_clear_packed(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
                             int transpose, const void *d_operand, int64_t T, const void *d_kprep,
                             void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream);
+/* phe_server_matvec_packed_host: phe_server_matvec_host for the packed primitive: host seeds /
+ * bodies in, h_out_packed uint32 [T][G][2][N] out (chunked, copies overlapped; allocates its
+ * own device workspace).                                                                    */
+int phe_server_matvec_packed_host(const phe_params *p, const void *d_wprep, int64_t d_out,
+                                  int64_t d_in, int transpose, const void *d_kprep,
+                                  const uint64_t *h_seeds, const uint64_t *h_body, int64_t T,
+                                  int64_t chunk_tokens, uint32_t *h_out_packed, void *stream);
 /* phe_decrypt_packed (client): d_y int32 [T][rows] = decode(B' - A'S) coefficient-wise. */
 int phe_decrypt_packed(const phe_params *p, const uint8_t *d_S, const uint32_t *d_packed, int64_t T,
                        int64_t rows, int32_t q_bits, int32_t *d_y, void *stream);

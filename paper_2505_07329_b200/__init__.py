@@ -30,7 +30,8 @@ EXPORTS = [
     "phe_matmul_clear_T", "phe_modswitch", "phe_decrypt_unpack", "phe_server_matvec_host",
     "phe_last_launch_count", "phe_matmul_clear_simt",
     "phe_ksk_bytes", "phe_ksk_gen", "phe_ksk_prep_bytes", "phe_ksk_prepare", "phe_packed_ws_bytes",
-    "phe_matmul_clear_packed", "phe_decrypt_packed",
+    "phe_matmul_clear_packed", "phe_decrypt_packed", "phe_matmul_clear_digits", "phe_pack_acc_bytes",
+    "phe_pack", "phe_server_matvec_packed_host",
 ]
 
 
@@ -97,6 +98,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_matmul_clear_packed": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp, _vp, _sz, _vp, _vp],
                                     ctypes.c_int),
         "phe_decrypt_packed": ([_P, _vp, _vp, _i64, _i64, _i32, _vp, _vp], ctypes.c_int),
+        "phe_matmul_clear_digits": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp, _vp, _vp], ctypes.c_int),
+        "phe_pack_acc_bytes": ([_P, _i64, _i64], _sz),
+        "phe_pack": ([_P, _vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
+        "phe_server_matvec_packed_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _vp,
+                                           _vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -341,3 +347,43 @@ def decrypt_packed(p: Params, S: torch.Tensor, packed: torch.Tensor, rows: int, 
     _check(load().phe_decrypt_packed(ctypes.byref(p), _ptr(S), _ptr(packed), T, rows, q_bits, _ptr(y), _stream()),
            "phe_decrypt_packed")
     return y
+
+
+def matmul_clear_digits(p: Params, w: Weights, operand: torch.Tensor, T: int, digits=None, body=None):
+    """Stage 1 of the packed primitive: Eq. 6 with masks as Decomp digits (int8 [T][R256][3][N])
+    and bodies uint64 [T][R] (int64 storage)."""
+    r256 = (w.rows + 255) // 256 * 256
+    if digits is None:
+        digits = torch.empty((T, r256, 3, p.N), dtype=torch.int8, device=operand.device)
+    if body is None:
+        body = torch.empty((T, w.rows), dtype=torch.int64, device=operand.device)
+    _check(load().phe_matmul_clear_digits(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
+                                          _ptr(operand), T, _ptr(digits), _ptr(body), _stream()),
+           "phe_matmul_clear_digits")
+    return digits, body
+
+
+def pack(p: Params, digits: torch.Tensor, body: torch.Tensor, ksk: KeySwitchKey, out=None, acc=None):
+    """Stage 2: Eq. 8 + Eq. 7 (KeySwitch GEMM, Rotate, sum) + ModulusSwitch."""
+    T, rows = body.shape
+    G = (rows + p.N - 1) // p.N
+    if out is None:
+        out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=body.device)
+    nbytes = load().phe_pack_acc_bytes(ctypes.byref(p), rows, T)
+    if acc is None:
+        acc = torch.empty(nbytes, dtype=torch.uint8, device=body.device)
+    _check(load().phe_pack(ctypes.byref(p), _ptr(digits), _ptr(body), T, rows, _ptr(ksk.buf), _ptr(acc),
+                           acc.numel(), _ptr(out), _stream()), "phe_pack")
+    return out
+
+
+def server_matvec_packed_host(p: Params, w: Weights, ksk: KeySwitchKey, h_seeds: torch.Tensor,
+                              h_body: torch.Tensor, h_out: torch.Tensor, chunk_tokens: int = 256) -> None:
+    """End to end with HOST buffers for the packed primitive: h_out int32 [T][G][2][N]."""
+    for t, n in [(h_seeds, "h_seeds"), (h_body, "h_body"), (h_out, "h_out")]:
+        if t.is_cuda or not t.is_contiguous():
+            raise PheError(f"{n} must be a contiguous host tensor")
+    _check(load().phe_server_matvec_packed_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
+                                                _ptr(ksk.buf), _ptr(h_seeds), _ptr(h_body), h_seeds.shape[0],
+                                                chunk_tokens, _ptr(h_out), _stream()),
+           "phe_server_matvec_packed_host")

@@ -380,6 +380,81 @@ size_t phe_packed_ws_bytes(const phe_params *p, int64_t rows, int64_t T) {
   return (size_t)(round_up(T * rp * 3 * N, 256) + round_up(T * rows * 8, 256) + round_up(T * G * 2 * N * 8, 256));
 }
 
+int phe_matmul_clear_digits(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                            int transpose, const void *d_operand, int64_t T, void *d_digits,
+                            uint64_t *d_body, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_pack(p, &kp);
+  if (rc) return rc;
+  if (d_out < 1 || d_in < 1 || T < 0 || (transpose != 0 && transpose != 1)) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_wprep || !d_operand || !d_digits || !d_body) return PHE_EINVAL;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  const int64_t N = p->N, rp = round_up(rows, 256);
+  uint8_t *digits = static_cast<uint8_t *>(d_digits);
+  cudaStream_t st = S(stream);
+  int launches = 0;
+  rc = matmul_common(p, d_wprep, rows, cols, 0, rows, d_operand, T, p->q_in, nullptr, d_body, stream);
+  if (rc) return rc;
+  launches += g_last_launches;
+  if (rp > rows) {  // zero digit rows of the 256-row padding (they contribute nothing)
+    if (cudaMemset2DAsync(digits + rows * 3 * N, (size_t)(rp * 3 * N), 0, (size_t)((rp - rows) * 3 * N),
+                          (size_t)T, st) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+  }
+  const int64_t Lc = phe_num_blocks(p, cols);
+  phe::GemmArgs a{};
+  a.kp = kp;
+  a.wexp = static_cast<const uint8_t *>(d_wprep);
+  a.wplain = reinterpret_cast<const int8_t *>(a.wexp + rows * Lc * 2 * N * 16);
+  a.rows = rows; a.wplain_rows = round_up(rows, 128); a.op_rows = op_rows(T, kp.ell);
+  a.Lc = Lc; a.cols = cols; a.row_begin = 0; a.row_end = rows;
+  a.mplanes = static_cast<const uint8_t *>(d_operand);
+  a.bplanes = a.mplanes + a.op_rows * Lc * N;
+  a.T = T; a.out_bits = p->q_in; a.out_mask = digits; a.out_body = nullptr;
+  a.digits = 1; a.digit_rows = rp;
+  int n = 0;
+  rc = phe::launch_limb_gemm(a, st, &n);
+  if (rc) return rc;
+  g_last_launches = launches + n;
+  return PHE_OK;
+}
+
+size_t phe_pack_acc_bytes(const phe_params *p, int64_t rows, int64_t T) {
+  if (!p || rows < 1 || T < 0) return 0;
+  const int64_t G = (rows + p->N - 1) / p->N;
+  return (size_t)(T * G * 2 * p->N * 8);
+}
+
+int phe_pack(const phe_params *p, const void *d_digits, const uint64_t *d_body, int64_t T, int64_t rows,
+             const void *d_kprep, void *d_acc, size_t acc_bytes, uint32_t *d_out_packed, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_pack(p, &kp);
+  if (rc) return rc;
+  if (rows < 1 || T < 0) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_digits || !d_body || !d_kprep || !d_acc || !d_out_packed) return PHE_EINVAL;
+  if (acc_bytes < phe_pack_acc_bytes(p, rows, T)) return PHE_ENOMEM;
+  const int64_t N = p->N, rp = round_up(rows, 256), G = (rows + N - 1) / N;
+  cudaStream_t st = S(stream);
+  if (cudaMemsetAsync(d_acc, 0, (size_t)(T * G * 2 * N * 8), st) != cudaSuccess)
+    return phe_set_cuda_error(cudaGetLastError());
+  phe::PackArgs pa{};
+  pa.N = (int)N; pa.ell = kp.ell; pa.T = T; pa.rows_pad = rp; pa.G = (int)G;
+  pa.digits = static_cast<const uint8_t *>(d_digits);
+  pa.kplanes = static_cast<const uint8_t *>(d_kprep);
+  pa.kplane_rows = ks_plane_rows(p);
+  pa.acc = d_acc;
+  rc = phe::launch_pack_gemm(pa, st);
+  if (rc) return rc;
+  rc = phe::launch_pack_finalize(kp, d_acc, d_body, T, rows, (int)G, d_out_packed, st);
+  if (rc) return rc;
+  g_last_launches = 2;
+  return PHE_OK;
+}
+
 int phe_matmul_clear_packed(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
                             int transpose, const void *d_operand, int64_t T, const void *d_kprep,
                             void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream) {
@@ -390,54 +465,20 @@ int phe_matmul_clear_packed(const phe_params *p, const void *d_wprep, int64_t d_
   if (d_out < 1 || d_in < 1 || T < 0 || (transpose != 0 && transpose != 1)) return PHE_EINVAL;
   if (T == 0) return PHE_OK;
   if (!d_wprep || !d_operand || !d_kprep || !d_ws || !d_out_packed) return PHE_EINVAL;
-  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  const int64_t rows = transpose ? d_in : d_out;
   if (ws_bytes < phe_packed_ws_bytes(p, rows, T)) return PHE_ENOMEM;
-  const int64_t N = p->N, rp = round_up(rows, 256), G = (rows + N - 1) / N;
+  const int64_t N = p->N, rp = round_up(rows, 256);
   uint8_t *digits = static_cast<uint8_t *>(d_ws);
   uint64_t *body = reinterpret_cast<uint64_t *>(digits + round_up(T * rp * 3 * N, 256));
   void *acc = reinterpret_cast<uint8_t *>(body) + round_up(T * rows * 8, 256);
-  cudaStream_t st = S(stream);
-  int launches = 0;
   // (1) LWE outputs of Eq. 6: body at q_in, masks as Decomp digits (Eq. 8's left operand)
-  rc = matmul_common(p, d_wprep, rows, cols, 0, rows, d_operand, T, p->q_in, nullptr, body, stream);
+  rc = phe_matmul_clear_digits(p, d_wprep, d_out, d_in, transpose, d_operand, T, digits, body, stream);
   if (rc) return rc;
-  launches += g_last_launches;
-  if (rp > rows) {  // zero digit rows of the 256-row padding (they contribute nothing)
-    if (cudaMemset2DAsync(digits + rows * 3 * N, (size_t)(rp * 3 * N), 0, (size_t)((rp - rows) * 3 * N),
-                          (size_t)T, st) != cudaSuccess)
-      return phe_set_cuda_error(cudaGetLastError());
-  }
-  {
-    const int64_t Lc = phe_num_blocks(p, cols);
-    phe::GemmArgs a{};
-    a.kp = kp;
-    a.wexp = static_cast<const uint8_t *>(d_wprep);
-    a.wplain = reinterpret_cast<const int8_t *>(a.wexp + rows * Lc * 2 * N * 16);
-    a.rows = rows; a.wplain_rows = round_up(rows, 128); a.op_rows = op_rows(T, kp.ell);
-    a.Lc = Lc; a.cols = cols; a.row_begin = 0; a.row_end = rows;
-    a.mplanes = static_cast<const uint8_t *>(d_operand);
-    a.bplanes = a.mplanes + a.op_rows * Lc * N;
-    a.T = T; a.out_bits = p->q_in; a.out_mask = digits; a.out_body = nullptr;
-    a.digits = 1; a.digit_rows = rp;
-    int n = 0;
-    rc = phe::launch_limb_gemm(a, st, &n);
-    if (rc) return rc;
-    launches += n;
-  }
-  // (2) Eq. 8 + Eq. 7: KeySwitch GEMM with Rotate-and-sum into the packed accumulator
-  if (cudaMemsetAsync(acc, 0, (size_t)(T * G * 2 * N * 8), st) != cudaSuccess)
-    return phe_set_cuda_error(cudaGetLastError());
-  phe::PackArgs pa{};
-  pa.N = (int)N; pa.ell = kp.ell; pa.T = T; pa.rows_pad = rp; pa.G = (int)G;
-  pa.digits = digits; pa.kplanes = static_cast<const uint8_t *>(d_kprep); pa.kplane_rows = ks_plane_rows(p);
-  pa.acc = acc;
-  rc = phe::launch_pack_gemm(pa, st);
+  const int l1 = g_last_launches;
+  // (2) Eq. 8 + Eq. 7 (KeySwitch GEMM, Rotate, sum), (0, b) - ..., ModulusSwitch to q_out
+  rc = phe_pack(p, digits, body, T, rows, d_kprep, acc, phe_pack_acc_bytes(p, rows, T), d_out_packed, stream);
   if (rc) return rc;
-  launches++;
-  // (3) (0, b) - ..., reduce mod 2^q_in, ModulusSwitch to q_out
-  rc = phe::launch_pack_finalize(kp, acc, body, T, rows, (int)G, d_out_packed, st);
-  if (rc) return rc;
-  g_last_launches = launches + 1;
+  g_last_launches += l1;
   return PHE_OK;
 }
 
@@ -454,3 +495,64 @@ int phe_decrypt_packed(const phe_params *p, const uint8_t *d_S, const uint32_t *
 }
 
 }  // extern "C"
+
+extern "C" int phe_server_matvec_packed_host(const phe_params *p, const void *d_wprep, int64_t d_out,
+                                             int64_t d_in, int transpose, const void *d_kprep,
+                                             const uint64_t *h_seeds, const uint64_t *h_body, int64_t T,
+                                             int64_t chunk_tokens, uint32_t *h_out_packed, void *stream) {
+  KParams kp;
+  int rc = check_pack(p, &kp);
+  if (rc) return rc;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  if (rows < 1 || cols < 1 || T < 0 || chunk_tokens < 1) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_wprep || !d_kprep || !h_seeds || !h_body || !h_out_packed) return PHE_EINVAL;
+  const int64_t N = p->N, L = phe_num_blocks(p, cols), G = (rows + N - 1) / N;
+  const int64_t C = chunk_tokens < T ? chunk_tokens : T;
+  const size_t b_seeds = round_up(C * L * 8, 256), b_body = round_up(C * L * N * 8, 256);
+  const size_t b_op = round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256);
+  const size_t b_ws = round_up((int64_t)phe_packed_ws_bytes(p, rows, C), 256);
+  const size_t b_out = round_up(C * G * 2 * N * 4, 256);
+  const size_t slot = b_seeds + b_body + b_op + b_ws + b_out;
+  if (g_ws.bytes < 2 * slot) {
+    if (g_ws.buf) cudaFree(g_ws.buf);
+    g_ws.buf = nullptr; g_ws.bytes = 0;
+    if (cudaMalloc(&g_ws.buf, 2 * slot) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+    g_ws.bytes = 2 * slot;
+  }
+  if (!g_ws.st[0]) {
+    for (int s = 0; s < 2; s++)
+      if (cudaStreamCreateWithFlags(&g_ws.st[s], cudaStreamNonBlocking) != cudaSuccess)
+        return phe_set_cuda_error(cudaGetLastError());
+    if (cudaEventCreateWithFlags(&g_ws.ev, cudaEventDisableTiming) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+  }
+  cudaEventRecord(g_ws.ev, S(stream));
+  cudaStreamWaitEvent(g_ws.st[0], g_ws.ev, 0);
+  cudaStreamWaitEvent(g_ws.st[1], g_ws.ev, 0);
+  int64_t c = 0;
+  for (int64_t t0 = 0; t0 < T; t0 += C, c++) {
+    const int64_t n = (T - t0) < C ? (T - t0) : C;
+    cudaStream_t st = g_ws.st[c & 1];
+    uint8_t *base = static_cast<uint8_t *>(g_ws.buf) + (c & 1) * slot;
+    uint64_t *d_seeds = reinterpret_cast<uint64_t *>(base);
+    uint64_t *d_bod = reinterpret_cast<uint64_t *>(base + b_seeds);
+    void *d_op = base + b_seeds + b_body;
+    void *d_wsp = base + b_seeds + b_body + b_op;
+    uint32_t *d_o = reinterpret_cast<uint32_t *>(base + b_seeds + b_body + b_op + b_ws);
+    cudaMemcpyAsync(d_seeds, h_seeds + t0 * L, n * L * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_bod, h_body + t0 * L * N, n * L * N * 8, cudaMemcpyHostToDevice, st);
+    rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
+    if (rc) return rc;
+    rc = phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws, d_o, st);
+    if (rc) return rc;
+    cudaMemcpyAsync(h_out_packed + t0 * G * 2 * N, d_o, n * G * 2 * N * 4, cudaMemcpyDeviceToHost, st);
+  }
+  cudaError_t e0 = cudaStreamSynchronize(g_ws.st[0]);
+  cudaError_t e1 = cudaStreamSynchronize(g_ws.st[1]);
+  if (e0 != cudaSuccess) return phe_set_cuda_error(e0);
+  if (e1 != cudaSuccess) return phe_set_cuda_error(e1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return phe_set_cuda_error(e);
+  return PHE_OK;
+}

@@ -78,3 +78,22 @@ def test_packed_transpose_backward(phe, coracle):
         PA, PB = coracle.pack(op, m, b, KA, KB, nthreads=os.cpu_count())
         assert np.array_equal(got[tau, :, 0], O.modswitch(PA, 39, 26))
         assert np.array_equal(got[tau, :, 1], O.modswitch(PB, 39, 26))
+
+
+def test_packed_host_path_and_stages_agree(phe):
+    """phe_server_matvec_packed_host (host buffers, chunked) == device call == staged calls."""
+    p = phe.params(phe.PRESET_PAPER, N=256)
+    W = synth.weights_int8(512, 256)
+    x = synth.activations_int8(70, 256)
+    S = phe.keygen(p, 3)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).to(DEV), 4)
+    w = phe.Weights(p, torch.from_numpy(W).to(DEV))
+    K = phe.KeySwitchKey(p, phe.ksk_gen(p, S, 5))
+    opnd = phe.ct_prepare(p, seeds, body)
+    ref = phe.matmul_clear_packed(p, w, opnd, 70, K)
+    dig, bod = phe.matmul_clear_digits(p, w, opnd, 70)
+    staged = phe.pack(p, dig, bod, K)
+    assert torch.equal(staged, ref)
+    ho = torch.empty((70, 2, 2, 256), dtype=torch.int32).pin_memory()
+    phe.server_matvec_packed_host(p, w, K, seeds.cpu().pin_memory(), body.cpu().pin_memory(), ho, chunk_tokens=33)
+    assert torch.equal(ho, ref.cpu())
