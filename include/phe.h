@@ -216,6 +216,29 @@ int phe_server_matvec_packed_host(const phe_params *p, const void *d_wprep, int6
 int phe_decrypt_packed(const phe_params *p, const uint8_t *d_S, const uint32_t *d_packed, int64_t T,
                        int64_t rows, int32_t q_bits, int32_t *d_y, void *stream);
 
+/* ---- NEXT #2: wire format ------------------------------------
+ * Little-endian contiguous bitstream, no per-coefficient padding (R22).
+ * Input block (client -> server): [LE64 seed][N body coefficients at q_in bits]
+ *   = 8 + N*q_in/8 bytes (9992 at Table 1).
+ * Packed output (server -> client): [A' at q_out bits][B' at q_out bits] = 2*N*q_out/8 bytes
+ *   (13312 at Table 1).  Requires q_in <= 57, N % 8 == 0.
+ * d_seeds [T][L] / d_body [T][L][N] uint64; d_packed uint32 [n_ct][2][N]; d_wire bytes.     */
+size_t phe_wire_input_bytes(const phe_params *p);
+size_t phe_wire_output_bytes(const phe_params *p);
+int phe_wire_serialize_inputs(const phe_params *p, const uint64_t *d_seeds, const uint64_t *d_body,
+                              int64_t T, int64_t L, uint8_t *d_wire, void *stream);
+int phe_wire_deserialize_inputs(const phe_params *p, const uint8_t *d_wire, int64_t T, int64_t L,
+                                uint64_t *d_seeds, uint64_t *d_body, void *stream);
+int phe_wire_serialize_packed(const phe_params *p, const uint32_t *d_packed, int64_t n_ct,
+                              uint8_t *d_wire, void *stream);
+int phe_wire_deserialize_packed(const phe_params *p, const uint8_t *d_wire, int64_t n_ct,
+                                uint32_t *d_packed, void *stream);
+/* The server step as the network sees it: h_wire_in [T][L] input blocks -> h_wire_out [T][G]
+ * packed ciphertexts (host buffers; chunked; allocates its own device workspace).           */
+int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                         int transpose, const void *d_kprep, const uint8_t *h_wire_in, int64_t T,
+                         int64_t chunk_tokens, uint8_t *h_wire_out, void *stream);
+
 /* ---- introspection (tests / bench) -------------------------------------------------- */
 /* Number of kernel launches the last phe_matmul_clear[_T] on this thread enqueued. */
 int phe_last_launch_count(void);

@@ -549,3 +549,55 @@ def decrypt_packed(params: Params, A: np.ndarray, B: np.ndarray, S: np.ndarray, 
     with np.errstate(over="ignore"):
         phi = (B.astype(U64) - AS) & U64((1 << q_bits) - 1)
     return np.array([decode(int(p), q_bits, params.beta) for p in phi], dtype=np.int64)
+
+
+# ======================================================================================
+# NEXT #2: wire format.  Little-endian contiguous bitstream, no
+# per-coefficient padding: coefficient k occupies bits [k*b, (k+1)*b) (DESIGN R22).
+# ======================================================================================
+def bitpack(values, bits: int) -> bytes:
+    acc = 0
+    for k, v in enumerate(values):
+        acc |= (int(v) & ((1 << bits) - 1)) << (k * bits)
+    nbytes = (len(values) * bits + 7) // 8
+    return acc.to_bytes(nbytes, "little")
+
+
+def bitunpack(data: bytes, bits: int, count: int) -> np.ndarray:
+    acc = int.from_bytes(data, "little")
+    m = (1 << bits) - 1
+    return np.array([(acc >> (k * bits)) & m for k in range(count)], dtype=U64)
+
+
+def serialize_input(seed: int, body: np.ndarray, q_bits: int) -> bytes:
+    """Seeded RLWE block as sent by the client: 8-byte seed + N coefficients at q_in bits
+    (8 + 2048*39/8 = 9992 bytes)."""
+    return struct.pack("<Q", seed & MASK64) + bitpack(body, q_bits)
+
+
+def deserialize_input(data: bytes, N: int, q_bits: int):
+    if len(data) != 8 + (N * q_bits + 7) // 8:
+        raise ValueError("truncated or oversized input block")
+    return struct.unpack("<Q", data[:8])[0], bitunpack(data[8:], q_bits, N)
+
+
+def serialize_output(A: np.ndarray, B: np.ndarray, q_bits: int) -> bytes:
+    """Packed RLWE output (A', B') at q_out bits (2 * 2048*26/8 = 13312 bytes)."""
+    return bitpack(A, q_bits) + bitpack(B, q_bits)
+
+
+def deserialize_output(data: bytes, N: int, q_bits: int):
+    half = (N * q_bits + 7) // 8
+    if len(data) != 2 * half:
+        raise ValueError("truncated or oversized output ciphertext")
+    return bitunpack(data[:half], q_bits, N), bitunpack(data[half:], q_bits, N)
+
+
+def expansion_report(params: Params) -> dict:
+    """Expansion factors computed from the serializers: input bytes per N int8
+    plaintext bytes; output bytes per N*gamma/8 bytes of guaranteed plaintext."""
+    N = params.N
+    zi = serialize_input(0, np.zeros(N, U64), params.q_in)
+    zo = serialize_output(np.zeros(N, U64), np.zeros(N, U64), params.q_out)
+    return {"input_bytes": len(zi), "output_bytes": len(zo),
+            "input_factor": len(zi) / N, "output_factor": len(zo) / (N * params.gamma / 8)}

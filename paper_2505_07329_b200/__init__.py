@@ -32,6 +32,8 @@ EXPORTS = [
     "phe_ksk_bytes", "phe_ksk_gen", "phe_ksk_prep_bytes", "phe_ksk_prepare", "phe_packed_ws_bytes",
     "phe_matmul_clear_packed", "phe_decrypt_packed", "phe_matmul_clear_digits", "phe_pack_acc_bytes",
     "phe_pack", "phe_server_matvec_packed_host",
+    "phe_wire_input_bytes", "phe_wire_output_bytes", "phe_wire_serialize_inputs", "phe_wire_deserialize_inputs",
+    "phe_wire_serialize_packed", "phe_wire_deserialize_packed", "phe_server_wire_host",
 ]
 
 
@@ -103,6 +105,13 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_pack": ([_P, _vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
         "phe_server_matvec_packed_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _vp,
                                            _vp], ctypes.c_int),
+        "phe_wire_input_bytes": ([_P], _sz),
+        "phe_wire_output_bytes": ([_P], _sz),
+        "phe_wire_serialize_inputs": ([_P, _vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
+        "phe_wire_deserialize_inputs": ([_P, _vp, _i64, _i64, _vp, _vp, _vp], ctypes.c_int),
+        "phe_wire_serialize_packed": ([_P, _vp, _i64, _vp, _vp], ctypes.c_int),
+        "phe_wire_deserialize_packed": ([_P, _vp, _i64, _vp, _vp], ctypes.c_int),
+        "phe_server_wire_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -387,3 +396,56 @@ def server_matvec_packed_host(p: Params, w: Weights, ksk: KeySwitchKey, h_seeds:
                                                 _ptr(ksk.buf), _ptr(h_seeds), _ptr(h_body), h_seeds.shape[0],
                                                 chunk_tokens, _ptr(h_out), _stream()),
            "phe_server_matvec_packed_host")
+
+
+# ------------------------------------------------------------------ NEXT #2: wire format
+def wire_input_bytes(p: Params) -> int:
+    return load().phe_wire_input_bytes(ctypes.byref(p))
+
+
+def wire_output_bytes(p: Params) -> int:
+    return load().phe_wire_output_bytes(ctypes.byref(p))
+
+
+def wire_serialize_inputs(p: Params, seeds: torch.Tensor, body: torch.Tensor) -> torch.Tensor:
+    T, L = seeds.shape
+    out = torch.empty((T, L, wire_input_bytes(p)), dtype=torch.uint8, device=seeds.device)
+    _check(load().phe_wire_serialize_inputs(ctypes.byref(p), _ptr(seeds), _ptr(body), T, L, _ptr(out), _stream()),
+           "phe_wire_serialize_inputs")
+    return out
+
+
+def wire_deserialize_inputs(p: Params, wire: torch.Tensor):
+    T, L, _ = wire.shape
+    seeds = torch.empty((T, L), dtype=torch.int64, device=wire.device)
+    body = torch.empty((T, L, p.N), dtype=torch.int64, device=wire.device)
+    _check(load().phe_wire_deserialize_inputs(ctypes.byref(p), _ptr(wire), T, L, _ptr(seeds), _ptr(body),
+                                              _stream()), "phe_wire_deserialize_inputs")
+    return seeds, body
+
+
+def wire_serialize_packed(p: Params, packed: torch.Tensor) -> torch.Tensor:
+    T, G = packed.shape[:2]
+    out = torch.empty((T, G, wire_output_bytes(p)), dtype=torch.uint8, device=packed.device)
+    _check(load().phe_wire_serialize_packed(ctypes.byref(p), _ptr(packed), T * G, _ptr(out), _stream()),
+           "phe_wire_serialize_packed")
+    return out
+
+
+def wire_deserialize_packed(p: Params, wire: torch.Tensor) -> torch.Tensor:
+    T, G = wire.shape[:2]
+    out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=wire.device)
+    _check(load().phe_wire_deserialize_packed(ctypes.byref(p), _ptr(wire), T * G, _ptr(out), _stream()),
+           "phe_wire_deserialize_packed")
+    return out
+
+
+def server_wire_host(p: Params, w: Weights, ksk: KeySwitchKey, h_wire_in: torch.Tensor, h_wire_out: torch.Tensor,
+                     chunk_tokens: int = 255) -> None:
+    """The server step on wire bytes (host buffers): [T][L][9992] in -> [T][G][13312] out."""
+    for t, n in [(h_wire_in, "h_wire_in"), (h_wire_out, "h_wire_out")]:
+        if t.is_cuda or not t.is_contiguous():
+            raise PheError(f"{n} must be a contiguous host tensor")
+    _check(load().phe_server_wire_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
+                                       _ptr(ksk.buf), _ptr(h_wire_in), h_wire_in.shape[0], chunk_tokens,
+                                       _ptr(h_wire_out), _stream()), "phe_server_wire_host")

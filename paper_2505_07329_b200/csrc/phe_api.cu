@@ -556,3 +556,134 @@ extern "C" int phe_server_matvec_packed_host(const phe_params *p, const void *d_
   if (e != cudaSuccess) return phe_set_cuda_error(e);
   return PHE_OK;
 }
+
+// ------------------------------------------------------------------ NEXT #2: wire format
+static int check_wire(const phe_params *p, KParams *kp) {
+  int rc = check_gpu(p, kp);
+  if (rc) return rc;
+  if (p->q_in > 57 || p->N % 8) return PHE_EUNSUPPORTED;
+  return PHE_OK;
+}
+
+extern "C" {
+
+size_t phe_wire_input_bytes(const phe_params *p) {
+  return p ? (size_t)(8 + (int64_t)p->N * p->q_in / 8) : 0;
+}
+size_t phe_wire_output_bytes(const phe_params *p) {
+  return p ? (size_t)(2 * (int64_t)p->N * p->q_out / 8) : 0;
+}
+
+int phe_wire_serialize_inputs(const phe_params *p, const uint64_t *d_seeds, const uint64_t *d_body, int64_t T,
+                              int64_t L, uint8_t *d_wire, void *stream) {
+  KParams kp;
+  int rc = check_wire(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || L < 1) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_seeds || !d_body || !d_wire) return PHE_EINVAL;
+  return phe::launch_wire_inputs(kp, const_cast<uint64_t *>(d_seeds), const_cast<uint64_t *>(d_body), T * L, d_wire, 0,
+                                 S(stream));
+}
+
+int phe_wire_deserialize_inputs(const phe_params *p, const uint8_t *d_wire, int64_t T, int64_t L,
+                                uint64_t *d_seeds, uint64_t *d_body, void *stream) {
+  KParams kp;
+  int rc = check_wire(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || L < 1) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_seeds || !d_body || !d_wire) return PHE_EINVAL;
+  return phe::launch_wire_inputs(kp, d_seeds, d_body, T * L, const_cast<uint8_t *>(d_wire), 1, S(stream));
+}
+
+int phe_wire_serialize_packed(const phe_params *p, const uint32_t *d_packed, int64_t n_ct, uint8_t *d_wire,
+                              void *stream) {
+  KParams kp;
+  int rc = check_wire(p, &kp);
+  if (rc) return rc;
+  if (n_ct < 0) return PHE_EINVAL;
+  if (n_ct == 0) return PHE_OK;
+  if (!d_packed || !d_wire) return PHE_EINVAL;
+  return phe::launch_wire_packed(kp, const_cast<uint32_t *>(d_packed), n_ct, d_wire, 0, S(stream));
+}
+
+int phe_wire_deserialize_packed(const phe_params *p, const uint8_t *d_wire, int64_t n_ct, uint32_t *d_packed,
+                                void *stream) {
+  KParams kp;
+  int rc = check_wire(p, &kp);
+  if (rc) return rc;
+  if (n_ct < 0) return PHE_EINVAL;
+  if (n_ct == 0) return PHE_OK;
+  if (!d_packed || !d_wire) return PHE_EINVAL;
+  return phe::launch_wire_packed(kp, d_packed, n_ct, const_cast<uint8_t *>(d_wire), 1, S(stream));
+}
+
+// The server step as the network sees it (Fig. 1): wire-format input blocks in (9992 B each at
+// Table 1), wire-format packed ciphertexts out (13312 B each).  Chunked, two streams.
+int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
+                         const void *d_kprep, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
+                         uint8_t *h_wire_out, void *stream) {
+  KParams kp;
+  int rc = check_pack(p, &kp);
+  if (!rc) rc = check_wire(p, &kp);
+  if (rc) return rc;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  if (rows < 1 || cols < 1 || T < 0 || chunk_tokens < 1) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_wprep || !d_kprep || !h_wire_in || !h_wire_out) return PHE_EINVAL;
+  const int64_t N = p->N, L = phe_num_blocks(p, cols), G = (rows + N - 1) / N;
+  const int64_t bin = (int64_t)phe_wire_input_bytes(p), bout = (int64_t)phe_wire_output_bytes(p);
+  const int64_t C = chunk_tokens < T ? chunk_tokens : T;
+  const size_t b_win = round_up(C * L * bin, 256), b_seeds = round_up(C * L * 8, 256);
+  const size_t b_body = round_up(C * L * N * 8, 256);
+  const size_t b_op = round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256);
+  const size_t b_ws = round_up((int64_t)phe_packed_ws_bytes(p, rows, C), 256);
+  const size_t b_pk = round_up(C * G * 2 * N * 4, 256), b_wout = round_up(C * G * bout, 256);
+  const size_t slot = b_win + b_seeds + b_body + b_op + b_ws + b_pk + b_wout;
+  if (g_ws.bytes < 2 * slot) {
+    if (g_ws.buf) cudaFree(g_ws.buf);
+    g_ws.buf = nullptr; g_ws.bytes = 0;
+    if (cudaMalloc(&g_ws.buf, 2 * slot) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+    g_ws.bytes = 2 * slot;
+  }
+  if (!g_ws.st[0]) {
+    for (int s = 0; s < 2; s++)
+      if (cudaStreamCreateWithFlags(&g_ws.st[s], cudaStreamNonBlocking) != cudaSuccess)
+        return phe_set_cuda_error(cudaGetLastError());
+    if (cudaEventCreateWithFlags(&g_ws.ev, cudaEventDisableTiming) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+  }
+  cudaEventRecord(g_ws.ev, S(stream));
+  cudaStreamWaitEvent(g_ws.st[0], g_ws.ev, 0);
+  cudaStreamWaitEvent(g_ws.st[1], g_ws.ev, 0);
+  int64_t c = 0;
+  for (int64_t t0 = 0; t0 < T; t0 += C, c++) {
+    const int64_t n = (T - t0) < C ? (T - t0) : C;
+    cudaStream_t st = g_ws.st[c & 1];
+    uint8_t *base = static_cast<uint8_t *>(g_ws.buf) + (c & 1) * slot;
+    uint8_t *d_win = base;
+    uint64_t *d_seeds = reinterpret_cast<uint64_t *>(base + b_win);
+    uint64_t *d_bod = reinterpret_cast<uint64_t *>(base + b_win + b_seeds);
+    void *d_op = base + b_win + b_seeds + b_body;
+    void *d_wsp = base + b_win + b_seeds + b_body + b_op;
+    uint32_t *d_pk = reinterpret_cast<uint32_t *>(base + b_win + b_seeds + b_body + b_op + b_ws);
+    uint8_t *d_wout = base + b_win + b_seeds + b_body + b_op + b_ws + b_pk;
+    cudaMemcpyAsync(d_win, h_wire_in + t0 * L * bin, n * L * bin, cudaMemcpyHostToDevice, st);
+    rc = phe_wire_deserialize_inputs(p, d_win, n, L, d_seeds, d_bod, st);
+    if (!rc) rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
+    if (!rc) rc = phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws, d_pk, st);
+    if (!rc) rc = phe_wire_serialize_packed(p, d_pk, n * G, d_wout, st);
+    if (rc) return rc;
+    cudaMemcpyAsync(h_wire_out + t0 * G * bout, d_wout, n * G * bout, cudaMemcpyDeviceToHost, st);
+  }
+  cudaError_t e0 = cudaStreamSynchronize(g_ws.st[0]);
+  cudaError_t e1 = cudaStreamSynchronize(g_ws.st[1]);
+  if (e0 != cudaSuccess) return phe_set_cuda_error(e0);
+  if (e1 != cudaSuccess) return phe_set_cuda_error(e1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return phe_set_cuda_error(e);
+  return PHE_OK;
+}
+
+}  // extern "C"

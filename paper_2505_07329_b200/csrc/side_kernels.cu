@@ -536,4 +536,81 @@ int launch_decrypt_packed(const KParams &kp, const uint8_t *S, const uint32_t *p
   return PHE_OK;
 }
 
+// ================================================================== NEXT #2: wire format
+// Little-endian contiguous bitstream (R22): 8 words of `bits` bits -> exactly `bits`
+// bytes, one thread per 8-word group.  bits <= 57.
+template <typename WordT>
+__device__ __forceinline__ void pack8(const WordT *in, int bits, uint8_t *out) {
+  const uint64_t m = mask_bits(bits);
+  uint64_t buf = 0;
+  int nb = 0, o = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    buf |= ((uint64_t)in[k] & m) << nb;
+    nb += bits;
+    while (nb >= 8) { out[o++] = (uint8_t)buf; buf >>= 8; nb -= 8; }
+  }
+}
+template <typename WordT>
+__device__ __forceinline__ void unpack8(const uint8_t *in, int bits, WordT *out) {
+  const uint64_t m = mask_bits(bits);
+  uint64_t buf = 0;
+  int nb = 0, i = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    while (nb < bits) { buf |= (uint64_t)in[i++] << nb; nb += 8; }
+    out[k] = (WordT)(buf & m);
+    buf >>= bits;
+    nb -= bits;
+  }
+}
+
+// inputs: block (tau, i) -> [LE64 seed][N coefficients at q_in bits]
+__global__ void wire_inputs_kernel(int N, int q, uint64_t *__restrict__ seeds, uint64_t *__restrict__ body,
+                                   int64_t nblk, uint8_t *__restrict__ wire, int dir) {
+  const int64_t gpb = N / 8 + 1;  // 8-word groups per block, +1 for the seed
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nblk * gpb) return;
+  const int64_t blk = idx / gpb, g = idx % gpb;
+  const int64_t bb = 8 + (int64_t)N * q / 8;
+  uint8_t *w = wire + blk * bb;
+  if (g == N / 8) {  // the seed
+    if (dir == 0) for (int b = 0; b < 8; b++) w[b] = (uint8_t)(seeds[blk] >> (8 * b));
+    else { uint64_t sd = 0; for (int b = 0; b < 8; b++) sd |= (uint64_t)w[b] << (8 * b); seeds[blk] = sd; }
+    return;
+  }
+  if (dir == 0) pack8<uint64_t>(body + blk * N + 8 * g, q, w + 8 + g * q);
+  else unpack8<uint64_t>(w + 8 + g * q, q, body + blk * N + 8 * g);
+}
+
+// packed outputs: ciphertext (tau, g) -> [A' at q_out bits][B' at q_out bits]
+__global__ void wire_packed_kernel(int N, int q, uint32_t *__restrict__ packed, int64_t nct, uint8_t *__restrict__ wire,
+                                   int dir) {
+  const int64_t gpc = 2 * (int64_t)N / 8;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nct * gpc) return;
+  const int64_t ct = idx / gpc, g = idx % gpc;
+  uint8_t *w = wire + ct * (2 * (int64_t)N * q / 8) + g * q;
+  uint32_t *v = packed + ct * 2 * N + 8 * g;
+  if (dir == 0) pack8<uint32_t>(v, q, w);
+  else unpack8<uint32_t>(w, q, v);
+}
+
+int launch_wire_inputs(const KParams &kp, uint64_t *seeds, uint64_t *body, int64_t nblk, uint8_t *wire,
+                       int dir, cudaStream_t st) {
+  const int64_t n = nblk * (kp.N / 8 + 1);
+  if (n == 0) return PHE_OK;
+  wire_inputs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kp.N, kp.q_in, seeds, body, nblk, wire, dir);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_wire_packed(const KParams &kp, uint32_t *packed, int64_t nct, uint8_t *wire, int dir, cudaStream_t st) {
+  const int64_t n = nct * 2 * kp.N / 8;
+  if (n == 0) return PHE_OK;
+  wire_packed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kp.N, kp.q_out, packed, nct, wire, dir);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
 }  // namespace phe

@@ -32,6 +32,10 @@ int launch_pack_finalize(const KParams &kp, const void *acc, const uint64_t *bod
 int launch_decrypt_packed(const KParams &kp, const uint8_t *S, const uint32_t *packed, int64_t T, int64_t R,
                           int G, int q_bits, int32_t *y, cudaStream_t st);
 
+int launch_wire_inputs(const KParams &kp, uint64_t *seeds, uint64_t *body, int64_t nblk, uint8_t *wire,
+                       int dir, cudaStream_t st);
+int launch_wire_packed(const KParams &kp, uint32_t *packed, int64_t nct, uint8_t *wire, int dir, cudaStream_t st);
+
 // limb_gemm.cu: the tcgen05 int8 limb GEMM (mask = Hankel operand, body = plain operand).
 struct GemmArgs {
   KParams kp;

@@ -105,3 +105,11 @@ def test_product_package_does_not_import_oracle():
                 code = re.sub(r"#.*|//.*", "", code)
                 for bad in ("import oracle", "from oracle", "phe_oracle", "c_oracle"):
                     assert bad not in code, (f, bad)
+
+
+def test_wire_sizes_match_paper(lib):
+    """P:223-224 print 9992 B per seeded input block and 13312 B per packed output ciphertext."""
+    import paper_2505_07329_b200 as phe
+    p = phe.params(phe.PRESET_PAPER)
+    assert phe.wire_input_bytes(p) == 9992
+    assert phe.wire_output_bytes(p) == 13312
