@@ -341,25 +341,27 @@ def run_ours(args):
     # ---------------- e2e through the C ABI with host buffers
     e2e = None
     if not args.no_e2e and not args.profile and packed and not rows_mode:
+        # the server step as the network sees it: wire-format input blocks (9992 B) in,
+        # wire-format packed RLWE ciphertexts (13312 B) out, through host buffers
         name, w, _ = regs[0]
         seeds, body = inputs[(w.cols, w.transpose)]
-        hs = seeds.cpu().pin_memory()
-        hb = body.cpu().pin_memory()
-        ho = torch.empty((T, (w.rows + p.N - 1) // p.N, 2, p.N), dtype=torch.int32, pin_memory=True)
-        phe.server_matvec_packed_host(p, w, K, hs, hb, ho, chunk_tokens=255)
+        hi = phe.wire_serialize_inputs(p, seeds, body).cpu().pin_memory()
+        G0 = (w.rows + p.N - 1) // p.N
+        ho = torch.empty((T, G0, phe.wire_output_bytes(p)), dtype=torch.uint8, pin_memory=True)
+        phe.server_wire_host(p, w, K, hi, ho, chunk_tokens=255)
         wall = []
         for _ in range(max(2, min(args.steps, 3))):
             t0 = time.perf_counter()
-            phe.server_matvec_packed_host(p, w, K, hs, hb, ho, chunk_tokens=255)
+            phe.server_wire_host(p, w, K, hi, ho, chunk_tokens=255)
             wall.append(time.perf_counter() - t0)
         e2e_s = statistics.mean(wall)
         te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(world * T / float(te.item()), 2), "unit": "tokens/s",
-               "h2d_bytes_per_step": int(hs.numel() * 8 + hb.numel() * 8), "d2h_bytes_per_step": int(ho.numel() * 4),
+               "h2d_bytes_per_step": int(hi.numel()), "d2h_bytes_per_step": int(ho.numel()),
                "ms_per_step": round(float(te.item()) * 1e3, 2),
-               "api": "phe_server_matvec_packed_host (pinned host buffers, 255-token chunks, 2 streams)"}
+               "api": "phe_server_wire_host (wire-format bytes in/out, pinned host buffers, 255-token chunks)"}
     if not args.no_e2e and not args.profile and args.workload == "q_proj" and not rows_mode:
         name, w, _ = regs[0]
         seeds, body = inputs[(w.cols, w.transpose)]
