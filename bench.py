@@ -192,7 +192,7 @@ def run_ours(args):
         name0, w0, _ = regs[0]
         r256 = (w0.rows + 255) // 256 * 256
         G0 = (w0.rows + p.N - 1) // p.N
-        dig_buf = torch.empty((chunk, r256, 3, p.N), dtype=torch.int8, device=dev)
+        dig_buf = torch.empty((chunk, r256, phe.KS_LEVELS, p.N), dtype=torch.int8, device=dev)
         bod_buf = torch.empty((chunk, w0.rows), dtype=torch.int64, device=dev)
         acc_buf = torch.empty(phe.load().phe_pack_acc_bytes(__import__("ctypes").byref(p), w0.rows, chunk),
                               dtype=torch.uint8, device=dev)
@@ -316,8 +316,8 @@ def run_ours(args):
     mask_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") for n_, w, _ in regs)
     mask_ms = statistics.mean(parts_ms["mask_gemm"])
     pack_ops = 0.0
-    if packed:  # Eq. 8: 2 parts x Decomp(A_LWE) [rows x 3N] x KSK [3N x N], ell int8 MACs each
-        pack_ops = sum(2.0 * 2 * p.ell * 3 * p.N * p.N * w.rows * T for _, w, _ in regs)
+    if packed:  # Eq. 8: 2 parts x Decomp(A_LWE) [rows x 4N] x KSK [4N x N], ell int8 MACs each
+        pack_ops = sum(2.0 * 2 * p.ell * phe.KS_LEVELS * p.N * p.N * w.rows * T for _, w, _ in regs)
         mask_ops, mask_ms = pack_ops, statistics.mean(parts_ms["mask_gemm"])
     achieved = mask_ops / (mask_ms / 1e3) / 1e12
     traffic = None

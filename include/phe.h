@@ -168,18 +168,19 @@ int phe_server_matvec_host(const phe_params *p, const void *d_wprep, int64_t d_o
 
 /* ---- NEXT #1: KeySwitch packing of the LWE outputs into RLWE (Eq. 7; Eq. 8,
  * P:233-249) --------------------------------------------------------------------------------
- * Gadget: Decomp = signed balanced base-2^8 digits of the top 24 bits (3 levels) after rounding
- * the q_in - 24 bit tail half up (R18).  Requires q_in > 24.
- * KSK_{i,l} = RLWE_S(S'_i * 2^(q_in - 8(l+1))) for i < N, l < 3.
+ * Gadget: Decomp = signed balanced base-2^8 digits of the top 32 bits (4 levels) after rounding
+ * the q_in - 32 bit tail half up (R18: 4 levels because P:396's Fig. 4 claim
+ * fails with 3).  Requires q_in >= 32.
+ * KSK_{i,l} = RLWE_S(S'_i * 2^(q_in - 8(l+1))) for i < N, l < 4.
  *
- * phe_ksk_gen (client): d_ksk = uint64 [2][3N][N]: part 0 = KSK_A, part 1 = KSK_B, row l*N + i
+ * phe_ksk_gen (client): d_ksk = uint64 [2][4N][N]: part 0 = KSK_A, part 1 = KSK_B, row l*N + i
  *   (the batched matrices of Eq. 8).  Masks from ChaCha20(ksk_seed, "phe-ksk"), noise CBD(eta)
  *   from "phe-ksknoise" (R19).  Public key material: the server may hold it.            */
 size_t phe_ksk_bytes(const phe_params *p);
 int phe_ksk_gen(const phe_params *p, const uint8_t *d_S, uint64_t ksk_seed, void *d_ksk,
                 size_t bytes, void *stream);
 /* phe_ksk_prepare (server, once per key): KSK limb planes, the B operand of the packing GEMM
- * (uint8 [rows][3N], rows = phe_ksk_prep_bytes / 3N).                                      */
+ * (uint8 [rows][4N], rows = phe_ksk_prep_bytes / 4N).                                      */
 size_t phe_ksk_prep_bytes(const phe_params *p);
 int phe_ksk_prepare(const phe_params *p, const void *d_ksk, void *d_kprep, size_t bytes, void *stream);
 /* phe_matmul_clear_packed (server): the paper's whole primitive RLWE(Wx) for T tokens:
@@ -188,11 +189,11 @@ int phe_ksk_prepare(const phe_params *p, const void *d_ksk, void *d_kprep, size_
  *   d_out_packed: uint32 [T][G][2][N], G = ceil(R / N), R = rows of M (d_out, or d_in with
  *   transpose = 1); [..][0][..] = A', [..][1][..] = B'; output j sits in coefficient j mod N
  *   of ciphertext j / N.  d_ws: workspace of phe_packed_ws_bytes(p, R, T) bytes.
- *   Errors: EUNSUPPORTED unless ell in {4,5}, N % 256 == 0, q_in > 24.                       */
+ *   Errors: EUNSUPPORTED unless ell in {4,5}, N % 256 == 0, q_in >= 32.                      */
 size_t phe_packed_ws_bytes(const phe_params *p, int64_t rows, int64_t T);
 /* The two stages of phe_matmul_clear_packed, callable separately:
  * phe_matmul_clear_digits: Eq. 6 with the LWE masks written as Decomp digits, int8
- *   d_digits [T][R256][3][N] (R256 = R rounded up to 256; pad rows zeroed; plane l = digit of
+ *   d_digits [T][R256][4][N] (R256 = R rounded up to 256; pad rows zeroed; plane l = digit of
  *   weight 2^(q_in - 8(l+1))) and bodies d_body uint64 [T][R] at q_in.
  * phe_pack: Eq. 8 + Eq. 7 from those digits/bodies; d_acc: uint64 scratch of
  *   phe_pack_acc_bytes(p, R, T) bytes; output as phe_matmul_clear_packed.                    */

@@ -95,7 +95,7 @@ class COracle:
         return out
 
 
-    def ksk_gen(self, params, S, ksk_seed: int, eta: int = 0, base_log: int = 8, levels: int = 3,
+    def ksk_gen(self, params, S, ksk_seed: int, eta: int = 0, base_log: int = 8, levels: int = 4,
                 nthreads: int = 1):
         N = params.N
         S = np.ascontiguousarray(S, dtype=np.uint8)
@@ -105,7 +105,7 @@ class COracle:
                                 _p(KA, _u64p), _p(KB, _u64p), nthreads)
         return KA, KB
 
-    def pack(self, params, A_lwe, b_lwe, KA, KB, base_log: int = 8, levels: int = 3, nthreads: int = 1):
+    def pack(self, params, A_lwe, b_lwe, KA, KB, base_log: int = 8, levels: int = 4, nthreads: int = 1):
         N = params.N
         A_lwe = np.ascontiguousarray(A_lwe, dtype=np.uint64)
         b_lwe = np.ascontiguousarray(b_lwe, dtype=np.uint64)

@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libphe.so")
 
 PHE_OK, PHE_EINVAL, PHE_ERANGE, PHE_EMODULUS, PHE_ENOMEM, PHE_ECUDA, PHE_EUNSUPPORTED = range(7)
 PRESET_PAPER, PRESET_TOY = 0, 1
+KS_LEVELS = 4  # KeySwitch gadget levels (base 2^8), R18
 
 # every symbol include/phe.h declares (checked by tests/test_boundary.py)
 EXPORTS = [
@@ -359,11 +360,11 @@ def decrypt_packed(p: Params, S: torch.Tensor, packed: torch.Tensor, rows: int, 
 
 
 def matmul_clear_digits(p: Params, w: Weights, operand: torch.Tensor, T: int, digits=None, body=None):
-    """Stage 1 of the packed primitive: Eq. 6 with masks as Decomp digits (int8 [T][R256][3][N])
-    and bodies uint64 [T][R] (int64 storage)."""
+    """Stage 1 of the packed primitive: Eq. 6 with masks as Decomp digits (int8 [T][R256][4][N],
+    KS_LEVELS = 4) and bodies uint64 [T][R] (int64 storage)."""
     r256 = (w.rows + 255) // 256 * 256
     if digits is None:
-        digits = torch.empty((T, r256, 3, p.N), dtype=torch.int8, device=operand.device)
+        digits = torch.empty((T, r256, KS_LEVELS, p.N), dtype=torch.int8, device=operand.device)
     if body is None:
         body = torch.empty((T, w.rows), dtype=torch.int64, device=operand.device)
     _check(load().phe_matmul_clear_digits(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),

@@ -432,7 +432,7 @@ template <int MODE> struct Cfg2 {
   using OutT = typename std::conditional<MODE == OUT_U64, unsigned long long,
                typename std::conditional<MODE == OUT_U32, uint32_t, uint8_t>::type>::type;
   static constexpr int STAGES = MODE == OUT_U64 ? 6 : 8;
-  static constexpr int OUT_BUF = EPI_TOK * BM * (MODE == OUT_DIG ? 3 : (int)sizeof(OutT));  // 8/16/6 KB
+  static constexpr int OUT_BUF = EPI_TOK * BM * (MODE == OUT_DIG ? KS_LEVELS : (int)sizeof(OutT));  // 8/16/8 KB
   static constexpr int SMEM = 1024 + STAGES * (B_HALF_MAX + 4096) + 4 * OUT_BUF + 256;
 };
 
@@ -533,7 +533,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
                      const __grid_constant__ CUtensorMap map_out_tail, KArgs ka) {
   using C2 = Cfg2<MODE>;
   using OutT = typename C2::OutT;
-  constexpr bool SW = MODE != OUT_U64;  // OUT_DIG shifts by q_in - 24 (ka.out_bits = 24)
+  constexpr bool SW = MODE != OUT_U64;  // OUT_DIG shifts by q_in - 32 (ka.out_bits = 32)
   constexpr int S = C2::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -696,20 +696,26 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         named_bar(1 + grp, 128);  // the store that last read buffer nbuf has drained
         if (ka.dbg != 1) {
           if constexpr (MODE == OUT_DIG) {
-            // r = top 24 bits of v after rounding (tail q_in - 24); signed base-2^8 digits, least
-            // significant first with carry (Decomp, Eq. 4 / S:59-67); planes [tk][l][t]
+            // r = top 32 bits of v after rounding the q_in - 32 bit tail half up; signed base-2^8
+            // digits, least significant first with carry (Decomp, Eq. 4 / S:59-67; R18);
+            // planes [tk][l][t], plane l has weight 2^(q_in - 8(l+1))
             uint8_t *od = reinterpret_cast<uint8_t *>(ob);
 #pragma unroll
             for (int tk = 0; tk < EPI_TOK; tk++) {
               uint32_t r;
-              if constexpr (SH > 0) r = finish_sw<ELL, SH>(&v[tk * ELL], 0xFFFFFFu);
-              else r = (uint32_t)finish<ELL, true, uint32_t>(&v[tk * ELL], half, shift, 0xFFFFFFull);
-              int d2 = (int)(r & 255u); r >>= 8; if (d2 >= 128) { d2 -= 256; r += 1; }
-              int d1 = (int)(r & 255u); r >>= 8; if (d1 >= 128) { d1 -= 256; r += 1; }
-              int d0 = (int)(r & 255u);
-              od[(tk * 3 + 0) * BM + row] = (uint8_t)d0;
-              od[(tk * 3 + 1) * BM + row] = (uint8_t)d1;
-              od[(tk * 3 + 2) * BM + row] = (uint8_t)d2;
+              if constexpr (SH > 0) r = finish_sw<ELL, SH>(&v[tk * ELL], 0xFFFFFFFFu);
+              else if (shift == 0) r = (uint32_t)finish<ELL, false, uint64_t>(&v[tk * ELL], 0, 0, ~0ull);
+              else r = (uint32_t)finish<ELL, true, uint64_t>(&v[tk * ELL], half, shift, 0xFFFFFFFFull);
+              int d[KS_LEVELS];
+#pragma unroll
+              for (int l = KS_LEVELS - 1; l >= 0; l--) {
+                int dl = (int)(r & 255u);
+                r >>= 8;
+                if (dl >= 128) { dl -= 256; r += 1; }
+                d[l] = dl;
+              }
+#pragma unroll
+              for (int l = 0; l < KS_LEVELS; l++) od[(tk * KS_LEVELS + l) * BM + row] = (uint8_t)d[l];
             }
           } else {
 #pragma unroll
@@ -754,7 +760,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
 // Eq. 8 + the rotate-and-sum of Eq. 7 for T tokens at once:
 //   C[(tau,j), (part,k)] = sum_{(l,i)} Decomp(a_{tau,j})[l*N+i] * KSK_part[l*N+i][k]   (mod 2^q)
 // as an int8 (digits) x u8 (KSK limbs) GEMM on tcgen05 cta_group::2: M = rows (tau, j) (256
-// per pair), N = 51 coefficient slots x 5 limbs, K = 3N.  The epilogue recombines limbs and
+// per pair), N = 51 coefficient slots x 5 limbs, K = KS_LEVELS*N.  The epilogue recombines limbs and
 // applies Rotate(., j mod N) + the sum over j of Eq. 7 in shared-memory bins (a CTA's 128 rows
 // and 51 slots land on 178 consecutive output coefficients), then reduces the bins into the
 // packed accumulator [T][G][part][N] (uint64, mod 2^64) with global atomics.
@@ -767,7 +773,7 @@ struct PArgs {
   int64_t rows_pad;   // digit rows per token (multiple of 256)
   int G;              // output RLWE groups per token = ceil(R / N)
   int64_t total_tiles;
-  int k_blocks;       // 3N / BK
+  int k_blocks;       // KS_LEVELS*N / BK
   unsigned long long *acc;
 };
 constexpr int PK_STAGES = 6;
@@ -1044,7 +1050,7 @@ static int dispatch_2sm(int ell, const CUtensorMap &ma, const CUtensorMap &mb, c
                         const CUtensorMap &mot, const KArgs &ka, cudaStream_t st) {
   const int sh = ka.q_in - ka.out_bits;
   if (MODE != OUT_U64 && ell == 5 && sh == 13) return launch_2sm<5, MODE, 13>(ma, mb, mo, mot, ka, st);  // Table 1
-  if (MODE != OUT_U64 && ell == 5 && sh == 15) return launch_2sm<5, MODE, 15>(ma, mb, mo, mot, ka, st);  // digits, q=39
+  if (MODE != OUT_U64 && ell == 5 && sh == 7) return launch_2sm<5, MODE, 7>(ma, mb, mo, mot, ka, st);  // digits, q=39
   if (MODE != OUT_U64 && ell == 4 && sh == 4) return launch_2sm<4, MODE, 4>(ma, mb, mo, mot, ka, st);    // toy
   switch (ell) {
     case 4: return launch_2sm<4, MODE, 0>(ma, mb, mo, mot, ka, st);
@@ -1067,9 +1073,9 @@ static int choose_tpt(int64_t T, int ell, int *n_mma) {
 static int make_map_digits(CUtensorMap *m, void *base, int64_t N, int64_t Rpad, int64_t T, int box_tok) {
   auto enc = get_encode();
   if (!enc) return PHE_ECUDA;
-  cuuint64_t dims[4] = {(cuuint64_t)N, 3, (cuuint64_t)Rpad, (cuuint64_t)T};
-  cuuint64_t strides[3] = {(cuuint64_t)N, (cuuint64_t)(3 * N), (cuuint64_t)(3 * N * Rpad)};
-  cuuint32_t box[4] = {(cuuint32_t)BM, 3, 1, (cuuint32_t)box_tok};
+  cuuint64_t dims[4] = {(cuuint64_t)N, KS_LEVELS, (cuuint64_t)Rpad, (cuuint64_t)T};
+  cuuint64_t strides[3] = {(cuuint64_t)N, (cuuint64_t)(KS_LEVELS * N), (cuuint64_t)(KS_LEVELS * N * Rpad)};
+  cuuint32_t box[4] = {(cuuint32_t)BM, KS_LEVELS, 1, (cuuint32_t)box_tok};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -1166,7 +1172,7 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
       unsigned long long zero[8] = {0};
       if (km.dbg == 4) cudaMemcpyToSymbolAsync(g_dbg_cnt, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
       if (a.digits) {
-        km.out_bits = a.kp.q_in - 24 >= 1 ? 24 : a.kp.q_in;  // digits keep the top 24 bits
+        km.out_bits = KS_BITS;  // digits keep the top 32 bits (q_in >= 32)
         rc = dispatch_2sm<OUT_DIG>(ell, ma, mb, mo, mot, km, st);
       } else {
         rc = sw ? dispatch_2sm<OUT_U32>(ell, ma, mb, mo, mot, km, st) : dispatch_2sm<OUT_U64>(ell, ma, mb, mo, mot, km, st);
@@ -1206,13 +1212,13 @@ int launch_pack_gemm(const PackArgs &a, cudaStream_t st) {
   pa.tpt_rows = (int)(a.rows_pad / (2 * BM));
   pa.G = a.G;
   pa.total_tiles = (int64_t)a.T * pa.tpt_rows * pa.n_tiles;
-  pa.k_blocks = 3 * N / BK;
+  pa.k_blocks = KS_LEVELS * N / BK;
   pa.acc = static_cast<unsigned long long *>(a.acc);
   CUtensorMap ma, mb;
-  int rc = make_map_2d(&ma, a.digits, (uint64_t)(3 * N), (uint64_t)(a.T * a.rows_pad), (uint64_t)(3 * N), BK, BM,
+  int rc = make_map_2d(&ma, a.digits, (uint64_t)(KS_LEVELS * N), (uint64_t)(a.T * a.rows_pad), (uint64_t)(KS_LEVELS * N), BK, BM,
                        CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  rc = make_map_2d(&mb, a.kplanes, (uint64_t)(3 * N), (uint64_t)a.kplane_rows, (uint64_t)(3 * N), BK, BN / 2,
+  rc = make_map_2d(&mb, a.kplanes, (uint64_t)(KS_LEVELS * N), (uint64_t)a.kplane_rows, (uint64_t)(KS_LEVELS * N), BK, BN / 2,
                    CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   auto kern = ell == 5 ? pack_gemm_2sm_kernel<5> : pack_gemm_2sm_kernel<4>;

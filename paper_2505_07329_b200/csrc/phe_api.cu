@@ -339,14 +339,14 @@ static inline int64_t ks_plane_rows(const phe_params *p) {
 static int check_pack(const phe_params *p, KParams *kp) {
   int rc = check_gpu(p, kp);
   if (rc) return rc;
-  if (p->q_in <= 24 || (kp->ell != 4 && kp->ell != 5) || p->N % 256) return PHE_EUNSUPPORTED;
+  if (p->q_in < phe::KS_BITS || (kp->ell != 4 && kp->ell != 5) || p->N % 256) return PHE_EUNSUPPORTED;
   return PHE_OK;
 }
 
 extern "C" {
 
 size_t phe_ksk_bytes(const phe_params *p) {
-  return p ? (size_t)2 * 3 * p->N * (size_t)p->N * 8 : 0;
+  return p ? (size_t)2 * phe::KS_LEVELS * p->N * (size_t)p->N * 8 : 0;
 }
 
 int phe_ksk_gen(const phe_params *p, const uint8_t *d_S, uint64_t ksk_seed, void *d_ksk, size_t bytes,
@@ -356,12 +356,12 @@ int phe_ksk_gen(const phe_params *p, const uint8_t *d_S, uint64_t ksk_seed, void
   if (rc) return rc;
   if (!d_S || !d_ksk) return PHE_EINVAL;
   if (bytes < phe_ksk_bytes(p)) return PHE_ENOMEM;
-  uint64_t *KA = static_cast<uint64_t *>(d_ksk), *KB = KA + (int64_t)3 * p->N * p->N;
+  uint64_t *KA = static_cast<uint64_t *>(d_ksk), *KB = KA + (int64_t)phe::KS_LEVELS * p->N * p->N;
   return phe::launch_ksk_gen(kp, d_S, ksk_seed, KA, KB, S(stream));
 }
 
 size_t phe_ksk_prep_bytes(const phe_params *p) {
-  return p ? (size_t)ks_plane_rows(p) * 3 * (size_t)p->N : 0;
+  return p ? (size_t)ks_plane_rows(p) * phe::KS_LEVELS * (size_t)p->N : 0;
 }
 
 int phe_ksk_prepare(const phe_params *p, const void *d_ksk, void *d_kprep, size_t bytes, void *stream) {
@@ -377,7 +377,8 @@ int phe_ksk_prepare(const phe_params *p, const void *d_ksk, void *d_kprep, size_
 size_t phe_packed_ws_bytes(const phe_params *p, int64_t rows, int64_t T) {
   if (!p || rows < 1 || T < 0) return 0;
   const int64_t N = p->N, rp = round_up(rows, 256), G = (rows + N - 1) / N;
-  return (size_t)(round_up(T * rp * 3 * N, 256) + round_up(T * rows * 8, 256) + round_up(T * G * 2 * N * 8, 256));
+  return (size_t)(round_up(T * rp * phe::KS_LEVELS * N, 256) + round_up(T * rows * 8, 256) +
+                  round_up(T * G * 2 * N * 8, 256));
 }
 
 int phe_matmul_clear_digits(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
@@ -399,7 +400,8 @@ int phe_matmul_clear_digits(const phe_params *p, const void *d_wprep, int64_t d_
   if (rc) return rc;
   launches += g_last_launches;
   if (rp > rows) {  // zero digit rows of the 256-row padding (they contribute nothing)
-    if (cudaMemset2DAsync(digits + rows * 3 * N, (size_t)(rp * 3 * N), 0, (size_t)((rp - rows) * 3 * N),
+    const int64_t KL = phe::KS_LEVELS * N;
+    if (cudaMemset2DAsync(digits + rows * KL, (size_t)(rp * KL), 0, (size_t)((rp - rows) * KL),
                           (size_t)T, st) != cudaSuccess)
       return phe_set_cuda_error(cudaGetLastError());
   }
@@ -469,7 +471,7 @@ int phe_matmul_clear_packed(const phe_params *p, const void *d_wprep, int64_t d_
   if (ws_bytes < phe_packed_ws_bytes(p, rows, T)) return PHE_ENOMEM;
   const int64_t N = p->N, rp = round_up(rows, 256);
   uint8_t *digits = static_cast<uint8_t *>(d_ws);
-  uint64_t *body = reinterpret_cast<uint64_t *>(digits + round_up(T * rp * 3 * N, 256));
+  uint64_t *body = reinterpret_cast<uint64_t *>(digits + round_up(T * rp * phe::KS_LEVELS * N, 256));
   void *acc = reinterpret_cast<uint8_t *>(body) + round_up(T * rows * 8, 256);
   // (1) LWE outputs of Eq. 6: body at q_in, masks as Decomp digits (Eq. 8's left operand)
   rc = phe_matmul_clear_digits(p, d_wprep, d_out, d_in, transpose, d_operand, T, digits, body, stream);

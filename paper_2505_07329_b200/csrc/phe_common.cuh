@@ -33,9 +33,11 @@ __host__ __device__ constexpr Nonce nonce_noise() { return {0x2d656870u, 0x73696
 __host__ __device__ constexpr Nonce nonce_ksk() { return {0x2d656870u, 0x006b736bu, 0u}; }
 __host__ __device__ constexpr Nonce nonce_ksk_noise() { return {0x2d656870u, 0x6e6b736bu, 0x6573696fu}; }
 
-// KeySwitch gadget (Decomp) parameters: base 2^8, 3 levels (R18)
+// KeySwitch gadget (Decomp) parameters: base 2^8, 4 levels = top 32 bits (R18: P:396's
+// Fig. 4 claim, < 1% error at bit positions >= 12, needs the 4th level; 3 levels fail it)
 constexpr int KS_BASE_LOG = 8;
-constexpr int KS_LEVELS = 3;
+constexpr int KS_LEVELS = 4;
+constexpr int KS_BITS = KS_BASE_LOG * KS_LEVELS;  // 32
 
 __device__ __forceinline__ uint32_t rotl(uint32_t v, int c) { return __funnelshift_l(v, v, c); }
 

@@ -417,7 +417,7 @@ ksk_gen_kernel(KParams kp, const uint8_t *__restrict__ S, uint64_t seed, uint64_
 __global__ void ksk_planes_kernel(const uint64_t *__restrict__ ksk, int N, int ell, int kpad,
                                   int64_t rows, uint8_t *__restrict__ planes) {
   __shared__ uint64_t tile[32][33];
-  const int64_t K3 = 3 * (int64_t)N;
+  const int64_t K3 = KS_LEVELS * (int64_t)N;
   const int part = blockIdx.z;
   const int64_t c0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
   const uint64_t *src = ksk + (int64_t)part * K3 * N;
@@ -509,9 +509,9 @@ int launch_ksk_gen(const KParams &kp, const uint8_t *S, uint64_t seed, uint64_t 
 
 int launch_ksk_planes(const KParams &kp, const uint64_t *ksk, int kpad, int64_t rows, uint8_t *planes,
                       cudaStream_t st) {
-  if (cudaMemsetAsync(planes, 0, (size_t)rows * 3 * kp.N, st) != cudaSuccess)
+  if (cudaMemsetAsync(planes, 0, (size_t)rows * KS_LEVELS * kp.N, st) != cudaSuccess)
     return phe_set_cuda_error(cudaGetLastError());
-  dim3 grid((unsigned)((kpad + 31) / 32), (unsigned)((3 * kp.N + 31) / 32), 2);
+  dim3 grid((unsigned)((kpad + 31) / 32), (unsigned)((KS_LEVELS * kp.N + 31) / 32), 2);
   ksk_planes_kernel<<<grid, dim3(32, 8), 0, st>>>(ksk, kp.N, kp.ell, kpad, rows, planes);
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;

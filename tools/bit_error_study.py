@@ -1,0 +1,71 @@
+"""Fig. 4 analog: bit-error rate of decrypted homomorphic dot products
+by bit position, for d_in in {768, 2048, 8192} at N = 2048, through the whole server primitive
+(seeded RLWE inputs with noise, Eq. 6, KeySwitch packing Eq. 7/8, 39 -> 26 switch).
+
+Random integer vectors (uniform int8) x and weights w.  Noise (R5): Table 1's
+sigma_ksk = 2.845e-15 is ~1.6e-3 at q = 2^39, i.e. E_ksk = 0 after rounding; the input noise
+uses CBD(eta) as a stand-in (the same sigma also rounds to 0, but some input noise is what makes
+the LSB error grow with d_in).  Packing noise from a noisy KSK would grow with d_out.  Writes CSV rows (d_in, bit_position, error_rate, trials) — the data behind a
+Fig. 4 heatmap.  GPU tool; the assertion of the paper's claim lives in tests/test_gpu_fig4.py.
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def run(d_ins=(768, 2048, 8192), trials=65536, eta=21, seed=4, beta_bits=27):
+    import torch
+
+    import paper_2505_07329_b200 as phe
+    import synth
+
+    p = phe.params(phe.PRESET_PAPER, noise_eta=eta)
+    p_ksk = phe.params(phe.PRESET_PAPER, noise_eta=0)   # sigma_ksk rounds to 0 (R5)
+    S = phe.keygen(p, seed)
+    K = phe.KeySwitchKey(p_ksk, phe.ksk_gen(p_ksk, S, seed + 1))
+    d_out = 2048
+    T = max(1, trials // d_out)
+    rows = []
+    for d_in in d_ins:
+        W = torch.from_numpy(synth.uniform_int8((d_out, d_in), seed + d_in)).cuda()
+        x = torch.from_numpy(synth.uniform_int8((T, d_in), seed + 2 * d_in)).cuda()
+        seeds, body = phe.encrypt_pack(p, S, x, 1000 + d_in, 7 + d_in)
+        w = phe.Weights(p, W)
+        op = phe.ct_prepare(p, seeds, body)
+        packed = phe.matmul_clear_packed(p, w, op, T, K)
+        y = phe.decrypt_packed(p, S, packed, d_out).cpu().numpy().astype(np.int64)
+        truth = (x.cpu().numpy().astype(np.int64) @ W.cpu().numpy().astype(np.int64).T)
+        diff = (y ^ truth) & ((1 << beta_bits) - 1)
+        n = diff.size
+        for b in range(beta_bits):
+            rows.append((d_in, b, float(((diff >> b) & 1).sum()) / n, n))
+        del w, op, packed
+    return rows
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--trials", type=int, default=65536)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_fig4_bit_errors.csv"))
+    a = ap.parse_args()
+    rows = run(trials=a.trials)
+    with open(a.out, "w", newline="") as f:
+        wr = csv.writer(f)
+        wr.writerow(["d_in", "bit_position", "error_rate", "trials"])
+        wr.writerows(rows)
+    for d_in in sorted({r[0] for r in rows}):
+        rr = [r for r in rows if r[0] == d_in]
+        print(d_in, " ".join(f"{r[1]}:{r[2]:.4f}" for r in rr if r[1] in (0, 4, 6, 8, 10, 11, 12, 13, 14, 16, 20)),
+              "max>=12:", max(r[2] for r in rr if r[1] >= 12))
+
+
+if __name__ == "__main__":
+    main()

@@ -28,7 +28,7 @@ for _ in range(a.reps):
     e0.record(); phe.matmul_clear_packed(p, w, op, a.T, K, out=out); e1.record()
     torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
 ms = statistics.median(ts)
-pack_ops = 2.0 * 2 * p.ell * 3 * p.N * p.N * a.d_out * a.T
+pack_ops = 2.0 * 2 * p.ell * phe.KS_LEVELS * p.N * p.N * a.d_out * a.T
 hot_ops = 2.0 * p.ell * a.d_out * a.d_in * (p.N + 1) * a.T
 print(f"{a.d_out}x{a.d_in} T={a.T}: packed primitive {ms:.2f} ms, {a.T / ms * 1e3:.1f} tok/s, "
       f"int8 TOP/s (pack+hot) {(pack_ops + hot_ops) / ms / 1e9:.0f}")
