@@ -308,9 +308,9 @@ def last_launch_count() -> int:
 
 # ------------------------------------------------------------------ NEXT #1: KeySwitch packing
 def ksk_gen(p: Params, S: torch.Tensor, ksk_seed: int) -> torch.Tensor:
-    """Client: KSK_A, KSK_B as int64 [2][3N][N] (u64 bits), row l*N + i (Eq. 8's matrices)."""
+    """Client: KSK_A, KSK_B as int64 [2][4N][N] (u64 bits), row l*N + i (Eq. 8 matrices)."""
     _dev(S, torch.uint8, "S")
-    ksk = torch.empty((2, 3 * p.N, p.N), dtype=torch.int64, device=S.device)
+    ksk = torch.empty((2, KS_LEVELS * p.N, p.N), dtype=torch.int64, device=S.device)
     _check(load().phe_ksk_gen(ctypes.byref(p), _ptr(S), ksk_seed & (2**64 - 1), _ptr(ksk), ksk.numel() * 8,
                               _stream()), "phe_ksk_gen")
     return ksk
