@@ -240,6 +240,45 @@ int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out
                          int transpose, const void *d_kprep, const uint8_t *h_wire_in, int64_t T,
                          int64_t chunk_tokens, uint8_t *h_wire_out, void *stream);
 
+/* ---- NEXT #4: the mask contraction a5 in the NTT domain ---------
+ * Same contract and bit-identical results as phe_matmul_clear(_T): Eq. 6 defines the
+ * LWE outputs uniquely.  Computed as negacyclic products in Z_p[X]/(X^N + 1) (X^N = -1)
+ * for two primes p0 = 15*2^27+1 and p1 = 63*2^25+1 (forward NTT, pointwise sum over blocks i,
+ * inverse NTT; CUDA cores, not tensor cores); the exact integer product is recovered by CRT and
+ * reduced mod 2^q_in, since power-of-two moduli admit no NTT (R23).
+ * Requirements: N a power of two in [512, 8192] and L <= phe_ntt_max_blocks(p) (CRT
+ * exactness: L*N*(2^q_in - 1)*128 < p0*p1/2; 14 blocks for Table 1), else PHE_EUNSUPPORTED.
+ *   d_tables  phe_ntt_tables_bytes(p): uint2 [2 dirs][2 primes][N] twiddles (w, floor(w 2^32/p)),
+ *             dir 0 = psi^bitrev(k), dir 1 = psi^-bitrev(k), then uint2 [2 primes][15][N/16], the
+ *             inverse twiddles of stages 0-3 regrouped per thread of the hot kernel; written
+ *             once by phe_ntt_tables_init; read-only afterwards; shared by every call with p.
+ *   d_nttw    phe_ntt_weights_bytes(p, rows, cols), rows/cols of M = W (transpose 0) or W^T:
+ *               [rows][Lc][2][N] uint32  NTT_p(w_hat_ij) * N^-1 * 2^32 mod p (bit-reversed order;
+ *                                        w_hat_ij[k] = M[j, iN+N-1-k])
+ *               [round128(rows)][Lc*N] int8  M zero-padded (body GEMM operand)
+ *   d_operand phe_ntt_operand_bytes(p, T, L):
+ *               [T][L][2][N] uint32  NTT_p(A_{tau,i} mod p), A = PRNG(seed) mod 2^q_in
+ *               [op_rows][L*N] uint8 body limb planes (the second half of phe_ct_prepare's layout)
+ * Errors as phe_matmul_clear; EUNSUPPORTED for N or L outside the range above.              */
+int phe_ntt_primes(uint32_t *out2);
+int64_t phe_ntt_max_blocks(const phe_params *p);
+size_t phe_ntt_tables_bytes(const phe_params *p);
+int phe_ntt_tables_init(const phe_params *p, void *d_tables, size_t bytes, void *stream);
+size_t phe_ntt_weights_bytes(const phe_params *p, int64_t rows, int64_t cols);
+int phe_ntt_weights_prepare(const phe_params *p, const void *d_tables, const int8_t *d_W,
+                            int64_t d_out, int64_t d_in, int transpose, void *d_nttw, size_t bytes,
+                            void *stream);
+size_t phe_ntt_operand_bytes(const phe_params *p, int64_t T, int64_t L);
+int phe_ntt_ct_prepare(const phe_params *p, const void *d_tables, const uint64_t *d_seeds,
+                       const uint64_t *d_body, int64_t T, int64_t L, void *d_operand, size_t bytes,
+                       void *stream);
+int phe_matmul_clear_ntt(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                         int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
+                         int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);
+int phe_matmul_clear_ntt_T(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                           int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
+                           int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);
+
 /* ---- introspection (tests / bench) -------------------------------------------------- */
 /* Number of kernel launches the last phe_matmul_clear[_T] on this thread enqueued. */
 int phe_last_launch_count(void);

@@ -35,6 +35,9 @@ EXPORTS = [
     "phe_pack", "phe_server_matvec_packed_host",
     "phe_wire_input_bytes", "phe_wire_output_bytes", "phe_wire_serialize_inputs", "phe_wire_deserialize_inputs",
     "phe_wire_serialize_packed", "phe_wire_deserialize_packed", "phe_server_wire_host",
+    "phe_ntt_primes", "phe_ntt_max_blocks", "phe_ntt_tables_bytes", "phe_ntt_tables_init",
+    "phe_ntt_weights_bytes", "phe_ntt_weights_prepare", "phe_ntt_operand_bytes", "phe_ntt_ct_prepare",
+    "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T",
 ]
 
 
@@ -113,6 +116,18 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_wire_serialize_packed": ([_P, _vp, _i64, _vp, _vp], ctypes.c_int),
         "phe_wire_deserialize_packed": ([_P, _vp, _i64, _vp, _vp], ctypes.c_int),
         "phe_server_wire_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
+        "phe_ntt_primes": ([_vp], ctypes.c_int),
+        "phe_ntt_max_blocks": ([_P], _i64),
+        "phe_ntt_tables_bytes": ([_P], _sz),
+        "phe_ntt_tables_init": ([_P, _vp, _sz, _vp], ctypes.c_int),
+        "phe_ntt_weights_bytes": ([_P, _i64, _i64], _sz),
+        "phe_ntt_weights_prepare": ([_P, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _sz, _vp], ctypes.c_int),
+        "phe_ntt_operand_bytes": ([_P, _i64, _i64], _sz),
+        "phe_ntt_ct_prepare": ([_P, _vp, _vp, _vp, _i64, _i64, _vp, _sz, _vp], ctypes.c_int),
+        "phe_matmul_clear_ntt": ([_P, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _i32, _vp, _vp, _vp],
+                                 ctypes.c_int),
+        "phe_matmul_clear_ntt_T": ([_P, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _i32, _vp, _vp, _vp],
+                                   ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -450,3 +465,70 @@ def server_wire_host(p: Params, w: Weights, ksk: KeySwitchKey, h_wire_in: torch.
     _check(load().phe_server_wire_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
                                        _ptr(ksk.buf), _ptr(h_wire_in), h_wire_in.shape[0], chunk_tokens,
                                        _ptr(h_wire_out), _stream()), "phe_server_wire_host")
+
+
+# ------------------------------------------------------------------ NEXT #4: NTT-domain contraction
+def ntt_primes() -> tuple[int, int]:
+    """The two NTT primes (p0, p1) of the NTT path (host query, no GPU needed)."""
+    out = (ctypes.c_uint32 * 2)()
+    _check(load().phe_ntt_primes(ctypes.cast(out, ctypes.c_void_p)), "phe_ntt_primes")
+    return int(out[0]), int(out[1])
+
+
+def ntt_max_blocks(p: Params) -> int:
+    """Largest L = ceil(cols/N) for which the two-prime CRT recovers Eq. 6's integers exactly."""
+    return int(load().phe_ntt_max_blocks(ctypes.byref(p)))
+
+
+class NttTables:
+    """Twiddle tables for params p (phe_ntt_tables_init); shared by every NTT-path call."""
+
+    def __init__(self, p: Params, device="cuda"):
+        self.p = p
+        nbytes = load().phe_ntt_tables_bytes(ctypes.byref(p))
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _check(load().phe_ntt_tables_init(ctypes.byref(p), _ptr(self.buf), nbytes, _stream()),
+               "phe_ntt_tables_init")
+
+
+class NttWeights:
+    """W (or W^T) registered in the NTT domain (phe_ntt_weights_prepare)."""
+
+    def __init__(self, p: Params, tables: NttTables, W: torch.Tensor, transpose: bool = False):
+        _dev(W, torch.int8, "W")
+        self.p, self.tables = p, tables
+        self.d_out, self.d_in = W.shape
+        self.transpose = bool(transpose)
+        self.rows, self.cols = (self.d_in, self.d_out) if transpose else (self.d_out, self.d_in)
+        nbytes = load().phe_ntt_weights_bytes(ctypes.byref(p), self.rows, self.cols)
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=W.device)
+        _check(load().phe_ntt_weights_prepare(ctypes.byref(p), _ptr(tables.buf), _ptr(W), self.d_out, self.d_in,
+                                              int(transpose), _ptr(self.buf), nbytes, _stream()),
+               "phe_ntt_weights_prepare")
+
+
+def ntt_ct_prepare(p: Params, tables: NttTables, seeds: torch.Tensor, body: torch.Tensor,
+                   out: torch.Tensor | None = None):
+    """Forward NTTs of the expanded masks + body limb planes (phe_ntt_ct_prepare)."""
+    _dev(seeds, torch.int64, "seeds"); _dev(body, torch.int64, "body")
+    T, L = seeds.shape
+    nbytes = load().phe_ntt_operand_bytes(ctypes.byref(p), T, L)
+    if out is None:
+        out = torch.empty(nbytes, dtype=torch.uint8, device=seeds.device)
+    _check(load().phe_ntt_ct_prepare(ctypes.byref(p), _ptr(tables.buf), _ptr(seeds), _ptr(body), T, L,
+                                     _ptr(out), out.numel(), _stream()), "phe_ntt_ct_prepare")
+    return out
+
+
+def matmul_clear_ntt(p: Params, w: NttWeights, operand: torch.Tensor, T: int, out_bits: int | None = None,
+                     row_begin: int = 0, row_end: int | None = None, out_mask=None, out_body=None):
+    """Same contract and bit-identical result as matmul_clear / matmul_clear_T (by w.transpose),
+    mask contraction in the NTT domain (NEXT #4)."""
+    out_bits = p.q_out if out_bits is None else out_bits
+    row_end = w.rows if row_end is None else row_end
+    out_mask, out_body = _outputs(p, T, row_end - row_begin, out_bits, operand.device, out_mask, out_body)
+    fn = load().phe_matmul_clear_ntt_T if w.transpose else load().phe_matmul_clear_ntt
+    _check(fn(ctypes.byref(p), _ptr(w.tables.buf), _ptr(w.buf), w.d_out, w.d_in, row_begin, row_end,
+              _ptr(operand), T, out_bits, _ptr(out_mask), _ptr(out_body), _stream()), "phe_matmul_clear_ntt")
+    return out_mask, out_body
+

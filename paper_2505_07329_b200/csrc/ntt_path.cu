@@ -1,0 +1,507 @@
+// ntt_path.cu — NEXT #4: the mask contraction a5 computed in the NTT domain.
+//
+// Eq. 6 needs, per token tau and output row j, the mask polynomial
+//   P_{tau,j} = sum_i A_{tau,i} * w_hat_ij   in Z[X]/(X^N + 1)          (negacyclic)
+// and then SampleExtract at h = N-1 (Eq. 2): a'_t = P[N-1-t].  The paper computes the
+// products "coefficient-wise".  Power-of-two moduli have no NTT, so this path
+// computes the EXACT integer P (|P| <= L*N*(2^q_in - 1)*128 < 2^60 for Table 1 parameters)
+// with negacyclic NTTs modulo two 31-bit primes p0, p1 (p0*p1 > 2^61.8), recovers it by CRT,
+// and reduces mod 2^q_in.  The result is bit-identical to the dense limb GEMM (limb_gemm.cu):
+// both produce the unique value Eq. 6 defines.
+//
+// Work per output coefficient: L Montgomery products per prime (pointwise) + (log2 N)/2 GS
+// butterflies per prime (inverse NTT) + CRT + ModulusSwitch — O(L + log N) instead of the
+// dense path's O(L*N) MACs; it runs on the integer ALUs (CUDA cores), not the tensor cores.
+//
+// Kernels:
+//   ntt_tables_kernel    psi^{bitrev(k)}, psi^{-bitrev(k)} with Shoup companions, both primes
+//   ntt_weights_kernel   W_hat_ij = NTT(w_hat_ij) * N^{-1} * 2^32 (Montgomery form)  [server, once]
+//   ntt_masks_kernel     A_hat_{tau,i} = NTT(PRNG(seed_{tau,i}) mod p)                [per batch]
+//   ntt_mask_kernel<LOGN> the hot kernel: pointwise sum over i, inverse NTT in registers +
+//                        shared memory (N/16 threads, 16 values per prime per thread, 4-bit
+//                        phases, XOR-swizzled exchanges: tools/ntt_model.py checks the index
+//                        scheme and bank-conflict freedom), CRT, mod 2^q_in, SampleExtract
+//                        reversal, fused ModulusSwitch, coalesced stores.
+#include <cstdint>
+#include <cstdio>
+
+#include "phe_common.cuh"
+#include "side_kernels.cuh"
+
+namespace phe {
+namespace ntt {
+
+// ---------------------------------------------------------------- primes and constants
+// p0 = 15*2^27 + 1 (generator 31), p1 = 63*2^25 + 1 (generator 5): both < 2^31, both
+// = 1 mod 2^14 (negacyclic NTTs up to N = 8192).  p0 < p1 (the CRT step needs r0 < p1).
+constexpr uint32_t P0 = 2013265921u, P1 = 2113929217u;
+constexpr uint32_t GEN0 = 31u, GEN1 = 5u;
+
+__host__ __device__ constexpr uint32_t neg_inv32(uint32_t p) {
+  uint32_t x = p;  // Newton: x <- x*(2 - p*x) doubles the correct low bits (p odd)
+  for (int i = 0; i < 5; i++) x *= 2u - p * x;
+  return 0u - x;
+}
+__host__ __device__ constexpr uint32_t pw(uint64_t b, uint64_t e, uint32_t p) {
+  uint64_t r = 1;
+  b %= p;
+  while (e) {
+    if (e & 1) r = r * b % p;
+    b = b * b % p;
+    e >>= 1;
+  }
+  return (uint32_t)r;
+}
+constexpr uint32_t PINV0 = neg_inv32(P0), PINV1 = neg_inv32(P1);
+constexpr uint32_t CRT_C = pw(P0, P1 - 2, P1);  // p0^{-1} mod p1
+constexpr uint32_t CRT_CQ = (uint32_t)(((uint64_t)CRT_C << 32) / P1);
+constexpr uint64_t CRT_M = (uint64_t)P0 * P1;
+static_assert((uint32_t)(P0 * (0u - PINV0)) == 1u, "Montgomery constant p0");
+static_assert((uint32_t)(P1 * (0u - PINV1)) == 1u, "Montgomery constant p1");
+static_assert((uint64_t)P0 * CRT_C % P1 == 1, "CRT constant");
+
+__device__ __forceinline__ uint32_t prime(int pr) { return pr ? P1 : P0; }
+__device__ __forceinline__ uint32_t pinv(int pr) { return pr ? PINV1 : PINV0; }
+
+// a, b < p < 2^31
+__device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) {
+  const uint32_t s = a + b;
+  return min(s, s - p);
+}
+// x < 2^32 arbitrary, w < p, wq = floor(w 2^32 / p): x*w mod p (Shoup), result < p
+__device__ __forceinline__ uint32_t mul_shoup(uint32_t x, uint32_t w, uint32_t wq, uint32_t p) {
+  const uint32_t q = __umulhi(x, wq);
+  const uint32_t r = x * w - q * p;
+  return min(r, r - p);
+}
+// a, b < p: a*b*2^-32 mod p (Montgomery), result < p
+__device__ __forceinline__ uint32_t mul_mont(uint32_t a, uint32_t b, uint32_t p, uint32_t pi) {
+  const uint64_t t = (uint64_t)a * b;
+  const uint32_t m = (uint32_t)t * pi;
+  const uint32_t u = (uint32_t)((t + (uint64_t)m * p) >> 32);
+  return min(u, u - p);
+}
+
+__device__ __forceinline__ uint32_t brev(uint32_t k, int logN) { return __brev(k) >> (32 - logN); }
+
+// ---------------------------------------------------------------- tables
+// d_tables layout: uint2 [2 dirs][2 primes][N]; dir 0 = psi^{bitrev(k)} (forward CT),
+// dir 1 = psi^{-bitrev(k)} (inverse GS); .x = w, .y = floor(w 2^32 / p).  psi = g^((p-1)/2N)
+// is a primitive 2N-th root of unity (psi^N = -1: the negacyclic twist, X^N = -1).
+// Followed by the phase-1 section used by the hot kernel: uint2 [2 primes][15][N/16], entry
+// [pr][P1OFF[s] + m][t] = inverse twiddle (N >> (s+1)) + t 2^(3-s) + m for stages s = 0..3 of the
+// inverse NTT (thread t's m-th twiddle of stage s), so that a warp's loads are contiguous.
+__host__ __device__ constexpr int p1off(int s) { return s == 0 ? 0 : s == 1 ? 8 : s == 2 ? 12 : 14; }
+__global__ void ntt_tables_kernel(int logN, uint32_t psi0, uint32_t psi1, uint2 *__restrict__ tab) {
+  const int N = 1 << logN, NT = N / 16;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= 4 * N + 2 * 15 * NT) return;
+  int k, pr, dir;
+  if (idx < 4 * N) {
+    k = idx % N; pr = (idx / N) & 1; dir = idx / (2 * N);
+  } else {
+    const int r = idx - 4 * N, t = r % NT, slot = (r / NT) % 15;
+    pr = r / (15 * NT); dir = 1;
+    const int s = slot >= 14 ? 3 : slot >= 12 ? 2 : slot >= 8 ? 1 : 0;
+    k = (N >> (s + 1)) + t * (1 << (3 - s)) + (slot - p1off(s));
+  }
+  const uint32_t p = prime(pr), psi = pr ? psi1 : psi0;
+  const uint32_t e = brev((uint32_t)k, logN);
+  const uint32_t ex = dir ? (uint32_t)((2 * N - e) % (2 * N)) : e;
+  const uint32_t w = pw(psi, ex, p);
+  tab[idx] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));
+}
+
+// In-place forward negacyclic NTT (Cooley-Tukey, natural order in, bit-reversed out) of the two
+// prime residue arrays x[pr][N] in shared memory; all threads of the CTA take part.
+__device__ void ntt_forward_smem(uint32_t *x, const uint2 *__restrict__ tab, int logN) {
+  const int N = 1 << logN;
+  for (int s = logN - 1, m = 1; s >= 0; s--, m <<= 1) {  // half-distance t = 2^s
+    const int t = 1 << s;
+    for (int b = threadIdx.x; b < 2 * (N / 2); b += blockDim.x) {
+      const int pr = b / (N / 2), bb = b % (N / 2);
+      const int i = bb >> s, j = 2 * i * t + (bb & (t - 1));
+      const uint32_t p = prime(pr);
+      const uint2 w = __ldg(&tab[pr * N + m + i]);  // forward slice [pr][N]
+      uint32_t *a = x + pr * N;
+      const uint32_t U = a[j], V = mul_shoup(a[j + t], w.x, w.y, p);
+      a[j] = add_mod(U, V, p);
+      a[j + t] = add_mod(U, p - V, p);
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int PREP_THREADS = 256;
+
+// W_hat for row j, block i of the prepared matrix M (= W or W^T):
+// w_hat_ij[k] = M[j, iN + N-1-k] (0 beyond cols), then NTT, then * N^{-1} 2^32 mod p.
+__global__ void __launch_bounds__(PREP_THREADS)
+ntt_weights_kernel(int logN, const int8_t *__restrict__ W, int64_t d_in, int transpose, int64_t cols,
+                   int64_t Lc, const uint2 *__restrict__ tab, uint32_t c0, uint32_t c1,
+                   uint32_t *__restrict__ out) {
+  extern __shared__ uint32_t xs[];
+  const int N = 1 << logN;
+  const int64_t ji = blockIdx.x, j = ji / Lc, i = ji % Lc;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const int64_t c = i * N + (N - 1 - k);
+    int v = 0;
+    if (c < cols) v = transpose ? W[c * d_in + j] : W[j * d_in + c];
+    xs[k] = v < 0 ? (uint32_t)((int64_t)P0 + v) : (uint32_t)v;
+    xs[N + k] = v < 0 ? (uint32_t)((int64_t)P1 + v) : (uint32_t)v;
+  }
+  __syncthreads();
+  ntt_forward_smem(xs, tab, logN);
+  uint32_t *o = out + ji * 2 * N;
+  for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) {
+    const int pr = k / N;
+    o[k] = (uint32_t)((uint64_t)xs[k] * (pr ? c1 : c0) % prime(pr));
+  }
+}
+
+// A_hat for token tau, block i: A = ChaCha20(seed_{tau,i}) mod 2^q_in (R6), mod p, NTT.
+__global__ void __launch_bounds__(PREP_THREADS)
+ntt_masks_kernel(KParams kp, int logN, const uint64_t *__restrict__ seeds,
+                 const uint2 *__restrict__ tab, uint32_t *__restrict__ out) {
+  extern __shared__ uint32_t xs[];
+  const int N = 1 << logN;
+  const int64_t blk = blockIdx.x;  // tau * L + i
+  const uint64_t seed = seeds[blk];
+  for (int g = threadIdx.x; g < N / 8; g += blockDim.x) {
+    uint64_t w[8];
+    chacha20_u64x8(seed, (uint32_t)g, nonce_mask(), w);
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const uint64_t a = w[e] & kp.qmask;
+      xs[8 * g + e] = (uint32_t)(a % P0);
+      xs[N + 8 * g + e] = (uint32_t)(a % P1);
+    }
+  }
+  __syncthreads();
+  ntt_forward_smem(xs, tab, logN);
+  uint32_t *o = out + blk * 2 * N;
+  for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) o[k] = xs[k];
+}
+
+// ---------------------------------------------------------------- the hot kernels
+struct MaskArgs {
+  const uint2 *tinv;        // inverse twiddles [2][N] (dir-1 slice of the table)
+  const uint32_t *what;     // [rows][Lc][2][N]
+  const uint32_t *ahat;     // [T][Lc][2][N]
+  int64_t Lc, rows, row_begin, R, T;
+  int tok_per_cta;
+  int64_t n_chunks;         // ceil(T / tok_per_cta)
+  int q_in, out_bits;
+  uint64_t qmask;
+  void *out;                // [T][R][N] uint32 (switched) or uint64
+};
+
+// Thread/element mapping of the inverse NTT: N/16 threads per residue array, 16 values each;
+// phase (S0, B) makes index bits [S0, S0+B) thread-local (B <= 4).  Element e of thread tid:
+template <int LOGN, int S0, int B>
+__device__ __forceinline__ int eidx(int tid, int e) {
+  const int el = e & ((1 << B) - 1), g = e >> B;
+  const int o = tid | (g << (LOGN - 4));
+  return (o & ((1 << S0) - 1)) | (el << S0) | ((o >> S0) << (S0 + B));
+}
+// The thread bits and element bits of eidx are disjoint, so any function linear in the index
+// bits splits into a per-thread base plus a compile-time constant per element (immediate
+// offsets in LDS/STS, no per-element address registers).
+//
+// Shared-memory layout of exchange X (written with phase X's mapping, read with phase X+1's):
+// chosen so that both warp-wide access patterns hit 32 distinct banks (tools/ntt_model.py
+// checks every N in [512, 8192]); exchange 0: j + j/16, exchange 1: j + 16 (j/256), else j.
+template <int X>
+__device__ __forceinline__ int lay(int j) { return X == 0 ? j + (j >> 4) : X == 1 ? j + 16 * (j >> 8) : j; }
+template <int LOGN>
+__host__ __device__ constexpr int xwords() { return (1 << LOGN) + (1 << LOGN) / 16; }  // per prime
+
+// Gentleman-Sande stages S0..S0+B-1 (half-distance 2^s) on NP residue arrays in registers.
+// Twiddles in shared memory: tw1 = phase-1 table [NP][15][N/16] (see ntt_tables_kernel), twl =
+// inverse-table entries [NP][N/16] (phases >= 2 only index below N/16; their loads are
+// broadcasts).  All warp-wide twiddle loads are conflict-free.
+template <int LOGN, int S0, int B, int NP>
+__device__ __forceinline__ void gs_phase(uint32_t (&r)[NP][16], const uint2 *tw1, const uint2 *twl,
+                                         const uint32_t (&p)[NP], int tid) {
+  constexpr int N = 1 << LOGN, NT = N / 16;
+  const int jt = eidx<LOGN, S0, B>(tid, 0);
+#pragma unroll
+  for (int s = S0; s < S0 + B; s++) {
+    const int d = 1 << (s - S0);
+    const int tb = (N >> (s + 1)) + (jt >> (s + 1));
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+      if (e & d) continue;
+      const int ti = tb + (eidx<LOGN, S0, B>(0, e) >> (s + 1));
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        const uint2 w = S0 == 0 ? tw1[(q * 15 + p1off(s) + (e >> (s + 1))) * NT + tid] : twl[q * NT + ti];
+        const uint32_t U = r[q][e], V = r[q][e | d];
+        r[q][e] = add_mod(U, V, p[q]);
+        r[q][e | d] = mul_shoup(U - V + p[q], w.x, w.y, p[q]);
+      }
+    }
+  }
+}
+template <int LOGN, int S0, int B, int X, int NP>
+__device__ __forceinline__ void xstore(const uint32_t (&r)[NP][16], uint32_t *xb, int tid) {
+  const int base = lay<X>(eidx<LOGN, S0, B>(tid, 0));
+#pragma unroll
+  for (int e = 0; e < 16; e++)
+#pragma unroll
+    for (int q = 0; q < NP; q++) xb[q * xwords<LOGN>() + base + lay<X>(eidx<LOGN, S0, B>(0, e))] = r[q][e];
+}
+template <int LOGN, int S0, int B, int X, int NP>
+__device__ __forceinline__ void xload(uint32_t (&r)[NP][16], const uint32_t *xb, int tid) {
+  const int base = lay<X>(eidx<LOGN, S0, B>(tid, 0));
+#pragma unroll
+  for (int e = 0; e < 16; e++)
+#pragma unroll
+    for (int q = 0; q < NP; q++) r[q][e] = xb[q * xwords<LOGN>() + base + lay<X>(eidx<LOGN, S0, B>(0, e))];
+}
+
+// CRT of (r0 mod p0, r1 mod p1) -> the centred integer mod 2^q_in -> [switch] -> store at a'_t,
+// t = N-1-jj (SampleExtract at h = N-1, Eq. 2: a'_t = P[N-1-t]).
+template <bool SW>
+__device__ __forceinline__ void crt_store(const MaskArgs &a, uint32_t r0, uint32_t r1, int64_t o,
+                                          uint64_t rnd, int s_shift, uint32_t omask) {
+  const uint32_t h = mul_shoup(add_mod(r1, P1 - r0, P1), CRT_C, CRT_CQ, P1);
+  uint64_t val = (uint64_t)r0 + (uint64_t)P0 * h;   // in [0, p0 p1)
+  if (val >= CRT_M / 2) val -= CRT_M;               // centred; wraps mod 2^64
+  if (SW) {
+    static_cast<uint32_t *>(a.out)[o] = (uint32_t)(((val & a.qmask) + rnd) >> s_shift) & omask;
+  } else {
+    static_cast<uint64_t *>(a.out)[o] = val & a.qmask;
+  }
+}
+
+// Barrier over the N/16 threads of one token group (named barrier 1 + group; NG = 1 uses the
+// CTA barrier).
+template <int LOGN, int NG>
+__device__ __forceinline__ void gsync(int grp) {
+  if (NG == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"((1 << LOGN) / 16) : "memory");
+  }
+}
+
+// The inverse NTT by phases, exchanges through `xb` (NBUF = 2: alternate halves, one barrier
+// per exchange; NBUF = 1: a barrier before every store as well).
+template <int LOGN, int NP, int NBUF, int NG>
+__device__ __forceinline__ void intt(uint32_t (&r)[NP][16], const uint2 *tw1, const uint2 *twl,
+                                     const uint32_t (&p)[NP], uint32_t *xb, int tid, int grp) {
+  uint32_t *x0 = xb, *x1 = NBUF == 2 ? xb + NP * xwords<LOGN>() : xb;
+  gs_phase<LOGN, 0, 4, NP>(r, tw1, twl, p, tid);
+  if (NBUF == 1) gsync<LOGN, NG>(grp);
+  xstore<LOGN, 0, 4, 0, NP>(r, x0, tid);
+  gsync<LOGN, NG>(grp);
+  xload<LOGN, 4, 4, 0, NP>(r, x0, tid);
+  gs_phase<LOGN, 4, 4, NP>(r, tw1, twl, p, tid);
+  constexpr int B2 = LOGN - 8 < 4 ? LOGN - 8 : 4;
+  if (NBUF == 1) gsync<LOGN, NG>(grp);
+  xstore<LOGN, 4, 4, 1, NP>(r, x1, tid);
+  gsync<LOGN, NG>(grp);
+  xload<LOGN, 8, B2, 1, NP>(r, x1, tid);
+  gs_phase<LOGN, 8, B2, NP>(r, tw1, twl, p, tid);
+  if constexpr (LOGN > 12) {  // N = 8192: a fourth (1-bit) phase
+    gsync<LOGN, NG>(grp);
+    xstore<LOGN, 8, 4, 2, NP>(r, x0, tid);
+    gsync<LOGN, NG>(grp);
+    xload<LOGN, 12, 1, 2, NP>(r, x0, tid);
+    gs_phase<LOGN, 12, 1, NP>(r, tw1, twl, p, tid);
+  }
+}
+template <int LOGN>
+struct LastPhase {
+  static constexpr int S0 = LOGN > 12 ? 12 : 8;
+  static constexpr int B = LOGN > 12 ? 1 : (LOGN - 8 < 4 ? LOGN - 8 : 4);
+};
+
+// ---- the hot kernel: NG token groups of N/16 threads per CTA share one twiddle copy; each
+// group computes both residues of its (j, tau) polynomials, 16 values per prime per thread.
+template <int LOGN>
+__host__ __device__ constexpr int tw_smem_entries() { return 2 * 16 * ((1 << LOGN) / 16); }  // tw1 + twl
+template <int LOGN, int NG, int NB>
+__host__ __device__ constexpr int ntt_smem() {
+  return tw_smem_entries<LOGN>() * 8 + NG * NB * 2 * xwords<LOGN>() * 4;
+}
+// stage the kernel's twiddles: tw1 <- table section [4N, 4N + 30 NT), twl <- inverse [pr][0, NT)
+template <int LOGN>
+__device__ __forceinline__ void load_twiddles(const uint2 *tinv, uint2 *tw1, uint2 *twl, int t0, int nthr) {
+  constexpr int N = 1 << LOGN, NT = N / 16;
+  const uint2 *p1 = tinv + 2 * N;  // tinv = inverse slice [2][N]; the phase-1 section follows it
+  for (int k = t0; k < 30 * NT; k += nthr) tw1[k] = p1[k];
+  for (int k = t0; k < 2 * NT; k += nthr) twl[k] = tinv[(k / NT) * N + (k % NT)];
+}
+
+template <int LOGN, int NG, int NB>
+__host__ __device__ constexpr int ntt_min_blocks() {  // CTAs/SM the shared memory allows (<= 8)
+  return (227 * 1024) / ntt_smem<LOGN, NG, NB>() < 8 ? (227 * 1024) / ntt_smem<LOGN, NG, NB>() : 8;
+}
+
+template <int LOGN, bool SW, int NG, int NB>
+__global__ void __launch_bounds__(NG * (1 << LOGN) / 16, ntt_min_blocks<LOGN, NG, NB>())
+ntt_mask_kernel(MaskArgs a) {
+  constexpr int N = 1 << LOGN, NT = N / 16;
+  static_assert(LOGN >= 9 && LOGN <= 13, "N in [512, 8192]");
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint2 *tw1 = reinterpret_cast<uint2 *>(smem_raw);
+  uint2 *twl = tw1 + 30 * NT;
+  const int grp = threadIdx.x / NT;   // token group (warp-aligned)
+  const int tid = threadIdx.x % NT;
+  uint32_t *xb = reinterpret_cast<uint32_t *>(tw1 + tw_smem_entries<LOGN>()) + grp * NB * 2 * xwords<LOGN>();
+  load_twiddles<LOGN>(a.tinv, tw1, twl, threadIdx.x, NG * NT);
+  const uint32_t p[2] = {P0, P1};
+
+  const int64_t cta = blockIdx.x;
+  const int64_t jr = cta / a.n_chunks, chunk = cta % a.n_chunks;  // row-major: CTAs of a row adjacent
+  const int64_t j = a.row_begin + jr;
+  const int64_t t_begin = chunk * a.tok_per_cta;
+  const int64_t t_end = min(a.T, t_begin + a.tok_per_cta);
+  const uint4 *wrow = reinterpret_cast<const uint4 *>(a.what + j * a.Lc * 2 * N) + tid * 4;
+  const int64_t tok4 = a.Lc * 2 * (N / 4);
+  const int s_shift = a.q_in - a.out_bits;
+  const uint64_t rnd = s_shift ? (1ull << (s_shift - 1)) : 0ull;
+  const uint32_t omask = (uint32_t)mask_bits(a.out_bits);
+  __syncthreads();
+
+  for (int64_t tau = t_begin + grp; tau < t_end; tau += NG) {
+    uint32_t r[2][16];
+    // ---- pointwise: sum_i W_hat_ij o A_hat_{tau,i} (N^{-1} folded into W_hat), elements 16 tid..+15
+    const uint4 *arow = reinterpret_cast<const uint4 *>(a.ahat) + tau * tok4 + tid * 4;
+    for (int64_t i = 0; i < a.Lc; i++) {
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const uint32_t pi = q ? PINV1 : PINV0;
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+          const int64_t off = (i * 2 + q) * (N / 4) + v;
+          const uint4 wv = __ldg(wrow + off), av = __ldg(arow + off);
+          const uint32_t m[4] = {mul_mont(wv.x, av.x, p[q], pi), mul_mont(wv.y, av.y, p[q], pi),
+                                 mul_mont(wv.z, av.z, p[q], pi), mul_mont(wv.w, av.w, p[q], pi)};
+#pragma unroll
+          for (int k = 0; k < 4; k++) r[q][4 * v + k] = i ? add_mod(r[q][4 * v + k], m[k], p[q]) : m[k];
+        }
+      }
+    }
+    intt<LOGN, 2, NB, NG>(r, tw1, twl, p, xb, tid, grp);
+    // ---- CRT, mod 2^q_in, SampleExtract reversal, ModulusSwitch, store
+    const int64_t obase = (tau * a.R + jr) * (int64_t)N + (N - 1);
+    const int jt = eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(tid, 0);
+#pragma unroll
+    for (int e = 0; e < 16; e++)
+      crt_store<SW>(a, r[0][e], r[1][e],
+                    obase - jt - eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(0, e), rnd, s_shift, omask);
+  }
+}
+
+template <int LOGN, bool SW, int NG, int NB>
+int launch_mask_cfg(const MaskArgs &a, cudaStream_t st) {
+  auto kern = ntt_mask_kernel<LOGN, SW, NG, NB>;
+  constexpr int smem = ntt_smem<LOGN, NG, NB>();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return phe_set_cuda_error(e);
+  kern<<<(unsigned)(a.R * a.n_chunks), NG * (1 << LOGN) / 16, smem, st>>>(a);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+// One token group and one exchange buffer per CTA (smallest shared-memory footprint: 4 CTAs /
+// 16 warps per SM at N = 2048).  Measured alternatives (2 groups sharing the twiddles, 2
+// alternating buffers) were within 2% on q_proj and slower at L = 4.
+template <int LOGN, bool SW>
+int launch_mask(const MaskArgs &a, cudaStream_t st) {
+  return launch_mask_cfg<LOGN, SW, 1, 1>(a, st);
+}
+
+}  // namespace ntt
+
+// ---------------------------------------------------------------- launchers (host)
+static uint32_t host_psi(uint32_t p, uint32_t g, int N) {
+  return ntt::pw(g, (p - 1) / (2 * (uint32_t)N), p);
+}
+
+int ntt_primes(uint32_t out[2]) {
+  out[0] = ntt::P0;
+  out[1] = ntt::P1;
+  return PHE_OK;
+}
+
+int launch_ntt_tables(const KParams &kp, void *tables, cudaStream_t st) {
+  const int N = kp.N;
+  ntt::ntt_tables_kernel<<<(4 * N + 2 * 15 * (N / 16) + 255) / 256, 256, 0, st>>>(
+      kp.log2N, host_psi(ntt::P0, ntt::GEN0, N), host_psi(ntt::P1, ntt::GEN1, N),
+      static_cast<uint2 *>(tables));
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_ntt_weights(const KParams &kp, const void *tables, const int8_t *W, int64_t d_out,
+                       int64_t d_in, int transpose, uint32_t *what, cudaStream_t st) {
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  const int N = kp.N;
+  const int64_t Lc = (cols + N - 1) / N;
+  // N^{-1} * 2^32 mod p: Montgomery form with the inverse transform's scaling folded in
+  const uint32_t c0 = (uint32_t)((uint64_t)ntt::pw(N, ntt::P0 - 2, ntt::P0) * ((1ull << 32) % ntt::P0) % ntt::P0);
+  const uint32_t c1 = (uint32_t)((uint64_t)ntt::pw(N, ntt::P1 - 2, ntt::P1) * ((1ull << 32) % ntt::P1) % ntt::P1);
+  const size_t smem = 2 * N * sizeof(uint32_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(ntt::ntt_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return phe_set_cuda_error(e);
+  }
+  ntt::ntt_weights_kernel<<<(unsigned)(rows * Lc), ntt::PREP_THREADS, smem, st>>>(
+      kp.log2N, W, d_in, transpose, cols, Lc, static_cast<const uint2 *>(tables), c0, c1, what);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_ntt_masks(const KParams &kp, const void *tables, const uint64_t *seeds, int64_t T, int64_t L,
+                     uint32_t *ahat, cudaStream_t st) {
+  if (T * L == 0) return PHE_OK;
+  const size_t smem = 2 * kp.N * sizeof(uint32_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(ntt::ntt_masks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return phe_set_cuda_error(e);
+  }
+  ntt::ntt_masks_kernel<<<(unsigned)(T * L), ntt::PREP_THREADS, smem, st>>>(
+      kp, kp.log2N, seeds, static_cast<const uint2 *>(tables), ahat);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, int64_t rows, int64_t Lc,
+                    int64_t row_begin, int64_t row_end, const uint32_t *ahat, int64_t T, int out_bits,
+                    void *out, cudaStream_t st) {
+  ntt::MaskArgs a{};
+  a.tinv = static_cast<const uint2 *>(tables) + 2 * kp.N;  // inverse slice [pr][N]
+  a.what = what;
+  a.ahat = ahat;
+  a.Lc = Lc;
+  a.rows = rows;
+  a.row_begin = row_begin;
+  a.R = row_end - row_begin;
+  a.T = T;
+  a.q_in = kp.q_in;
+  a.out_bits = out_bits;
+  a.qmask = kp.qmask;
+  a.out = out;
+  if (a.R == 0 || T == 0) return PHE_OK;
+  const char *e = getenv("PHE_NTT_TOK");
+  a.tok_per_cta = e ? atoi(e) : 16;
+  if (a.tok_per_cta < 1) a.tok_per_cta = 1;
+  a.n_chunks = (T + a.tok_per_cta - 1) / a.tok_per_cta;
+  const bool sw = out_bits != kp.q_in;
+  switch (kp.log2N) {
+    case 9: return sw ? ntt::launch_mask<9, true>(a, st) : ntt::launch_mask<9, false>(a, st);
+    case 10: return sw ? ntt::launch_mask<10, true>(a, st) : ntt::launch_mask<10, false>(a, st);
+    case 11: return sw ? ntt::launch_mask<11, true>(a, st) : ntt::launch_mask<11, false>(a, st);
+    case 12: return sw ? ntt::launch_mask<12, true>(a, st) : ntt::launch_mask<12, false>(a, st);
+    case 13: return sw ? ntt::launch_mask<13, true>(a, st) : ntt::launch_mask<13, false>(a, st);
+    default: return PHE_EUNSUPPORTED;
+  }
+}
+
+}  // namespace phe

@@ -688,4 +688,153 @@ int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out
   return PHE_OK;
 }
 
+
+// ================================================================ NEXT #4: NTT-domain contraction
+static int check_ntt(const phe_params *p, KParams *kp) {
+  int rc = check_gpu(p, kp);
+  if (rc) return rc;
+  if (p->N < 512 || p->N > 8192) return PHE_EUNSUPPORTED;
+  if (phe_ntt_max_blocks(p) < 1) return PHE_EUNSUPPORTED;
+  return PHE_OK;
+}
+
+int phe_ntt_primes(uint32_t *out2) {
+  if (!out2) return PHE_EINVAL;
+  return phe::ntt_primes(out2);
+}
+
+int64_t phe_ntt_max_blocks(const phe_params *p) {
+  if (phe_params_validate(p)) return 0;
+  uint32_t pr[2];
+  phe::ntt_primes(pr);
+  const unsigned __int128 half = ((unsigned __int128)pr[0] * pr[1]) / 2;  // |P| < p0 p1 / 2
+  const unsigned __int128 per_block =
+      (unsigned __int128)p->N * (((unsigned __int128)1 << p->q_in) - 1) * 128;
+  const unsigned __int128 L = (half - 1) / per_block;
+  return L > 1000000 ? 1000000 : (int64_t)L;
+}
+
+size_t phe_ntt_tables_bytes(const phe_params *p) {
+  if (!p || p->N < 16) return 0;
+  return (size_t)(4 * p->N + 2 * 15 * (p->N / 16)) * 8;
+}
+
+int phe_ntt_tables_init(const phe_params *p, void *d_tables, size_t bytes, void *stream) {
+  KParams kp;
+  int rc = check_ntt(p, &kp);
+  if (rc) return rc;
+  if (!d_tables) return PHE_EINVAL;
+  if (bytes < phe_ntt_tables_bytes(p)) return PHE_ENOMEM;
+  return phe::launch_ntt_tables(kp, d_tables, S(stream));
+}
+
+size_t phe_ntt_weights_bytes(const phe_params *p, int64_t rows, int64_t cols) {
+  if (!p || rows < 1 || cols < 1 || p->N < 1) return 0;
+  const int64_t Lc = phe_num_blocks(p, cols);
+  return (size_t)(rows * Lc * 2 * p->N * 4) + (size_t)(round_up(rows, 128) * Lc * p->N);
+}
+
+int phe_ntt_weights_prepare(const phe_params *p, const void *d_tables, const int8_t *d_W,
+                            int64_t d_out, int64_t d_in, int transpose, void *d_nttw, size_t bytes,
+                            void *stream) {
+  KParams kp;
+  int rc = check_ntt(p, &kp);
+  if (rc) return rc;
+  if (!d_tables || !d_W || !d_nttw || d_out < 1 || d_in < 1 || (transpose != 0 && transpose != 1))
+    return PHE_EINVAL;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  if (bytes < phe_ntt_weights_bytes(p, rows, cols)) return PHE_ENOMEM;
+  const int64_t Lc = phe_num_blocks(p, cols);
+  uint32_t *what = static_cast<uint32_t *>(d_nttw);
+  rc = phe::launch_ntt_weights(kp, d_tables, d_W, d_out, d_in, transpose, what, S(stream));
+  if (rc) return rc;
+  int8_t *plain = reinterpret_cast<int8_t *>(what + rows * Lc * 2 * p->N);
+  return phe::launch_weights_plain(kp, d_W, d_out, d_in, transpose, plain, S(stream));
+}
+
+size_t phe_ntt_operand_bytes(const phe_params *p, int64_t T, int64_t L) {
+  if (!p || T < 0 || L < 1 || p->N < 1) return 0;
+  const int ell = (p->q_in + 7) / 8;
+  return (size_t)(T * L * 2 * p->N * 4) + (size_t)(op_rows(T, ell) * L * p->N);
+}
+
+int phe_ntt_ct_prepare(const phe_params *p, const void *d_tables, const uint64_t *d_seeds,
+                       const uint64_t *d_body, int64_t T, int64_t L, void *d_operand, size_t bytes,
+                       void *stream) {
+  KParams kp;
+  int rc = check_ntt(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || L < 1 || !d_operand || !d_tables) return PHE_EINVAL;
+  if (T > 0 && (!d_seeds || !d_body)) return PHE_EINVAL;
+  if (bytes < phe_ntt_operand_bytes(p, T, L)) return PHE_ENOMEM;
+  if (T == 0) return PHE_OK;
+  uint32_t *ahat = static_cast<uint32_t *>(d_operand);
+  rc = phe::launch_ntt_masks(kp, d_tables, d_seeds, T, L, ahat, S(stream));
+  if (rc) return rc;
+  uint8_t *bp = reinterpret_cast<uint8_t *>(ahat + T * L * 2 * p->N);
+  return phe::launch_ct_prepare(kp, d_seeds, d_body, T, L, nullptr, bp, S(stream));
+}
+
+static int ntt_common(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t rows,
+                      int64_t cols, int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
+                      int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_ntt(p, &kp);
+  if (rc) return rc;
+  if (rows < 1 || cols < 1 || T < 0) return PHE_EINVAL;
+  if (row_begin < 0 || row_end > rows || row_begin > row_end) return PHE_EINVAL;
+  if (out_bits != p->q_in && out_bits != p->q_out) return PHE_EMODULUS;
+  const int64_t N = p->N, Lc = phe_num_blocks(p, cols);
+  if (Lc > phe_ntt_max_blocks(p)) return PHE_EUNSUPPORTED;
+  if (T == 0 || row_end == row_begin) return PHE_OK;
+  if (!d_tables || !d_nttw || !d_operand || (!d_out_mask && !d_out_body)) return PHE_EINVAL;
+  const uint32_t *what = static_cast<const uint32_t *>(d_nttw);
+  const uint32_t *ahat = static_cast<const uint32_t *>(d_operand);
+  int n = 0;
+  if (d_out_body) {
+    phe::GemmArgs a{};
+    a.kp = kp;
+    a.wexp = nullptr;
+    a.wplain = reinterpret_cast<const int8_t *>(what + rows * Lc * 2 * N);
+    a.rows = rows;
+    a.wplain_rows = round_up(rows, 128);
+    a.op_rows = op_rows(T, kp.ell);
+    a.Lc = Lc;
+    a.cols = cols;
+    a.row_begin = row_begin;
+    a.row_end = row_end;
+    a.mplanes = nullptr;
+    a.bplanes = reinterpret_cast<const uint8_t *>(ahat + T * Lc * 2 * N);
+    a.T = T;
+    a.out_bits = out_bits;
+    a.out_mask = nullptr;
+    a.out_body = d_out_body;
+    rc = phe::launch_limb_gemm(a, S(stream), &n);
+    if (rc) return rc;
+  }
+  if (d_out_mask) {
+    rc = phe::launch_ntt_mask(kp, d_tables, what, rows, Lc, row_begin, row_end, ahat, T, out_bits,
+                              d_out_mask, S(stream));
+    if (rc) return rc;
+    n++;
+  }
+  g_last_launches = n;
+  return PHE_OK;
+}
+
+int phe_matmul_clear_ntt(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                         int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
+                         int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
+  return ntt_common(p, d_tables, d_nttw, d_out, d_in, row_begin, row_end, d_operand, T, out_bits,
+                    d_out_mask, d_out_body, stream);
+}
+
+int phe_matmul_clear_ntt_T(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                           int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
+                           int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
+  return ntt_common(p, d_tables, d_nttw, d_in, d_out, row_begin, row_end, d_operand, T, out_bits,
+                    d_out_mask, d_out_body, stream);
+}
+
 }  // extern "C"

@@ -144,8 +144,8 @@ __global__ void ct_prepare_kernel(KParams kp, const uint64_t *__restrict__ seeds
   int64_t blk = idx / groups;  // tau * L + i
   int64_t tau = blk / L, i = blk % L;
   const int64_t K = L * N;
-  uint64_t w[8];
-  chacha20_u64x8(seeds[blk], (uint32_t)g, nonce_mask(), w);
+  uint64_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (mask_planes) chacha20_u64x8(seeds[blk], (uint32_t)g, nonce_mask(), w);  // NULL: bodies only
   const uint64_t *bsrc = body + blk * (int64_t)N + 8 * g;
   uint64_t bw[8];
   {
@@ -165,7 +165,7 @@ __global__ void ct_prepare_kernel(KParams kp, const uint64_t *__restrict__ seeds
       pb |= (((bw[e] & kp.qmask) >> (8 * l)) & 0xffull) << (8 * e);
     }
     int64_t row = tau * kp.ell + l;
-    *reinterpret_cast<uint64_t *>(mask_planes + row * K + col) = pm;
+    if (mask_planes) *reinterpret_cast<uint64_t *>(mask_planes + row * K + col) = pm;
     *reinterpret_cast<uint64_t *>(body_planes + row * K + col) = pb;
   }
 }
@@ -318,6 +318,18 @@ int launch_weights_prepare(const KParams &kp, const int8_t *W, int64_t d_out, in
   int64_t n_plain = rows_pad * Lc * N;
   weights_plain_kernel<<<(unsigned)((n_plain + 255) / 256), 256, 0, st>>>(
       W, d_in, transpose, rows, rows_pad, cols, Lc * N, reinterpret_cast<int8_t *>(base + n_exp * 16));
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_weights_plain(const KParams &kp, const int8_t *W, int64_t d_out, int64_t d_in, int transpose,
+                         int8_t *plain, cudaStream_t st) {
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  const int64_t K = (cols + kp.N - 1) / kp.N * kp.N;
+  const int64_t rows_pad = (rows + 127) / 128 * 128;
+  const int64_t n = rows_pad * K;
+  weights_plain_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W, d_in, transpose, rows, rows_pad,
+                                                                    cols, K, plain);
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
 }

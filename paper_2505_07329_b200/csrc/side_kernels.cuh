@@ -36,6 +36,20 @@ int launch_wire_inputs(const KParams &kp, uint64_t *seeds, uint64_t *body, int64
                        int dir, cudaStream_t st);
 int launch_wire_packed(const KParams &kp, uint32_t *packed, int64_t nct, uint8_t *wire, int dir, cudaStream_t st);
 
+int launch_weights_plain(const KParams &kp, const int8_t *W, int64_t d_out, int64_t d_in, int transpose,
+                         int8_t *plain, cudaStream_t st);
+
+// ntt_path.cu (NEXT #4): the mask contraction in the NTT domain (two 31-bit primes + CRT).
+int ntt_primes(uint32_t out[2]);
+int launch_ntt_tables(const KParams &kp, void *tables, cudaStream_t st);
+int launch_ntt_weights(const KParams &kp, const void *tables, const int8_t *W, int64_t d_out,
+                       int64_t d_in, int transpose, uint32_t *what, cudaStream_t st);
+int launch_ntt_masks(const KParams &kp, const void *tables, const uint64_t *seeds, int64_t T, int64_t L,
+                     uint32_t *ahat, cudaStream_t st);
+int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, int64_t rows, int64_t Lc,
+                    int64_t row_begin, int64_t row_end, const uint32_t *ahat, int64_t T, int out_bits,
+                    void *out, cudaStream_t st);
+
 // limb_gemm.cu: the tcgen05 int8 limb GEMM (mask = Hankel operand, body = plain operand).
 struct GemmArgs {
   KParams kp;

@@ -1,0 +1,169 @@
+"""GPU parity tests (-m gpu) for NEXT #4, the NTT-domain mask contraction
+(phe_matmul_clear_ntt[_T], paper_2505_07329_b200/csrc/ntt_path.cu).
+
+Bar: bit-exact against the oracle's literal Eq. 6 (C path, oracle/phe_oracle.c) and bit-identical
+to the tensor-core limb GEMM on the same inputs — Eq. 6 defines every output word
+uniquely, so two correct paths cannot differ in a single bit.  Cases cover every N the kernel
+is specialised for (512 ... 8192), ragged rows/blocks/tokens, both output widths, the backward
+W^T registration, row sharding, the CRT range near its bound and the EUNSUPPORTED boundary.
+"""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import phe_oracle as O
+from oracle.phe_oracle import Params
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def oparams(p):
+    return Params(N=p.N, q_in=p.q_in, q_out=p.q_out, beta=p.beta, gamma=p.gamma, eta=p.noise_eta)
+
+
+def u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def encrypt(phe, p, x, sbase=4242, sk_seed=7, noise_seed=0):
+    S = phe.keygen(p, sk_seed)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).to(DEV), sbase, noise_seed)
+    return S, seeds, body
+
+
+def oracle_literal(coracle, p, M, seeds, body):
+    """Literal Eq. 6 on the oracle side from the same public ciphertext (seeds, bodies): the
+    masks are re-expanded by the oracle's own ChaCha20 (oracle/phe_oracle.c)."""
+    op = oparams(p)
+    sd, bd = u64(seeds), u64(body)
+    masks, bodies = [], []
+    for tau in range(sd.shape[0]):
+        A = np.stack([coracle.expand_mask(int(s), op.N, op.q_in) for s in sd[tau]])
+        m, b = coracle.matmul_clear_literal(op, M, A, bd[tau], nthreads=os.cpu_count())
+        masks.append(m); bodies.append(b)
+    return np.stack(masks), np.stack(bodies)
+
+
+def ntt_run(phe, p, W, seeds, body, transpose=False, out_bits=None, **kw):
+    tabs = phe.NttTables(p)
+    w = phe.NttWeights(p, tabs, torch.from_numpy(W).to(DEV), transpose=transpose)
+    op = phe.ntt_ct_prepare(p, tabs, seeds, body)
+    res = phe.matmul_clear_ntt(p, w, op, seeds.shape[0], out_bits=out_bits, **kw)
+    torch.cuda.synchronize()
+    return w, op, res
+
+
+@pytest.mark.parametrize("preset,over,d_out,d_in,T", [
+    ("TOY", {}, 64, 64, 16),                                  # BASELINE configs[0] shape
+    ("PAPER", {}, 200, 4100, 5),                              # ragged rows, L = 3 ragged block
+    ("PAPER", {}, 37, 2048, 70),                              # many tokens (several CTAs/row)
+    ("PAPER", dict(N=512), 40, 1100, 9),                      # LOGN 9, L = 3
+    ("PAPER", dict(N=4096), 5, 4096, 3),                      # LOGN 12
+    ("PAPER", dict(N=8192), 3, 8192, 2),                      # LOGN 13 (4th exchange phase)
+    ("PAPER", dict(N=2048, q_in=32, q_out=24), 33, 2048, 11),  # P2: q 2^32 -> 2^24
+])
+def test_ntt_bit_exact_vs_oracle(phe, coracle, preset, over, d_out, d_in, T):
+    p = phe.params(getattr(phe, "PRESET_" + preset), **over)
+    W = synth.uniform_int8((d_out, d_in), d_in + T, -128, 127)
+    x = synth.uniform_int8((T, d_in), d_out + T, -100, 100)
+    S, seeds, body = encrypt(phe, p, x)
+    w, opnd, (mq, bq) = ntt_run(phe, p, W, seeds, body, out_bits=p.q_in)
+    mask_o, body_o = oracle_literal(coracle, p, W, seeds, body)
+    assert np.array_equal(u64(mq), mask_o)
+    assert np.array_equal(u64(bq), body_o)
+    ms, bs = phe.matmul_clear_ntt(p, w, opnd, T)  # switched to q_out in the epilogue
+    assert np.array_equal(ms.cpu().numpy().astype(np.uint32).astype(np.uint64),
+                          O.modswitch(mask_o, p.q_in, p.q_out))
+    assert np.array_equal(bs.cpu().numpy().astype(np.uint32).astype(np.uint64),
+                          O.modswitch(body_o, p.q_in, p.q_out))
+    y = phe.decrypt_unpack(p, S, mq, bq, p.q_in).cpu().numpy()   # E = 0: exact W x
+    assert np.array_equal(y, (W.astype(np.int64) @ x.astype(np.int64).T).T)
+
+
+def test_ntt_identical_to_tensor_core_path(phe):
+    """Same inputs through both contractions: identical words (Eq. 6 is unique)."""
+    p = phe.params(phe.PRESET_PAPER, noise_eta=21)
+    W = synth.weights_int8(300, 8192, seed=5)   # down_proj-like d_in, L = 4
+    x = synth.activations_int8(60, 8192, seed=6)
+    S, seeds, body = encrypt(phe, p, x, noise_seed=77)
+    _, _, (mn, bn) = ntt_run(phe, p, W, seeds, body)
+    wd = phe.Weights(p, torch.from_numpy(W).to(DEV))
+    md, bd = phe.matmul_clear(p, wd, phe.ct_prepare(p, seeds, body), 60)
+    assert torch.equal(mn, md) and torch.equal(bn, bd)
+
+
+def test_ntt_backward_transpose(phe, coracle):
+    p = phe.params(phe.PRESET_PAPER)
+    W = synth.weights_int8(2100, 70, seed=3)    # W^T . g with g in Z^2100: L = 2 ragged
+    g = synth.gradients_int8(4, 2100, seed=4)
+    S, seeds, body = encrypt(phe, p, g)
+    w, opnd, (m, b) = ntt_run(phe, p, W, seeds, body, transpose=True, out_bits=p.q_in)
+    assert m.shape == (4, 70, p.N)
+    mask_o, body_o = oracle_literal(coracle, p, np.ascontiguousarray(W.T), seeds, body)
+    assert np.array_equal(u64(m), mask_o) and np.array_equal(u64(b), body_o)
+
+
+def test_ntt_row_sharding_and_empty(phe):
+    p = phe.params(phe.PRESET_PAPER)
+    W = synth.weights_int8(300, 2048)
+    x = synth.activations_int8(20, 2048)
+    S, seeds, body = encrypt(phe, p, x)
+    w, opnd, (m, b) = ntt_run(phe, p, W, seeds, body)
+    for r0, r1 in [(0, 128), (128, 300), (17, 18), (5, 5)]:
+        ms, bs = phe.matmul_clear_ntt(p, w, opnd, 20, row_begin=r0, row_end=r1)
+        assert torch.equal(ms, m[:, r0:r1]) and torch.equal(bs, b[:, r0:r1])
+    empty = torch.zeros(phe.load().phe_ntt_operand_bytes(ctypes.byref(p), 0, 1), dtype=torch.uint8, device=DEV)
+    m0, b0 = phe.matmul_clear_ntt(p, w, empty, 0)
+    assert m0.shape == (0, 300, p.N)
+    S1, s1, b1 = encrypt(phe, p, x[:1])
+    _, _, (m1, bb1) = ntt_run(phe, p, W, s1, b1)
+    assert torch.equal(m1[0], m[0]) and torch.equal(bb1[0], b[0])
+
+
+@pytest.mark.parametrize("sign", [1, -1])
+def test_ntt_crt_range_near_bound(phe, coracle, sign):
+    """N = 512, q_in = 39: the CRT allows 59 blocks; at L = 59 with every weight at +127 / -128
+    the exact integer products reach ~2^59.9 of the 2^60.9 bound (both signs)."""
+    p = phe.params(phe.PRESET_PAPER, N=512)
+    Lmax = phe.ntt_max_blocks(p)
+    assert Lmax == 59
+    d_in = Lmax * 512
+    W = np.full((2, d_in), 127 if sign > 0 else -128, np.int8)
+    x = synth.uniform_int8((2, d_in), 11, -3, 3)
+    S, seeds, body = encrypt(phe, p, x)
+    _, _, (m, b) = ntt_run(phe, p, W, seeds, body, out_bits=39)
+    mask_o, body_o = oracle_literal(coracle, p, W, seeds, body)
+    assert np.array_equal(u64(m), mask_o) and np.array_equal(u64(b), body_o)
+    # one block more is refused (EUNSUPPORTED), never silently wrong
+    W2 = np.ones((2, d_in + 512), np.int8)
+    tabs = phe.NttTables(p)
+    w2 = phe.NttWeights(p, tabs, torch.from_numpy(W2).to(DEV))
+    x2 = synth.uniform_int8((1, d_in + 512), 12, -3, 3)
+    _, s2, b2 = encrypt(phe, p, x2)
+    op2 = phe.ntt_ct_prepare(p, tabs, s2, b2)
+    with pytest.raises(phe.PheError, match="unsupported"):
+        phe.matmul_clear_ntt(p, w2, op2, 1)
+
+
+def test_ntt_full_size_q_proj_sampled(phe, coracle):
+    """configs[1] shape (q_proj 2048x2048, T = 2048) through the NTT path: identical to the
+    tensor-core path on every word, plus one full token against the oracle's literal Eq. 6."""
+    p = phe.params(phe.PRESET_PAPER)
+    d, T = 2048, 2048
+    W = synth.weights_int8(d, d)
+    x = synth.activations_int8(T, d)
+    S, seeds, body = encrypt(phe, p, x)
+    w, opnd, (mn, bn) = ntt_run(phe, p, W, seeds, body)
+    wd = phe.Weights(p, torch.from_numpy(W).to(DEV))
+    md, bd = phe.matmul_clear(p, wd, phe.ct_prepare(p, seeds, body), T)
+    assert torch.equal(bn, bd)
+    assert torch.equal(mn, md)
+    del md
+    tau = 777
+    mask_o, body_o = oracle_literal(coracle, p, W, seeds[tau:tau + 1], body[tau:tau + 1])
+    assert np.array_equal(mn[tau].cpu().numpy().astype(np.uint32).astype(np.uint64), O.modswitch(mask_o[0], 39, 26))
