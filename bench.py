@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["q_proj", "ffn", "stack", "q_proj_packed"], default="q_proj")
+    ap.add_argument("--contraction", choices=["tc", "ntt", "hybrid"], default="tc",
+                    help="mask contraction a5: tc = int8 limb GEMM on tcgen05 (north_star), ntt = NTT domain "
+                         "(NEXT #4, CUDA cores), hybrid = ntt for multi-block (L >= 2) linears, tc otherwise")
     ap.add_argument("--tokens", type=int, default=2048, help="tokens per rank (B*C = 8*256)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -128,6 +131,15 @@ def linears(workload: str):
     return calls
 
 
+def alg_imad_ops(p, rows, cols, T):
+    """NTT path (NEXT #4): algorithmic 32-bit integer multiplies per output coefficient =
+    2 primes x (3 per Shoup twiddle product x log2(N)/2 butterflies + 3 per Montgomery product
+    x L blocks) + 4 for the CRT (Shoup + one wide multiply)."""
+    L = (cols + p.N - 1) // p.N
+    per_coef = 2 * (3 * (p.N.bit_length() - 1) / 2 + 3 * L) + 4
+    return per_coef * rows * p.N * T
+
+
 def alg_int8_ops(p, rows, cols, T, part):
     """per token per linear d_out*d_in*(N+1) Z_Q-MACs = N mask + 1 body; each costs
     ell int8 MACs; 2 ops per MAC.  K is the unpadded d_in."""
@@ -156,11 +168,20 @@ def run_ours(args):
     # ---------------- untimed setup: weights (server registration) and client encryption
     from paper_2505_07329_b200.dist import gather_rows, shard_range
     rows_mode = args.shard == "rows" and world > 1
-    regs = []   # (name, Weights, input_key)
+    regs = []   # (name, Weights | NttWeights, input_key)
+    tabs = phe.NttTables(p, device=dev) if args.contraction != "tc" else None
+
+    def use_ntt(d_out, d_in, tr):
+        L = p.L(d_out if tr else d_in)
+        return args.contraction == "ntt" or (args.contraction == "hybrid" and L >= 2)
     for name, d_out, d_in, tr, ikey in lins:
         W = synth.weights_int8_torch(d_out, d_in, seed=synth.MASTER_SEED + len(regs), device=dev)
-        regs.append((name, phe.Weights(p, W, transpose=tr), ikey))
+        if use_ntt(d_out, d_in, tr) and not args.workload.endswith("_packed"):
+            regs.append((name, phe.NttWeights(p, tabs, W, transpose=tr), ikey))
+        else:
+            regs.append((name, phe.Weights(p, W, transpose=tr), ikey))
         del W
+    is_ntt = {name: isinstance(w, phe.NttWeights) for name, w, _ in regs}
     # this rank's output rows of each linear (all rows unless row-sharded)
     rr = {name: (shard_range(w.rows, world, rank) if rows_mode else (0, w.rows)) for name, w, _ in regs}
     S = phe.keygen(p, synth.MASTER_SEED + 17)
@@ -201,6 +222,9 @@ def run_ours(args):
     max_L = max(p.L(w.cols) for _, w, _ in regs)
     operand = torch.empty(phe.load().phe_ct_operand_bytes(__import__("ctypes").byref(p), chunk, max_L),
                           dtype=torch.uint8, device=dev)
+    ntt_L = max([p.L(w.cols) for n_, w, _ in regs if is_ntt[n_]] or [0])
+    ntt_operand = (torch.empty(phe.load().phe_ntt_operand_bytes(__import__("ctypes").byref(p), chunk, ntt_L),
+                               dtype=torch.uint8, device=dev) if ntt_L else None)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
@@ -216,8 +240,12 @@ def run_ours(args):
                 seeds, body = inputs[(w.cols, w.transpose)]
                 e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                 e[0].record(stream)
-                phe.ct_prepare(p, seeds[t0:t0 + n], body[t0:t0 + n], out=operand)  # a3, a4
-                launches[0] += 1
+                if is_ntt[name]:  # NEXT #4: masks expanded straight into the NTT domain
+                    phe.ntt_ct_prepare(p, tabs, seeds[t0:t0 + n], body[t0:t0 + n], out=ntt_operand)
+                    launches[0] += 2
+                else:
+                    phe.ct_prepare(p, seeds[t0:t0 + n], body[t0:t0 + n], out=operand)  # a3, a4
+                    launches[0] += 1
                 e[1].record(stream)
                 if packed:  # Eq. 6 -> digits + bodies, then Eq. 8 + Eq. 7 + switch
                     phe.matmul_clear_digits(p, w, operand, n, digits=dig_buf[:n], body=bod_buf[:n])
@@ -228,15 +256,18 @@ def run_ours(args):
                     e[3].record(stream)
                     evs.append((name, e))
                     continue
-                f = phe.matmul_clear_T if w.transpose else phe.matmul_clear
+                if is_ntt[name]:
+                    f, opnd = phe.matmul_clear_ntt, ntt_operand
+                else:
+                    f, opnd = (phe.matmul_clear_T if w.transpose else phe.matmul_clear), operand
                 r0, r1 = rr[name]
                 nr = r1 - r0
                 mview = out_mask.view(-1)[: n * nr * p.N].view(n, nr, p.N)
                 bview = out_body.view(-1)[: n * nr].view(n, nr)
-                f(p, w, operand, n, out_mask=phe.SKIP, out_body=bview, row_begin=r0, row_end=r1)  # a6
+                f(p, w, opnd, n, out_mask=phe.SKIP, out_body=bview, row_begin=r0, row_end=r1)  # a6
                 launches[0] += phe.last_launch_count()
                 e[2].record(stream)
-                f(p, w, operand, n, out_mask=mview, out_body=phe.SKIP, row_begin=r0, row_end=r1)  # a5
+                f(p, w, opnd, n, out_mask=mview, out_body=phe.SKIP, row_begin=r0, row_end=r1)  # a5
                 launches[0] += phe.last_launch_count()
                 e[3].record(stream)
                 evs.append((name, e))
@@ -256,6 +287,7 @@ def run_ours(args):
         clk = None if args.profile else ClockSampler(local)
         step_ms = []
         per_kind = {}
+        mask_by_path = {}
         for k in parts_ms:
             parts_ms[k] = []
         launches[0] = 0
@@ -269,6 +301,8 @@ def run_ours(args):
             for name, e in evs:
                 kind = name.split(".")[-1]
                 per_kind.setdefault(kind, []).append(e[0].elapsed_time(e[3]))
+                key = "mask_ntt" if is_ntt[name] else "mask_tc"
+                mask_by_path.setdefault(key, []).append(e[2].elapsed_time(e[3]))
             flush.zero_()  # L2 flush between timed steps (outside the events)
         torch.cuda.synchronize()
         clocks = clk.stop() if clk else None
@@ -310,16 +344,19 @@ def run_ours(args):
         gather = {"ms": round(float(tg.item()), 2), "bytes": int(T * w.rows * (p.N + 1) * 4),
                   "api": "paper_2505_07329_b200.dist.gather_rows (NCCL send/recv to rank 0)"}
 
-    # ---------------- roofline of the dominant kernel (mask limb GEMM)
+    # ---------------- roofline of the dominant kernel (mask limb GEMM, or the NTT kernel if the
+    # NTT-domain contraction takes more of the step)
     mp, src = measured_peaks()
     peak = 2.0 * float(mp["bf16_tflops"])  # int8 dense = 2x bf16 (guide's nominal ratio)
-    mask_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") for n_, w, _ in regs)
-    mask_ms = statistics.mean(parts_ms["mask_gemm"])
+    mask_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") for n_, w, _ in regs
+                   if not is_ntt[n_])
+    mask_ms = sum(mask_by_path.get("mask_tc", [0.0])) / args.steps
+    ntt_ms = sum(mask_by_path.get("mask_ntt", [0.0])) / args.steps
     pack_ops = 0.0
     if packed:  # Eq. 8: 2 parts x Decomp(A_LWE) [rows x 4N] x KSK [4N x N], ell int8 MACs each
         pack_ops = sum(2.0 * 2 * p.ell * phe.KS_LEVELS * p.N * p.N * w.rows * T for _, w, _ in regs)
         mask_ops, mask_ms = pack_ops, statistics.mean(parts_ms["mask_gemm"])
-    achieved = mask_ops / (mask_ms / 1e3) / 1e12
+    achieved = mask_ops / (mask_ms / 1e3) / 1e12 if mask_ms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -329,14 +366,26 @@ def run_ours(args):
             traffic = None
     total_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") +
                     alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "body") for n_, w, _ in regs) + pack_ops
-    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": ("pack_gemm_2sm_kernel<5> (KeySwitch GEMM Eq. 8 + rotate-sum Eq. 7)" if packed else
-                           "limb_gemm_2sm_kernel<5,SW,13> (mask contraction, tcgen05 cta_group::2)"),
-                "ops": "int8 tensor ops (2 per MAC), algorithmic: 2*ell*d_out*d_in*N per token",
-                "peak_source": f"{src}: 2 x bf16_tflops (burst) of MEASURED_PEAKS.json",
-                "frac_of_nominal_4500": round(achieved / NOMINAL_INT8_TOPS, 4),
-                "step_frac": round(total_ops / (ms_max / 1e3) / 1e12 / peak, 4)}
+    if ntt_ms > mask_ms:  # NTT kernel dominates: ALU (integer-multiply pipe) roofline
+        imad = sum(alg_imad_ops(p, rr[n_][1] - rr[n_][0], w.cols, T) for n_, w, _ in regs if is_ntt[n_])
+        smax = (clocks or {}).get("sm_max_mhz") or 1965.0
+        peak_imad = 148 * 4 * 16 * smax * 1e6 / 1e12  # T IMAD/s: 148 SMs x 4 SMSPs x 16 lanes/clk
+        ach = imad / (ntt_ms / 1e3) / 1e12
+        roofline = {"bound": "alu", "achieved": round(ach, 3), "peak": round(peak_imad, 3), "unit": "T IMAD/s",
+                    "frac": round(ach / peak_imad, 4), "traffic": None,
+                    "kernel": "ntt_mask_kernel<11,SW,1,1> (NTT-domain mask contraction, NEXT #4)",
+                    "ops": "algorithmic 32-bit multiplies: (2*(3*log2(N)/2 + 3L) + 4) per output coefficient",
+                    "peak_source": "IMAD issue rate from B300_MICROARCH.md (fma pipe, rt_SMSP = 2 -> 16 lanes/clk"
+                                   "/SMSP) x 148 SMs x sm_max clock (DESIGN.md §6)"}
+    else:
+        roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "kernel": ("pack_gemm_2sm_kernel<5> (KeySwitch GEMM Eq. 8 + rotate-sum Eq. 7)" if packed else
+                               "limb_gemm_2sm_kernel<5,SW,13> (mask contraction, tcgen05 cta_group::2)"),
+                    "ops": "int8 tensor ops (2 per MAC), algorithmic: 2*ell*d_out*d_in*N per token",
+                    "peak_source": f"{src}: 2 x bf16_tflops (burst) of MEASURED_PEAKS.json",
+                    "frac_of_nominal_4500": round(achieved / NOMINAL_INT8_TOPS, 4),
+                    "step_frac": round(total_ops / (ms_max / 1e3) / 1e12 / peak, 4)}
 
     # ---------------- e2e through the C ABI with host buffers
     e2e = None
@@ -362,7 +411,8 @@ def run_ours(args):
                "h2d_bytes_per_step": int(hi.numel()), "d2h_bytes_per_step": int(ho.numel()),
                "ms_per_step": round(float(te.item()) * 1e3, 2),
                "api": "phe_server_wire_host (wire-format bytes in/out, pinned host buffers, 255-token chunks)"}
-    if not args.no_e2e and not args.profile and args.workload == "q_proj" and not rows_mode:
+    if (not args.no_e2e and not args.profile and args.workload == "q_proj" and not rows_mode
+            and args.contraction == "tc"):
         name, w, _ = regs[0]
         seeds, body = inputs[(w.cols, w.transpose)]
         hs = seeds.cpu().pin_memory()
@@ -425,7 +475,10 @@ def config_dict(args, world, T, rows_mode=False):
                            "Eq. 7/8 -> RLWE(Wx), 39->26 switch (configs[1] + SURVEY NEXT #1)",
           "stack": "Llama-3.2-1B all linears x 16 layers (qkv fused 3072x2048, o, gate_up fused 16384x2048, "
                    "down; bwd W^T incl. GQA k/v 512x2048), fwd + bwd (configs[3])"}[args.workload]
-    return {"workload": wl, "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": 8, "C": 256, "N": 2048, "q_in": 39, "q_out": 26,
+    if args.contraction != "tc":
+        wl += {"ntt": "; mask contraction in the NTT domain (NEXT #4, CUDA cores)",
+               "hybrid": "; NTT-domain mask contraction for L >= 2 linears (NEXT #4), tcgen05 otherwise"}[args.contraction]
+    return {"workload": wl, "contraction": args.contraction, "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": 8, "C": 256, "N": 2048, "q_in": 39, "q_out": 26,
             "beta": 27,
             "parallelism": (f"row-sharded x{world}" if rows_mode else f"token-sharded x{world}") if world > 1
             else "single GPU",
