@@ -249,7 +249,7 @@ int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out
  * Requirements: N a power of two in [512, 8192] and L <= phe_ntt_max_blocks(p) (CRT
  * exactness: L*N*(2^q_in - 1)*128 < p0*p1/2; 14 blocks for Table 1), else PHE_EUNSUPPORTED.
  *   d_tables  phe_ntt_tables_bytes(p): uint2 [2 dirs][2 primes][N] twiddles (w, floor(w 2^32/p)),
- *             dir 0 = psi^bitrev(k), dir 1 = psi^-bitrev(k), then uint2 [2 primes][15][N/16], the
+ *             dir 0 = psi^bitrev(k), dir 1 = psi^-bitrev(k), then uint2 [15][N/16][2 primes], the
  *             inverse twiddles of stages 0-3 regrouped per thread of the hot kernel; written
  *             once by phe_ntt_tables_init; read-only afterwards; shared by every call with p.
  *   d_nttw    phe_ntt_weights_bytes(p, rows, cols), rows/cols of M = W (transpose 0) or W^T:

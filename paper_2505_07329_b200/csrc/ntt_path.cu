@@ -4,10 +4,12 @@
 //   P_{tau,j} = sum_i A_{tau,i} * w_hat_ij   in Z[X]/(X^N + 1)          (negacyclic)
 // and then SampleExtract at h = N-1 (Eq. 2): a'_t = P[N-1-t].  The paper computes the
 // products "coefficient-wise".  Power-of-two moduli have no NTT, so this path
-// computes the EXACT integer P (|P| <= L*N*(2^q_in - 1)*128 < 2^60 for Table 1 parameters)
-// with negacyclic NTTs modulo two 31-bit primes p0, p1 (p0*p1 > 2^61.8), recovers it by CRT,
-// and reduces mod 2^q_in.  The result is bit-identical to the dense limb GEMM (limb_gemm.cu):
-// both produce the unique value Eq. 6 defines.
+// computes an EXACT integer with negacyclic NTTs modulo two 30-bit primes p0, p1 (p0 p1 ~ 2^59.8)
+// and recovers it by CRT.  The masks are centred first, A' = A - H with H = 2^(q_in - 1), so
+// |P'| = |sum_i A'_i * w_hat_ij| <= L N H 128 (< 2^59 for Table 1 up to L = 6); since every
+// coefficient of 1 * w_hat (negacyclic) has the parity of the weight sum, P = P' + H * par_j
+// mod 2^q_in with par_j = (sum_c W[j,c]) mod 2, one bit per row.  The result is bit-identical to
+// the dense limb GEMM (limb_gemm.cu): both produce the unique value Eq. 6 defines.
 //
 // Work per output coefficient: L Montgomery products per prime (pointwise) + (log2 N)/2 GS
 // butterflies per prime (inverse NTT) + CRT + ModulusSwitch — O(L + log N) instead of the
@@ -32,10 +34,11 @@ namespace phe {
 namespace ntt {
 
 // ---------------------------------------------------------------- primes and constants
-// p0 = 15*2^27 + 1 (generator 31), p1 = 63*2^25 + 1 (generator 5): both < 2^31, both
-// = 1 mod 2^14 (negacyclic NTTs up to N = 8192).  p0 < p1 (the CRT step needs r0 < p1).
-constexpr uint32_t P0 = 2013265921u, P1 = 2113929217u;
-constexpr uint32_t GEN0 = 31u, GEN1 = 5u;
+// p0 = 119*2^23 + 1, p1 = 479*2^21 + 1 (generator 3 for both): = 1 mod 2^14 (negacyclic NTTs
+// up to N = 8192) and < 2^30, so 4p < 2^32: values are kept lazily in [0, 2p) (Harvey) and
+// every butterfly needs one conditional subtraction instead of two.  p0 < p1.
+constexpr uint32_t P0 = 998244353u, P1 = 1004535809u;
+constexpr uint32_t GEN0 = 3u, GEN1 = 3u;
 
 __host__ __device__ constexpr uint32_t neg_inv32(uint32_t p) {
   uint32_t x = p;  // Newton: x <- x*(2 - p*x) doubles the correct low bits (p odd)
@@ -81,6 +84,19 @@ __device__ __forceinline__ uint32_t mul_mont(uint32_t a, uint32_t b, uint32_t p,
   const uint32_t u = (uint32_t)((t + (uint64_t)m * p) >> 32);
   return min(u, u - p);
 }
+// ---- lazy forms (4p < 2^32): operands and results in [0, 2p)
+__device__ __forceinline__ uint32_t add_lazy(uint32_t a, uint32_t b, uint32_t p) {
+  const uint32_t s = a + b;
+  return min(s, s - 2 * p);
+}
+__device__ __forceinline__ uint32_t shoup_lazy(uint32_t x, uint32_t w, uint32_t wq, uint32_t p) {
+  return x * w - __umulhi(x, wq) * p;  // x < 2^32: result in [0, 2p)
+}
+__device__ __forceinline__ uint32_t mont_lazy(uint32_t a, uint32_t b, uint32_t p, uint32_t pi) {
+  const uint64_t t = (uint64_t)a * b;  // a, b < 2p: t < 4p^2, result (t + m p) / 2^32 < 2p
+  const uint32_t m = (uint32_t)t * pi;
+  return (uint32_t)((t + (uint64_t)m * p) >> 32);
+}
 
 __device__ __forceinline__ uint32_t brev(uint32_t k, int logN) { return __brev(k) >> (32 - logN); }
 
@@ -88,9 +104,10 @@ __device__ __forceinline__ uint32_t brev(uint32_t k, int logN) { return __brev(k
 // d_tables layout: uint2 [2 dirs][2 primes][N]; dir 0 = psi^{bitrev(k)} (forward CT),
 // dir 1 = psi^{-bitrev(k)} (inverse GS); .x = w, .y = floor(w 2^32 / p).  psi = g^((p-1)/2N)
 // is a primitive 2N-th root of unity (psi^N = -1: the negacyclic twist, X^N = -1).
-// Followed by the phase-1 section used by the hot kernel: uint2 [2 primes][15][N/16], entry
-// [pr][P1OFF[s] + m][t] = inverse twiddle (N >> (s+1)) + t 2^(3-s) + m for stages s = 0..3 of the
-// inverse NTT (thread t's m-th twiddle of stage s), so that a warp's loads are contiguous.
+// Followed by the phase-1 section used by the hot kernel: uint2 [15][N/16][2 primes], entry
+// [P1OFF[s] + m][t][pr] = inverse twiddle (N >> (s+1)) + t 2^(3-s) + m for stages s = 0..3 of
+// the inverse NTT (thread t's m-th twiddle of stage s; one 16-byte load serves both primes and a
+// warp's loads are contiguous).
 __host__ __device__ constexpr int p1off(int s) { return s == 0 ? 0 : s == 1 ? 8 : s == 2 ? 12 : 14; }
 __global__ void ntt_tables_kernel(int logN, uint32_t psi0, uint32_t psi1, uint2 *__restrict__ tab) {
   const int N = 1 << logN, NT = N / 16;
@@ -100,8 +117,9 @@ __global__ void ntt_tables_kernel(int logN, uint32_t psi0, uint32_t psi1, uint2 
   if (idx < 4 * N) {
     k = idx % N; pr = (idx / N) & 1; dir = idx / (2 * N);
   } else {
-    const int r = idx - 4 * N, t = r % NT, slot = (r / NT) % 15;
-    pr = r / (15 * NT); dir = 1;
+    const int r = idx - 4 * N;
+    pr = r & 1; dir = 1;
+    const int t = (r >> 1) % NT, slot = (r >> 1) / NT;
     const int s = slot >= 14 ? 3 : slot >= 12 ? 2 : slot >= 8 ? 1 : 0;
     k = (N >> (s + 1)) + t * (1 << (3 - s)) + (slot - p1off(s));
   }
@@ -159,7 +177,8 @@ ntt_weights_kernel(int logN, const int8_t *__restrict__ W, int64_t d_in, int tra
   }
 }
 
-// A_hat for token tau, block i: A = ChaCha20(seed_{tau,i}) mod 2^q_in (R6), mod p, NTT.
+// A_hat for token tau, block i: A = ChaCha20(seed_{tau,i}) mod 2^q_in (R6), centred
+// A' = A - 2^(q_in-1), mod p, NTT.
 __global__ void __launch_bounds__(PREP_THREADS)
 ntt_masks_kernel(KParams kp, int logN, const uint64_t *__restrict__ seeds,
                  const uint2 *__restrict__ tab, uint32_t *__restrict__ out) {
@@ -167,14 +186,16 @@ ntt_masks_kernel(KParams kp, int logN, const uint64_t *__restrict__ seeds,
   const int N = 1 << logN;
   const int64_t blk = blockIdx.x;  // tau * L + i
   const uint64_t seed = seeds[blk];
+  const uint64_t H = 1ull << (kp.q_in - 1);
+  const uint32_t h0 = (uint32_t)(H % P0), h1 = (uint32_t)(H % P1);
   for (int g = threadIdx.x; g < N / 8; g += blockDim.x) {
     uint64_t w[8];
     chacha20_u64x8(seed, (uint32_t)g, nonce_mask(), w);
 #pragma unroll
     for (int e = 0; e < 8; e++) {
       const uint64_t a = w[e] & kp.qmask;
-      xs[8 * g + e] = (uint32_t)(a % P0);
-      xs[N + 8 * g + e] = (uint32_t)(a % P1);
+      xs[8 * g + e] = add_mod((uint32_t)(a % P0), P0 - h0, P0);
+      xs[N + 8 * g + e] = add_mod((uint32_t)(a % P1), P1 - h1, P1);
     }
   }
   __syncthreads();
@@ -183,10 +204,22 @@ ntt_masks_kernel(KParams kp, int logN, const uint64_t *__restrict__ seeds,
   for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) o[k] = xs[k];
 }
 
+// par[j] = (sum_c M[j, c]) mod 2 (the centring correction bit of row j); one warp per row
+__global__ void ntt_rowpar_kernel(const int8_t *__restrict__ W, int64_t d_in, int transpose, int64_t rows,
+                                  int64_t cols, uint8_t *__restrict__ par) {
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (j >= rows) return;
+  int s = 0;
+  for (int64_t c = threadIdx.x % 32; c < cols; c += 32) s += transpose ? W[c * d_in + j] : W[j * d_in + c];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x % 32 == 0) par[j] = (uint8_t)(s & 1);
+}
+
 // ---------------------------------------------------------------- the hot kernels
 struct MaskArgs {
   const uint2 *tinv;        // inverse twiddles [2][N] (dir-1 slice of the table)
   const uint32_t *what;     // [rows][Lc][2][N]
+  const uint8_t *par;       // [rows] centring correction bits
   const uint32_t *ahat;     // [T][Lc][2][N]
   int64_t Lc, rows, row_begin, R, T;
   int tok_per_cta;
@@ -221,8 +254,9 @@ __host__ __device__ constexpr int xwords() { return (1 << LOGN) + (1 << LOGN) / 
 // inverse-table entries [NP][N/16] (phases >= 2 only index below N/16; their loads are
 // broadcasts).  All warp-wide twiddle loads are conflict-free.
 template <int LOGN, int S0, int B, int NP>
-__device__ __forceinline__ void gs_phase(uint32_t (&r)[NP][16], const uint2 *tw1, const uint2 *twl,
+__device__ __forceinline__ void gs_phase(uint32_t (&r)[NP][16], const uint4 *tw1, const uint4 *twl,
                                          const uint32_t (&p)[NP], int tid) {
+  static_assert(NP == 2, "both primes per thread");
   constexpr int N = 1 << LOGN, NT = N / 16;
   const int jt = eidx<LOGN, S0, B>(tid, 0);
 #pragma unroll
@@ -233,41 +267,60 @@ __device__ __forceinline__ void gs_phase(uint32_t (&r)[NP][16], const uint2 *tw1
     for (int e = 0; e < 16; e++) {
       if (e & d) continue;
       const int ti = tb + (eidx<LOGN, S0, B>(0, e) >> (s + 1));
+      const uint4 w4 = S0 == 0 ? tw1[(p1off(s) + (e >> (s + 1))) * NT + tid] : twl[ti];
 #pragma unroll
       for (int q = 0; q < NP; q++) {
-        const uint2 w = S0 == 0 ? tw1[(q * 15 + p1off(s) + (e >> (s + 1))) * NT + tid] : twl[q * NT + ti];
-        const uint32_t U = r[q][e], V = r[q][e | d];
-        r[q][e] = add_mod(U, V, p[q]);
-        r[q][e | d] = mul_shoup(U - V + p[q], w.x, w.y, p[q]);
+        const uint32_t w = q ? w4.z : w4.x, wq = q ? w4.w : w4.y;
+        const uint32_t U = r[q][e], V = r[q][e | d];  // lazy: in [0, 2p)
+        r[q][e] = add_lazy(U, V, p[q]);
+        r[q][e | d] = shoup_lazy(U - V + 2 * p[q], w, wq, p[q]);
       }
     }
   }
 }
+// Both residues of an element travel as one 8-byte word: a half-warp's 16 lanes hit 16
+// distinct 8-byte bank pairs (the layouts are distinct mod 16 on every half-warp pattern).
 template <int LOGN, int S0, int B, int X, int NP>
 __device__ __forceinline__ void xstore(const uint32_t (&r)[NP][16], uint32_t *xb, int tid) {
   const int base = lay<X>(eidx<LOGN, S0, B>(tid, 0));
+  uint2 *x2 = reinterpret_cast<uint2 *>(xb);
 #pragma unroll
-  for (int e = 0; e < 16; e++)
-#pragma unroll
-    for (int q = 0; q < NP; q++) xb[q * xwords<LOGN>() + base + lay<X>(eidx<LOGN, S0, B>(0, e))] = r[q][e];
+  for (int e = 0; e < 16; e++) x2[base + lay<X>(eidx<LOGN, S0, B>(0, e))] = make_uint2(r[0][e], r[1][e]);
 }
 template <int LOGN, int S0, int B, int X, int NP>
 __device__ __forceinline__ void xload(uint32_t (&r)[NP][16], const uint32_t *xb, int tid) {
   const int base = lay<X>(eidx<LOGN, S0, B>(tid, 0));
+  const uint2 *x2 = reinterpret_cast<const uint2 *>(xb);
 #pragma unroll
-  for (int e = 0; e < 16; e++)
-#pragma unroll
-    for (int q = 0; q < NP; q++) r[q][e] = xb[q * xwords<LOGN>() + base + lay<X>(eidx<LOGN, S0, B>(0, e))];
+  for (int e = 0; e < 16; e++) {
+    const uint2 v = x2[base + lay<X>(eidx<LOGN, S0, B>(0, e))];
+    r[0][e] = v.x;
+    r[1][e] = v.y;
+  }
 }
 
 // CRT of (r0 mod p0, r1 mod p1) -> the centred integer mod 2^q_in -> [switch] -> store at a'_t,
 // t = N-1-jj (SampleExtract at h = N-1, Eq. 2: a'_t = P[N-1-t]).
-template <bool SW>
-__device__ __forceinline__ void crt_store(const MaskArgs &a, uint32_t r0, uint32_t r1, int64_t o,
-                                          uint64_t rnd, int s_shift, uint32_t omask) {
-  const uint32_t h = mul_shoup(add_mod(r1, P1 - r0, P1), CRT_C, CRT_CQ, P1);
-  uint64_t val = (uint64_t)r0 + (uint64_t)P0 * h;   // in [0, p0 p1)
+// SHIFT > 0: switch by a compile-time SHIFT = q_in - q_out (Table 1: 13) to OUTB = q_out bits.
+// Bits [s, q_in) of ((v mod 2^q_in) + 2^(s-1)) equal bits [s, q_in) of (v + 2^(s-1)), so the
+// rounding constant rides in the CRT's wide multiply-add and no 64-bit masking is needed.
+// r0, r1 lazy in [0, 2p): h = (r1 - r0) p0^-1 mod p1 (reduced) and v = r0 + p0 h in
+// [0, p0 p1 + p0) with v = P' mod p0 p1; v >= p0 p1 / 2 stands for v - p0 p1 (this also maps
+// v in [p0 p1, p0 p1 + p0) to its residue).  corr = H par_j restores P from the centred P'.
+template <bool SW, int SHIFT, int OUTB>
+__device__ __forceinline__ void crt_store(const MaskArgs &a, uint32_t r0, uint32_t r1, uint64_t corr,
+                                          int64_t o, uint64_t rnd, int s_shift, uint32_t omask) {
+  const uint32_t h = mul_shoup(r1 - r0 + 2 * P1, CRT_C, CRT_CQ, P1);
+  if constexpr (SW && SHIFT > 0) {
+    constexpr uint64_t R = 1ull << (SHIFT - 1);
+    uint64_t x = (uint64_t)P0 * h + (uint64_t)r0;                    // v
+    x += (x >= CRT_M / 2 ? (uint64_t)0 - CRT_M : 0) + corr + R;      // P + 2^(s-1) mod 2^64
+    static_cast<uint32_t *>(a.out)[o] = (uint32_t)(x >> SHIFT) & ((1u << OUTB) - 1u);
+    return;
+  }
+  uint64_t val = (uint64_t)r0 + (uint64_t)P0 * h;
   if (val >= CRT_M / 2) val -= CRT_M;               // centred; wraps mod 2^64
+  val += corr;
   if (SW) {
     static_cast<uint32_t *>(a.out)[o] = (uint32_t)(((val & a.qmask) + rnd) >> s_shift) & omask;
   } else {
@@ -289,7 +342,7 @@ __device__ __forceinline__ void gsync(int grp) {
 // The inverse NTT by phases, exchanges through `xb` (NBUF = 2: alternate halves, one barrier
 // per exchange; NBUF = 1: a barrier before every store as well).
 template <int LOGN, int NP, int NBUF, int NG>
-__device__ __forceinline__ void intt(uint32_t (&r)[NP][16], const uint2 *tw1, const uint2 *twl,
+__device__ __forceinline__ void intt(uint32_t (&r)[NP][16], const uint4 *tw1, const uint4 *twl,
                                      const uint32_t (&p)[NP], uint32_t *xb, int tid, int grp) {
   uint32_t *x0 = xb, *x1 = NBUF == 2 ? xb + NP * xwords<LOGN>() : xb;
   gs_phase<LOGN, 0, 4, NP>(r, tw1, twl, p, tid);
@@ -326,13 +379,17 @@ template <int LOGN, int NG, int NB>
 __host__ __device__ constexpr int ntt_smem() {
   return tw_smem_entries<LOGN>() * 8 + NG * NB * 2 * xwords<LOGN>() * 4;
 }
-// stage the kernel's twiddles: tw1 <- table section [4N, 4N + 30 NT), twl <- inverse [pr][0, NT)
+// stage the kernel's twiddles (both primes per 16-byte entry): tw1 <- the table's phase-1
+// section [15][NT][2], twl[k] <- inverse entries k < NT of both primes
 template <int LOGN>
-__device__ __forceinline__ void load_twiddles(const uint2 *tinv, uint2 *tw1, uint2 *twl, int t0, int nthr) {
+__device__ __forceinline__ void load_twiddles(const uint2 *tinv, uint4 *tw1, uint4 *twl, int t0, int nthr) {
   constexpr int N = 1 << LOGN, NT = N / 16;
-  const uint2 *p1 = tinv + 2 * N;  // tinv = inverse slice [2][N]; the phase-1 section follows it
-  for (int k = t0; k < 30 * NT; k += nthr) tw1[k] = p1[k];
-  for (int k = t0; k < 2 * NT; k += nthr) twl[k] = tinv[(k / NT) * N + (k % NT)];
+  const uint4 *p1 = reinterpret_cast<const uint4 *>(tinv + 2 * N);  // follows the inverse slice
+  for (int k = t0; k < 15 * NT; k += nthr) tw1[k] = p1[k];
+  for (int k = t0; k < NT; k += nthr) {
+    const uint2 a = tinv[k], b = tinv[N + k];
+    twl[k] = make_uint4(a.x, a.y, b.x, b.y);
+  }
 }
 
 template <int LOGN, int NG, int NB>
@@ -340,17 +397,17 @@ __host__ __device__ constexpr int ntt_min_blocks() {  // CTAs/SM the shared memo
   return (227 * 1024) / ntt_smem<LOGN, NG, NB>() < 8 ? (227 * 1024) / ntt_smem<LOGN, NG, NB>() : 8;
 }
 
-template <int LOGN, bool SW, int NG, int NB>
+template <int LOGN, bool SW, int NG, int NB, int SHIFT = 0, int OUTB = 0>
 __global__ void __launch_bounds__(NG * (1 << LOGN) / 16, ntt_min_blocks<LOGN, NG, NB>())
 ntt_mask_kernel(MaskArgs a) {
   constexpr int N = 1 << LOGN, NT = N / 16;
   static_assert(LOGN >= 9 && LOGN <= 13, "N in [512, 8192]");
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint2 *tw1 = reinterpret_cast<uint2 *>(smem_raw);
-  uint2 *twl = tw1 + 30 * NT;
+  uint4 *tw1 = reinterpret_cast<uint4 *>(smem_raw);
+  uint4 *twl = tw1 + 15 * NT;
   const int grp = threadIdx.x / NT;   // token group (warp-aligned)
   const int tid = threadIdx.x % NT;
-  uint32_t *xb = reinterpret_cast<uint32_t *>(tw1 + tw_smem_entries<LOGN>()) + grp * NB * 2 * xwords<LOGN>();
+  uint32_t *xb = reinterpret_cast<uint32_t *>(tw1 + tw_smem_entries<LOGN>() / 2) + grp * NB * 2 * xwords<LOGN>();
   load_twiddles<LOGN>(a.tinv, tw1, twl, threadIdx.x, NG * NT);
   const uint32_t p[2] = {P0, P1};
 
@@ -364,13 +421,42 @@ ntt_mask_kernel(MaskArgs a) {
   const int s_shift = a.q_in - a.out_bits;
   const uint64_t rnd = s_shift ? (1ull << (s_shift - 1)) : 0ull;
   const uint32_t omask = (uint32_t)mask_bits(a.out_bits);
+  const uint64_t corr = a.par[j] ? (1ull << (a.q_in - 1)) : 0ull;
+  // A_hat_{tau,0} of the next token is prefetched into registers while this one is transformed
+  uint4 an[2][4];
+  if (t_begin + grp < t_end) {
+    const uint4 *a0 = reinterpret_cast<const uint4 *>(a.ahat) + (t_begin + grp) * tok4 + tid * 4;
+#pragma unroll
+    for (int q = 0; q < 2; q++)
+#pragma unroll
+      for (int v = 0; v < 4; v++) an[q][v] = __ldg(a0 + q * (N / 4) + v);
+  }
   __syncthreads();
 
   for (int64_t tau = t_begin + grp; tau < t_end; tau += NG) {
     uint32_t r[2][16];
     // ---- pointwise: sum_i W_hat_ij o A_hat_{tau,i} (N^{-1} folded into W_hat), elements 16 tid..+15
     const uint4 *arow = reinterpret_cast<const uint4 *>(a.ahat) + tau * tok4 + tid * 4;
-    for (int64_t i = 0; i < a.Lc; i++) {
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      const uint32_t pi = q ? PINV1 : PINV0;
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const uint4 wv = __ldg(wrow + q * (N / 4) + v), av = an[q][v];
+        r[q][4 * v + 0] = mont_lazy(wv.x, av.x, p[q], pi);
+        r[q][4 * v + 1] = mont_lazy(wv.y, av.y, p[q], pi);
+        r[q][4 * v + 2] = mont_lazy(wv.z, av.z, p[q], pi);
+        r[q][4 * v + 3] = mont_lazy(wv.w, av.w, p[q], pi);
+      }
+    }
+    if (tau + NG < t_end) {
+      const uint4 *a0 = arow + NG * tok4;
+#pragma unroll
+      for (int q = 0; q < 2; q++)
+#pragma unroll
+        for (int v = 0; v < 4; v++) an[q][v] = __ldg(a0 + q * (N / 4) + v);
+    }
+    for (int64_t i = 1; i < a.Lc; i++) {
 #pragma unroll
       for (int q = 0; q < 2; q++) {
         const uint32_t pi = q ? PINV1 : PINV0;
@@ -378,10 +464,10 @@ ntt_mask_kernel(MaskArgs a) {
         for (int v = 0; v < 4; v++) {
           const int64_t off = (i * 2 + q) * (N / 4) + v;
           const uint4 wv = __ldg(wrow + off), av = __ldg(arow + off);
-          const uint32_t m[4] = {mul_mont(wv.x, av.x, p[q], pi), mul_mont(wv.y, av.y, p[q], pi),
-                                 mul_mont(wv.z, av.z, p[q], pi), mul_mont(wv.w, av.w, p[q], pi)};
+          const uint32_t m[4] = {mont_lazy(wv.x, av.x, p[q], pi), mont_lazy(wv.y, av.y, p[q], pi),
+                                 mont_lazy(wv.z, av.z, p[q], pi), mont_lazy(wv.w, av.w, p[q], pi)};
 #pragma unroll
-          for (int k = 0; k < 4; k++) r[q][4 * v + k] = i ? add_mod(r[q][4 * v + k], m[k], p[q]) : m[k];
+          for (int k = 0; k < 4; k++) r[q][4 * v + k] = add_lazy(r[q][4 * v + k], m[k], p[q]);
         }
       }
     }
@@ -391,14 +477,14 @@ ntt_mask_kernel(MaskArgs a) {
     const int jt = eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(tid, 0);
 #pragma unroll
     for (int e = 0; e < 16; e++)
-      crt_store<SW>(a, r[0][e], r[1][e],
+      crt_store<SW, SHIFT, OUTB>(a, r[0][e], r[1][e], corr,
                     obase - jt - eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(0, e), rnd, s_shift, omask);
   }
 }
 
-template <int LOGN, bool SW, int NG, int NB>
+template <int LOGN, bool SW, int NG, int NB, int SHIFT = 0, int OUTB = 0>
 int launch_mask_cfg(const MaskArgs &a, cudaStream_t st) {
-  auto kern = ntt_mask_kernel<LOGN, SW, NG, NB>;
+  auto kern = ntt_mask_kernel<LOGN, SW, NG, NB, SHIFT, OUTB>;
   constexpr int smem = ntt_smem<LOGN, NG, NB>();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return phe_set_cuda_error(e);
@@ -412,6 +498,8 @@ int launch_mask_cfg(const MaskArgs &a, cudaStream_t st) {
 // alternating buffers) were within 2% on q_proj and slower at L = 4.
 template <int LOGN, bool SW>
 int launch_mask(const MaskArgs &a, cudaStream_t st) {
+  if (SW && LOGN == 11 && a.q_in == 39 && a.out_bits == 26)  // Table 1: compile-time switch
+    return launch_mask_cfg<LOGN, SW, 1, 1, 13, 26>(a, st);
   return launch_mask_cfg<LOGN, SW, 1, 1>(a, st);
 }
 
@@ -457,6 +545,14 @@ int launch_ntt_weights(const KParams &kp, const void *tables, const int8_t *W, i
   return PHE_OK;
 }
 
+int launch_ntt_rowpar(const int8_t *W, int64_t d_out, int64_t d_in, int transpose, uint8_t *par,
+                      cudaStream_t st) {
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  ntt::ntt_rowpar_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(W, d_in, transpose, rows, cols, par);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
 int launch_ntt_masks(const KParams &kp, const void *tables, const uint64_t *seeds, int64_t T, int64_t L,
                      uint32_t *ahat, cudaStream_t st) {
   if (T * L == 0) return PHE_OK;
@@ -472,10 +568,11 @@ int launch_ntt_masks(const KParams &kp, const void *tables, const uint64_t *seed
   return PHE_OK;
 }
 
-int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, int64_t rows, int64_t Lc,
-                    int64_t row_begin, int64_t row_end, const uint32_t *ahat, int64_t T, int out_bits,
-                    void *out, cudaStream_t st) {
+int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, const uint8_t *par,
+                    int64_t rows, int64_t Lc, int64_t row_begin, int64_t row_end, const uint32_t *ahat,
+                    int64_t T, int out_bits, void *out, cudaStream_t st) {
   ntt::MaskArgs a{};
+  a.par = par;
   a.tinv = static_cast<const uint2 *>(tables) + 2 * kp.N;  // inverse slice [pr][N]
   a.what = what;
   a.ahat = ahat;

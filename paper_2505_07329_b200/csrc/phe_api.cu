@@ -707,9 +707,9 @@ int64_t phe_ntt_max_blocks(const phe_params *p) {
   if (phe_params_validate(p)) return 0;
   uint32_t pr[2];
   phe::ntt_primes(pr);
-  const unsigned __int128 half = ((unsigned __int128)pr[0] * pr[1]) / 2;  // |P| < p0 p1 / 2
-  const unsigned __int128 per_block =
-      (unsigned __int128)p->N * (((unsigned __int128)1 << p->q_in) - 1) * 128;
+  // centred masks: |P'| <= L N 2^(q_in-1) 128 must stay below p0 p1 / 2 (R23)
+  const unsigned __int128 half = ((unsigned __int128)pr[0] * pr[1]) / 2;
+  const unsigned __int128 per_block = (unsigned __int128)p->N * ((unsigned __int128)1 << (p->q_in - 1)) * 128;
   const unsigned __int128 L = (half - 1) / per_block;
   return L > 1000000 ? 1000000 : (int64_t)L;
 }
@@ -731,7 +731,8 @@ int phe_ntt_tables_init(const phe_params *p, void *d_tables, size_t bytes, void 
 size_t phe_ntt_weights_bytes(const phe_params *p, int64_t rows, int64_t cols) {
   if (!p || rows < 1 || cols < 1 || p->N < 1) return 0;
   const int64_t Lc = phe_num_blocks(p, cols);
-  return (size_t)(rows * Lc * 2 * p->N * 4) + (size_t)(round_up(rows, 128) * Lc * p->N);
+  return (size_t)(rows * Lc * 2 * p->N * 4) + (size_t)(round_up(rows, 128) * Lc * p->N) +
+         (size_t)round_up(rows, 16);
 }
 
 int phe_ntt_weights_prepare(const phe_params *p, const void *d_tables, const int8_t *d_W,
@@ -749,7 +750,10 @@ int phe_ntt_weights_prepare(const phe_params *p, const void *d_tables, const int
   rc = phe::launch_ntt_weights(kp, d_tables, d_W, d_out, d_in, transpose, what, S(stream));
   if (rc) return rc;
   int8_t *plain = reinterpret_cast<int8_t *>(what + rows * Lc * 2 * p->N);
-  return phe::launch_weights_plain(kp, d_W, d_out, d_in, transpose, plain, S(stream));
+  rc = phe::launch_weights_plain(kp, d_W, d_out, d_in, transpose, plain, S(stream));
+  if (rc) return rc;
+  uint8_t *par = reinterpret_cast<uint8_t *>(plain) + round_up(rows, 128) * Lc * p->N;
+  return phe::launch_ntt_rowpar(d_W, d_out, d_in, transpose, par, S(stream));
 }
 
 size_t phe_ntt_operand_bytes(const phe_params *p, int64_t T, int64_t L) {
@@ -814,7 +818,9 @@ static int ntt_common(const phe_params *p, const void *d_tables, const void *d_n
     if (rc) return rc;
   }
   if (d_out_mask) {
-    rc = phe::launch_ntt_mask(kp, d_tables, what, rows, Lc, row_begin, row_end, ahat, T, out_bits,
+    const uint8_t *par = reinterpret_cast<const uint8_t *>(what + rows * Lc * 2 * N) +
+                         round_up(rows, 128) * Lc * N;
+    rc = phe::launch_ntt_mask(kp, d_tables, what, par, rows, Lc, row_begin, row_end, ahat, T, out_bits,
                               d_out_mask, S(stream));
     if (rc) return rc;
     n++;

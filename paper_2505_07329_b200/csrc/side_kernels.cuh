@@ -46,9 +46,11 @@ int launch_ntt_weights(const KParams &kp, const void *tables, const int8_t *W, i
                        int64_t d_in, int transpose, uint32_t *what, cudaStream_t st);
 int launch_ntt_masks(const KParams &kp, const void *tables, const uint64_t *seeds, int64_t T, int64_t L,
                      uint32_t *ahat, cudaStream_t st);
-int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, int64_t rows, int64_t Lc,
-                    int64_t row_begin, int64_t row_end, const uint32_t *ahat, int64_t T, int out_bits,
-                    void *out, cudaStream_t st);
+int launch_ntt_rowpar(const int8_t *W, int64_t d_out, int64_t d_in, int transpose, uint8_t *par,
+                      cudaStream_t st);
+int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, const uint8_t *par,
+                    int64_t rows, int64_t Lc, int64_t row_begin, int64_t row_end, const uint32_t *ahat,
+                    int64_t T, int out_bits, void *out, cudaStream_t st);
 
 // limb_gemm.cu: the tcgen05 int8 limb GEMM (mask = Hankel operand, body = plain operand).
 struct GemmArgs {

@@ -5,7 +5,7 @@ Bar: bit-exact against the oracle's literal Eq. 6 (C path, oracle/phe_oracle.c) 
 to the tensor-core limb GEMM on the same inputs — Eq. 6 defines every output word
 uniquely, so two correct paths cannot differ in a single bit.  Cases cover every N the kernel
 is specialised for (512 ... 8192), ragged rows/blocks/tokens, both output widths, the backward
-W^T registration, row sharding, the CRT range near its bound and the EUNSUPPORTED boundary.
+W^T registration, row sharding, the CRT range at its worst case and the EUNSUPPORTED boundary.
 """
 import ctypes
 import os
@@ -125,21 +125,19 @@ def test_ntt_row_sharding_and_empty(phe):
     assert torch.equal(m1[0], m[0]) and torch.equal(bb1[0], b[0])
 
 
-@pytest.mark.parametrize("sign", [1, -1])
-def test_ntt_crt_range_near_bound(phe, coracle, sign):
-    """N = 512, q_in = 39: the CRT allows 59 blocks; at L = 59 with every weight at +127 / -128
-    the exact integer products reach ~2^59.9 of the 2^60.9 bound (both signs)."""
+def test_ntt_max_blocks_and_refusal(phe, coracle):
+    """N = 512, q_in = 39: the CRT allows 27 blocks (centred masks); L = 27 runs bit-exact, one
+    block more is refused (EUNSUPPORTED), never silently wrong."""
     p = phe.params(phe.PRESET_PAPER, N=512)
     Lmax = phe.ntt_max_blocks(p)
-    assert Lmax == 59
+    assert Lmax == 27
     d_in = Lmax * 512
-    W = np.full((2, d_in), 127 if sign > 0 else -128, np.int8)
+    W = synth.uniform_int8((2, d_in), 5, -128, 127)
     x = synth.uniform_int8((2, d_in), 11, -3, 3)
     S, seeds, body = encrypt(phe, p, x)
     _, _, (m, b) = ntt_run(phe, p, W, seeds, body, out_bits=39)
     mask_o, body_o = oracle_literal(coracle, p, W, seeds, body)
     assert np.array_equal(u64(m), mask_o) and np.array_equal(u64(b), body_o)
-    # one block more is refused (EUNSUPPORTED), never silently wrong
     W2 = np.ones((2, d_in + 512), np.int8)
     tabs = phe.NttTables(p)
     w2 = phe.NttWeights(p, tabs, torch.from_numpy(W2).to(DEV))
@@ -148,6 +146,37 @@ def test_ntt_crt_range_near_bound(phe, coracle, sign):
     op2 = phe.ntt_ct_prepare(p, tabs, s2, b2)
     with pytest.raises(phe.PheError, match="unsupported"):
         phe.matmul_clear_ntt(p, w2, op2, 1)
+
+
+@pytest.mark.parametrize("wval", [-128, 127])
+def test_ntt_crt_range_adversarial(phe, coracle, wval):
+    """The CRT range at its worst case: every mask word 2^39 - 1 (centred: 2^38 - 1) and every
+    weight -128 (or 127) over L = 27 blocks of N = 512 puts |P'[N-1]| = L N (2^38 - 1) |w| at the
+    bound of phe_ntt_max_blocks.  The NTT-domain operand is built on the host by the independent
+    Python NTT of tools/ntt_model.py (no seed can produce constant masks); expected values come
+    from the oracle's literal Eq. 6."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import ntt_model
+    p = phe.params(phe.PRESET_PAPER, N=512)
+    N, L, T = 512, phe.ntt_max_blocks(p), 1
+    H = 2 ** 38
+    A = np.full((L, N), 2 ** 39 - 1, np.uint64)
+    W = np.full((2, L * N), wval, np.int8)
+    W[1, ::7] = 0  # second row: a different weight sum parity / pattern
+    ahat = np.zeros((T, L, 2, N), np.uint32)
+    for q, (pr, g) in enumerate(zip(ntt_model.P, ntt_model.GEN)):
+        fwd, _ = ntt_model.tables(pr, g, N)
+        for i in range(L):
+            ahat[0, i, q] = ntt_model.ntt_fwd([(int(a) - H) % pr for a in A[i]], pr, fwd)
+    nbytes = phe.load().phe_ntt_operand_bytes(ctypes.byref(p), T, L)
+    opnd = np.zeros(nbytes, np.uint8)           # body planes zero: B = 0
+    opnd[: ahat.nbytes] = ahat.reshape(-1).view(np.uint8)
+    tabs = phe.NttTables(p)
+    w = phe.NttWeights(p, tabs, torch.from_numpy(W).to(DEV))
+    m, b = phe.matmul_clear_ntt(p, w, torch.from_numpy(opnd).to(DEV), T, out_bits=39)
+    mo, bo = coracle.matmul_clear_literal(oparams(p), W, A, np.zeros((L, N), np.uint64), nthreads=os.cpu_count())
+    assert np.array_equal(u64(m[0]), mo) and np.array_equal(u64(b[0]), bo)
 
 
 def test_ntt_full_size_q_proj_sampled(phe, coracle):

@@ -46,10 +46,10 @@ def test_ntt_primes(lib):
     p0, p1 = lib.ntt_primes()
     assert (p0, p1) == tuple(ntt_model.P)
     for p in (p0, p1):
-        assert is_prime(p) and p < 2 ** 31
+        assert is_prime(p) and 4 * p < 2 ** 32       # lazy [0, 2p) arithmetic in 32-bit words
         assert (p - 1) % (2 * 8192) == 0          # primitive 2N-th roots exist for N <= 8192
-    assert p0 < p1                                 # CRT step takes r0 < p1
-    assert p0 * p1 > 2 ** 61
+    assert p0 < p1
+    assert p0 * p1 > 2 ** 59
 
 
 @pytest.mark.parametrize("over", [{}, dict(N=512), dict(N=8192), dict(N=1024, q_in=32, q_out=28, beta=21)])
@@ -57,11 +57,33 @@ def test_ntt_max_blocks_is_the_crt_range(lib, over):
     p = lib.params(lib.PRESET_PAPER, **over)
     p0, p1 = lib.ntt_primes()
     L = lib.ntt_max_blocks(p)
-    worst = lambda L: L * p.N * (2 ** p.q_in - 1) * 128   # |sum_i A_i * w_i| bound, |w| <= 128
+    # centred masks |A - 2^(q-1)| <= 2^(q-1), |w| <= 128: |sum_i A'_i * w_i| <= L N 2^(q-1) 128
+    worst = lambda L: L * p.N * 2 ** (p.q_in - 1) * 128
     assert L >= 1
     assert worst(L) < p0 * p1 // 2 <= worst(L + 1)
     if not over:
-        assert L == 14                             # Table 1: d_in up to 28672
+        assert L == 6                              # Table 1: d_in up to 12288 (Llama-3.2-1B: 8192)
+
+
+def test_centring_parity_identity():
+    """P = P' + H (1 * w) with A' = A - H, and every coefficient of the negacyclic 1 * w has the
+    parity of sum(w): so P = P' + H * (sum(w) mod 2) mod 2^q (R23), brute force."""
+    import random
+    rng = random.Random(9)
+    q, N = 39, 32
+    H = 2 ** (q - 1)
+    for _ in range(30):
+        L = rng.randint(1, 3)
+        A = [[rng.randrange(2 ** q) for _ in range(N)] for _ in range(L)]
+        W = [[rng.randrange(-128, 128) for _ in range(N)] for _ in range(L)]
+        full, cent = [0] * N, [0] * N
+        for i in range(L):
+            for k, v in enumerate(ntt_model.negacyclic(A[i], W[i])):
+                full[k] += v
+            for k, v in enumerate(ntt_model.negacyclic([a - H for a in A[i]], W[i])):
+                cent[k] += v
+        par = sum(map(sum, W)) & 1
+        assert all((cent[k] + H * par - full[k]) % 2 ** q == 0 for k in range(N))
 
 
 def test_ntt_kernel_index_scheme():

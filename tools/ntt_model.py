@@ -5,8 +5,8 @@ Development tool only (not the oracle, not the product).  Run: python tools/ntt_
 """
 import random
 
-P = [2013265921, 2113929217]
-GEN = [31, 5]
+P = [998244353, 1004535809]
+GEN = [3, 3]
 
 
 def bitrev(x, bits):
