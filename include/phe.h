@@ -253,12 +253,16 @@ int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out
  *             inverse twiddles of stages 0-3 regrouped per thread of the hot kernel; written
  *             once by phe_ntt_tables_init; read-only afterwards; shared by every call with p.
  *   d_nttw    phe_ntt_weights_bytes(p, rows, cols), rows/cols of M = W (transpose 0) or W^T:
- *               [rows][Lc][2][N] uint32  NTT_p(w_hat_ij) * N^-1 * 2^32 mod p (bit-reversed order;
- *                                        w_hat_ij[k] = M[j, iN+N-1-k])
+ *               [rows][Lc][2][N] uint32  NTT_p(w_hat_ij) * N^-1 * 2^32 mod p (w_hat_ij[k] =
+ *                                        M[j, iN+N-1-k])
  *               [round128(rows)][Lc*N] int8  M zero-padded (body GEMM operand)
+ *               [round16(rows)] uint8    (sum_c M[j,c]) mod 2, the centring correction (R23)
  *   d_operand phe_ntt_operand_bytes(p, T, L):
- *               [T][L][2][N] uint32  NTT_p(A_{tau,i} mod p), A = PRNG(seed) mod 2^q_in
+ *               [T][L][2][N] uint32  NTT_p(A_{tau,i} - 2^(q_in-1) mod p), A = PRNG(seed) mod 2^q_in
+ *                                    (centred, R23)
  *               [op_rows][L*N] uint8 body limb planes (the second half of phe_ct_prepare's layout)
+ *             NTT-domain vectors: element k of the bit-reversed transform output is stored at
+ *             word 4*(((k>>2)&3)*(N/16) + (k>>4)) + (k&3) (the hot kernel's thread order).
  * Errors as phe_matmul_clear; EUNSUPPORTED for N or L outside the range above.              */
 int phe_ntt_primes(uint32_t *out2);
 int64_t phe_ntt_max_blocks(const phe_params *p);

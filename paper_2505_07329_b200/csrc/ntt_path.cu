@@ -100,6 +100,14 @@ __device__ __forceinline__ uint32_t mont_lazy(uint32_t a, uint32_t b, uint32_t p
 
 __device__ __forceinline__ uint32_t brev(uint32_t k, int logN) { return __brev(k) >> (32 - logN); }
 
+// Storage order of NTT-domain vectors (W_hat, A_hat; per prime, N words): element k (bit-reversed
+// transform order) of thread t = k/16 of the hot kernel, k = 16t + 4v + c, is stored at word
+// 4 (v NT + t) + c (NT = N/16), so each of the thread's four 16-byte loads is one contiguous
+// 512-byte warp access.
+__host__ __device__ __forceinline__ int tpos(int k, int N) {
+  return 4 * (((k >> 2) & 3) * (N / 16) + (k >> 4)) + (k & 3);
+}
+
 // ---------------------------------------------------------------- tables
 // d_tables layout: uint2 [2 dirs][2 primes][N]; dir 0 = psi^{bitrev(k)} (forward CT),
 // dir 1 = psi^{-bitrev(k)} (inverse GS); .x = w, .y = floor(w 2^32 / p).  psi = g^((p-1)/2N)
@@ -173,7 +181,7 @@ ntt_weights_kernel(int logN, const int8_t *__restrict__ W, int64_t d_in, int tra
   uint32_t *o = out + ji * 2 * N;
   for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) {
     const int pr = k / N;
-    o[k] = (uint32_t)((uint64_t)xs[k] * (pr ? c1 : c0) % prime(pr));
+    o[pr * N + tpos(k % N, N)] = (uint32_t)((uint64_t)xs[k] * (pr ? c1 : c0) % prime(pr));
   }
 }
 
@@ -201,7 +209,7 @@ ntt_masks_kernel(KParams kp, int logN, const uint64_t *__restrict__ seeds,
   __syncthreads();
   ntt_forward_smem(xs, tab, logN);
   uint32_t *o = out + blk * 2 * N;
-  for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) o[k] = xs[k];
+  for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) o[(k / N) * N + tpos(k % N, N)] = xs[k];
 }
 
 // par[j] = (sum_c M[j, c]) mod 2 (the centring correction bit of row j); one warp per row
@@ -392,13 +400,15 @@ __device__ __forceinline__ void load_twiddles(const uint2 *tinv, uint4 *tw1, uin
   }
 }
 
-template <int LOGN, int NG, int NB>
-__host__ __device__ constexpr int ntt_min_blocks() {  // CTAs/SM the shared memory allows (<= 8)
-  return (227 * 1024) / ntt_smem<LOGN, NG, NB>() < 8 ? (227 * 1024) / ntt_smem<LOGN, NG, NB>() : 8;
+template <int LOGN, int NG>
+__host__ __device__ constexpr int ntt_min_blocks() {  // target 512 threads / SM: 128 registers
+  return 512 / (NG * (1 << LOGN) / 16) > 1 ? 512 / (NG * (1 << LOGN) / 16) : 1;
 }
 
-template <int LOGN, bool SW, int NG, int NB, int SHIFT = 0, int OUTB = 0>
-__global__ void __launch_bounds__(NG * (1 << LOGN) / 16, ntt_min_blocks<LOGN, NG, NB>())
+// WSM: W_hat_j (all Lc blocks, 8 N bytes each) staged in shared memory once per CTA and shared
+// by the NG token groups; else read through L1/L2.
+template <int LOGN, bool SW, int NG, int NB, bool WSM, int SHIFT = 0, int OUTB = 0>
+__global__ void __launch_bounds__(NG * (1 << LOGN) / 16, ntt_min_blocks<LOGN, NG>())
 ntt_mask_kernel(MaskArgs a) {
   constexpr int N = 1 << LOGN, NT = N / 16;
   static_assert(LOGN >= 9 && LOGN <= 13, "N in [512, 8192]");
@@ -416,8 +426,14 @@ ntt_mask_kernel(MaskArgs a) {
   const int64_t j = a.row_begin + jr;
   const int64_t t_begin = chunk * a.tok_per_cta;
   const int64_t t_end = min(a.T, t_begin + a.tok_per_cta);
-  const uint4 *wrow = reinterpret_cast<const uint4 *>(a.what + j * a.Lc * 2 * N) + tid * 4;
+  const uint4 *wrow = reinterpret_cast<const uint4 *>(a.what + j * a.Lc * 2 * N) + tid;
   const int64_t tok4 = a.Lc * 2 * (N / 4);
+  if constexpr (WSM) {  // stage W_hat_j after the exchange buffers
+    uint4 *wsm = reinterpret_cast<uint4 *>(xb - grp * NB * 2 * xwords<LOGN>() + NG * NB * 2 * xwords<LOGN>());
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.what + j * a.Lc * 2 * N);
+    for (int64_t k = threadIdx.x; k < tok4; k += NG * NT) wsm[k] = src[k];
+    wrow = wsm + tid;
+  }
   const int s_shift = a.q_in - a.out_bits;
   const uint64_t rnd = s_shift ? (1ull << (s_shift - 1)) : 0ull;
   const uint32_t omask = (uint32_t)mask_bits(a.out_bits);
@@ -425,24 +441,24 @@ ntt_mask_kernel(MaskArgs a) {
   // A_hat_{tau,0} of the next token is prefetched into registers while this one is transformed
   uint4 an[2][4];
   if (t_begin + grp < t_end) {
-    const uint4 *a0 = reinterpret_cast<const uint4 *>(a.ahat) + (t_begin + grp) * tok4 + tid * 4;
+    const uint4 *a0 = reinterpret_cast<const uint4 *>(a.ahat) + (t_begin + grp) * tok4 + tid;
 #pragma unroll
     for (int q = 0; q < 2; q++)
 #pragma unroll
-      for (int v = 0; v < 4; v++) an[q][v] = __ldg(a0 + q * (N / 4) + v);
+      for (int v = 0; v < 4; v++) an[q][v] = __ldg(a0 + q * (N / 4) + v * NT);
   }
   __syncthreads();
 
   for (int64_t tau = t_begin + grp; tau < t_end; tau += NG) {
     uint32_t r[2][16];
     // ---- pointwise: sum_i W_hat_ij o A_hat_{tau,i} (N^{-1} folded into W_hat), elements 16 tid..+15
-    const uint4 *arow = reinterpret_cast<const uint4 *>(a.ahat) + tau * tok4 + tid * 4;
+    const uint4 *arow = reinterpret_cast<const uint4 *>(a.ahat) + tau * tok4 + tid;
 #pragma unroll
     for (int q = 0; q < 2; q++) {
       const uint32_t pi = q ? PINV1 : PINV0;
 #pragma unroll
       for (int v = 0; v < 4; v++) {
-        const uint4 wv = __ldg(wrow + q * (N / 4) + v), av = an[q][v];
+        const uint4 wv = WSM ? wrow[q * (N / 4) + v * NT] : __ldg(wrow + q * (N / 4) + v * NT), av = an[q][v];
         r[q][4 * v + 0] = mont_lazy(wv.x, av.x, p[q], pi);
         r[q][4 * v + 1] = mont_lazy(wv.y, av.y, p[q], pi);
         r[q][4 * v + 2] = mont_lazy(wv.z, av.z, p[q], pi);
@@ -454,7 +470,7 @@ ntt_mask_kernel(MaskArgs a) {
 #pragma unroll
       for (int q = 0; q < 2; q++)
 #pragma unroll
-        for (int v = 0; v < 4; v++) an[q][v] = __ldg(a0 + q * (N / 4) + v);
+        for (int v = 0; v < 4; v++) an[q][v] = __ldg(a0 + q * (N / 4) + v * NT);
     }
     for (int64_t i = 1; i < a.Lc; i++) {
 #pragma unroll
@@ -462,8 +478,8 @@ ntt_mask_kernel(MaskArgs a) {
         const uint32_t pi = q ? PINV1 : PINV0;
 #pragma unroll
         for (int v = 0; v < 4; v++) {
-          const int64_t off = (i * 2 + q) * (N / 4) + v;
-          const uint4 wv = __ldg(wrow + off), av = __ldg(arow + off);
+          const int64_t off = (i * 2 + q) * (N / 4) + v * NT;
+          const uint4 wv = WSM ? wrow[off] : __ldg(wrow + off), av = __ldg(arow + off);
           const uint32_t m[4] = {mont_lazy(wv.x, av.x, p[q], pi), mont_lazy(wv.y, av.y, p[q], pi),
                                  mont_lazy(wv.z, av.z, p[q], pi), mont_lazy(wv.w, av.w, p[q], pi)};
 #pragma unroll
@@ -482,12 +498,16 @@ ntt_mask_kernel(MaskArgs a) {
   }
 }
 
-template <int LOGN, bool SW, int NG, int NB, int SHIFT = 0, int OUTB = 0>
-int launch_mask_cfg(const MaskArgs &a, cudaStream_t st) {
-  auto kern = ntt_mask_kernel<LOGN, SW, NG, NB, SHIFT, OUTB>;
-  constexpr int smem = ntt_smem<LOGN, NG, NB>();
+template <int LOGN, bool SW, int NG, int NB, bool WSM, int SHIFT = 0, int OUTB = 0>
+int launch_mask_cfg(MaskArgs a, cudaStream_t st) {
+  auto kern = ntt_mask_kernel<LOGN, SW, NG, NB, WSM, SHIFT, OUTB>;
+  const int smem = ntt_smem<LOGN, NG, NB>() + (WSM ? (int)(a.Lc * 2 * (1 << LOGN) * 4) : 0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return phe_set_cuda_error(e);
+  const char *ev = getenv("PHE_NTT_TOK");
+  a.tok_per_cta = ev ? atoi(ev) : 8 * NG;  // 8 tokens per group
+  if (a.tok_per_cta < 1) a.tok_per_cta = 1;
+  a.n_chunks = (a.T + a.tok_per_cta - 1) / a.tok_per_cta;
   kern<<<(unsigned)(a.R * a.n_chunks), NG * (1 << LOGN) / 16, smem, st>>>(a);
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
@@ -496,11 +516,23 @@ int launch_mask_cfg(const MaskArgs &a, cudaStream_t st) {
 // One token group and one exchange buffer per CTA (smallest shared-memory footprint: 4 CTAs /
 // 16 warps per SM at N = 2048).  Measured alternatives (2 groups sharing the twiddles, 2
 // alternating buffers) were within 2% on q_proj and slower at L = 4.
+// N = 2048: W_hat_j in shared memory, shared by 2 token groups (L <= 2: 83-99 KB, 2 CTAs/SM) or 4
+// (L <= 6: 150-198 KB, 1 CTA of 16 warps); Table 1's switch compiled in.  Other N: one group,
+// W_hat_j staged when it fits.
+constexpr int SMEM_BUDGET = 200 * 1024;
 template <int LOGN, bool SW>
 int launch_mask(const MaskArgs &a, cudaStream_t st) {
-  if (SW && LOGN == 11 && a.q_in == 39 && a.out_bits == 26)  // Table 1: compile-time switch
-    return launch_mask_cfg<LOGN, SW, 1, 1, 13, 26>(a, st);
-  return launch_mask_cfg<LOGN, SW, 1, 1>(a, st);
+  if constexpr (LOGN == 11) {
+    if (a.Lc <= 6) {
+      const bool t1 = SW && a.q_in == 39 && a.out_bits == 26;
+      if (a.Lc <= 2)
+        return t1 ? launch_mask_cfg<LOGN, SW, 2, 1, true, 13, 26>(a, st) : launch_mask_cfg<LOGN, SW, 2, 1, true>(a, st);
+      return t1 ? launch_mask_cfg<LOGN, SW, 4, 1, true, 13, 26>(a, st) : launch_mask_cfg<LOGN, SW, 4, 1, true>(a, st);
+    }
+  }
+  if (ntt_smem<LOGN, 1, 1>() + a.Lc * 2 * (1 << LOGN) * 4 <= SMEM_BUDGET)
+    return launch_mask_cfg<LOGN, SW, 1, 1, true>(a, st);
+  return launch_mask_cfg<LOGN, SW, 1, 1, false>(a, st);
 }
 
 }  // namespace ntt
@@ -586,10 +618,6 @@ int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what,
   a.qmask = kp.qmask;
   a.out = out;
   if (a.R == 0 || T == 0) return PHE_OK;
-  const char *e = getenv("PHE_NTT_TOK");
-  a.tok_per_cta = e ? atoi(e) : 16;
-  if (a.tok_per_cta < 1) a.tok_per_cta = 1;
-  a.n_chunks = (T + a.tok_per_cta - 1) / a.tok_per_cta;
   const bool sw = out_bits != kp.q_in;
   switch (kp.log2N) {
     case 9: return sw ? ntt::launch_mask<9, true>(a, st) : ntt::launch_mask<9, false>(a, st);

@@ -165,10 +165,12 @@ def test_ntt_crt_range_adversarial(phe, coracle, wval):
     W = np.full((2, L * N), wval, np.int8)
     W[1, ::7] = 0  # second row: a different weight sum parity / pattern
     ahat = np.zeros((T, L, 2, N), np.uint32)
+    # storage order of NTT-domain vectors (include/phe.h): element k at 4*(((k>>2)&3)*N/16 + (k>>4)) + (k&3)
+    pos = np.array([4 * (((k >> 2) & 3) * (N // 16) + (k >> 4)) + (k & 3) for k in range(N)])
     for q, (pr, g) in enumerate(zip(ntt_model.P, ntt_model.GEN)):
         fwd, _ = ntt_model.tables(pr, g, N)
         for i in range(L):
-            ahat[0, i, q] = ntt_model.ntt_fwd([(int(a) - H) % pr for a in A[i]], pr, fwd)
+            ahat[0, i, q, pos] = ntt_model.ntt_fwd([(int(a) - H) % pr for a in A[i]], pr, fwd)
     nbytes = phe.load().phe_ntt_operand_bytes(ctypes.byref(p), T, L)
     opnd = np.zeros(nbytes, np.uint8)           # body planes zero: B = 0
     opnd[: ahat.nbytes] = ahat.reshape(-1).view(np.uint8)
