@@ -234,6 +234,8 @@ struct MaskArgs {
   int64_t n_chunks;         // ceil(T / tok_per_cta)
   int q_in, out_bits;
   uint64_t qmask;
+  uint32_t crt_k1;          // ((Z mod p1 - Z mod p0) mod p1) + 2 p1, Z the CRT offset (crt_store)
+  uint32_t crt_z0;          // Z mod p0
   void *out;                // [T][R][N] uint32 (switched) or uint64
 };
 
@@ -312,27 +314,23 @@ __device__ __forceinline__ void xload(uint32_t (&r)[NP][16], const uint32_t *xb,
 // SHIFT > 0: switch by a compile-time SHIFT = q_in - q_out (Table 1: 13) to OUTB = q_out bits.
 // Bits [s, q_in) of ((v mod 2^q_in) + 2^(s-1)) equal bits [s, q_in) of (v + 2^(s-1)), so the
 // rounding constant rides in the CRT's wide multiply-add and no 64-bit masking is needed.
-// r0, r1 lazy in [0, 2p): h = (r1 - r0) p0^-1 mod p1 (reduced) and v = r0 + p0 h in
-// [0, p0 p1 + p0) with v = P' mod p0 p1; v >= p0 p1 / 2 stands for v - p0 p1 (this also maps
-// v in [p0 p1, p0 p1 + p0) to its residue).  corr = H par_j restores P from the centred P'.
+// CRT without a centring compare.  Z is a multiple of 2^q_in with P' + Z in [2 p0, p0 p1) for
+// every P' the launch can produce (host: launch_ntt_mask), so with r0 in [0, 2p0) (lazy),
+// r1 reduced, h = (r1 - r0 + Z1 - Z0) p0^-1 mod p1 and v = p0 h + r0 + Z0 in [0, p0 p1 + 2 p0)
+// the only representative is v = P' + Z exactly; Z vanishes mod 2^q_in.  kadd = Z0 + H par_j
+// (+ the switch's rounding constant) is a per-CTA constant.
 template <bool SW, int SHIFT, int OUTB>
-__device__ __forceinline__ void crt_store(const MaskArgs &a, uint32_t r0, uint32_t r1, uint64_t corr,
-                                          int64_t o, uint64_t rnd, int s_shift, uint32_t omask) {
-  const uint32_t h = mul_shoup(r1 - r0 + 2 * P1, CRT_C, CRT_CQ, P1);
+__device__ __forceinline__ void crt_store(const MaskArgs &a, uint32_t r0, uint32_t r1, uint64_t kadd,
+                                          int64_t o, int s_shift, uint32_t omask) {
+  r1 = min(r1, r1 - P1);
+  const uint32_t h = mul_shoup(r1 - r0 + a.crt_k1, CRT_C, CRT_CQ, P1);  // argument < 4 p1 < 2^32
+  const uint64_t x = (uint64_t)P0 * h + r0 + kadd;                       // P + Z [+ 2^(s-1)]
   if constexpr (SW && SHIFT > 0) {
-    constexpr uint64_t R = 1ull << (SHIFT - 1);
-    uint64_t x = (uint64_t)P0 * h + (uint64_t)r0;                    // v
-    x += (x >= CRT_M / 2 ? (uint64_t)0 - CRT_M : 0) + corr + R;      // P + 2^(s-1) mod 2^64
     static_cast<uint32_t *>(a.out)[o] = (uint32_t)(x >> SHIFT) & ((1u << OUTB) - 1u);
-    return;
-  }
-  uint64_t val = (uint64_t)r0 + (uint64_t)P0 * h;
-  if (val >= CRT_M / 2) val -= CRT_M;               // centred; wraps mod 2^64
-  val += corr;
-  if (SW) {
-    static_cast<uint32_t *>(a.out)[o] = (uint32_t)(((val & a.qmask) + rnd) >> s_shift) & omask;
+  } else if constexpr (SW) {
+    static_cast<uint32_t *>(a.out)[o] = (uint32_t)(x >> s_shift) & omask;
   } else {
-    static_cast<uint64_t *>(a.out)[o] = val & a.qmask;
+    static_cast<uint64_t *>(a.out)[o] = x & a.qmask;
   }
 }
 
@@ -435,9 +433,9 @@ ntt_mask_kernel(MaskArgs a) {
     wrow = wsm + tid;
   }
   const int s_shift = a.q_in - a.out_bits;
-  const uint64_t rnd = s_shift ? (1ull << (s_shift - 1)) : 0ull;
+  const uint64_t rnd = (SW && s_shift) ? (1ull << (s_shift - 1)) : 0ull;
   const uint32_t omask = (uint32_t)mask_bits(a.out_bits);
-  const uint64_t corr = a.par[j] ? (1ull << (a.q_in - 1)) : 0ull;
+  const uint64_t kadd = (uint64_t)a.crt_z0 + (a.par[j] ? (1ull << (a.q_in - 1)) : 0ull) + rnd;
   // A_hat_{tau,0} of the next token is prefetched into registers while this one is transformed
   uint4 an[2][4];
   if (t_begin + grp < t_end) {
@@ -493,8 +491,8 @@ ntt_mask_kernel(MaskArgs a) {
     const int jt = eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(tid, 0);
 #pragma unroll
     for (int e = 0; e < 16; e++)
-      crt_store<SW, SHIFT, OUTB>(a, r[0][e], r[1][e], corr,
-                    obase - jt - eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(0, e), rnd, s_shift, omask);
+      crt_store<SW, SHIFT, OUTB>(a, r[0][e], r[1][e], kadd,
+                    obase - jt - eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(0, e), s_shift, omask);
   }
 }
 
@@ -618,6 +616,15 @@ int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what,
   a.qmask = kp.qmask;
   a.out = out;
   if (a.R == 0 || T == 0) return PHE_OK;
+  {  // the CRT offset Z (crt_store): multiple of 2^q_in >= max|P'| + 2 p0
+    const unsigned __int128 maxP = (unsigned __int128)Lc * kp.N * ((unsigned __int128)1 << (kp.q_in - 1)) * 128;
+    const unsigned __int128 g = (unsigned __int128)1 << kp.q_in;
+    const unsigned __int128 Z = (maxP + 2 * (unsigned __int128)ntt::P0 + g - 1) / g * g;
+    if (Z + maxP >= (unsigned __int128)ntt::CRT_M) return PHE_EUNSUPPORTED;
+    const uint32_t z0 = (uint32_t)(Z % ntt::P0), z1 = (uint32_t)(Z % ntt::P1);
+    a.crt_z0 = z0;
+    a.crt_k1 = (uint32_t)(((uint64_t)z1 + ntt::P1 - (z0 % ntt::P1)) % ntt::P1 + 2ull * ntt::P1);
+  }
   const bool sw = out_bits != kp.q_in;
   switch (kp.log2N) {
     case 9: return sw ? ntt::launch_mask<9, true>(a, st) : ntt::launch_mask<9, false>(a, st);

@@ -707,11 +707,19 @@ int64_t phe_ntt_max_blocks(const phe_params *p) {
   if (phe_params_validate(p)) return 0;
   uint32_t pr[2];
   phe::ntt_primes(pr);
-  // centred masks: |P'| <= L N 2^(q_in-1) 128 must stay below p0 p1 / 2 (R23)
-  const unsigned __int128 half = ((unsigned __int128)pr[0] * pr[1]) / 2;
-  const unsigned __int128 per_block = (unsigned __int128)p->N * ((unsigned __int128)1 << (p->q_in - 1)) * 128;
-  const unsigned __int128 L = (half - 1) / per_block;
-  return L > 1000000 ? 1000000 : (int64_t)L;
+  // centred masks: |P'| <= maxP(L) = L N 2^(q_in-1) 128; the CRT needs Z(L) + maxP(L) < p0 p1 with
+  // Z(L) = the least multiple of 2^q_in >= maxP(L) + 2 p0 (R23, ntt_path.cu crt_store)
+  const unsigned __int128 M = (unsigned __int128)pr[0] * pr[1];
+  const unsigned __int128 per = (unsigned __int128)p->N * ((unsigned __int128)1 << (p->q_in - 1)) * 128;
+  const unsigned __int128 g = (unsigned __int128)1 << p->q_in;
+  auto fits = [&](unsigned __int128 L) {
+    const unsigned __int128 mp = L * per, Z = (mp + 2 * (unsigned __int128)pr[0] + g - 1) / g * g;
+    return Z + mp < M;
+  };
+  unsigned __int128 L = M / (2 * per) + 1;
+  if (L > 1000000) L = 1000000;
+  while (L > 0 && !fits(L)) L--;
+  return (int64_t)L;
 }
 
 size_t phe_ntt_tables_bytes(const phe_params *p) {

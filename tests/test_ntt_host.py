@@ -57,10 +57,14 @@ def test_ntt_max_blocks_is_the_crt_range(lib, over):
     p = lib.params(lib.PRESET_PAPER, **over)
     p0, p1 = lib.ntt_primes()
     L = lib.ntt_max_blocks(p)
-    # centred masks |A - 2^(q-1)| <= 2^(q-1), |w| <= 128: |sum_i A'_i * w_i| <= L N 2^(q-1) 128
+    # centred masks |A - 2^(q-1)| <= 2^(q-1), |w| <= 128: |sum_i A'_i * w_i| <= L N 2^(q-1) 128;
+    # the CRT offset Z = least multiple of 2^q >= worst + 2 p0 must keep worst + Z < p0 p1
     worst = lambda L: L * p.N * 2 ** (p.q_in - 1) * 128
+    g = 2 ** p.q_in
+    fits = lambda L: worst(L) + -(-(worst(L) + 2 * p0) // g) * g < p0 * p1
     assert L >= 1
-    assert worst(L) < p0 * p1 // 2 <= worst(L + 1)
+    assert fits(L) and not fits(L + 1)
+    assert worst(L) < p0 * p1 // 2                 # implies the centred range rule
     if not over:
         assert L == 6                              # Table 1: d_in up to 12288 (Llama-3.2-1B: 8192)
 
