@@ -223,7 +223,8 @@ int phe_decrypt_packed(const phe_params *p, const uint8_t *d_S, const uint32_t *
  *   = 8 + N*q_in/8 bytes (9992 at Table 1).
  * Packed output (server -> client): [A' at q_out bits][B' at q_out bits] = 2*N*q_out/8 bytes
  *   (13312 at Table 1).  Requires q_in <= 57, N % 8 == 0.
- * d_seeds [T][L] / d_body [T][L][N] uint64; d_packed uint32 [n_ct][2][N]; d_wire bytes.     */
+ * d_seeds [T][L] / d_body [T][L][N] uint64; d_packed uint32 [n_ct][2][N]; d_wire bytes, 8-byte
+ * aligned (else EINVAL); requires N % 64 == 0 and q_in <= 57 (else EUNSUPPORTED).           */
 size_t phe_wire_input_bytes(const phe_params *p);
 size_t phe_wire_output_bytes(const phe_params *p);
 int phe_wire_serialize_inputs(const phe_params *p, const uint64_t *d_seeds, const uint64_t *d_body,

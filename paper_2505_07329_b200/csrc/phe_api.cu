@@ -563,7 +563,7 @@ extern "C" int phe_server_matvec_packed_host(const phe_params *p, const void *d_
 static int check_wire(const phe_params *p, KParams *kp) {
   int rc = check_gpu(p, kp);
   if (rc) return rc;
-  if (p->q_in > 57 || p->N % 8) return PHE_EUNSUPPORTED;
+  if (p->q_in > 57 || p->N % 64) return PHE_EUNSUPPORTED;  // whole 64-bit stream words per segment
   return PHE_OK;
 }
 
@@ -583,7 +583,7 @@ int phe_wire_serialize_inputs(const phe_params *p, const uint64_t *d_seeds, cons
   if (rc) return rc;
   if (T < 0 || L < 1) return PHE_EINVAL;
   if (T == 0) return PHE_OK;
-  if (!d_seeds || !d_body || !d_wire) return PHE_EINVAL;
+  if (!d_seeds || !d_body || !d_wire || ((uintptr_t)d_wire & 7)) return PHE_EINVAL;
   return phe::launch_wire_inputs(kp, const_cast<uint64_t *>(d_seeds), const_cast<uint64_t *>(d_body), T * L, d_wire, 0,
                                  S(stream));
 }
@@ -595,7 +595,7 @@ int phe_wire_deserialize_inputs(const phe_params *p, const uint8_t *d_wire, int6
   if (rc) return rc;
   if (T < 0 || L < 1) return PHE_EINVAL;
   if (T == 0) return PHE_OK;
-  if (!d_seeds || !d_body || !d_wire) return PHE_EINVAL;
+  if (!d_seeds || !d_body || !d_wire || ((uintptr_t)d_wire & 7)) return PHE_EINVAL;
   return phe::launch_wire_inputs(kp, d_seeds, d_body, T * L, const_cast<uint8_t *>(d_wire), 1, S(stream));
 }
 
@@ -606,7 +606,7 @@ int phe_wire_serialize_packed(const phe_params *p, const uint32_t *d_packed, int
   if (rc) return rc;
   if (n_ct < 0) return PHE_EINVAL;
   if (n_ct == 0) return PHE_OK;
-  if (!d_packed || !d_wire) return PHE_EINVAL;
+  if (!d_packed || !d_wire || ((uintptr_t)d_wire & 7)) return PHE_EINVAL;
   return phe::launch_wire_packed(kp, const_cast<uint32_t *>(d_packed), n_ct, d_wire, 0, S(stream));
 }
 
@@ -617,7 +617,7 @@ int phe_wire_deserialize_packed(const phe_params *p, const uint8_t *d_wire, int6
   if (rc) return rc;
   if (n_ct < 0) return PHE_EINVAL;
   if (n_ct == 0) return PHE_OK;
-  if (!d_packed || !d_wire) return PHE_EINVAL;
+  if (!d_packed || !d_wire || ((uintptr_t)d_wire & 7)) return PHE_EINVAL;
   return phe::launch_wire_packed(kp, d_packed, n_ct, const_cast<uint8_t *>(d_wire), 1, S(stream));
 }
 

@@ -549,78 +549,89 @@ int launch_decrypt_packed(const KParams &kp, const uint8_t *S, const uint32_t *p
 }
 
 // ================================================================== NEXT #2: wire format
-// Little-endian contiguous bitstream (R22): 8 words of `bits` bits -> exactly `bits`
-// bytes, one thread per 8-word group.  bits <= 57.
+// Little-endian contiguous bitstream (R22).  Every segment (input block: LE64 seed, then
+// N coefficients at q_in bits; packed ciphertext: 2N coefficients at q_out bits) is a whole
+// number of 64-bit words (N % 64 == 0) and starts 8-byte aligned, so the stream is handled as
+// aligned uint64 words: serialize = one thread per stream word, gathering the <= 4 coefficients
+// that overlap it; deserialize = one thread per coefficient, reading the <= 2 words that cover
+// it.  Both directions are fully coalesced.  bits <= 57.
 template <typename WordT>
-__device__ __forceinline__ void pack8(const WordT *in, int bits, uint8_t *out) {
+__device__ __forceinline__ uint64_t gather_word(const WordT *vals, int nvals, int bits, int w) {
   const uint64_t m = mask_bits(bits);
-  uint64_t buf = 0;
-  int nb = 0, o = 0;
-#pragma unroll
-  for (int k = 0; k < 8; k++) {
-    buf |= ((uint64_t)in[k] & m) << nb;
-    nb += bits;
-    while (nb >= 8) { out[o++] = (uint8_t)buf; buf >>= 8; nb -= 8; }
+  const int b0 = 64 * w;  // in-segment bit offsets fit 32 bits (N <= 16384, bits <= 57)
+  uint64_t out = 0;
+#pragma unroll 4
+  for (int k = b0 / bits; k < nvals && k * bits < b0 + 64; k++) {
+    const int sh = k * bits - b0;  // in (-bits, 64)
+    const uint64_t v = (uint64_t)vals[k] & m;
+    out |= sh >= 0 ? (v << sh) : (v >> (-sh));
   }
+  return out;
 }
-template <typename WordT>
-__device__ __forceinline__ void unpack8(const uint8_t *in, int bits, WordT *out) {
-  const uint64_t m = mask_bits(bits);
-  uint64_t buf = 0;
-  int nb = 0, i = 0;
-#pragma unroll
-  for (int k = 0; k < 8; k++) {
-    while (nb < bits) { buf |= (uint64_t)in[i++] << nb; nb += 8; }
-    out[k] = (WordT)(buf & m);
-    buf >>= bits;
-    nb -= bits;
-  }
+__device__ __forceinline__ uint64_t extract_bits(const uint64_t *words, int k, int bits) {
+  const int b = k * bits;
+  const int w = b >> 6, r = b & 63;
+  uint64_t v = words[w] >> r;
+  if (r + bits > 64) v |= words[w + 1] << (64 - r);
+  return v & mask_bits(bits);
 }
 
-// inputs: block (tau, i) -> [LE64 seed][N coefficients at q_in bits]
+// 2-D grids: y = segment (grid-strided), x = stream word (serialize) or coefficient (deserialize)
+// inputs: block (tau, i) -> [LE64 seed][N coefficients at q_in bits], as 1 + N q/64 words
 __global__ void wire_inputs_kernel(int N, int q, uint64_t *__restrict__ seeds, uint64_t *__restrict__ body,
-                                   int64_t nblk, uint8_t *__restrict__ wire, int dir) {
-  const int64_t gpb = N / 8 + 1;  // 8-word groups per block, +1 for the seed
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= nblk * gpb) return;
-  const int64_t blk = idx / gpb, g = idx % gpb;
-  const int64_t bb = 8 + (int64_t)N * q / 8;
-  uint8_t *w = wire + blk * bb;
-  if (g == N / 8) {  // the seed
-    if (dir == 0) for (int b = 0; b < 8; b++) w[b] = (uint8_t)(seeds[blk] >> (8 * b));
-    else { uint64_t sd = 0; for (int b = 0; b < 8; b++) sd |= (uint64_t)w[b] << (8 * b); seeds[blk] = sd; }
-    return;
+                                   int64_t nblk, uint64_t *__restrict__ wire, int dir) {
+  const int nw = N * q / 64;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t blk = blockIdx.y; blk < nblk; blk += gridDim.y) {
+    uint64_t *wb = wire + blk * (1 + nw);
+    if (dir == 0) {
+      if (x <= nw) wb[x] = x == 0 ? seeds[blk] : gather_word<uint64_t>(body + blk * N, N, q, x - 1);
+    } else {  // 4 coefficients per thread (16-byte stores)
+      if (4 * x < N) {
+        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(body + blk * N + 4 * x);
+        dst[0] = make_ulonglong2(extract_bits(wb + 1, 4 * x, q), extract_bits(wb + 1, 4 * x + 1, q));
+        dst[1] = make_ulonglong2(extract_bits(wb + 1, 4 * x + 2, q), extract_bits(wb + 1, 4 * x + 3, q));
+      } else if (4 * x == N) {
+        seeds[blk] = wb[0];
+      }
+    }
   }
-  if (dir == 0) pack8<uint64_t>(body + blk * N + 8 * g, q, w + 8 + g * q);
-  else unpack8<uint64_t>(w + 8 + g * q, q, body + blk * N + 8 * g);
 }
 
-// packed outputs: ciphertext (tau, g) -> [A' at q_out bits][B' at q_out bits]
-__global__ void wire_packed_kernel(int N, int q, uint32_t *__restrict__ packed, int64_t nct, uint8_t *__restrict__ wire,
-                                   int dir) {
-  const int64_t gpc = 2 * (int64_t)N / 8;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= nct * gpc) return;
-  const int64_t ct = idx / gpc, g = idx % gpc;
-  uint8_t *w = wire + ct * (2 * (int64_t)N * q / 8) + g * q;
-  uint32_t *v = packed + ct * 2 * N + 8 * g;
-  if (dir == 0) pack8<uint32_t>(v, q, w);
-  else unpack8<uint32_t>(w, q, v);
+// packed outputs: ciphertext (tau, g) -> [A' at q_out bits][B' at q_out bits], 2N q/64 words
+__global__ void wire_packed_kernel(int N, int q, uint32_t *__restrict__ packed, int64_t nct,
+                                   uint64_t *__restrict__ wire, int dir) {
+  const int nw = 2 * N * q / 64;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t ct = blockIdx.y; ct < nct; ct += gridDim.y) {
+    if (dir == 0) {
+      if (x < nw) wire[ct * nw + x] = gather_word<uint32_t>(packed + ct * 2 * N, 2 * N, q, x);
+    } else {  // 4 coefficients per thread (16-byte stores)
+      if (4 * x < 2 * N) {
+        const uint64_t *wc = wire + ct * nw;
+        *reinterpret_cast<uint4 *>(packed + ct * 2 * N + 4 * x) =
+            make_uint4((uint32_t)extract_bits(wc, 4 * x, q), (uint32_t)extract_bits(wc, 4 * x + 1, q),
+                       (uint32_t)extract_bits(wc, 4 * x + 2, q), (uint32_t)extract_bits(wc, 4 * x + 3, q));
+      }
+    }
+  }
 }
 
 int launch_wire_inputs(const KParams &kp, uint64_t *seeds, uint64_t *body, int64_t nblk, uint8_t *wire,
                        int dir, cudaStream_t st) {
-  const int64_t n = nblk * (kp.N / 8 + 1);
-  if (n == 0) return PHE_OK;
-  wire_inputs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kp.N, kp.q_in, seeds, body, nblk, wire, dir);
+  if (nblk == 0) return PHE_OK;
+  const int nx = dir == 0 ? 1 + kp.N * kp.q_in / 64 : kp.N / 4 + 1;
+  const dim3 grid((unsigned)((nx + 255) / 256), (unsigned)(nblk < 65535 ? nblk : 65535));
+  wire_inputs_kernel<<<grid, 256, 0, st>>>(kp.N, kp.q_in, seeds, body, nblk, reinterpret_cast<uint64_t *>(wire), dir);
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
 }
 
 int launch_wire_packed(const KParams &kp, uint32_t *packed, int64_t nct, uint8_t *wire, int dir, cudaStream_t st) {
-  const int64_t n = nct * 2 * kp.N / 8;
-  if (n == 0) return PHE_OK;
-  wire_packed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kp.N, kp.q_out, packed, nct, wire, dir);
+  if (nct == 0) return PHE_OK;
+  const int nx = dir == 0 ? 2 * kp.N * kp.q_out / 64 : 2 * kp.N / 4;
+  const dim3 grid((unsigned)((nx + 255) / 256), (unsigned)(nct < 65535 ? nct : 65535));
+  wire_packed_kernel<<<grid, 256, 0, st>>>(kp.N, kp.q_out, packed, nct, reinterpret_cast<uint64_t *>(wire), dir);
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
 }
