@@ -138,6 +138,16 @@ int phe_matmul_clear_T(const phe_params *p, const void *d_wprep, int64_t d_out, 
                        int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
                        int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);
 
+/* ---- matmul_clear(W, ct): the north_star's one-call form on device buffers ------------------
+ * phe_ct_prepare of (d_seeds, d_body) into the caller's workspace d_ws (>= phe_ct_operand_bytes(p,
+ * T, L), L = blocks of the input length: d_in forward, d_out backward), then phe_matmul_clear
+ * (transpose = 0, d_wprep of W) or phe_matmul_clear_T (transpose = 1, d_wprep of W^T).  Same
+ * outputs, layouts and errors as those two calls; ENOMEM if ws_bytes is too small.          */
+int phe_matmul_clear_ct(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                        int transpose, int64_t row_begin, int64_t row_end, const uint64_t *d_seeds,
+                        const uint64_t *d_body, int64_t T, int32_t out_bits, void *d_ws,
+                        size_t ws_bytes, void *d_out_mask, void *d_out_body, void *stream);
+
 /* ---- a8 standalone: ModulusSwitch --------------------------
  * d_out[k] = floor((d_in[k] + 2^(f-t-1)) / 2^(f-t)) mod 2^t, f = from_bits, t = to_bits,
  * round half up on the non-negative residue (R8).  Requires 1 <= t <= f <= 64, t <= 32.  */

@@ -37,7 +37,7 @@ EXPORTS = [
     "phe_wire_serialize_packed", "phe_wire_deserialize_packed", "phe_server_wire_host",
     "phe_ntt_primes", "phe_ntt_max_blocks", "phe_ntt_tables_bytes", "phe_ntt_tables_init",
     "phe_ntt_weights_bytes", "phe_ntt_weights_prepare", "phe_ntt_operand_bytes", "phe_ntt_ct_prepare",
-    "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T",
+    "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T", "phe_matmul_clear_ct",
 ]
 
 
@@ -116,6 +116,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_wire_serialize_packed": ([_P, _vp, _i64, _vp, _vp], ctypes.c_int),
         "phe_wire_deserialize_packed": ([_P, _vp, _i64, _vp, _vp], ctypes.c_int),
         "phe_server_wire_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
+        "phe_matmul_clear_ct": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _sz,
+                                 _vp, _vp, _vp], ctypes.c_int),
         "phe_ntt_primes": ([_vp], ctypes.c_int),
         "phe_ntt_max_blocks": ([_P], _i64),
         "phe_ntt_tables_bytes": ([_P], _sz),
@@ -278,6 +280,23 @@ def matmul_clear_T(p: Params, w: Weights, operand: torch.Tensor, T: int, out_bit
     _check(load().phe_matmul_clear_T(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, row_begin, row_end,
                                      _ptr(operand), T, out_bits, _ptr(out_mask), _ptr(out_body), _stream()),
            "phe_matmul_clear_T")
+    return out_mask, out_body
+
+
+def matmul_clear_ct(p: Params, w: Weights, seeds: torch.Tensor, body: torch.Tensor, out_bits: int | None = None,
+                    row_begin: int = 0, row_end: int | None = None, ws: torch.Tensor | None = None):
+    """matmul_clear(W, ct) in one call (phe_matmul_clear_ct): expands the seeded ciphertext into a
+    workspace and contracts it; forward or backward by w.transpose."""
+    _dev(seeds, torch.int64, "seeds"); _dev(body, torch.int64, "body")
+    T, L = seeds.shape
+    out_bits = p.q_out if out_bits is None else out_bits
+    row_end = w.rows if row_end is None else row_end
+    if ws is None:
+        ws = torch.empty(load().phe_ct_operand_bytes(ctypes.byref(p), T, L), dtype=torch.uint8, device=seeds.device)
+    out_mask, out_body = _outputs(p, T, row_end - row_begin, out_bits, seeds.device, None, None)
+    _check(load().phe_matmul_clear_ct(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose), row_begin,
+                                      row_end, _ptr(seeds), _ptr(body), T, out_bits, _ptr(ws), ws.numel(),
+                                      _ptr(out_mask), _ptr(out_body), _stream()), "phe_matmul_clear_ct")
     return out_mask, out_body
 
 

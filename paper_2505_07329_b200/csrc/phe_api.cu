@@ -206,6 +206,20 @@ int phe_matmul_clear_T(const phe_params *p, const void *d_wprep, int64_t d_out, 
                        d_out_mask, d_out_body, stream);
 }
 
+int phe_matmul_clear_ct(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                        int transpose, int64_t row_begin, int64_t row_end, const uint64_t *d_seeds,
+                        const uint64_t *d_body, int64_t T, int32_t out_bits, void *d_ws,
+                        size_t ws_bytes, void *d_out_mask, void *d_out_body, void *stream) {
+  if (!p || (transpose != 0 && transpose != 1) || d_out < 1 || d_in < 1) return PHE_EINVAL;
+  const int64_t L = phe_num_blocks(p, transpose ? d_out : d_in);
+  int rc = phe_ct_prepare(p, d_seeds, d_body, T, L, d_ws, ws_bytes, stream);
+  if (rc) return rc;
+  return transpose ? phe_matmul_clear_T(p, d_wprep, d_out, d_in, row_begin, row_end, d_ws, T, out_bits,
+                                        d_out_mask, d_out_body, stream)
+                   : phe_matmul_clear(p, d_wprep, d_out, d_in, row_begin, row_end, d_ws, T, out_bits,
+                                      d_out_mask, d_out_body, stream);
+}
+
 int phe_matmul_clear_simt(const phe_params *p, const int8_t *d_W, int64_t d_out, int64_t d_in,
                           int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
                           int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {

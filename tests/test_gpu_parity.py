@@ -161,6 +161,23 @@ def test_extreme_limbs_and_weights(phe, coracle):
         assert np.array_equal(u64(m[tau]), mo) and np.array_equal(u64(b[tau]), bo)
 
 
+def test_matmul_clear_ct_one_call(phe):
+    """phe_matmul_clear_ct (north_star's matmul_clear(W, ct)) == ct_prepare + matmul_clear[_T]."""
+    p = phe.params(phe.PRESET_PAPER)
+    W = synth.weights_int8(300, 2100)
+    x = synth.activations_int8(9, 2100)
+    S, seeds, body, w, opnd, (m, b) = run_gpu(phe, p, W, x)
+    m1, b1 = phe.matmul_clear_ct(p, w, seeds, body, row_begin=7, row_end=299)
+    assert torch.equal(m1, m[:, 7:299]) and torch.equal(b1, b[:, 7:299])
+    g = synth.gradients_int8(5, 300)
+    S, sg, bg, wT, og, (mT, bT) = run_gpu(phe, p, W, g, transpose=True)
+    mT1, bT1 = phe.matmul_clear_ct(p, wT, sg, bg)
+    assert torch.equal(mT1, mT) and torch.equal(bT1, bT)
+    small = torch.empty(16, dtype=torch.uint8, device=DEV)
+    with pytest.raises(phe.PheError, match="buffer too small"):
+        phe.matmul_clear_ct(p, w, seeds, body, ws=small)
+
+
 def test_simt_cross_check_matches_tensor_core(phe):
     p = phe.params(phe.PRESET_PAPER)
     W = synth.weights_int8(24, 4100)
