@@ -514,23 +514,25 @@ int launch_mask_cfg(MaskArgs a, cudaStream_t st) {
 // One token group and one exchange buffer per CTA (smallest shared-memory footprint: 4 CTAs /
 // 16 warps per SM at N = 2048).  Measured alternatives (2 groups sharing the twiddles, 2
 // alternating buffers) were within 2% on q_proj and slower at L = 4.
-// N = 2048: W_hat_j in shared memory, shared by 2 token groups (L <= 2: 83-99 KB, 2 CTAs/SM) or 4
-// (L <= 6: 150-198 KB, 1 CTA of 16 warps); Table 1's switch compiled in.  Other N: one group,
-// W_hat_j staged when it fits.
+// Launch policy: NG token groups per CTA so that a CTA has 16 warps (NG = min(8, 512 / (N/16))), all
+// sharing one twiddle copy and (if it fits) the shared-memory copy of W_hat_j; at N = 2048 and
+// L <= 2, two CTAs of 2 groups instead (83-99 KB each).  Table 1's switch (39 -> 26) is compiled in.
 constexpr int SMEM_BUDGET = 200 * 1024;
+template <int LOGN, bool SW, int NG, int NB>
+int launch_mask_ng(const MaskArgs &a, cudaStream_t st) {
+  const bool t1 = SW && a.q_in == 39 && a.out_bits == 26;
+  const bool wsm = ntt_smem<LOGN, NG, NB>() + a.Lc * 2 * (1 << LOGN) * 4 <= SMEM_BUDGET;
+  if (wsm) return t1 ? launch_mask_cfg<LOGN, SW, NG, NB, true, 13, 26>(a, st) : launch_mask_cfg<LOGN, SW, NG, NB, true>(a, st);
+  return t1 ? launch_mask_cfg<LOGN, SW, NG, NB, false, 13, 26>(a, st) : launch_mask_cfg<LOGN, SW, NG, NB, false>(a, st);
+}
 template <int LOGN, bool SW>
 int launch_mask(const MaskArgs &a, cudaStream_t st) {
+  // <= 8 groups: named barriers 1..NG of the 16 hardware barriers
+  constexpr int NGF = 512 / ((1 << LOGN) / 16) < 8 ? 512 / ((1 << LOGN) / 16) : 8;
   if constexpr (LOGN == 11) {
-    if (a.Lc <= 6) {
-      const bool t1 = SW && a.q_in == 39 && a.out_bits == 26;
-      if (a.Lc <= 2)
-        return t1 ? launch_mask_cfg<LOGN, SW, 2, 1, true, 13, 26>(a, st) : launch_mask_cfg<LOGN, SW, 2, 1, true>(a, st);
-      return t1 ? launch_mask_cfg<LOGN, SW, 4, 1, true, 13, 26>(a, st) : launch_mask_cfg<LOGN, SW, 4, 1, true>(a, st);
-    }
+    if (a.Lc <= 2) return launch_mask_ng<LOGN, SW, 2, 1>(a, st);
   }
-  if (ntt_smem<LOGN, 1, 1>() + a.Lc * 2 * (1 << LOGN) * 4 <= SMEM_BUDGET)
-    return launch_mask_cfg<LOGN, SW, 1, 1, true>(a, st);
-  return launch_mask_cfg<LOGN, SW, 1, 1, false>(a, st);
+  return launch_mask_ng<LOGN, SW, NGF, 1>(a, st);
 }
 
 }  // namespace ntt
