@@ -287,6 +287,13 @@ size_t phe_ntt_operand_bytes(const phe_params *p, int64_t T, int64_t L);
 int phe_ntt_ct_prepare(const phe_params *p, const void *d_tables, const uint64_t *d_seeds,
                        const uint64_t *d_body, int64_t T, int64_t L, void *d_operand, size_t bytes,
                        void *stream);
+/* encrypt_pack with the product A*S through the NTT (client side): same contract and
+ * bit-identical output as phe_encrypt_pack; A*S (|A*S| < N 2^q_in) is computed exactly as
+ * INTT(NTT(A) o NTT(S)) mod p0, p1 and a centred CRT -- O(N log N) per block instead of N^2/2.
+ * d_tables from phe_ntt_tables_init.  EUNSUPPORTED if N 2^q_in >= p0 p1 / 2.                 */
+int phe_encrypt_pack_ntt(const phe_params *p, const void *d_tables, const uint8_t *d_S, const int8_t *d_x,
+                         int64_t T, int64_t d_in, uint64_t seed_base, uint64_t noise_seed, uint64_t *d_seeds,
+                         uint64_t *d_body, void *stream);
 int phe_matmul_clear_ntt(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
                          int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
                          int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);

@@ -37,7 +37,7 @@ EXPORTS = [
     "phe_wire_serialize_packed", "phe_wire_deserialize_packed", "phe_server_wire_host",
     "phe_ntt_primes", "phe_ntt_max_blocks", "phe_ntt_tables_bytes", "phe_ntt_tables_init",
     "phe_ntt_weights_bytes", "phe_ntt_weights_prepare", "phe_ntt_operand_bytes", "phe_ntt_ct_prepare",
-    "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T", "phe_matmul_clear_ct",
+    "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T", "phe_matmul_clear_ct", "phe_encrypt_pack_ntt",
 ]
 
 
@@ -119,6 +119,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_matmul_clear_ct": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _sz,
                                  _vp, _vp, _vp], ctypes.c_int),
         "phe_ntt_primes": ([_vp], ctypes.c_int),
+        "phe_encrypt_pack_ntt": ([_P, _vp, _vp, _vp, _i64, _i64, _u64, _u64, _vp, _vp, _vp], ctypes.c_int),
         "phe_ntt_max_blocks": ([_P], _i64),
         "phe_ntt_tables_bytes": ([_P], _sz),
         "phe_ntt_tables_init": ([_P, _vp, _sz, _vp], ctypes.c_int),
@@ -550,4 +551,18 @@ def matmul_clear_ntt(p: Params, w: NttWeights, operand: torch.Tensor, T: int, ou
     _check(fn(ctypes.byref(p), _ptr(w.tables.buf), _ptr(w.buf), w.d_out, w.d_in, row_begin, row_end,
               _ptr(operand), T, out_bits, _ptr(out_mask), _ptr(out_body), _stream()), "phe_matmul_clear_ntt")
     return out_mask, out_body
+
+
+def encrypt_pack_ntt(p: Params, tables: NttTables, S: torch.Tensor, x: torch.Tensor, seed_base: int,
+                     noise_seed: int = 0):
+    """encrypt_pack with A*S through the NTT (phe_encrypt_pack_ntt); bit-identical output."""
+    _dev(S, torch.uint8, "S"); _dev(x, torch.int8, "x")
+    T, d_in = x.shape
+    L = p.L(d_in)
+    seeds = torch.empty((T, L), dtype=torch.int64, device=x.device)
+    body = torch.empty((T, L, p.N), dtype=torch.int64, device=x.device)
+    _check(load().phe_encrypt_pack_ntt(ctypes.byref(p), _ptr(tables.buf), _ptr(S), _ptr(x), T, d_in,
+                                       seed_base & (2**64 - 1), noise_seed & (2**64 - 1), _ptr(seeds), _ptr(body),
+                                       _stream()), "phe_encrypt_pack_ntt")
+    return seeds, body
 

@@ -160,6 +160,26 @@ __device__ void ntt_forward_smem(uint32_t *x, const uint2 *__restrict__ tab, int
 
 constexpr int PREP_THREADS = 256;
 
+// In-place inverse negacyclic NTT (Gentleman-Sande, bit-reversed in, natural out, unscaled) of the
+// two prime residue arrays x[pr][N] in shared memory; tinv = inverse slice [2][N] of the table.
+__device__ void ntt_inverse_smem(uint32_t *x, const uint2 *__restrict__ tinv, int logN) {
+  const int N = 1 << logN;
+  for (int s = 0; s < logN; s++) {  // half-distance t = 2^s, twiddle (N >> (s+1)) + group
+    const int t = 1 << s, h = N >> (s + 1);
+    for (int b = threadIdx.x; b < 2 * (N / 2); b += blockDim.x) {
+      const int pr = b / (N / 2), bb = b % (N / 2);
+      const int i = bb >> s, j = 2 * i * t + (bb & (t - 1));
+      const uint32_t p = prime(pr);
+      const uint2 w = __ldg(&tinv[pr * N + h + i]);
+      uint32_t *a = x + pr * N;
+      const uint32_t U = a[j], V = a[j + t];
+      a[j] = add_mod(U, V, p);
+      a[j + t] = mul_shoup(U - V + p, w.x, w.y, p);
+    }
+    __syncthreads();
+  }
+}
+
 // W_hat for row j, block i of the prepared matrix M (= W or W^T):
 // w_hat_ij[k] = M[j, iN + N-1-k] (0 beyond cols), then NTT, then * N^{-1} 2^32 mod p.
 __global__ void __launch_bounds__(PREP_THREADS)
@@ -221,6 +241,66 @@ __global__ void ntt_rowpar_kernel(const int8_t *__restrict__ W, int64_t d_in, in
   for (int64_t c = threadIdx.x % 32; c < cols; c += 32) s += transpose ? W[c * d_in + j] : W[j * d_in + c];
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (threadIdx.x % 32 == 0) par[j] = (uint8_t)(s & 1);
+}
+
+// encrypt_pack through the NTT (client side): B = A*S + E + Delta*x_hat mod 2^q_in (P:58, P:62,
+// P:174), with the negacyclic product A*S (|A*S| < N 2^q_in) computed exactly as
+// INTT(NTT(A) o NTT(S) N^-1) modulo p0, p1 and recovered by a centred CRT.  One CTA per block;
+// bit-identical to encrypt_kernel (side_kernels.cu).
+__global__ void __launch_bounds__(PREP_THREADS)
+ntt_encrypt_kernel(KParams kp, int logN, const uint8_t *__restrict__ S, const int8_t *__restrict__ x,
+                   int64_t d_in, int64_t L, uint64_t seed_base, uint64_t noise_seed,
+                   const uint2 *__restrict__ tab, uint32_t c0, uint32_t c1, uint64_t *__restrict__ seeds,
+                   uint64_t *__restrict__ body) {
+  extern __shared__ uint32_t xs[];  // [2][N] A, then [2][N] S
+  const int N = 1 << logN;
+  uint32_t *ys = xs + 2 * N;
+  const int64_t blk = blockIdx.x;  // tau * L + i
+  const int64_t tau = blk / L, i = blk % L;
+  const uint64_t seed = seed_base + (uint64_t)blk;
+  if (threadIdx.x == 0) seeds[blk] = seed;
+  for (int g = threadIdx.x; g < N / 8; g += blockDim.x) {
+    uint64_t w[8];
+    chacha20_u64x8(seed, (uint32_t)g, nonce_mask(), w);
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const uint64_t a = w[e] & kp.qmask;
+      xs[8 * g + e] = (uint32_t)(a % P0);
+      xs[N + 8 * g + e] = (uint32_t)(a % P1);
+    }
+  }
+  for (int k = threadIdx.x; k < N; k += blockDim.x) ys[k] = ys[N + k] = S[k];
+  __syncthreads();
+  ntt_forward_smem(xs, tab, logN);
+  ntt_forward_smem(ys, tab, logN);
+  for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) {
+    const int pr = k / N;
+    const uint32_t p = prime(pr);
+    const uint32_t sm = (uint32_t)((uint64_t)ys[k] * (pr ? c1 : c0) % p);  // S_hat N^-1 2^32
+    xs[k] = mul_mont(xs[k], sm, p, pinv(pr));
+  }
+  __syncthreads();
+  ntt_inverse_smem(xs, tab + 2 * N, logN);
+  const uint64_t delta = 1ull << (kp.q_in - kp.beta);
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const uint32_t r0 = xs[k], r1 = xs[N + k];
+    const uint32_t h = mul_shoup(add_mod(r1, P1 - r0, P1), CRT_C, CRT_CQ, P1);
+    uint64_t v = (uint64_t)r0 + (uint64_t)P0 * h;
+    if (v >= CRT_M / 2) v -= CRT_M;  // centred A*S; wraps mod 2^64
+    const int64_t c = i * (int64_t)N + k;
+    const int64_t xv = (c < d_in) ? (int64_t)x[tau * d_in + c] : 0;
+    int64_t ev = 0;
+    if (kp.eta > 0) {  // as encrypt_kernel: one keystream word per coefficient, order (tau, i, k)
+      const uint64_t widx = (uint64_t)blk * (uint64_t)N + (uint64_t)k;
+      uint32_t o[16];
+      chacha20_block(noise_seed, (uint32_t)(widx >> 3), nonce_noise(), o);
+      const int q = (int)(widx & 7);
+      const uint64_t wd = (uint64_t)o[2 * q] | ((uint64_t)o[2 * q + 1] << 32);
+      const uint64_t m = mask_bits(kp.eta);
+      ev = (int64_t)__popcll(wd & m) - (int64_t)__popcll((wd >> kp.eta) & m);
+    }
+    body[blk * (int64_t)N + k] = (v + (uint64_t)ev + delta * (uint64_t)xv) & kp.qmask;
+  }
 }
 
 // ---------------------------------------------------------------- the hot kernels
@@ -573,6 +653,22 @@ int launch_ntt_weights(const KParams &kp, const void *tables, const int8_t *W, i
   }
   ntt::ntt_weights_kernel<<<(unsigned)(rows * Lc), ntt::PREP_THREADS, smem, st>>>(
       kp.log2N, W, d_in, transpose, cols, Lc, static_cast<const uint2 *>(tables), c0, c1, what);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+int launch_ntt_encrypt(const KParams &kp, const void *tables, const uint8_t *S, const int8_t *x, int64_t T,
+                       int64_t d_in, int64_t L, uint64_t seed_base, uint64_t noise_seed, uint64_t *seeds,
+                       uint64_t *body, cudaStream_t st) {
+  if (T * L == 0) return PHE_OK;
+  const int N = kp.N;
+  const uint32_t c0 = (uint32_t)((uint64_t)ntt::pw(N, ntt::P0 - 2, ntt::P0) * ((1ull << 32) % ntt::P0) % ntt::P0);
+  const uint32_t c1 = (uint32_t)((uint64_t)ntt::pw(N, ntt::P1 - 2, ntt::P1) * ((1ull << 32) % ntt::P1) % ntt::P1);
+  const size_t smem = 4 * (size_t)N * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(ntt::ntt_encrypt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return phe_set_cuda_error(e);
+  ntt::ntt_encrypt_kernel<<<(unsigned)(T * L), ntt::PREP_THREADS, smem, st>>>(
+      kp, kp.log2N, S, x, d_in, L, seed_base, noise_seed, static_cast<const uint2 *>(tables), c0, c1, seeds, body);
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
 }

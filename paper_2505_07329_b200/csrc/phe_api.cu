@@ -801,6 +801,23 @@ int phe_ntt_ct_prepare(const phe_params *p, const void *d_tables, const uint64_t
   return phe::launch_ct_prepare(kp, d_seeds, d_body, T, L, nullptr, bp, S(stream));
 }
 
+int phe_encrypt_pack_ntt(const phe_params *p, const void *d_tables, const uint8_t *d_S, const int8_t *d_x,
+                         int64_t T, int64_t d_in, uint64_t seed_base, uint64_t noise_seed, uint64_t *d_seeds,
+                         uint64_t *d_body, void *stream) {
+  KParams kp;
+  int rc = check_ntt(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || d_in < 1) return PHE_EINVAL;
+  if (T > 0 && (!d_tables || !d_S || !d_x || !d_seeds || !d_body)) return PHE_EINVAL;
+  if (p->beta < 9) return PHE_ERANGE;
+  // |A*S| < N 2^q_in must stay below p0 p1 / 2 for the centred CRT
+  uint32_t pr[2];
+  phe::ntt_primes(pr);
+  if ((unsigned __int128)p->N << p->q_in >= ((unsigned __int128)pr[0] * pr[1]) / 2) return PHE_EUNSUPPORTED;
+  return phe::launch_ntt_encrypt(kp, d_tables, d_S, d_x, T, d_in, phe_num_blocks(p, d_in), seed_base, noise_seed,
+                                 d_seeds, d_body, S(stream));
+}
+
 static int ntt_common(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t rows,
                       int64_t cols, int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
                       int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {

@@ -46,6 +46,9 @@ int launch_ntt_weights(const KParams &kp, const void *tables, const int8_t *W, i
                        int64_t d_in, int transpose, uint32_t *what, cudaStream_t st);
 int launch_ntt_masks(const KParams &kp, const void *tables, const uint64_t *seeds, int64_t T, int64_t L,
                      uint32_t *ahat, cudaStream_t st);
+int launch_ntt_encrypt(const KParams &kp, const void *tables, const uint8_t *S, const int8_t *x, int64_t T,
+                       int64_t d_in, int64_t L, uint64_t seed_base, uint64_t noise_seed, uint64_t *seeds,
+                       uint64_t *body, cudaStream_t st);
 int launch_ntt_rowpar(const int8_t *W, int64_t d_out, int64_t d_in, int transpose, uint8_t *par,
                       cudaStream_t st);
 int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, const uint8_t *par,

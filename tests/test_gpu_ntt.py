@@ -198,3 +198,25 @@ def test_ntt_full_size_q_proj_sampled(phe, coracle):
     tau = 777
     mask_o, body_o = oracle_literal(coracle, p, W, seeds[tau:tau + 1], body[tau:tau + 1])
     assert np.array_equal(mn[tau].cpu().numpy().astype(np.uint32).astype(np.uint64), O.modswitch(mask_o[0], 39, 26))
+
+
+@pytest.mark.parametrize("preset,over,eta,d_in,T", [
+    ("TOY", {}, 0, 64, 16), ("PAPER", {}, 0, 4100, 7), ("PAPER", {}, 21, 2048, 5),
+    ("PAPER", dict(N=512), 21, 1100, 3), ("PAPER", dict(N=8192), 0, 8192, 2),
+])
+def test_encrypt_pack_ntt_identical(phe, coracle, preset, over, eta, d_in, T):
+    """phe_encrypt_pack_ntt == phe_encrypt_pack word for word (the latter is pinned to the oracle:
+    test_gpu_parity.py::test_keygen_and_encrypt_match_oracle); one block also against the oracle."""
+    p = phe.params(getattr(phe, "PRESET_" + preset), noise_eta=eta, **over)
+    x = torch.from_numpy(synth.uniform_int8((T, d_in), 3 + T, -100, 100)).to(DEV)
+    S = phe.keygen(p, 11)
+    s1, b1 = phe.encrypt_pack(p, S, x, 777, 99)
+    tabs = phe.NttTables(p)
+    s2, b2 = phe.encrypt_pack_ntt(p, tabs, S, x, 777, 99)
+    assert torch.equal(s1, s2) and torch.equal(b1, b2)
+    op = oparams(p)
+    So = O.keygen(11, op.N)
+    E = O.noise(op, 99, T, op.L(d_in))
+    A, B = O.encrypt(op, So, x[0].cpu().numpy(), O.block_seeds(777, T, op.L(d_in))[0], E[0])
+    assert np.array_equal(u64(b2[0]), B)
+

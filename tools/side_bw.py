@@ -51,13 +51,17 @@ def main():
     f(); ms = timeit(f, a.reps)
     rep("encrypt_kernel (encrypt_pack, client)", ms, T * d + N, T * 8 + T * N * 8, "alu",
         "B = A*S + E + Delta*x: N^2/2 adds per block (binary S), ChaCha20 expansion of A")
+    tabs = phe.NttTables(p)
+    f = lambda: phe.encrypt_pack_ntt(p, tabs, S, x, 5)
+    f(); ms = timeit(f, a.reps)
+    rep("ntt_encrypt_kernel (encrypt_pack_ntt, client)", ms, T * d + N, T * 8 + T * N * 8, "alu",
+        "A*S through NTT(A) o NTT(S) mod 2 primes + CRT: O(N log N) per block; bit-identical to encrypt_kernel")
     seeds, body = phe.encrypt_pack(p, S, x, 5)
     op = phe.ct_prepare(p, seeds, body)
     f = lambda: phe.ct_prepare(p, seeds, body, out=op)
     f(); ms = timeit(f, a.reps)
     rep("ct_prepare_kernel (a3+a4)", ms, T * 8 + T * N * 8, 2 * T * ell * N, "alu",
         "ChaCha20 mask expansion (N/8 blocks per input block) + limb planes of masks and bodies")
-    tabs = phe.NttTables(p)
     opn = phe.ntt_ct_prepare(p, tabs, seeds, body)
     f = lambda: phe.ntt_ct_prepare(p, tabs, seeds, body, out=opn)
     f(); ms = timeit(f, a.reps)
