@@ -301,6 +301,24 @@ int phe_matmul_clear_ntt_T(const phe_params *p, const void *d_tables, const void
                            int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
                            int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);
 
+/* ---- LWE outputs on the wire: the switched LWE ciphertexts at q_out bits (R22's bitstream) ----
+ * Per token: R mask segments of N coefficients (N q_out / 64 words each), then the R bodies at
+ * q_out bits padded to a whole 64-bit word: phe_wire_lwe_bytes(p, R) bytes per token (Table 1,
+ * R = 2048: 13,638,144 B = 0.8125 of the uint32 form).  d_mask uint32 [T][R][N], d_body uint32
+ * [T][R] (as phe_matmul_clear at out_bits = q_out); d_wire 8-byte aligned.                     */
+size_t phe_wire_lwe_bytes(const phe_params *p, int64_t R);
+int phe_wire_serialize_lwe(const phe_params *p, const uint32_t *d_mask, const uint32_t *d_body, int64_t T,
+                           int64_t R, uint8_t *d_wire, void *stream);
+int phe_wire_deserialize_lwe(const phe_params *p, const uint8_t *d_wire, int64_t T, int64_t R,
+                             uint32_t *d_mask, uint32_t *d_body, void *stream);
+/* The LWE server step as the network sees it: h_wire_in [T][L] wire input blocks (9992 B each)
+ * -> h_wire_out [T][phe_wire_lwe_bytes(p, R)], R = row_end - row_begin; chunked H2D, deserialize,
+ * ct_prepare, matmul_clear(_T) with the fused switch, serialize, D2H on two internal streams
+ * (same workspace exception as phe_server_matvec_host).  Synchronous.                       */
+int phe_server_matvec_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                                int transpose, int64_t row_begin, int64_t row_end, const uint8_t *h_wire_in,
+                                int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *stream);
+
 /* ---- introspection (tests / bench) -------------------------------------------------- */
 /* Number of kernel launches the last phe_matmul_clear[_T] on this thread enqueued. */
 int phe_last_launch_count(void);

@@ -38,6 +38,7 @@ EXPORTS = [
     "phe_ntt_primes", "phe_ntt_max_blocks", "phe_ntt_tables_bytes", "phe_ntt_tables_init",
     "phe_ntt_weights_bytes", "phe_ntt_weights_prepare", "phe_ntt_operand_bytes", "phe_ntt_ct_prepare",
     "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T", "phe_matmul_clear_ct", "phe_encrypt_pack_ntt",
+    "phe_wire_lwe_bytes", "phe_wire_serialize_lwe", "phe_wire_deserialize_lwe", "phe_server_matvec_wire_host",
 ]
 
 
@@ -119,6 +120,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_matmul_clear_ct": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _sz,
                                  _vp, _vp, _vp], ctypes.c_int),
         "phe_ntt_primes": ([_vp], ctypes.c_int),
+        "phe_wire_lwe_bytes": ([_P, _i64], _sz),
+        "phe_wire_serialize_lwe": ([_P, _vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
+        "phe_wire_deserialize_lwe": ([_P, _vp, _i64, _i64, _vp, _vp, _vp], ctypes.c_int),
+        "phe_server_matvec_wire_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _i64, _i64, _vp, _vp],
+                                        ctypes.c_int),
         "phe_encrypt_pack_ntt": ([_P, _vp, _vp, _vp, _i64, _i64, _u64, _u64, _vp, _vp, _vp], ctypes.c_int),
         "phe_ntt_max_blocks": ([_P], _i64),
         "phe_ntt_tables_bytes": ([_P], _sz),
@@ -565,4 +571,43 @@ def encrypt_pack_ntt(p: Params, tables: NttTables, S: torch.Tensor, x: torch.Ten
                                        seed_base & (2**64 - 1), noise_seed & (2**64 - 1), _ptr(seeds), _ptr(body),
                                        _stream()), "phe_encrypt_pack_ntt")
     return seeds, body
+
+
+# ------------------------------------------------------------------ LWE outputs on the wire
+def wire_lwe_bytes(p: Params, R: int) -> int:
+    return int(load().phe_wire_lwe_bytes(ctypes.byref(p), R))
+
+
+def wire_serialize_lwe(p: Params, mask: torch.Tensor, body: torch.Tensor) -> torch.Tensor:
+    """uint32 LWE outputs [T][R][N], [T][R] -> bytes [T][wire_lwe_bytes(p, R)] at q_out bits."""
+    _dev(mask, torch.int32, "mask"); _dev(body, torch.int32, "body")
+    T, R = body.shape
+    out = torch.empty((T, wire_lwe_bytes(p, R)), dtype=torch.uint8, device=mask.device)
+    _check(load().phe_wire_serialize_lwe(ctypes.byref(p), _ptr(mask), _ptr(body), T, R, _ptr(out), _stream()),
+           "phe_wire_serialize_lwe")
+    return out
+
+
+def wire_deserialize_lwe(p: Params, wire: torch.Tensor, R: int):
+    _dev(wire, torch.uint8, "wire")
+    T = wire.shape[0]
+    mask = torch.empty((T, R, p.N), dtype=torch.int32, device=wire.device)
+    body = torch.empty((T, R), dtype=torch.int32, device=wire.device)
+    _check(load().phe_wire_deserialize_lwe(ctypes.byref(p), _ptr(wire), T, R, _ptr(mask), _ptr(body), _stream()),
+           "phe_wire_deserialize_lwe")
+    return mask, body
+
+
+def server_matvec_wire_host(p: Params, w: Weights, h_wire_in: torch.Tensor, h_wire_out: torch.Tensor,
+                            chunk_tokens: int = 256, row_begin: int = 0, row_end: int | None = None) -> None:
+    """End to end on wire bytes with HOST buffers: input blocks [T][L][9992] -> switched LWE outputs
+    at q_out bits [T][wire_lwe_bytes(p, R)] (phe_server_matvec_wire_host)."""
+    for t, n in [(h_wire_in, "h_wire_in"), (h_wire_out, "h_wire_out")]:
+        if t.is_cuda or not t.is_contiguous():
+            raise PheError(f"{n} must be a contiguous host tensor")
+    T = h_wire_in.shape[0]
+    row_end = w.rows if row_end is None else row_end
+    _check(load().phe_server_matvec_wire_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
+                                              row_begin, row_end, _ptr(h_wire_in), T, chunk_tokens,
+                                              _ptr(h_wire_out), _stream()), "phe_server_matvec_wire_host")
 

@@ -703,6 +703,115 @@ int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out
 }
 
 
+// ================================================================ LWE outputs on the wire
+static inline int64_t lwe_seg_words(const phe_params *p) { return (int64_t)p->N * p->q_out / 64; }
+static inline int64_t lwe_body_words(const phe_params *p, int64_t R) { return (R * p->q_out + 63) / 64; }
+
+extern "C" {
+
+size_t phe_wire_lwe_bytes(const phe_params *p, int64_t R) {
+  if (!p || R < 1 || p->N % 64) return 0;
+  return (size_t)(8 * (R * lwe_seg_words(p) + lwe_body_words(p, R)));
+}
+
+int phe_wire_serialize_lwe(const phe_params *p, const uint32_t *d_mask, const uint32_t *d_body, int64_t T,
+                           int64_t R, uint8_t *d_wire, void *stream) {
+  KParams kp;
+  int rc = check_wire(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || R < 1) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_mask || !d_body || !d_wire || ((uintptr_t)d_wire & 7)) return PHE_EINVAL;
+  const int64_t tw = (int64_t)phe_wire_lwe_bytes(p, R) / 8, sw = lwe_seg_words(p);
+  rc = phe::launch_wire_u32(const_cast<uint32_t *>(d_mask), T * R, p->N, p->q_out, d_wire, sw, R, tw, 0, 0,
+                            S(stream));
+  if (rc) return rc;
+  return phe::launch_wire_u32(const_cast<uint32_t *>(d_body), T, (int)R, p->q_out, d_wire, lwe_body_words(p, R),
+                              1, tw, R * sw, 0, S(stream));
+}
+
+int phe_wire_deserialize_lwe(const phe_params *p, const uint8_t *d_wire, int64_t T, int64_t R, uint32_t *d_mask,
+                             uint32_t *d_body, void *stream) {
+  KParams kp;
+  int rc = check_wire(p, &kp);
+  if (rc) return rc;
+  if (T < 0 || R < 1) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_mask || !d_body || !d_wire || ((uintptr_t)d_wire & 7)) return PHE_EINVAL;
+  const int64_t tw = (int64_t)phe_wire_lwe_bytes(p, R) / 8, sw = lwe_seg_words(p);
+  uint8_t *w = const_cast<uint8_t *>(d_wire);
+  rc = phe::launch_wire_u32(d_mask, T * R, p->N, p->q_out, w, sw, R, tw, 0, 1, S(stream));
+  if (rc) return rc;
+  return phe::launch_wire_u32(d_body, T, (int)R, p->q_out, w, lwe_body_words(p, R), 1, tw, R * sw, 1, S(stream));
+}
+
+int phe_server_matvec_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                                int transpose, int64_t row_begin, int64_t row_end, const uint8_t *h_wire_in,
+                                int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *stream) {
+  KParams kp;
+  int rc = check_wire(p, &kp);
+  if (rc) return rc;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  if (rows < 1 || cols < 1 || T < 0 || chunk_tokens < 1) return PHE_EINVAL;
+  if (row_begin < 0 || row_end > rows || row_begin > row_end) return PHE_EINVAL;
+  if (T == 0 || row_end == row_begin) return PHE_OK;
+  if (!d_wprep || !h_wire_in || !h_wire_out) return PHE_EINVAL;
+  const int64_t N = p->N, L = phe_num_blocks(p, cols), R = row_end - row_begin;
+  const int64_t C = chunk_tokens < T ? chunk_tokens : T;
+  const int64_t bin = (int64_t)phe_wire_input_bytes(p), bout = (int64_t)phe_wire_lwe_bytes(p, R);
+  const size_t b_win = round_up(C * L * bin, 256), b_seeds = round_up(C * L * 8, 256);
+  const size_t b_body = round_up(C * L * N * 8, 256);
+  const size_t b_op = round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256);
+  const size_t b_om = round_up(C * R * N * 4, 256), b_ob = round_up(C * R * 4, 256);
+  const size_t b_wout = round_up(C * bout, 256);
+  const size_t slot = b_win + b_seeds + b_body + b_op + b_om + b_ob + b_wout;
+  if (g_ws.bytes < 2 * slot) {
+    if (g_ws.buf) cudaFree(g_ws.buf);
+    g_ws.buf = nullptr; g_ws.bytes = 0;
+    if (cudaMalloc(&g_ws.buf, 2 * slot) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+    g_ws.bytes = 2 * slot;
+  }
+  if (!g_ws.st[0]) {
+    for (int s = 0; s < 2; s++)
+      if (cudaStreamCreateWithFlags(&g_ws.st[s], cudaStreamNonBlocking) != cudaSuccess)
+        return phe_set_cuda_error(cudaGetLastError());
+    if (cudaEventCreateWithFlags(&g_ws.ev, cudaEventDisableTiming) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+  }
+  cudaEventRecord(g_ws.ev, S(stream));
+  cudaStreamWaitEvent(g_ws.st[0], g_ws.ev, 0);
+  cudaStreamWaitEvent(g_ws.st[1], g_ws.ev, 0);
+  int64_t c = 0;
+  for (int64_t t0 = 0; t0 < T; t0 += C, c++) {
+    const int64_t n = (T - t0) < C ? (T - t0) : C;
+    cudaStream_t st = g_ws.st[c & 1];
+    uint8_t *base = static_cast<uint8_t *>(g_ws.buf) + (c & 1) * slot;
+    uint8_t *d_win = base;
+    uint64_t *d_seeds = reinterpret_cast<uint64_t *>(base + b_win);
+    uint64_t *d_bod = reinterpret_cast<uint64_t *>(base + b_win + b_seeds);
+    void *d_op = base + b_win + b_seeds + b_body;
+    uint32_t *d_om = reinterpret_cast<uint32_t *>(base + b_win + b_seeds + b_body + b_op);
+    uint32_t *d_ob = reinterpret_cast<uint32_t *>(base + b_win + b_seeds + b_body + b_op + b_om);
+    uint8_t *d_wout = base + b_win + b_seeds + b_body + b_op + b_om + b_ob;
+    cudaMemcpyAsync(d_win, h_wire_in + t0 * L * bin, n * L * bin, cudaMemcpyHostToDevice, st);
+    rc = phe_wire_deserialize_inputs(p, d_win, n, L, d_seeds, d_bod, st);
+    if (!rc) rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
+    if (!rc) rc = matmul_common(p, d_wprep, rows, cols, row_begin, row_end, d_op, n, p->q_out, d_om, d_ob, st);
+    if (!rc) rc = phe_wire_serialize_lwe(p, d_om, d_ob, n, R, d_wout, st);
+    if (rc) return rc;
+    cudaMemcpyAsync(h_wire_out + t0 * bout, d_wout, n * bout, cudaMemcpyDeviceToHost, st);
+  }
+  cudaError_t e0 = cudaStreamSynchronize(g_ws.st[0]);
+  cudaError_t e1 = cudaStreamSynchronize(g_ws.st[1]);
+  if (e0 != cudaSuccess) return phe_set_cuda_error(e0);
+  if (e1 != cudaSuccess) return phe_set_cuda_error(e1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return phe_set_cuda_error(e);
+  return PHE_OK;
+}
+
+}  // extern "C"
+
 // ================================================================ NEXT #4: NTT-domain contraction
 static int check_ntt(const phe_params *p, KParams *kp) {
   int rc = check_gpu(p, kp);

@@ -617,6 +617,35 @@ __global__ void wire_packed_kernel(int N, int q, uint32_t *__restrict__ packed, 
   }
 }
 
+// Generic u32 segments at `bits` bits (LWE outputs at q_out bits): segment s = (group g, index j)
+// with g = s / per_group, j = s % per_group starts at word g * group_words + off_words +
+// j * seg_words (seg_words = ceil(seglen bits / 64); the tail of the last word is zero).
+__global__ void wire_u32_kernel(uint32_t *__restrict__ vals, int64_t nseg, int seglen, int bits,
+                                uint64_t *__restrict__ wire, int64_t seg_words, int64_t per_group,
+                                int64_t group_words, int64_t off_words, int dir) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t sg = blockIdx.y; sg < nseg; sg += gridDim.y) {
+    uint64_t *ws = wire + (sg / per_group) * group_words + off_words + (sg % per_group) * seg_words;
+    uint32_t *vs = vals + sg * seglen;
+    if (dir == 0) {
+      if (x < seg_words) ws[x] = gather_word<uint32_t>(vs, seglen, bits, x);
+    } else {
+      if (x < seglen) vs[x] = (uint32_t)extract_bits(ws, x, bits);
+    }
+  }
+}
+
+int launch_wire_u32(uint32_t *vals, int64_t nseg, int seglen, int bits, uint8_t *wire, int64_t seg_words,
+                    int64_t per_group, int64_t group_words, int64_t off_words, int dir, cudaStream_t st) {
+  if (nseg == 0) return PHE_OK;
+  const int64_t nx = dir == 0 ? seg_words : seglen;
+  const dim3 grid((unsigned)((nx + 255) / 256), (unsigned)(nseg < 65535 ? nseg : 65535));
+  wire_u32_kernel<<<grid, 256, 0, st>>>(vals, nseg, seglen, bits, reinterpret_cast<uint64_t *>(wire), seg_words,
+                                        per_group, group_words, off_words, dir);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
 int launch_wire_inputs(const KParams &kp, uint64_t *seeds, uint64_t *body, int64_t nblk, uint8_t *wire,
                        int dir, cudaStream_t st) {
   if (nblk == 0) return PHE_OK;

@@ -50,3 +50,42 @@ def test_wire_packed_bytes_match_oracle_and_server_wire_path(phe):
     h_out = torch.empty((40, 2, wire.shape[2]), dtype=torch.uint8).pin_memory()
     phe.server_wire_host(p, w, K, h_in, h_out, chunk_tokens=16)
     assert torch.equal(h_out, wire.cpu())
+
+
+def test_lwe_wire_roundtrip_and_bits(phe):
+    """LWE outputs at q_out bits: exact round trip, the byte count, and the bit layout of the
+    first token checked against a little-endian bitstream built here with Python ints."""
+    p = phe.params(phe.PRESET_PAPER)
+    W = synth.weights_int8(300, 2048)
+    x = synth.activations_int8(3, 2048)
+    S = phe.keygen(p, 5)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).cuda(), 91)
+    w = phe.Weights(p, torch.from_numpy(W).cuda())
+    m, b = phe.matmul_clear(p, w, phe.ct_prepare(p, seeds, body), 3)
+    wire = phe.wire_serialize_lwe(p, m, b)
+    assert wire.shape == (3, phe.wire_lwe_bytes(p, 300))
+    assert phe.wire_lwe_bytes(p, 300) == 300 * 2048 * 26 // 8 + 8 * ((300 * 26 + 63) // 64)
+    m2, b2 = phe.wire_deserialize_lwe(p, wire, 300)
+    assert torch.equal(m2, m) and torch.equal(b2, b)
+    vals = m[0].cpu().numpy().astype(np.uint64).reshape(-1).tolist()
+    acc = 0
+    for k, v in enumerate(vals[:4096]):       # first two mask segments, 26 bits each
+        acc |= int(v) << (26 * k)
+    ref = acc.to_bytes(26 * 4096 // 8, "little")
+    assert bytes(wire[0, : len(ref)].cpu().numpy().tobytes()) == ref
+
+
+def test_server_matvec_wire_host_matches_device(phe):
+    p = phe.params(phe.PRESET_PAPER)
+    W = synth.weights_int8(256, 2048)
+    x = synth.activations_int8(70, 2048)
+    S = phe.keygen(p, 6)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).cuda(), 92)
+    w = phe.Weights(p, torch.from_numpy(W).cuda())
+    m, b = phe.matmul_clear(p, w, phe.ct_prepare(p, seeds, body), 70, row_begin=3, row_end=250)
+    hi = phe.wire_serialize_inputs(p, seeds, body).cpu().pin_memory()
+    ho = torch.empty((70, phe.wire_lwe_bytes(p, 247)), dtype=torch.uint8, pin_memory=True)
+    phe.server_matvec_wire_host(p, w, hi, ho, chunk_tokens=32, row_begin=3, row_end=250)
+    m2, b2 = phe.wire_deserialize_lwe(p, ho.cuda(), 247)
+    assert torch.equal(m2, m) and torch.equal(b2, b)
+
