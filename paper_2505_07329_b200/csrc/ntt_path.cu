@@ -16,14 +16,18 @@
 // dense path's O(L*N) MACs; it runs on the integer ALUs (CUDA cores), not the tensor cores.
 //
 // Kernels:
-//   ntt_tables_kernel    psi^{bitrev(k)}, psi^{-bitrev(k)} with Shoup companions, both primes
+//   ntt_tables_kernel    psi^{bitrev(k)}, psi^{-bitrev(k)} with Shoup companions, both primes, and
+//                        the hot kernel's per-thread phase-1 twiddle table
 //   ntt_weights_kernel   W_hat_ij = NTT(w_hat_ij) * N^{-1} * 2^32 (Montgomery form)  [server, once]
-//   ntt_masks_kernel     A_hat_{tau,i} = NTT(PRNG(seed_{tau,i}) mod p)                [per batch]
-//   ntt_mask_kernel<LOGN> the hot kernel: pointwise sum over i, inverse NTT in registers +
-//                        shared memory (N/16 threads, 16 values per prime per thread, 4-bit
-//                        phases, XOR-swizzled exchanges: tools/ntt_model.py checks the index
-//                        scheme and bank-conflict freedom), CRT, mod 2^q_in, SampleExtract
-//                        reversal, fused ModulusSwitch, coalesced stores.
+//   ntt_rowpar_kernel    par_j = (sum_c W[j,c]) mod 2                                  [server, once]
+//   ntt_masks_kernel     A_hat_{tau,i} = NTT(PRNG(seed_{tau,i}) - H mod p)             [per batch]
+//   ntt_encrypt_kernel   client encrypt_pack with A*S = INTT(NTT(A) o NTT(S)) (phe_encrypt_pack_ntt)
+//   ntt_mask_kernel<LOGN, SW, NG, NB, WSM, SHIFT, OUTB>  the hot kernel: NG token groups of N/16
+//                        threads (16 values per prime per thread) share the twiddles and W_hat_j
+//                        in shared memory; pointwise sum over i, lazy inverse NTT in registers with
+//                        4-bit phases and additive bank-conflict-free exchange layouts
+//                        (tools/ntt_model.py checks the index scheme), compare-free CRT, parity
+//                        correction, SampleExtract reversal, fused ModulusSwitch, coalesced stores.
 #include <cstdint>
 #include <cstdio>
 
@@ -309,7 +313,7 @@ struct MaskArgs {
   const uint32_t *what;     // [rows][Lc][2][N]
   const uint8_t *par;       // [rows] centring correction bits
   const uint32_t *ahat;     // [T][Lc][2][N]
-  int64_t Lc, rows, row_begin, R, T;
+  int64_t Lc, row_begin, R, T;
   int tok_per_cta;
   int64_t n_chunks;         // ceil(T / tok_per_cta)
   int q_in, out_bits;
@@ -705,7 +709,6 @@ int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what,
   a.what = what;
   a.ahat = ahat;
   a.Lc = Lc;
-  a.rows = rows;
   a.row_begin = row_begin;
   a.R = row_end - row_begin;
   a.T = T;
