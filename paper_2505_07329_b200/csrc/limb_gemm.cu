@@ -92,6 +92,14 @@ struct KArgs {
   void *out;
 };
 
+// Experiment knobs (PHE_DEBUG_EPI: skip TMEM loads / stores / operand loads, clock64 pipeline
+// counters) exist only in builds with -DPHE_KERNEL_EXPERIMENTS=1; in production kdbg() is the
+// constant 0 and every instrumentation branch folds away.
+#ifndef PHE_KERNEL_EXPERIMENTS
+#define PHE_KERNEL_EXPERIMENTS 0
+#endif
+__host__ __device__ __forceinline__ int kdbg(const KArgs &ka) { return PHE_KERNEL_EXPERIMENTS ? ka.dbg : 0; }
+
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -506,7 +514,7 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
 // (bit kb = issue) is computed once per tile, identically by the producer and MMA warps, so
 // the smem ring stays in step.  Never empty for V >= 1.  Blocks kb >= 64 are never skipped.
 __device__ __forceinline__ uint64_t kblock_mask(const KArgs &ka, int tp) {
-  if (ka.full_k || ka.dbg == 9) return ~0ull;
+  if (ka.full_k || kdbg(ka) == 9) return ~0ull;
   // Closed form (checked against the per-block definition above for N in 256..4096, all
   // cols, all tp): only the last block il = Lc-1 can be partial (V < N); its needed kk are
   // [0, lo_end) U [hi_start, hi_end) with a = kk*BK + tp:
@@ -579,7 +587,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     // own half of B, bytes land on CTA 0's barrier =====
     int s = 0; uint32_t ph = 0;
     long long pw = 0;
-    const uint32_t tx = (uint32_t)(2 * ((ka.dbg == 5 ? 0 : A_BYTES_HANKEL) + (ka.dbg == 6 ? 0 : b_half)));
+    const uint32_t tx = (uint32_t)(2 * ((kdbg(ka) == 5 ? 0 : A_BYTES_HANKEL) + (kdbg(ka) == 6 ? 0 : b_half)));
     for (TileIter it(cid, ncl, ka.n_tiles); it.tile < total; it.next(ncl, ka.n_tiles)) {
       const int64_t m_tile = it.m;
       const int n_tile = it.n;
@@ -592,15 +600,15 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       int i = 0, kk = 0;
       for (int kb = 0; kb < ka.k_blocks; kb++) {
         if (kb_issue(km, kb)) {
-          long long w0 = ka.dbg == 4 ? clock64() : 0;
+          long long w0 = kdbg(ka) == 4 ? clock64() : 0;
           mbar_wait(&empty[s], ph ^ 1);
-          if (ka.dbg == 4) pw += clock64() - w0;
+          if (kdbg(ka) == 4) pw += clock64() - w0;
           if (elect_one()) {
             if (leader) mbar_expect_tx(&full[s], tx);
             const uint32_t fb = smem_u32(&full[s]) & PEER_MASK;
             const int64_t arow = abase + (int64_t)i * (2 * (int64_t)ka.N) + kk * BK;
-            if (ka.dbg != 5) tma_load_2d_2sm(smem_u32(sA + s * 4096), &map_a, 0, (int)arow, fb);
-            if (ka.dbg != 6) tma_load_2d_2sm(smem_u32(sB + s * B_HALF_MAX), &map_b, kb * BK, brow, fb);
+            if (kdbg(ka) != 5) tma_load_2d_2sm(smem_u32(sA + s * 4096), &map_a, 0, (int)arow, fb);
+            if (kdbg(ka) != 6) tma_load_2d_2sm(smem_u32(sB + s * B_HALF_MAX), &map_b, kb * BK, brow, fb);
           }
           __syncwarp();
           if (++s == S) { s = 0; ph ^= 1; }
@@ -608,17 +616,17 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         if (++kk == ka.kb_per_block) { kk = 0; i++; }
       }
     }
-    if (ka.dbg == 4 && lane == 0) dbg_add(5, pw);
+    if (kdbg(ka) == 4 && lane == 0) dbg_add(5, pw);
   } else if (warp == W_MMA) {
     // ===== MMA issuer (leader CTA only; warp-wide loop, elected lane issues + commits) =====
     if (leader) {
       const uint32_t idesc = idesc_i8(2 * BM, n_mma);
       int s = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
-      long long t_start = clock64(), wt = 0, wf = 0;
+      long long t_start = kdbg(ka) == 4 ? clock64() : 0, wt = 0, wf = 0;
       for (TileIter it(cid, ncl, ka.n_tiles); it.tile < total; it.next(ncl, ka.n_tiles)) {
-        long long w0 = ka.dbg == 4 ? clock64() : 0;
+        long long w0 = kdbg(ka) == 4 ? clock64() : 0;
         mbar_wait(&tempty[acc], aph ^ 1);
-        if (ka.dbg == 4) wt += clock64() - w0;
+        if (kdbg(ka) == 4) wt += clock64() - w0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         const int tp = (int)((uint32_t)it.m % (uint32_t)ka.tb_per_row) * (2 * BM);
@@ -626,9 +634,9 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         uint32_t acc_flag = 0;  // first issued MMA of the tile overwrites the accumulator
         for (int kb = 0; kb < ka.k_blocks; kb++) {
           if (!kb_issue(km, kb)) continue;
-          long long w1 = ka.dbg == 4 ? clock64() : 0;
+          long long w1 = kdbg(ka) == 4 ? clock64() : 0;
           mbar_wait(&full[s], ph);
-          if (ka.dbg == 4) wf += clock64() - w1;
+          if (kdbg(ka) == 4) wf += clock64() - w1;
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + s * 4096);
           const uint32_t b_addr = smem_u32(sB + s * B_HALF_MAX);
@@ -647,7 +655,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         __syncwarp();
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
-      if (ka.dbg == 4 && lane == 0) { dbg_add(0, wt); dbg_add(1, wf); dbg_add(2, clock64() - t_start); }
+      if (kdbg(ka) == 4 && lane == 0) { dbg_add(0, wt); dbg_add(1, wf); dbg_add(2, clock64() - t_start); }
     }
   } else if (warp < 8) {
     // ===== epilogue (both CTAs): own 128 TMEM lanes = own 128 rows t =====
@@ -671,10 +679,10 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       const int tb = ((int)it.m - jr * ka.tb_per_row) * (2 * BM) + (int)crank * BM;
       const int nchunks = (ntok + EPI_TOK - 1) / EPI_TOK;
       const int first = (grp + (int)(iter & 1)) & 1;
-      long long e0 = (ka.dbg == 4 && warp == 0 && lane == 0) ? clock64() : 0;
+      long long e0 = (kdbg(ka) == 4 && warp == 0 && lane == 0) ? clock64() : 0;
       mbar_wait(&tfull[acc], aph);
-      long long e1 = (ka.dbg == 4 && warp == 0 && lane == 0) ? clock64() : 0;
-      if (ka.dbg == 4 && warp == 0 && lane == 0) dbg_add(4, e1 - e0);
+      long long e1 = (kdbg(ka) == 4 && warp == 0 && lane == 0) ? clock64() : 0;
+      if (kdbg(ka) == 4 && warp == 0 && lane == 0) dbg_add(4, e1 - e0);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN);
       bool arrived = false;
@@ -694,7 +702,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         }
         OutT *ob = obuf + nbuf * OB_ELEMS;
         named_bar(1 + grp, 128);  // the store that last read buffer nbuf has drained
-        if (ka.dbg != 1) {
+        if (kdbg(ka) != 1) {
           if constexpr (MODE == OUT_DIG) {
             // r = top 32 bits of v after rounding the q_in - 32 bit tail half up; signed base-2^8
             // digits, least significant first with carry (Decomp, Eq. 4 / S:59-67; R18);
@@ -730,7 +738,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         if (issuer) {
           // a full 16-token box, or the tpt % 16 tail box of this tile (never past the tile)
           const CUtensorMap *mo = (c0 + EPI_TOK <= ka.tpt) ? &map_out : &map_out_tail;
-          if (ka.dbg == 0 || ka.dbg == 4) {
+          if (kdbg(ka) == 0 || kdbg(ka) == 4) {
             if constexpr (MODE == OUT_DIG) tma_store_4d(mo, smem_u32(ob), tb, 0, jr, tau0 + c0);
             else tma_store_3d(mo, smem_u32(ob), tb, jr, tau0 + c0);
           }
@@ -742,7 +750,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         tc_fence_before();
         mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)acc);
       }
-      if (ka.dbg == 4 && warp == 0 && lane == 0) { dbg_add(3, clock64() - e1); dbg_add(6, 1); }
+      if (kdbg(ka) == 4 && warp == 0 && lane == 0) { dbg_add(3, clock64() - e1); dbg_add(6, 1); }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
     if (issuer) bulk_wait_all();
@@ -1121,7 +1129,7 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
   ka.kb_per_block = N / BK; ka.Lc = a.Lc; ka.cols = a.cols; ka.row_begin = a.row_begin; ka.R = R; ka.T = a.T;
   ka.full_k = (a.cols == a.Lc * N) || (K / BK > 64);
   ka.q_in = a.kp.q_in; ka.out_bits = a.out_bits;
-  ka.dbg = getenv("PHE_DEBUG_EPI") ? atoi(getenv("PHE_DEBUG_EPI")) : 0;
+  ka.dbg = (PHE_KERNEL_EXPERIMENTS && getenv("PHE_DEBUG_EPI")) ? atoi(getenv("PHE_DEBUG_EPI")) : 0;
   // ---- body: plain W operand, M = rows in range (skipped when out_body == NULL)
   if (a.out_body) {
     CUtensorMap ma, mb;
@@ -1141,7 +1149,7 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
   }
   // ---- mask: Hankel operand, M = R * N (skipped when out_mask == NULL)
   if (a.out_mask) {
-    const bool two_sm = (ell == 4 || ell == 5) && (N % (2 * BM) == 0) && !getenv("PHE_FORCE_1SM");
+    const bool two_sm = (ell == 4 || ell == 5) && (N % (2 * BM) == 0) && !(PHE_KERNEL_EXPERIMENTS && getenv("PHE_FORCE_1SM"));
     const bool sw = a.out_bits != a.kp.q_in;
     KArgs km = ka;
     if (two_sm) km.tpt = choose_tpt(a.T, ell, &km.n_mma);
