@@ -39,11 +39,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["q_proj", "ffn", "stack", "q_proj_packed"], default="q_proj")
+    ap.add_argument("--workload", choices=["q_proj", "ffn", "stack", "q_proj_packed", "stack_packed"],
+                    default="q_proj")
     ap.add_argument("--contraction", choices=["tc", "ntt", "hybrid"], default="tc",
                     help="mask contraction a5: tc = int8 limb GEMM on tcgen05 (north_star), ntt = NTT domain "
                          "(NEXT #4, CUDA cores), hybrid = ntt for multi-block (L >= 2) linears, tc otherwise")
-    ap.add_argument("--tokens", type=int, default=2048, help="tokens per rank (B*C = 8*256)")
+    ap.add_argument("--tokens", type=int, default=None,
+                    help="tokens per rank (default B*C = 8*256 = 2048; stack_packed: the paper's training "
+                         "step, B*C = 1*16)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e/cpu/clocks)")
@@ -200,24 +203,24 @@ def run_ours(args):
             seeds, body = phe.encrypt_pack(p, S, x, synth.seed_base(xr * 131 + w.cols + 7 * w.transpose))
             inputs[base] = (seeds, body)
     max_rows = max(rr[name][1] - rr[name][0] for name, _, _ in regs)
-    if args.workload.endswith("_packed"):
-        max_rows = 1  # outputs are packed RLWE (16 KB per token per 2048 rows): no chunking needed
-    # token chunks: outputs stay <= ~34 GB (gate_up: 275 GB at T=2048) and a chunk is a whole
-    # number of 51-token tiles (no extra tile-padding waste)
+    # token chunks: outputs (LWE form: 4 B per coefficient; packed path: the Decomp digits,
+    # 4 levels x 1 B) stay <= ~34 GB (gate_up: 275 GB at T=2048) and a chunk is a whole number
+    # of 51-token tiles (no extra tile-padding waste)
     tpt = 256 // p.ell
-    chunk = min(T, max(tpt, (34_400_000_000 // (max_rows * p.N * 4)) // tpt * tpt))
+    per_row = (phe.KS_LEVELS if args.workload.endswith("_packed") else 4) * p.N
+    rows_for_chunk = (max_rows + 255) // 256 * 256 if args.workload.endswith("_packed") else max_rows
+    chunk = min(T, max(tpt, (34_400_000_000 // (rows_for_chunk * per_row)) // tpt * tpt))
     if not args.workload.endswith("_packed"):
         out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
         out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)
-    if packed:
-        name0, w0, _ = regs[0]
-        r256 = (w0.rows + 255) // 256 * 256
-        G0 = (w0.rows + p.N - 1) // p.N
-        dig_buf = torch.empty((chunk, r256, phe.KS_LEVELS, p.N), dtype=torch.int8, device=dev)
-        bod_buf = torch.empty((chunk, w0.rows), dtype=torch.int64, device=dev)
-        acc_buf = torch.empty(phe.load().phe_pack_acc_bytes(__import__("ctypes").byref(p), w0.rows, chunk),
-                              dtype=torch.uint8, device=dev)
-        pk_buf = torch.empty((chunk, G0, 2, p.N), dtype=torch.int32, device=dev)
+    if packed:  # flat buffers sized for the largest linear, viewed per linear
+        r256m = (max_rows + 255) // 256 * 256
+        Gm = (max_rows + p.N - 1) // p.N
+        dig_flat = torch.empty(chunk * r256m * phe.KS_LEVELS * p.N, dtype=torch.int8, device=dev)
+        bod_flat = torch.empty(chunk * max_rows, dtype=torch.int64, device=dev)
+        acc_buf = torch.empty(max(phe.load().phe_pack_acc_bytes(__import__("ctypes").byref(p), w.rows, chunk)
+                                  for _, w, _ in regs), dtype=torch.uint8, device=dev)
+        pk_flat = torch.empty(chunk * Gm * 2 * p.N, dtype=torch.int32, device=dev)
         out_mask = torch.empty(1, dtype=torch.int32, device=dev)  # unused: no LWE-form outputs
     max_L = max(p.L(w.cols) for _, w, _ in regs)
     operand = torch.empty(phe.load().phe_ct_operand_bytes(__import__("ctypes").byref(p), chunk, max_L),
@@ -248,10 +251,13 @@ def run_ours(args):
                     launches[0] += 1
                 e[1].record(stream)
                 if packed:  # Eq. 6 -> digits + bodies, then Eq. 8 + Eq. 7 + switch
-                    phe.matmul_clear_digits(p, w, operand, n, digits=dig_buf[:n], body=bod_buf[:n])
+                    r256, G = (w.rows + 255) // 256 * 256, (w.rows + p.N - 1) // p.N
+                    dig = dig_flat[: n * r256 * phe.KS_LEVELS * p.N].view(n, r256, phe.KS_LEVELS, p.N)
+                    bod = bod_flat[: n * w.rows].view(n, w.rows)
+                    phe.matmul_clear_digits(p, w, operand, n, digits=dig, body=bod)
                     launches[0] += phe.last_launch_count()
                     e[2].record(stream)
-                    phe.pack(p, dig_buf[:n], bod_buf[:n], K, out=pk_buf[:n], acc=acc_buf)
+                    phe.pack(p, dig, bod, K, out=pk_flat[: n * G * 2 * p.N].view(n, G, 2, p.N), acc=acc_buf)
                     launches[0] += phe.last_launch_count()
                     e[3].record(stream)
                     evs.append((name, e))
@@ -389,7 +395,7 @@ def run_ours(args):
 
     # ---------------- e2e through the C ABI with host buffers
     e2e = None
-    if not args.no_e2e and not args.profile and packed and not rows_mode:
+    if not args.no_e2e and not args.profile and args.workload == "q_proj_packed" and not rows_mode:
         # the server step as the network sees it: wire-format input blocks (9992 B) in,
         # wire-format packed RLWE ciphertexts (13312 B) out, through host buffers
         name, w, _ = regs[0]
@@ -504,16 +510,23 @@ def config_dict(args, world, T, rows_mode=False):
           "q_proj_packed": "Llama-3.2-1B q_proj 2048x2048 forward, full primitive: Eq. 6 + KeySwitch packing "
                            "Eq. 7/8 -> RLWE(Wx), 39->26 switch (configs[1] + SURVEY NEXT #1)",
           "stack": "Llama-3.2-1B all linears x 16 layers (qkv fused 3072x2048, o, gate_up fused 16384x2048, "
-                   "down; bwd W^T incl. GQA k/v 512x2048), fwd + bwd (configs[3])"}[args.workload]
+                   "down; bwd W^T incl. GQA k/v 512x2048), fwd + bwd (configs[3])",
+          "stack_packed": "Llama-3.2-1B all linears x 16 layers fwd + bwd, full primitive (Eq. 6 + KeySwitch "
+                          "packing Eq. 7/8 + switch): the HE server work of the paper's training step "
+                          "(P:432-435, B=1, C=16 by default)"}[args.workload]
     if args.contraction != "tc":
         wl += {"ntt": "; mask contraction in the NTT domain (NEXT #4, CUDA cores)",
                "hybrid": "; NTT-domain mask contraction for L >= 2 linears (NEXT #4), tcgen05 otherwise"}[args.contraction]
-    return {"workload": wl, "contraction": args.contraction, "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": 8, "C": 256, "N": 2048, "q_in": 39, "q_out": 26,
+    B, C = (1, T) if args.workload == "stack_packed" else (8, T // 8)
+    return {"workload": wl, "contraction": args.contraction, "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": B, "C": C, "N": 2048, "q_in": 39, "q_out": 26,
             "beta": 27,
             "parallelism": (f"row-sharded x{world}" if rows_mode else f"token-sharded x{world}") if world > 1
             else "single GPU",
-            "l2": "flushed between steps (256 MiB write), outputs 34 GB/step >> L2",
-            "output": "LWE ciphertexts, uint32 per coefficient after 39->26 modulus switch"}
+            "l2": ("flushed between steps (256 MiB write)" if args.workload.endswith("_packed") else
+                   "flushed between steps (256 MiB write), outputs 34 GB/step >> L2"),
+            "output": ("packed RLWE ciphertexts (Eq. 7), uint32 A', B' after the 39->26 switch"
+                       if args.workload.endswith("_packed") else
+                       "LWE ciphertexts, uint32 per coefficient after 39->26 modulus switch")}
 
 
 def cpu_baseline(args, lin, budget_s=12.0):
@@ -601,6 +614,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.tokens is None:  # B*C = 8*256; the paper's training step is B = 1, C = 16
+        args.tokens = 16 if args.workload == "stack_packed" else 2048
     if args.impl == "reference":
         run_reference(args)
     else:
