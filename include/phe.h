@@ -294,6 +294,12 @@ int phe_ntt_ct_prepare(const phe_params *p, const void *d_tables, const uint64_t
 int phe_encrypt_pack_ntt(const phe_params *p, const void *d_tables, const uint8_t *d_S, const int8_t *d_x,
                          int64_t T, int64_t d_in, uint64_t seed_base, uint64_t noise_seed, uint64_t *d_seeds,
                          uint64_t *d_body, void *stream);
+/* Stage 1 of the packed primitive through the NTT path: same contract and bit-identical output
+ * as phe_matmul_clear_digits (digits int8 [T][round256(rows)][4][N], bodies uint64 [T][rows] at
+ * q_in), mask contraction in the NTT domain; then phe_pack as usual.  Requires q_in >= 32.     */
+int phe_matmul_clear_digits_ntt(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                                int64_t d_in, int transpose, const void *d_operand, int64_t T, void *d_digits,
+                                uint64_t *d_body, void *stream);
 int phe_matmul_clear_ntt(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
                          int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
                          int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);

@@ -39,6 +39,7 @@ EXPORTS = [
     "phe_ntt_weights_bytes", "phe_ntt_weights_prepare", "phe_ntt_operand_bytes", "phe_ntt_ct_prepare",
     "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T", "phe_matmul_clear_ct", "phe_encrypt_pack_ntt",
     "phe_wire_lwe_bytes", "phe_wire_serialize_lwe", "phe_wire_deserialize_lwe", "phe_server_matvec_wire_host",
+    "phe_matmul_clear_digits_ntt",
 ]
 
 
@@ -120,6 +121,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_matmul_clear_ct": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _sz,
                                  _vp, _vp, _vp], ctypes.c_int),
         "phe_ntt_primes": ([_vp], ctypes.c_int),
+        "phe_matmul_clear_digits_ntt": ([_P, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp, _vp, _vp],
+                                        ctypes.c_int),
         "phe_wire_lwe_bytes": ([_P, _i64], _sz),
         "phe_wire_serialize_lwe": ([_P, _vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
         "phe_wire_deserialize_lwe": ([_P, _vp, _i64, _i64, _vp, _vp, _vp], ctypes.c_int),
@@ -610,4 +613,17 @@ def server_matvec_wire_host(p: Params, w: Weights, h_wire_in: torch.Tensor, h_wi
     _check(load().phe_server_matvec_wire_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
                                               row_begin, row_end, _ptr(h_wire_in), T, chunk_tokens,
                                               _ptr(h_wire_out), _stream()), "phe_server_matvec_wire_host")
+
+
+def matmul_clear_digits_ntt(p: Params, w: "NttWeights", operand: torch.Tensor, T: int, digits=None, body=None):
+    """matmul_clear_digits through the NTT-domain contraction (bit-identical); feeds phe.pack."""
+    r256 = (w.rows + 255) // 256 * 256
+    if digits is None:
+        digits = torch.empty((T, r256, KS_LEVELS, p.N), dtype=torch.int8, device=operand.device)
+    if body is None:
+        body = torch.empty((T, w.rows), dtype=torch.int64, device=operand.device)
+    _check(load().phe_matmul_clear_digits_ntt(ctypes.byref(p), _ptr(w.tables.buf), _ptr(w.buf), w.d_out, w.d_in,
+                                              int(w.transpose), _ptr(operand), T, _ptr(digits), _ptr(body),
+                                              _stream()), "phe_matmul_clear_digits_ntt")
+    return digits, body
 

@@ -320,7 +320,9 @@ struct MaskArgs {
   uint64_t qmask;
   uint32_t crt_k1;          // ((Z mod p1 - Z mod p0) mod p1) + 2 p1, Z the CRT offset (crt_store)
   uint32_t crt_z0;          // Z mod p0
-  void *out;                // [T][R][N] uint32 (switched) or uint64
+  void *out;                // [T][R][N] uint32 (switched) or uint64; DIG: int8 [T][digit_rows][4][N]
+  int64_t digit_rows;       // DIG: row stride of the digit tensor
+  int64_t plane;            // DIG: N (bytes between digit planes)
 };
 
 // Thread/element mapping of the inverse NTT: N/16 threads per residue array, 16 values each;
@@ -403,12 +405,27 @@ __device__ __forceinline__ void xload(uint32_t (&r)[NP][16], const uint32_t *xb,
 // r1 reduced, h = (r1 - r0 + Z1 - Z0) p0^-1 mod p1 and v = p0 h + r0 + Z0 in [0, p0 p1 + 2 p0)
 // the only representative is v = P' + Z exactly; Z vanishes mod 2^q_in.  kadd = Z0 + H par_j
 // (+ the switch's rounding constant) is a per-CTA constant.
-template <bool SW, int SHIFT, int OUTB>
+template <bool SW, int SHIFT, int OUTB, bool DIG = false>
 __device__ __forceinline__ void crt_store(const MaskArgs &a, uint32_t r0, uint32_t r1, uint64_t kadd,
                                           int64_t o, int s_shift, uint32_t omask) {
   r1 = min(r1, r1 - P1);
   const uint32_t h = mul_shoup(r1 - r0 + a.crt_k1, CRT_C, CRT_CQ, P1);  // argument < 4 p1 < 2^32
   const uint64_t x = (uint64_t)P0 * h + r0 + kadd;                       // P + Z [+ 2^(s-1)]
+  if constexpr (DIG) {
+    // Decomp (Eq. 4 / S:59-67; R18): r = top 32 bits of a'_t after rounding the q_in - 32 bit
+    // tail half up; signed base-2^8 digits, least significant first with carry.  o addresses
+    // plane 0 (weight 2^(q_in - 8)) of [tau][j][l][t]; plane l is l * N bytes further.
+    uint32_t r = (uint32_t)(x >> (SHIFT > 0 ? SHIFT : s_shift));
+    int8_t *od = static_cast<int8_t *>(a.out) + o;
+#pragma unroll
+    for (int l = KS_LEVELS - 1; l >= 0; l--) {
+      int dl = (int)(r & 255u);
+      r >>= 8;
+      if (dl >= 128) { dl -= 256; r += 1; }
+      od[(int64_t)l * a.plane] = (int8_t)dl;
+    }
+    return;
+  }
   if constexpr (SW && SHIFT > 0) {
     static_cast<uint32_t *>(a.out)[o] = (uint32_t)(x >> SHIFT) & ((1u << OUTB) - 1u);
   } else if constexpr (SW) {
@@ -489,7 +506,7 @@ __host__ __device__ constexpr int ntt_min_blocks() {  // target 512 threads / SM
 
 // WSM: W_hat_j (all Lc blocks, 8 N bytes each) staged in shared memory once per CTA and shared
 // by the NG token groups; else read through L1/L2.
-template <int LOGN, bool SW, int NG, int NB, bool WSM, int SHIFT = 0, int OUTB = 0>
+template <int LOGN, bool SW, int NG, int NB, bool WSM, int SHIFT = 0, int OUTB = 0, bool DIG = false>
 __global__ void __launch_bounds__(NG * (1 << LOGN) / 16, ntt_min_blocks<LOGN, NG>())
 ntt_mask_kernel(MaskArgs a) {
   constexpr int N = 1 << LOGN, NT = N / 16;
@@ -571,18 +588,18 @@ ntt_mask_kernel(MaskArgs a) {
     }
     intt<LOGN, 2, NB, NG>(r, tw1, twl, p, xb, tid, grp);
     // ---- CRT, mod 2^q_in, SampleExtract reversal, ModulusSwitch, store
-    const int64_t obase = (tau * a.R + jr) * (int64_t)N + (N - 1);
+    const int64_t obase = (DIG ? (tau * a.digit_rows + jr) * KS_LEVELS : tau * a.R + jr) * (int64_t)N + (N - 1);
     const int jt = eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(tid, 0);
 #pragma unroll
     for (int e = 0; e < 16; e++)
-      crt_store<SW, SHIFT, OUTB>(a, r[0][e], r[1][e], kadd,
+      crt_store<SW, SHIFT, OUTB, DIG>(a, r[0][e], r[1][e], kadd,
                     obase - jt - eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(0, e), s_shift, omask);
   }
 }
 
-template <int LOGN, bool SW, int NG, int NB, bool WSM, int SHIFT = 0, int OUTB = 0>
+template <int LOGN, bool SW, int NG, int NB, bool WSM, int SHIFT = 0, int OUTB = 0, bool DIG = false>
 int launch_mask_cfg(MaskArgs a, cudaStream_t st) {
-  auto kern = ntt_mask_kernel<LOGN, SW, NG, NB, WSM, SHIFT, OUTB>;
+  auto kern = ntt_mask_kernel<LOGN, SW, NG, NB, WSM, SHIFT, OUTB, DIG>;
   const int smem = ntt_smem<LOGN, NG, NB>() + (WSM ? (int)(a.Lc * 2 * (1 << LOGN) * 4) : 0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return phe_set_cuda_error(e);
@@ -606,6 +623,16 @@ template <int LOGN, bool SW, int NG, int NB>
 int launch_mask_ng(const MaskArgs &a, cudaStream_t st) {
   const bool t1 = SW && a.q_in == 39 && a.out_bits == 26;
   const bool wsm = ntt_smem<LOGN, NG, NB>() + a.Lc * 2 * (1 << LOGN) * 4 <= SMEM_BUDGET;
+  if (a.digit_rows > 0) {  // Decomp digits (out_bits = 32): Table 1 shift 7 compiled in
+    if constexpr (SW) {
+      const bool d1 = a.q_in == 39;
+      if (wsm) return d1 ? launch_mask_cfg<LOGN, true, NG, NB, true, 7, 32, true>(a, st)
+                         : launch_mask_cfg<LOGN, true, NG, NB, true, 0, 0, true>(a, st);
+      return d1 ? launch_mask_cfg<LOGN, true, NG, NB, false, 7, 32, true>(a, st)
+                : launch_mask_cfg<LOGN, true, NG, NB, false, 0, 0, true>(a, st);
+    }
+    return PHE_EINVAL;
+  }
   if (wsm) return t1 ? launch_mask_cfg<LOGN, SW, NG, NB, true, 13, 26>(a, st) : launch_mask_cfg<LOGN, SW, NG, NB, true>(a, st);
   return t1 ? launch_mask_cfg<LOGN, SW, NG, NB, false, 13, 26>(a, st) : launch_mask_cfg<LOGN, SW, NG, NB, false>(a, st);
 }
@@ -702,9 +729,11 @@ int launch_ntt_masks(const KParams &kp, const void *tables, const uint64_t *seed
 
 int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, const uint8_t *par,
                     int64_t rows, int64_t Lc, int64_t row_begin, int64_t row_end, const uint32_t *ahat,
-                    int64_t T, int out_bits, void *out, cudaStream_t st) {
+                    int64_t T, int out_bits, void *out, cudaStream_t st, int64_t digit_rows) {
   ntt::MaskArgs a{};
   a.par = par;
+  a.digit_rows = digit_rows;  // > 0: Decomp digits, out_bits must be 32
+  a.plane = kp.N;
   a.tinv = static_cast<const uint2 *>(tables) + 2 * kp.N;  // inverse slice [pr][N]
   a.what = what;
   a.ahat = ahat;
@@ -726,7 +755,7 @@ int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what,
     a.crt_z0 = z0;
     a.crt_k1 = (uint32_t)(((uint64_t)z1 + ntt::P1 - (z0 % ntt::P1)) % ntt::P1 + 2ull * ntt::P1);
   }
-  const bool sw = out_bits != kp.q_in;
+  const bool sw = digit_rows > 0 || out_bits != kp.q_in;
   switch (kp.log2N) {
     case 9: return sw ? ntt::launch_mask<9, true>(a, st) : ntt::launch_mask<9, false>(a, st);
     case 10: return sw ? ntt::launch_mask<10, true>(a, st) : ntt::launch_mask<10, false>(a, st);

@@ -977,6 +977,40 @@ static int ntt_common(const phe_params *p, const void *d_tables, const void *d_n
   return PHE_OK;
 }
 
+int phe_matmul_clear_digits_ntt(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                                int64_t d_in, int transpose, const void *d_operand, int64_t T, void *d_digits,
+                                uint64_t *d_body, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_ntt(p, &kp);
+  if (rc) return rc;
+  if (p->q_in < 32) return PHE_EUNSUPPORTED;  // Decomp keeps the top 32 bits (R18)
+  if (d_out < 1 || d_in < 1 || T < 0 || (transpose != 0 && transpose != 1)) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_tables || !d_nttw || !d_operand || !d_digits || !d_body) return PHE_EINVAL;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  const int64_t N = p->N, rp = round_up(rows, 256), Lc = phe_num_blocks(p, cols);
+  if (Lc > phe_ntt_max_blocks(p)) return PHE_EUNSUPPORTED;
+  // bodies at q_in (the tcgen05 body GEMM, as phe_matmul_clear_digits)
+  rc = ntt_common(p, d_tables, d_nttw, rows, cols, 0, rows, d_operand, T, p->q_in, nullptr, d_body, stream);
+  if (rc) return rc;
+  int launches = g_last_launches;
+  uint8_t *digits = static_cast<uint8_t *>(d_digits);
+  if (rp > rows) {  // zero digit rows of the 256-row padding (they contribute nothing)
+    const int64_t KL = phe::KS_LEVELS * N;
+    if (cudaMemset2DAsync(digits + rows * KL, (size_t)(rp * KL), 0, (size_t)((rp - rows) * KL), (size_t)T,
+                          S(stream)) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+  }
+  const uint32_t *what = static_cast<const uint32_t *>(d_nttw);
+  const uint8_t *par = reinterpret_cast<const uint8_t *>(what + rows * Lc * 2 * N) + round_up(rows, 128) * Lc * N;
+  rc = phe::launch_ntt_mask(kp, d_tables, what, par, rows, Lc, 0, rows, static_cast<const uint32_t *>(d_operand), T,
+                            phe::KS_BITS, d_digits, S(stream), rp);
+  if (rc) return rc;
+  g_last_launches = launches + 1;
+  return PHE_OK;
+}
+
 int phe_matmul_clear_ntt(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
                          int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
                          int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {

@@ -220,3 +220,23 @@ def test_encrypt_pack_ntt_identical(phe, coracle, preset, over, eta, d_in, T):
     A, B = O.encrypt(op, So, x[0].cpu().numpy(), O.block_seeds(777, T, op.L(d_in))[0], E[0])
     assert np.array_equal(u64(b2[0]), B)
 
+
+@pytest.mark.parametrize("transpose,d_out,d_in,T", [(False, 300, 2048, 5), (True, 700, 2100, 3), (False, 2048, 8192, 2)])
+def test_digits_ntt_identical_to_tensor_core(phe, transpose, d_out, d_in, T):
+    """Stage 1 of the packed primitive: NTT digits + bodies == tcgen05 digits + bodies (bitwise),
+    and the packed result through phe_pack is the same."""
+    p = phe.params(phe.PRESET_PAPER)
+    W = synth.weights_int8(d_out, d_in, seed=d_out + d_in)
+    x = synth.activations_int8(T, d_out if transpose else d_in, seed=T)
+    S, seeds, body = encrypt(phe, p, x)
+    w = phe.Weights(p, torch.from_numpy(W).to(DEV), transpose=transpose)
+    dg, bd = phe.matmul_clear_digits(p, w, phe.ct_prepare(p, seeds, body), T)
+    tabs = phe.NttTables(p)
+    wn = phe.NttWeights(p, tabs, torch.from_numpy(W).to(DEV), transpose=transpose)
+    dn, bn = phe.matmul_clear_digits_ntt(p, wn, phe.ntt_ct_prepare(p, tabs, seeds, body), T)
+    assert torch.equal(bn, bd)
+    assert torch.equal(dn, dg)
+    if not transpose and d_out <= 2048:
+        K = phe.KeySwitchKey(p, phe.ksk_gen(p, S, 3))
+        assert torch.equal(phe.pack(p, dn, bn, K), phe.pack(p, dg, bd, K))
+
