@@ -52,7 +52,10 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e/cpu/clocks)")
     ap.add_argument("--shard", choices=["tokens", "rows"], default="tokens",
                     help="N>1: tokens = each rank its own batch (weak); rows = W rows split (strong)")
-    ap.add_argument("--gather", action="store_true", help="rows mode: also time the NCCL gather to rank 0")
+    ap.add_argument("--gather", nargs="?", const="nccl", default="none", choices=["none", "nccl", "p2p"],
+                    help="rows mode (q_proj): nccl = time an NCCL send/recv gather to rank 0 after the step; "
+                         "p2p = fused gather: every rank's kernels write their row block straight into rank "
+                         "0's buffer (CUDA IPC / NVLink peer stores) inside the timed step")
     return ap.parse_args()
 
 
@@ -169,7 +172,7 @@ def run_ours(args):
     T = args.tokens
     lins = linears(args.workload)
     # ---------------- untimed setup: weights (server registration) and client encryption
-    from paper_2505_07329_b200.dist import gather_rows, shard_range
+    from paper_2505_07329_b200.dist import PeerGather, gather_rows, shard_range
     rows_mode = args.shard == "rows" and world > 1
     regs = []   # (name, Weights | NttWeights, input_key)
     tabs = phe.NttTables(p, device=dev) if args.contraction != "tc" else None
@@ -228,6 +231,9 @@ def run_ours(args):
     ntt_L = max([p.L(w.cols) for n_, w, _ in regs if is_ntt[n_]] or [0])
     ntt_operand = (torch.empty(phe.load().phe_ntt_operand_bytes(__import__("ctypes").byref(p), chunk, ntt_L),
                                dtype=torch.uint8, device=dev) if ntt_L else None)
+    peer = None
+    if rows_mode and args.gather == "p2p" and args.workload == "q_proj" and not packed:
+        peer = PeerGather(T, regs[0][1].rows, p.N, dtype=torch.int32, root=0)  # 34 GB on rank 0
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
@@ -271,6 +277,14 @@ def run_ours(args):
                     f, opnd = (phe.matmul_clear_T if w.transpose else phe.matmul_clear), operand
                 r0, r1 = rr[name]
                 nr = r1 - r0
+                if peer is not None:  # fused gather: a5 + a6 stores land in rank 0's buffer
+                    e[2].record(stream)
+                    phe.matmul_clear_into(p, w, opnd, n, peer.mask[t0:t0 + n, r0:r1], peer.body[t0:t0 + n, r0:r1],
+                                          r0, r1)
+                    launches[0] += phe.last_launch_count()
+                    e[3].record(stream)
+                    evs.append((name, e))
+                    continue
                 mview = out_mask.view(-1)[: n * nr * p.N].view(n, nr, p.N)
                 bview = out_body.view(-1)[: n * nr].view(n, nr)
                 f(p, w, opnd, n, out_mask=phe.SKIP, out_body=bview, row_begin=r0, row_end=r1)  # a6
@@ -337,7 +351,12 @@ def run_ours(args):
 
     # ---------------- optional: NCCL gather of the row-sharded output ciphertexts to rank 0
     gather = None
-    if rows_mode and args.gather and args.workload == "q_proj":
+    if peer is not None:
+        peer.complete()
+        gather = {"mode": "p2p: fused into the kernels' stores (dist.PeerGather, phe_matmul_clear_into); "
+                          "included in ms_per_step",
+                  "bytes": int(T * regs[0][1].rows * (p.N + 1) * 4)}
+    if rows_mode and args.gather == "nccl" and args.workload == "q_proj":
         name, w, _ = regs[0]
         r0, r1 = rr[name]
         dist.barrier()

@@ -138,6 +138,18 @@ int phe_matmul_clear_T(const phe_params *p, const void *d_wprep, int64_t d_out, 
                        int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
                        int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);
 
+/* ---- matmul_clear into a row block of a larger output (row sharding with a fused gather) -----
+ * Same contract as phe_matmul_clear (transpose = 0) / phe_matmul_clear_T (transpose = 1), except
+ * that the outputs are written with a row stride of out_rows (>= row_end - row_begin): mask word
+ * (tau, j, t) goes to d_out_mask[(tau * out_rows + (j - row_begin)) * N + t], body (tau, j) to
+ * d_out_body[tau * out_rows + (j - row_begin)].  Point d_out_mask/d_out_body at the rank's row
+ * block inside a [T][R_total][N] gather buffer -- also a peer GPU's buffer mapped through CUDA
+ * IPC (paper_2505_07329_b200.dist.PeerGather): the epilogue's TMA stores then move the shard
+ * over NVLink as it is produced, and no separate gather collective runs.       */
+int phe_matmul_clear_into(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
+                          int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T, int32_t out_bits,
+                          void *d_out_mask, void *d_out_body, int64_t out_rows, void *stream);
+
 /* ---- matmul_clear(W, ct): the north_star's one-call form on device buffers ------------------
  * phe_ct_prepare of (d_seeds, d_body) into the caller's workspace d_ws (>= phe_ct_operand_bytes(p,
  * T, L), L = blocks of the input length: d_in forward, d_out backward), then phe_matmul_clear
@@ -303,6 +315,10 @@ int phe_matmul_clear_digits_ntt(const phe_params *p, const void *d_tables, const
 int phe_matmul_clear_ntt(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
                          int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
                          int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);
+int phe_matmul_clear_ntt_into(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                              int64_t d_in, int transpose, int64_t row_begin, int64_t row_end,
+                              const void *d_operand, int64_t T, int32_t out_bits, void *d_out_mask,
+                              void *d_out_body, int64_t out_rows, void *stream);
 int phe_matmul_clear_ntt_T(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
                            int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
                            int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream);

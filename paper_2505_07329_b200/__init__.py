@@ -39,7 +39,7 @@ EXPORTS = [
     "phe_ntt_weights_bytes", "phe_ntt_weights_prepare", "phe_ntt_operand_bytes", "phe_ntt_ct_prepare",
     "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T", "phe_matmul_clear_ct", "phe_encrypt_pack_ntt",
     "phe_wire_lwe_bytes", "phe_wire_serialize_lwe", "phe_wire_deserialize_lwe", "phe_server_matvec_wire_host",
-    "phe_matmul_clear_digits_ntt",
+    "phe_matmul_clear_digits_ntt", "phe_matmul_clear_into", "phe_matmul_clear_ntt_into",
 ]
 
 
@@ -121,6 +121,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_matmul_clear_ct": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _sz,
                                  _vp, _vp, _vp], ctypes.c_int),
         "phe_ntt_primes": ([_vp], ctypes.c_int),
+        "phe_matmul_clear_into": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _i64, _i32, _vp, _vp, _i64,
+                                   _vp], ctypes.c_int),
+        "phe_matmul_clear_ntt_into": ([_P, _vp, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _i64, _i32, _vp, _vp,
+                                       _i64, _vp], ctypes.c_int),
         "phe_matmul_clear_digits_ntt": ([_P, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp, _vp, _vp],
                                         ctypes.c_int),
         "phe_wire_lwe_bytes": ([_P, _i64], _sz),
@@ -626,4 +630,31 @@ def matmul_clear_digits_ntt(p: Params, w: "NttWeights", operand: torch.Tensor, T
                                               int(w.transpose), _ptr(operand), T, _ptr(digits), _ptr(body),
                                               _stream()), "phe_matmul_clear_digits_ntt")
     return digits, body
+
+
+def matmul_clear_into(p: Params, w, operand: torch.Tensor, T: int, mask_block: torch.Tensor,
+                      body_block: torch.Tensor, row_begin: int, row_end: int, out_bits: int | None = None) -> None:
+    """matmul_clear / matmul_clear_T (by w.transpose; Weights or NttWeights) writing rows
+    [row_begin, row_end) into row-block views of larger [T][R_total][N] / [T][R_total] tensors --
+    also peer-mapped ones (dist.PeerGather): the fused gather (phe_matmul_clear_into)."""
+    out_bits = p.q_out if out_bits is None else out_bits
+    R = row_end - row_begin
+    dt = torch.int64 if out_bits == p.q_in else torch.int32
+    for t, n in [(mask_block, "mask_block"), (body_block, "body_block")]:
+        if not t.is_cuda or t.dtype != dt:
+            raise PheError(f"{n} must be a CUDA {dt} tensor")
+    if (tuple(mask_block.shape) != (T, R, p.N) or mask_block.stride(2) != 1 or mask_block.stride(1) != p.N
+            or tuple(body_block.shape) != (T, R) or body_block.stride(1) != 1
+            or mask_block.stride(0) != body_block.stride(0) * p.N):
+        raise PheError("mask_block/body_block must be row blocks [T][R][N] / [T][R] of [T][R_total][N] / [T][R_total]")
+    out_rows = body_block.stride(0)
+    if isinstance(w, NttWeights):
+        _check(load().phe_matmul_clear_ntt_into(ctypes.byref(p), _ptr(w.tables.buf), _ptr(w.buf), w.d_out, w.d_in,
+                                                int(w.transpose), row_begin, row_end, _ptr(operand), T, out_bits,
+                                                _ptr(mask_block), _ptr(body_block), out_rows, _stream()),
+               "phe_matmul_clear_ntt_into")
+    else:
+        _check(load().phe_matmul_clear_into(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
+                                            row_begin, row_end, _ptr(operand), T, out_bits, _ptr(mask_block),
+                                            _ptr(body_block), out_rows, _stream()), "phe_matmul_clear_into")
 

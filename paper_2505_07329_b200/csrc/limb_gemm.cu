@@ -86,6 +86,8 @@ struct KArgs {
   int full_k;         // no zero-padded K-blocks (or more than 64): no skipping
   int64_t row_begin;  // absolute first row
   int64_t R;          // rows in range
+  int64_t out_rows;   // row stride of the output tensor [T][out_rows][N] (>= R; > R when the
+                      // output is a row block of a larger, possibly peer-mapped, gather buffer)
   int64_t T;
   int q_in, out_bits;
   int dbg;            // experiments only (PHE_DEBUG_EPI): 1 = no TMEM loads/stores, 2 = no stores
@@ -371,12 +373,12 @@ limb_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       if (HANKEL) {
         const int64_t jr = m_tile / ka.tb_per_row;
         const int64_t t = (m_tile % ka.tb_per_row) * BM + row;
-        tstride = ka.R * N;
+        tstride = ka.out_rows * N;
         obase = tau0 * tstride + jr * N + t;
       } else {
         const int64_t jr = m_tile * BM + row;
         valid = jr < ka.R;
-        tstride = ka.R;
+        tstride = ka.out_rows;
         obase = tau0 * tstride + jr;
       }
       mbar_wait(&tfull[acc], aph);
@@ -1091,12 +1093,13 @@ static int make_map_digits(CUtensorMap *m, void *base, int64_t N, int64_t Rpad, 
   return r == CUDA_SUCCESS ? PHE_OK : PHE_EINVAL;
 }
 
-static int make_map_out(CUtensorMap *m, void *base, bool sw, int64_t N, int64_t R, int64_t T, int box_tok) {
+static int make_map_out(CUtensorMap *m, void *base, bool sw, int64_t N, int64_t R, int64_t T, int box_tok,
+                        int64_t out_rows) {
   auto enc = get_encode();
   if (!enc) return PHE_ECUDA;
   const uint64_t es = sw ? 4 : 8;
   cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)R, (cuuint64_t)T};
-  cuuint64_t strides[2] = {(cuuint64_t)(N * es), (cuuint64_t)(R * N * es)};
+  cuuint64_t strides[2] = {(cuuint64_t)(N * es), (cuuint64_t)(out_rows * N * es)};
   cuuint32_t box[3] = {(cuuint32_t)BM, 1, (cuuint32_t)box_tok};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, sw ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims,
@@ -1127,6 +1130,7 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
   KArgs ka{};
   ka.N = N; ka.tpt = tpt; ka.n_tiles = n_tiles; ka.k_blocks = (int)(K / BK);
   ka.kb_per_block = N / BK; ka.Lc = a.Lc; ka.cols = a.cols; ka.row_begin = a.row_begin; ka.R = R; ka.T = a.T;
+  ka.out_rows = a.out_rows > 0 ? a.out_rows : R;
   ka.full_k = (a.cols == a.Lc * N) || (K / BK > 64);
   ka.q_in = a.kp.q_in; ka.out_bits = a.out_bits;
   ka.dbg = (PHE_KERNEL_EXPERIMENTS && getenv("PHE_DEBUG_EPI")) ? atoi(getenv("PHE_DEBUG_EPI")) : 0;
@@ -1173,8 +1177,8 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
         rc = make_map_digits(&mo, a.out_mask, N, a.digit_rows, a.T, EPI_TOK);
         if (!rc) rc = make_map_digits(&mot, a.out_mask, N, a.digit_rows, a.T, tail);
       } else {
-        rc = make_map_out(&mo, a.out_mask, sw, N, R, a.T, EPI_TOK);
-        if (!rc) rc = make_map_out(&mot, a.out_mask, sw, N, R, a.T, tail);
+        rc = make_map_out(&mo, a.out_mask, sw, N, R, a.T, EPI_TOK, ka.out_rows);
+        if (!rc) rc = make_map_out(&mot, a.out_mask, sw, N, R, a.T, tail, ka.out_rows);
       }
       if (rc) return rc;
       unsigned long long zero[8] = {0};

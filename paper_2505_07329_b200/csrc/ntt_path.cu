@@ -322,6 +322,7 @@ struct MaskArgs {
   uint32_t crt_z0;          // Z mod p0
   void *out;                // [T][R][N] uint32 (switched) or uint64; DIG: int8 [T][digit_rows][4][N]
   int64_t digit_rows;       // DIG: row stride of the digit tensor
+  int64_t out_rows;         // row stride of the output tensor [T][out_rows][N] (>= R)
   int64_t plane;            // DIG: N (bytes between digit planes)
 };
 
@@ -588,7 +589,7 @@ ntt_mask_kernel(MaskArgs a) {
     }
     intt<LOGN, 2, NB, NG>(r, tw1, twl, p, xb, tid, grp);
     // ---- CRT, mod 2^q_in, SampleExtract reversal, ModulusSwitch, store
-    const int64_t obase = (DIG ? (tau * a.digit_rows + jr) * KS_LEVELS : tau * a.R + jr) * (int64_t)N + (N - 1);
+    const int64_t obase = (DIG ? (tau * a.digit_rows + jr) * KS_LEVELS : tau * a.out_rows + jr) * (int64_t)N + (N - 1);
     const int jt = eidx<LOGN, LastPhase<LOGN>::S0, LastPhase<LOGN>::B>(tid, 0);
 #pragma unroll
     for (int e = 0; e < 16; e++)
@@ -729,8 +730,9 @@ int launch_ntt_masks(const KParams &kp, const void *tables, const uint64_t *seed
 
 int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, const uint8_t *par,
                     int64_t rows, int64_t Lc, int64_t row_begin, int64_t row_end, const uint32_t *ahat,
-                    int64_t T, int out_bits, void *out, cudaStream_t st, int64_t digit_rows) {
+                    int64_t T, int out_bits, void *out, cudaStream_t st, int64_t digit_rows, int64_t out_rows) {
   ntt::MaskArgs a{};
+  a.out_rows = out_rows > 0 ? out_rows : row_end - row_begin;
   a.par = par;
   a.digit_rows = digit_rows;  // > 0: Decomp digits, out_bits must be 32
   a.plane = kp.N;

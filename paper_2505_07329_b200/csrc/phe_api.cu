@@ -154,7 +154,8 @@ int phe_ct_prepare(const phe_params *p, const uint64_t *d_seeds, const uint64_t 
 
 static int matmul_common(const phe_params *p, const void *d_wprep, int64_t rows, int64_t cols,
                          int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
-                         int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
+                         int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream,
+                         int64_t out_rows = 0) {
   g_last_launches = 0;
   KParams kp;
   int rc = check_gpu(p, &kp);
@@ -183,6 +184,7 @@ static int matmul_common(const phe_params *p, const void *d_wprep, int64_t rows,
   a.out_bits = out_bits;
   a.out_mask = d_out_mask;
   a.out_body = d_out_body;
+  a.out_rows = out_rows;
   int n = 0;
   rc = phe::launch_limb_gemm(a, S(stream), &n);
   g_last_launches = n;
@@ -204,6 +206,16 @@ int phe_matmul_clear_T(const phe_params *p, const void *d_wprep, int64_t d_out, 
   // M = W^T: rows = d_in, cols = d_out
   return matmul_common(p, d_wprep, d_in, d_out, row_begin, row_end, d_operand, T, out_bits,
                        d_out_mask, d_out_body, stream);
+}
+
+int phe_matmul_clear_into(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
+                          int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T, int32_t out_bits,
+                          void *d_out_mask, void *d_out_body, int64_t out_rows, void *stream) {
+  if (!p || (transpose != 0 && transpose != 1)) return PHE_EINVAL;
+  if (out_rows < row_end - row_begin) return PHE_EINVAL;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  return matmul_common(p, d_wprep, rows, cols, row_begin, row_end, d_operand, T, out_bits, d_out_mask,
+                       d_out_body, stream, out_rows);
 }
 
 int phe_matmul_clear_ct(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
@@ -929,7 +941,8 @@ int phe_encrypt_pack_ntt(const phe_params *p, const void *d_tables, const uint8_
 
 static int ntt_common(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t rows,
                       int64_t cols, int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T,
-                      int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
+                      int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream,
+                      int64_t out_rows = 0) {
   g_last_launches = 0;
   KParams kp;
   int rc = check_ntt(p, &kp);
@@ -962,6 +975,7 @@ static int ntt_common(const phe_params *p, const void *d_tables, const void *d_n
     a.out_bits = out_bits;
     a.out_mask = nullptr;
     a.out_body = d_out_body;
+    a.out_rows = out_rows;
     rc = phe::launch_limb_gemm(a, S(stream), &n);
     if (rc) return rc;
   }
@@ -969,7 +983,7 @@ static int ntt_common(const phe_params *p, const void *d_tables, const void *d_n
     const uint8_t *par = reinterpret_cast<const uint8_t *>(what + rows * Lc * 2 * N) +
                          round_up(rows, 128) * Lc * N;
     rc = phe::launch_ntt_mask(kp, d_tables, what, par, rows, Lc, row_begin, row_end, ahat, T, out_bits,
-                              d_out_mask, S(stream));
+                              d_out_mask, S(stream), 0, out_rows);
     if (rc) return rc;
     n++;
   }
@@ -1016,6 +1030,17 @@ int phe_matmul_clear_ntt(const phe_params *p, const void *d_tables, const void *
                          int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {
   return ntt_common(p, d_tables, d_nttw, d_out, d_in, row_begin, row_end, d_operand, T, out_bits,
                     d_out_mask, d_out_body, stream);
+}
+
+int phe_matmul_clear_ntt_into(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                              int64_t d_in, int transpose, int64_t row_begin, int64_t row_end,
+                              const void *d_operand, int64_t T, int32_t out_bits, void *d_out_mask,
+                              void *d_out_body, int64_t out_rows, void *stream) {
+  if (!p || (transpose != 0 && transpose != 1)) return PHE_EINVAL;
+  if (out_rows < row_end - row_begin) return PHE_EINVAL;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  return ntt_common(p, d_tables, d_nttw, rows, cols, row_begin, row_end, d_operand, T, out_bits, d_out_mask,
+                    d_out_body, stream, out_rows);
 }
 
 int phe_matmul_clear_ntt_T(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,

@@ -55,7 +55,8 @@ int launch_ntt_rowpar(const int8_t *W, int64_t d_out, int64_t d_in, int transpos
                       cudaStream_t st);
 int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what, const uint8_t *par,
                     int64_t rows, int64_t Lc, int64_t row_begin, int64_t row_end, const uint32_t *ahat,
-                    int64_t T, int out_bits, void *out, cudaStream_t st, int64_t digit_rows = 0);
+                    int64_t T, int out_bits, void *out, cudaStream_t st, int64_t digit_rows = 0,
+                    int64_t out_rows = 0);
 
 // limb_gemm.cu: the tcgen05 int8 limb GEMM (mask = Hankel operand, body = plain operand).
 struct GemmArgs {
@@ -73,6 +74,7 @@ struct GemmArgs {
   int64_t T;
   int out_bits;
   void *out_mask, *out_body;
+  int64_t out_rows;       // row stride of out_mask/out_body ([T][out_rows][N] / [T][out_rows]); 0 = R
   int digits;             // 1: out_mask receives Decomp digits int8 [T][digit_rows][3][N] (Eq. 8)
   int64_t digit_rows;     // row stride of the digit tensor (>= row_end - row_begin)
 };

@@ -6,9 +6,11 @@ collective on the data path:
     and every weight; weak scaling when each rank brings its own batch.
   * row sharding (north_star): rank r owns rows shard_range(R, W, r) of each linear for all
     tokens; the input ciphertexts (seeds + bodies, ~1.1 MB/token) are replicated.
-The only collective is the optional gather of output ciphertexts to one rank (NCCL over
-NVLink on the GPU box; gloo in the CPU tests).  This module is device-agnostic plumbing: the
-compute is the caller's (libphe on GPU).
+The only collective is the optional gather of output ciphertexts to one rank: either NCCL
+send/recv after the GEMM (`gather_rows`), or fused into the GEMM itself (`PeerGather`): rank 0's
+gather buffer is mapped into every rank through CUDA IPC and each rank's mask kernel TMA-stores
+its row block straight into it (NVLink peer writes, overlapped with the contraction tile by
+tile; `phe_matmul_clear_into`).  This module is plumbing: the compute is libphe's.
 """
 from __future__ import annotations
 
@@ -80,3 +82,39 @@ def gather_tokens(mask: torch.Tensor, body: torch.Tensor, T: int, world: int, ra
             dist.recv(full_m[t0:t1], k, group=group)  # token slices are contiguous
             dist.recv(full_b[t0:t1], k, group=group)
     return full_m, full_b
+
+
+class PeerGather:
+    """Fused gather for row sharding: rank `root` allocates the [T][R][N] mask and [T][R] body
+    buffers and shares them through CUDA IPC (torch's reduce_tensor handles, broadcast over the
+    process group); every other rank rebuilds tensors aliasing root's memory (peer-mapped: its
+    kernels' stores go over NVLink).  `block(r0, r1)` is a rank's row block, a strided view that
+    `paper_2505_07329_b200.matmul_clear_into` writes directly.  After the kernels: synchronize,
+    then barrier -- root may read once every rank has passed it."""
+
+    def __init__(self, T: int, R: int, N: int, dtype=torch.int32, root: int = 0, group=None, device=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.root = root
+        self.group = group
+        rank = dist.get_rank(group)
+        if rank == root:
+            dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+            self.mask = torch.empty((T, R, N), dtype=dtype, device=dev)
+            self.body = torch.empty((T, R), dtype=dtype, device=dev)
+            obj = [(reduce_tensor(self.mask), reduce_tensor(self.body))]
+        else:
+            obj = [None]
+        dist.broadcast_object_list(obj, src=root, group=group)
+        if rank != root:
+            (fm, am), (fb, ab) = obj[0]
+            self.mask = fm(*am)
+            self.body = fb(*ab)
+
+    def block(self, r0: int, r1: int):
+        return self.mask[:, r0:r1], self.body[:, r0:r1]
+
+    def complete(self):
+        """Make every rank's stores visible to root (call on all ranks after the kernels)."""
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+
