@@ -212,7 +212,8 @@ def run_ours(args):
     tpt = 256 // p.ell
     per_row = (phe.KS_LEVELS if args.workload.endswith("_packed") else 4) * p.N
     rows_for_chunk = (max_rows + 255) // 256 * 256 if args.workload.endswith("_packed") else max_rows
-    chunk = min(T, max(tpt, (34_400_000_000 // (rows_for_chunk * per_row)) // tpt * tpt))
+    cap = 34_400_000_000 // (rows_for_chunk * per_row)
+    chunk = T if T <= cap else max(tpt, cap // tpt * tpt)  # chunk only when the output does not fit
     if not args.workload.endswith("_packed"):
         out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
         out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)

@@ -48,7 +48,8 @@ def run(p, T, contraction, steps, warmup):
         inputs[d_in] = phe.encrypt_pack(p, S, x, synth.seed_base(d_in))
     tpt = 256 // p.ell
     max_rows = max(d for _, d, _ in LAYER)
-    chunk = min(T, max(tpt, (34_400_000_000 // (max_rows * p.N * 4)) // tpt * tpt))
+    cap = 34_400_000_000 // (max_rows * p.N * 4)
+    chunk = T if T <= cap else max(tpt, cap // tpt * tpt)
     out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
     out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)
     max_L = max(p.L(d) for _, _, d in LAYER)
