@@ -604,8 +604,12 @@ int launch_mask_cfg(MaskArgs a, cudaStream_t st) {
   const int smem = ntt_smem<LOGN, NG, NB>() + (WSM ? (int)(a.Lc * 2 * (1 << LOGN) * 4) : 0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return phe_set_cuda_error(e);
-  const char *ev = getenv("PHE_NTT_TOK");
-  a.tok_per_cta = ev ? atoi(ev) : 8 * NG;  // 8 tokens per group
+#ifndef PHE_KERNEL_EXPERIMENTS
+#define PHE_KERNEL_EXPERIMENTS 0
+#endif
+  // 8 tokens per group (PHE_NTT_TOK overrides it in experiment builds only)
+  const char *ev = PHE_KERNEL_EXPERIMENTS ? getenv("PHE_NTT_TOK") : nullptr;
+  a.tok_per_cta = ev ? atoi(ev) : 8 * NG;
   if (a.tok_per_cta < 1) a.tok_per_cta = 1;
   a.n_chunks = (a.T + a.tok_per_cta - 1) / a.tok_per_cta;
   kern<<<(unsigned)(a.R * a.n_chunks), NG * (1 << LOGN) / 16, smem, st>>>(a);

@@ -1,6 +1,7 @@
 """Ad-hoc probe (not product, not the bench contract): times the mask contraction of one linear
 through the NTT path (phe_matmul_clear_ntt) and the tensor-core path (phe_matmul_clear), same
-inputs, and reports ms, output coefficients/s and the SM clock.  PHE_NTT_TOK varies tokens/CTA."""
+inputs, and reports ms, output coefficients/s and the SM clock.  PHE_NTT_TOK varies tokens/CTA
+(experiment builds only: -DPHE_KERNEL_EXPERIMENTS=1)."""
 import argparse
 import os
 import statistics
