@@ -462,6 +462,26 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster)
       : "memory");
 }
+// Same with an L2 eviction-priority hint (createpolicy: evict_first for streamed operands,
+// evict_last for operands re-read by many tiles)
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_2sm_hint(uint32_t dst, const CUtensorMap *map, int x, int y,
+                                                     uint32_t bar_cluster, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t src, int x, int y, int z) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -783,9 +803,26 @@ struct PArgs {
   int64_t rows_pad;   // digit rows per token (multiple of 256)
   int G;              // output RLWE groups per token = ceil(R / N)
   int64_t total_tiles;
+  int64_t m_tiles;    // T * tpt_rows
+  int ng;             // N-tile group width of the rasterization (pack_tile)
+  int hints;          // L2 eviction hints on the operand loads
   int k_blocks;       // KS_LEVELS*N / BK
   unsigned long long *acc;
 };
+
+// Grouped rasterization: tiles sweep every M-tile (token rows) inside a group of `ng` N-tiles
+// (KSK coefficient slots), so the group's KSK limb planes (ng x 2 MB) stay L2-resident while
+// the digits stream through once per group.  (m-major order over all 82 N-tiles re-streamed the
+// whole 168 MB KSK -- more than L2 -- from HBM for every wave of 74 tiles.)
+__device__ __forceinline__ void pack_tile(const PArgs &pa, int64_t t, int64_t &m, int &n) {
+  const int64_t gsz = pa.m_tiles * pa.ng;
+  const int64_t g = t / gsz;
+  const int64_t r = t - g * gsz;
+  const int n0 = (int)g * pa.ng;
+  const int w = min(pa.ng, pa.n_tiles - n0);
+  m = r / w;
+  n = n0 + (int)(r - m * w);
+}
 constexpr int PK_STAGES = 6;
 constexpr int PK_A_BYTES = BM * BK;            // 16 KB per CTA per stage (digit rows)
 constexpr int PK_B_BYTES = (BN / 2) * BK;      // 16 KB per CTA per stage (KSK limb rows)
@@ -837,18 +874,26 @@ pack_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
   if (warp == W_PROD) {
     int s = 0; uint32_t ph = 0;
     const uint32_t tx = (uint32_t)(2 * (PK_A_BYTES + PK_B_BYTES));
-    for (TileIter it(cid, ncl, pa.n_tiles); it.tile < total; it.next(ncl, pa.n_tiles)) {
-      const int tau = (int)((uint64_t)it.m / (uint64_t)pa.tpt_rows);
-      const int64_t j0 = (it.m - (int64_t)tau * pa.tpt_rows) * (2 * BM);
+    const uint64_t pol_a = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
+    for (int64_t tile = cid; tile < total; tile += ncl) {
+      int64_t tm; int tn;
+      pack_tile(pa, tile, tm, tn);
+      const int tau = (int)((uint64_t)tm / (uint64_t)pa.tpt_rows);
+      const int64_t j0 = (tm - (int64_t)tau * pa.tpt_rows) * (2 * BM);
       const int64_t arow = (int64_t)tau * pa.rows_pad + j0 + (int)crank * BM;
-      const int brow = it.n * pa.spt * ELL + (int)crank * (BN / 2);
+      const int brow = tn * pa.spt * ELL + (int)crank * (BN / 2);
       for (int kb = 0; kb < pa.k_blocks; kb++) {
         mbar_wait(&empty[s], ph ^ 1);
         if (elect_one()) {
           if (leader) mbar_expect_tx(&full[s], tx);
           const uint32_t fb = smem_u32(&full[s]) & PEER_MASK;
-          tma_load_2d_2sm(smem_u32(sA + s * PK_A_BYTES), &map_a, kb * BK, (int)arow, fb);
-          tma_load_2d_2sm(smem_u32(sB + s * PK_B_BYTES), &map_b, kb * BK, brow, fb);
+          if (pa.hints) {  // digits stream (evict_first); the KSK group is re-read (evict_last)
+            tma_load_2d_2sm_hint(smem_u32(sA + s * PK_A_BYTES), &map_a, kb * BK, (int)arow, fb, pol_a);
+            tma_load_2d_2sm_hint(smem_u32(sB + s * PK_B_BYTES), &map_b, kb * BK, brow, fb, pol_b);
+          } else {
+            tma_load_2d_2sm(smem_u32(sA + s * PK_A_BYTES), &map_a, kb * BK, (int)arow, fb);
+            tma_load_2d_2sm(smem_u32(sB + s * PK_B_BYTES), &map_b, kb * BK, brow, fb);
+          }
         }
         __syncwarp();
         if (++s == S) { s = 0; ph ^= 1; }
@@ -890,12 +935,14 @@ pack_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     const uint32_t tempty_c0 = smem_u32(&tempty[0]) & PEER_MASK;
     const int nchunks = (pa.spt + EPI_TOK - 1) / EPI_TOK;
     int acc = 0; uint32_t aph = 0; int64_t iter = 0;
-    for (TileIter it(cid, ncl, pa.n_tiles); it.tile < total; it.next(ncl, pa.n_tiles), iter++) {
-      const int tau = (int)((uint64_t)it.m / (uint64_t)pa.tpt_rows);
-      const int64_t jc = (it.m - (int64_t)tau * pa.tpt_rows) * (2 * BM) + (int)crank * BM;
+    for (int64_t tile = cid; tile < total; tile += ncl, iter++) {
+      int64_t tm; int tn;
+      pack_tile(pa, tile, tm, tn);
+      const int tau = (int)((uint64_t)tm / (uint64_t)pa.tpt_rows);
+      const int64_t jc = (tm - (int64_t)tau * pa.tpt_rows) * (2 * BM) + (int)crank * BM;
       const int g = (int)(jc / pa.N);
       const int r_c0 = (int)(jc - (int64_t)g * pa.N);  // rotation of this CTA's first row
-      const int slot0 = it.n * pa.spt;
+      const int slot0 = tn * pa.spt;
       const int part = slot0 / pa.kpad;
       const int k0 = slot0 - part * pa.kpad;
       unsigned long long *bn = bins + acc * PK_BINS;
@@ -1224,6 +1271,16 @@ int launch_pack_gemm(const PackArgs &a, cudaStream_t st) {
   pa.tpt_rows = (int)(a.rows_pad / (2 * BM));
   pa.G = a.G;
   pa.total_tiles = (int64_t)a.T * pa.tpt_rows * pa.n_tiles;
+  pa.m_tiles = (int64_t)a.T * pa.tpt_rows;
+  // groups of 21 N-tiles (~42 MB of KSK limb planes at N = 2048) + L2 hints: measured best of
+  // {11, 14, 16, 21, 28, 41, 82 (= the plain m-major order)} (profiles/r1_summary.md)
+  pa.ng = 21;
+  pa.hints = 1;
+  if (PHE_KERNEL_EXPERIMENTS) {
+    if (const char *ev = getenv("PHE_PACK_NG")) pa.ng = atoi(ev);
+    if (const char *eh = getenv("PHE_PACK_HINTS")) pa.hints = atoi(eh);
+  }
+  if (pa.ng < 1 || pa.ng > pa.n_tiles) pa.ng = pa.n_tiles;
   pa.k_blocks = KS_LEVELS * N / BK;
   pa.acc = static_cast<unsigned long long *>(a.acc);
   CUtensorMap ma, mb;
