@@ -341,6 +341,27 @@ int phe_server_matvec_wire_host(const phe_params *p, const void *d_wprep, int64_
                                 int transpose, int64_t row_begin, int64_t row_end, const uint8_t *h_wire_in,
                                 int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *stream);
 
+/* ---- NEXT #1 stage 2 in the NTT domain (Eq. 7 + Eq. 8) ---------------
+ * Exchanging Eq. 7's sum over outputs j with Eq. 4's sum over KSK rows gives, for packed
+ * ciphertext g,  acc_g = sum_{l,i} D_{l,i}(X) * KSK_{l,i}(X),  D_{l,i}(X) = sum_r d_{gN+r,i,l} X^r
+ * (negacyclic, X^N = -1): 4N polynomial products, computed exactly modulo three 30-bit
+ * primes (forward NTT of every D_{l,i}, pointwise products with the registered KSK, inverse NTT)
+ * and recovered mod 2^q_in by CRT; then (0, b) - acc and the switch as phe_pack.  Same contract
+ * and bit-identical output as phe_pack (the value is Eq. 7's, unique); O(log N) work per (l, i,
+ * coefficient) instead of the MatMul's O(N).
+ * phe_ntt_ksk_prepare (server, once per key): d_nksk (phe_ntt_ksk_bytes(p) bytes, 256-aligned)
+ *   <- twiddle tables + NTT(centred KSK rows) N^-1 2^32 mod p for the three primes; d_ksk as
+ *   phe_ksk_gen writes it ([2][4N][N] uint64).  Public key material only.
+ * phe_pack_ntt: d_digits / d_body / d_out_packed as phe_pack; d_ws scratch of
+ *   phe_pack_ntt_ws_bytes(p, rows, T) bytes.
+ * Errors: EUNSUPPORTED unless 256 <= N <= 8192, q_in >= 32 and 2^(q_in + 2 log2 N + 9) <
+ *   p0 p1 p2 (Table 1: q_in <= 56 at N = 2048); ENOMEM for short buffers.                     */
+size_t phe_ntt_ksk_bytes(const phe_params *p);
+int phe_ntt_ksk_prepare(const phe_params *p, const void *d_ksk, void *d_nksk, size_t bytes, void *stream);
+size_t phe_pack_ntt_ws_bytes(const phe_params *p, int64_t rows, int64_t T);
+int phe_pack_ntt(const phe_params *p, const void *d_digits, const uint64_t *d_body, int64_t T, int64_t rows,
+                 const void *d_nksk, void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream);
+
 /* ---- introspection (tests / bench) -------------------------------------------------- */
 /* Number of kernel launches the last phe_matmul_clear[_T] on this thread enqueued. */
 int phe_last_launch_count(void);

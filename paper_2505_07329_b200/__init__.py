@@ -38,6 +38,7 @@ EXPORTS = [
     "phe_ntt_primes", "phe_ntt_max_blocks", "phe_ntt_tables_bytes", "phe_ntt_tables_init",
     "phe_ntt_weights_bytes", "phe_ntt_weights_prepare", "phe_ntt_operand_bytes", "phe_ntt_ct_prepare",
     "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T", "phe_matmul_clear_ct", "phe_encrypt_pack_ntt",
+    "phe_ntt_ksk_bytes", "phe_ntt_ksk_prepare", "phe_pack_ntt_ws_bytes", "phe_pack_ntt",
     "phe_wire_lwe_bytes", "phe_wire_serialize_lwe", "phe_wire_deserialize_lwe", "phe_server_matvec_wire_host",
     "phe_matmul_clear_digits_ntt", "phe_matmul_clear_into", "phe_matmul_clear_ntt_into",
 ]
@@ -144,6 +145,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                                  ctypes.c_int),
         "phe_matmul_clear_ntt_T": ([_P, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _i32, _vp, _vp, _vp],
                                    ctypes.c_int),
+        "phe_ntt_ksk_bytes": ([_P], _sz),
+        "phe_ntt_ksk_prepare": ([_P, _vp, _vp, _sz, _vp], ctypes.c_int),
+        "phe_pack_ntt_ws_bytes": ([_P, _i64, _i64], _sz),
+        "phe_pack_ntt": ([_P, _vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -432,6 +437,34 @@ def pack(p: Params, digits: torch.Tensor, body: torch.Tensor, ksk: KeySwitchKey,
         acc = torch.empty(nbytes, dtype=torch.uint8, device=body.device)
     _check(load().phe_pack(ctypes.byref(p), _ptr(digits), _ptr(body), T, rows, _ptr(ksk.buf), _ptr(acc),
                            acc.numel(), _ptr(out), _stream()), "phe_pack")
+    return out
+
+
+class NttKeySwitchKey:
+    """Server-side registration of a KSK in the NTT domain for stage 2 (phe_ntt_ksk_prepare)."""
+
+    def __init__(self, p: Params, ksk: torch.Tensor):
+        _dev(ksk, torch.int64, "ksk")
+        self.p = p
+        nbytes = load().phe_ntt_ksk_bytes(ctypes.byref(p))
+        if nbytes == 0:
+            raise PheError("phe_ntt_ksk_bytes: parameters unsupported by the NTT KeySwitch")
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=ksk.device)
+        _check(load().phe_ntt_ksk_prepare(ctypes.byref(p), _ptr(ksk), _ptr(self.buf), nbytes, _stream()),
+               "phe_ntt_ksk_prepare")
+
+
+def pack_ntt(p: Params, digits: torch.Tensor, body: torch.Tensor, nksk: NttKeySwitchKey, out=None, ws=None):
+    """Stage 2 in the NTT domain: same contract and bit-identical output as pack()."""
+    T, rows = body.shape
+    G = (rows + p.N - 1) // p.N
+    if out is None:
+        out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=body.device)
+    nbytes = load().phe_pack_ntt_ws_bytes(ctypes.byref(p), rows, T)
+    if ws is None:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=body.device)
+    _check(load().phe_pack_ntt(ctypes.byref(p), _ptr(digits), _ptr(body), T, rows, _ptr(nksk.buf), _ptr(ws),
+                               ws.numel(), _ptr(out), _stream()), "phe_pack_ntt")
     return out
 
 

@@ -1,0 +1,532 @@
+// ntt_keyswitch.cu — stage 2 of the packed primitive in the NTT domain.
+//
+// Eq. 7 with Eq. 4's KeySwitch packs the LWE outputs j = gN + r of group g as
+//   RLWE_g = sum_r X^r ((0, b_j) - sum_{l,i} d_{j,i,l} KSK_{l,i}),   d = Decomp(a_j[i]) digits
+// Eq. 8 evaluates the inner sums as a MatMul and rotates afterwards; that is
+// O(N) multiply-adds per (l, i, output coefficient).  Exchanging the sums gives the same value as
+//   sum_{l,i} D_{l,i}(X) * KSK_{l,i}(X),        D_{l,i}(X) = sum_r d_{gN+r,i,l} X^r
+// a sum of 4N negacyclic polynomial products (X^N = -1), computed here EXACTLY in the NTT
+// domain: |sum| <= 4N * N * 2^7 * 2^(q_in-1) (< 2^70 at Table 1), so three 30-bit primes
+// (p0 p1 p2 ~ 2^88.6) and a Garner CRT with an offset Z = 0 mod 2^q_in recover it; the result
+// mod 2^q_in is the accumulator the tensor-core path (pack_gemm_2sm_kernel) writes, and
+// pack_finalize_kernel finishes both identically ((0, b) - acc, ModulusSwitch).  Work per
+// (l, i, coefficient): (log2 N)/2 butterflies + 2 pointwise products per prime, O(log N)
+// instead of O(N).
+//
+// Kernels:
+//   ks_tables_kernel    psi^{+-bitrev(k)} with Shoup companions for the three primes, and the
+//                       per-thread regrouped table of the register NTT's last phase
+//   ks_khat_kernel      K_hat = NTT(centred KSK row) * N^-1 * 2^32 (Montgomery), thread order
+//                       [server, once per key]
+//   ks_ntt_kernel<LOGN> the hot kernel: one CTA per (token, group g, prime, K-split); NG groups
+//                       of N/16 threads each take columns (l, i) of a 16-column digit tile staged
+//                       in shared memory, run the forward NTT of D_{l,i} in registers (16 values
+//                       per thread, exchanges through conflict-free layouts, tools/ntt_ks_model.py)
+//                       and accumulate D_hat o K_hat_A, D_hat o K_hat_B (Montgomery, lazy)
+//   ks_finalize_kernel  sum of the K-split partials, inverse NTTs (3 primes x A/B), Garner CRT,
+//                       mod 2^q_in -> the uint64 accumulator of pack_finalize_kernel
+#include <cstdint>
+#include <cstdio>
+
+#include "phe_common.cuh"
+#include "side_kernels.cuh"
+
+namespace phe {
+namespace nks {
+
+constexpr int NPR = 3;
+// p = c 2^k + 1 with k >= 21 (negacyclic NTTs up to N = 8192 need 2N | p - 1), p < 2^30 so that
+// lazy values in [0, 4p) fit 32 bits; generator 3 for all three.
+constexpr uint32_t P0 = 998244353u, P1 = 1004535809u, P2 = 469762049u;
+__host__ __device__ constexpr uint32_t prime_h(int q) { return q == 0 ? P0 : q == 1 ? P1 : P2; }
+
+__host__ __device__ constexpr uint32_t neg_inv32(uint32_t p) {
+  uint32_t x = p;
+  for (int i = 0; i < 5; i++) x *= 2u - p * x;
+  return 0u - x;
+}
+__host__ __device__ constexpr uint32_t pw(uint64_t b, uint64_t e, uint32_t p) {
+  uint64_t r = 1;
+  b %= p;
+  while (e) {
+    if (e & 1) r = r * b % p;
+    b = b * b % p;
+    e >>= 1;
+  }
+  return (uint32_t)r;
+}
+static_assert((uint64_t)4 * P0 < (1ull << 32) && (uint64_t)4 * P1 < (1ull << 32), "lazy range");
+static_assert((P0 - 1) % (1u << 14) == 0 && (P1 - 1) % (1u << 14) == 0 && (P2 - 1) % (1u << 14) == 0,
+              "2N | p - 1 up to N = 8192");
+
+__device__ __forceinline__ uint32_t mul_shoup(uint32_t x, uint32_t w, uint32_t wq, uint32_t p) {
+  const uint32_t r = x * w - __umulhi(x, wq) * p;
+  return min(r, r - p);
+}
+__device__ __forceinline__ uint32_t shoup_lazy(uint32_t x, uint32_t w, uint32_t wq, uint32_t p) {
+  return x * w - __umulhi(x, wq) * p;  // any x < 2^32: [0, 2p)
+}
+__device__ __forceinline__ uint32_t mont_lazy(uint32_t a, uint32_t b, uint32_t p, uint32_t pi) {
+  const uint64_t t = (uint64_t)a * b;  // a < 4p, b < p: (t + m p) / 2^32 < 2p
+  const uint32_t m = (uint32_t)t * pi;
+  return (uint32_t)((t + (uint64_t)m * p) >> 32);
+}
+__device__ __forceinline__ uint32_t add_lazy(uint32_t a, uint32_t b, uint32_t p) {  // [0,2p)
+  const uint32_t s = a + b;
+  return min(s, s - 2 * p);
+}
+__device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) {  // [0,p)
+  const uint32_t s = a + b;
+  return min(s, s - p);
+}
+__host__ __device__ __forceinline__ uint32_t brev_n(uint32_t k, int logN) {
+#ifdef __CUDA_ARCH__
+  return __brev(k) >> (32 - logN);
+#else
+  uint32_t r = 0;
+  for (int i = 0; i < logN; i++) r |= ((k >> i) & 1u) << (logN - 1 - i);
+  return r;
+#endif
+}
+
+// Storage order of the K_hat rows (N words per (prime, row, part)): transform index k = 16 t + 4 v
+// + c (thread t of the hot kernel's last phase) at word 4 (v NT + t) + c, so each of a thread's four
+// 16-byte loads is one contiguous 512-byte warp access.
+__host__ __device__ __forceinline__ int tpos(int k, int N) {
+  return 4 * (((k >> 2) & 3) * (N / 16) + (k >> 4)) + (k & 3);
+}
+__host__ __device__ constexpr int p1off(int s) { return s == 0 ? 0 : s == 1 ? 8 : s == 2 ? 12 : 14; }
+
+// ---------------------------------------------------------------- buffer layout (d_khat)
+// uint2 fwd[3][N], inv[3][N], p1[3][15][N/16]; then (256-byte aligned) uint32 K_hat
+// [3][4N rows][2 parts][N] in tpos order.  Row = l N + i as in phe_ksk_gen (Eq. 8's K-index).
+__host__ __device__ inline size_t tables_bytes(int N) {
+  return ((size_t)NPR * (2 * N + 15 * (N / 16)) * 8 + 255) / 256 * 256;
+}
+__host__ __device__ inline size_t khat_bytes(int N) { return (size_t)NPR * KS_LEVELS * N * 2 * (size_t)N * 4; }
+
+__global__ void ks_tables_kernel(int logN, uint32_t psi0, uint32_t psi1, uint32_t psi2, uint2 *__restrict__ tab) {
+  const int N = 1 << logN, NT = N / 16;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nf = 2 * NPR * N;
+  if (idx >= nf + NPR * 15 * NT) return;
+  int q, k, dir;
+  if (idx < nf) {
+    dir = idx / (NPR * N); q = (idx / N) % NPR; k = idx % N;
+  } else {  // phase (0,4) of the forward NTT: [P1OFF[s] + m][t] = fwd[(N >> (s+1)) + t 2^(3-s) + m]
+    const int r = idx - nf;
+    q = r / (15 * NT);
+    const int slot = (r / NT) % 15, t = r % NT;
+    const int s = slot >= 14 ? 3 : slot >= 12 ? 2 : slot >= 8 ? 1 : 0;
+    dir = 0;
+    k = (N >> (s + 1)) + t * (1 << (3 - s)) + (slot - p1off(s));
+  }
+  const uint32_t p = prime_h(q), psi = q == 0 ? psi0 : q == 1 ? psi1 : psi2;
+  const uint32_t e = brev_n((uint32_t)k, logN);
+  const uint32_t ex = dir ? (uint32_t)((2 * N - e) % (2 * N)) : e;
+  const uint32_t w = pw(psi, ex, p);
+  tab[idx] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));
+}
+
+// In-place single-prime NTTs in shared memory (CTA-wide; prep/finalize only, not hot).
+__device__ void fntt_smem(uint32_t *x, const uint2 *__restrict__ fwd, int logN, uint32_t p) {
+  const int N = 1 << logN;
+  for (int s = logN - 1, m = 1; s >= 0; s--, m <<= 1) {
+    const int t = 1 << s;
+    for (int b = threadIdx.x; b < N / 2; b += blockDim.x) {
+      const int i = b >> s, j = 2 * i * t + (b & (t - 1));
+      const uint2 w = __ldg(&fwd[m + i]);
+      const uint32_t U = x[j], V = mul_shoup(x[j + t], w.x, w.y, p);
+      x[j] = add_mod(U, V, p);
+      x[j + t] = add_mod(U, p - V, p);
+    }
+    __syncthreads();
+  }
+}
+__device__ void intt_smem(uint32_t *x, const uint2 *__restrict__ inv, int logN, uint32_t p) {
+  const int N = 1 << logN;
+  for (int s = 0; s < logN; s++) {
+    const int t = 1 << s, h = N >> (s + 1);
+    for (int b = threadIdx.x; b < N / 2; b += blockDim.x) {
+      const int i = b >> s, j = 2 * i * t + (b & (t - 1));
+      const uint2 w = __ldg(&inv[h + i]);
+      const uint32_t U = x[j], V = x[j + t];
+      x[j] = add_mod(U, V, p);
+      x[j + t] = mul_shoup(U - V + p, w.x, w.y, p);
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int PREP_THREADS = 256;
+
+// K_hat for (prime q, row, part): centred K = KSK - 2^q_in [KSK >= 2^(q_in-1)] (same value mod
+// 2^q_in, half the CRT range), mod p, forward NTT, * N^-1 2^32 (Montgomery, inverse scaling folded).
+__global__ void __launch_bounds__(PREP_THREADS)
+ks_khat_kernel(KParams kp, const uint64_t *__restrict__ ksk, const uint2 *__restrict__ tabs,
+               uint32_t c0, uint32_t c1, uint32_t c2, uint32_t *__restrict__ khat) {
+  extern __shared__ uint32_t xs[];
+  const int N = kp.N;
+  const int64_t rows = (int64_t)KS_LEVELS * N;
+  const int64_t b = blockIdx.x;  // (q * rows + row) * 2 + part
+  const int part = (int)(b & 1);
+  const int64_t row = (b >> 1) % rows;
+  const int q = (int)((b >> 1) / rows);
+  const uint32_t p = prime_h(q);
+  const uint64_t *src = ksk + ((int64_t)part * rows + row) * N;
+  const uint64_t half = 1ull << (kp.q_in - 1);
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const uint64_t v = src[k] & kp.qmask;
+    xs[k] = v >= half ? (uint32_t)((p - (uint32_t)(((1ull << kp.q_in) - v) % p)) % p) : (uint32_t)(v % p);
+  }
+  __syncthreads();
+  fntt_smem(xs, tabs + (int64_t)q * N, kp.log2N, p);
+  const uint32_t c = q == 0 ? c0 : q == 1 ? c1 : c2;
+  uint32_t *o = khat + b * N;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) o[tpos(k, N)] = (uint32_t)((uint64_t)xs[k] * c % p);
+}
+
+// ---------------------------------------------------------------- the hot kernel
+struct KsArgs {
+  const uint2 *tabs;       // table section (fwd [3][N] first, p1 after inv)
+  const uint32_t *khat;    // [3][4N][2][N]
+  const int8_t *digits;    // [T][R256][4][N]
+  int64_t T, R256, G;
+  int S;                   // K-splits
+  int tiles_per_split;     // 16-row tiles of the 4N (l, i) rows per split
+  uint32_t *part;          // [S][T][G][3][2][N], natural transform index
+};
+
+// Thread/element mapping (as ntt_path.cu): N/16 threads per NTT, 16 values each; phase (S0, B)
+// makes index bits [S0, S0+B) thread-local.
+template <int LOGN, int S0, int B>
+__device__ __forceinline__ int eidx(int tid, int e) {
+  const int el = e & ((1 << B) - 1), g = e >> B;
+  const int o = tid | (g << (LOGN - 4));
+  return (o & ((1 << S0) - 1)) | (el << S0) | ((o >> S0) << (S0 + B));
+}
+// exchange layout, keyed by the stage the reading phase starts at (tools/ntt_ks_model.py)
+template <int S0R>
+__device__ __forceinline__ int lay(int j) { return S0R == 0 ? j + (j >> 4) : S0R == 4 ? j + 16 * (j >> 8) : j; }
+template <int LOGN>
+__host__ __device__ constexpr int xwords() { return (1 << LOGN) + (1 << LOGN) / 16; }
+template <int LOGN>
+__host__ __device__ constexpr int ks_nt() { return (1 << LOGN) / 16; }
+template <int LOGN>
+__host__ __device__ constexpr int ks_ng() { return 512 / ks_nt<LOGN>() < 16 ? 512 / ks_nt<LOGN>() : 16; }
+// first forward phase = last inverse phase
+template <int LOGN>
+struct FirstPhase {
+  static constexpr int S0 = LOGN > 12 ? 12 : LOGN > 8 ? 8 : 4;
+  static constexpr int B = LOGN > 12 ? 1 : LOGN > 8 ? LOGN - 8 : 4;
+};
+constexpr int TILE = 16;  // (l, i) columns per digit tile
+
+// Cooley-Tukey stages S0+B-1 .. S0 (half-distance 2^s), values lazily in [0, 4p).
+template <int LOGN, int S0, int B>
+__device__ __forceinline__ void ct_phase(uint32_t (&r)[16], const uint2 *tw1, const uint2 *twl, uint32_t p,
+                                         int tid) {
+  constexpr int N = 1 << LOGN, NT = N / 16;
+  const int jt = eidx<LOGN, S0, B>(tid, 0);
+#pragma unroll
+  for (int s = S0 + B - 1; s >= S0; s--) {
+    const int d = 1 << (s - S0);
+    const int tb = (N >> (s + 1)) + (jt >> (s + 1));
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+      if (e & d) continue;
+      const uint2 w = S0 == 0 ? tw1[(p1off(s) + (e >> (s + 1))) * NT + tid]
+                              : twl[tb + (eidx<LOGN, S0, B>(0, e) >> (s + 1))];
+      uint32_t U = r[e];
+      U = min(U, U - 2 * p);
+      const uint32_t V = shoup_lazy(r[e | d], w.x, w.y, p);
+      r[e] = U + V;
+      r[e | d] = U - V + 2 * p;
+    }
+  }
+}
+template <int LOGN, int S0, int B, int S0R>
+__device__ __forceinline__ void xstore(const uint32_t (&r)[16], uint32_t *xb, int tid) {
+  const int base = lay<S0R>(eidx<LOGN, S0, B>(tid, 0));
+#pragma unroll
+  for (int e = 0; e < 16; e++) xb[base + lay<S0R>(eidx<LOGN, S0, B>(0, e))] = r[e];
+}
+template <int LOGN, int S0, int B>
+__device__ __forceinline__ void xload(uint32_t (&r)[16], const uint32_t *xb, int tid) {
+  const int base = lay<S0>(eidx<LOGN, S0, B>(tid, 0));
+#pragma unroll
+  for (int e = 0; e < 16; e++) r[e] = xb[base + lay<S0>(eidx<LOGN, S0, B>(0, e))];
+}
+// one exchange between phases (S0, B) and (S0N, BN); the buffer is reused, so a barrier on both
+// sides of the store
+template <int LOGN, int S0, int B, int S0N, int BN>
+__device__ __forceinline__ void xchg(uint32_t (&r)[16], uint32_t *xb, int tid) {
+  __syncthreads();
+  xstore<LOGN, S0, B, S0N>(r, xb, tid);
+  __syncthreads();
+  xload<LOGN, S0N, BN>(r, xb, tid);
+}
+// forward negacyclic NTT (natural in, bit-reversed out: thread t ends with k = 16 t + e)
+template <int LOGN>
+__device__ __forceinline__ void fntt_regs(uint32_t (&r)[16], const uint2 *tw1, const uint2 *twl, uint32_t p,
+                                          uint32_t *xb, int tid) {
+  if constexpr (LOGN == 13) {
+    ct_phase<13, 12, 1>(r, tw1, twl, p, tid);
+    xchg<13, 12, 1, 8, 4>(r, xb, tid);
+    ct_phase<13, 8, 4>(r, tw1, twl, p, tid);
+    xchg<13, 8, 4, 4, 4>(r, xb, tid);
+  } else if constexpr (LOGN >= 9) {
+    ct_phase<LOGN, 8, LOGN - 8>(r, tw1, twl, p, tid);
+    xchg<LOGN, 8, LOGN - 8, 4, 4>(r, xb, tid);
+  }
+  ct_phase<LOGN, 4, 4>(r, tw1, twl, p, tid);
+  xchg<LOGN, 4, 4, 0, 4>(r, xb, tid);
+  ct_phase<LOGN, 0, 4>(r, tw1, twl, p, tid);
+}
+template <int LOGN>
+__host__ __device__ constexpr int ks_smem() {
+  return 16 * ks_nt<LOGN>() * 8                  // twiddles: tw1 [15][NT] + twl [NT]
+         + ks_ng<LOGN>() * xwords<LOGN>() * 4    // exchange buffers
+         + (1 << LOGN) * TILE;                   // digit tile [N rows][16 bytes]
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kernel(KsArgs a) {
+  constexpr int N = 1 << LOGN, NT = ks_nt<LOGN>(), NG = ks_ng<LOGN>(), NTH = NG * NT;
+  constexpr int COLS = TILE / NG;             // columns of a tile per group
+  constexpr int FS0 = FirstPhase<LOGN>::S0, FB = FirstPhase<LOGN>::B;
+  constexpr int SWS = LOGN == 8 ? 2 : 3;      // tile swizzle bits (r >> SWS) & 3
+  static_assert(TILE % NG == 0, "groups divide the tile");
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint2 *tw1 = reinterpret_cast<uint2 *>(smem_raw);
+  uint2 *twl = tw1 + 15 * NT;
+  uint32_t *xall = reinterpret_cast<uint32_t *>(twl + NT);
+  uint8_t *tile = reinterpret_cast<uint8_t *>(xall + NG * xwords<LOGN>());
+  const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
+  uint32_t *xb = xall + grp * xwords<LOGN>();
+
+  // blockIdx = (s * T G + tg) * 3 + q: the three primes of one token run side by side (shared
+  // digit tiles in L2), and concurrent CTAs sweep the same K_hat rows
+  const int64_t b = blockIdx.x;
+  const int q = (int)(b % NPR);
+  const int64_t tg = (b / NPR) % (a.T * a.G);
+  const int s = (int)(b / NPR / (a.T * a.G));
+  const int64_t tau = tg / a.G, g = tg % a.G;
+  const uint32_t p = prime_h(q), pinv = neg_inv32(p);
+
+  {  // twiddles of prime q
+    const uint2 *fwd = a.tabs + (int64_t)q * N;
+    const uint2 *p1 = a.tabs + 2 * NPR * N + (int64_t)q * 15 * NT;
+    for (int k = threadIdx.x; k < 15 * NT; k += NTH) tw1[k] = p1[k];
+    for (int k = threadIdx.x; k < NT; k += NTH) twl[k] = fwd[k];
+  }
+  uint32_t acc[2][16];
+#pragma unroll
+  for (int e = 0; e < 16; e++) acc[0][e] = acc[1][e] = 0;
+
+  const int jt = eidx<LOGN, FS0, FB>(tid, 0);
+  const int swt = (jt >> SWS) & 3;
+  const int64_t row_base = ((tau * a.R256 + g * N) * KS_LEVELS) * (int64_t)N;  // digits of row gN, plane 0
+  const int64_t rmax = a.R256 - g * N;       // rows of this group present in the digit tensor
+  const int tile0 = s * a.tiles_per_split;
+  for (int it = 0; it < a.tiles_per_split; it++) {
+    const int row0 = (tile0 + it) * TILE;    // (l, i) row l N + i of Eq. 8's K-index
+    const int l = row0 / N, i0 = row0 % N;
+    __syncthreads();  // every group is done with the previous tile
+    for (int r = threadIdx.x; r < N; r += NTH) {
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (r < rmax)
+        v = __ldg(reinterpret_cast<const uint4 *>(a.digits + row_base + ((int64_t)r * KS_LEVELS + l) * N + i0));
+      uint32_t *trow = reinterpret_cast<uint32_t *>(tile + r * TILE);
+      const int sw = (r >> SWS) & 3;
+      trow[0 ^ sw] = v.x; trow[1 ^ sw] = v.y; trow[2 ^ sw] = v.z; trow[3 ^ sw] = v.w;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int cc = 0; cc < COLS; cc++) {
+      const int c = grp * COLS + cc;
+      const uint8_t *cb = tile + jt * TILE + (c & 3);
+      const int cx = (c >> 2) ^ swt;
+      uint32_t r[16];
+#pragma unroll
+      for (int e = 0; e < 16; e++) {
+        const int je = eidx<LOGN, FS0, FB>(0, e);
+        const int swe = (je >> SWS) & 3;  // 0 for LOGN >= 9 (thread bits carry the swizzle)
+        const int8_t d = reinterpret_cast<const int8_t *>(cb)[je * TILE + 4 * (cx ^ swe)];
+        r[e] = (uint32_t)((int32_t)d + (int32_t)p);
+      }
+      fntt_regs<LOGN>(r, tw1, twl, p, xb, tid);
+      const uint4 *kr = reinterpret_cast<const uint4 *>(a.khat + (((int64_t)q * KS_LEVELS * N + row0 + c) * 2) * N) + tid;
+#pragma unroll
+      for (int pt = 0; pt < 2; pt++) {
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+          const uint4 kv = __ldg(kr + pt * (N / 4) + v * NT);
+          acc[pt][4 * v + 0] = add_lazy(acc[pt][4 * v + 0], mont_lazy(r[4 * v + 0], kv.x, p, pinv), p);
+          acc[pt][4 * v + 1] = add_lazy(acc[pt][4 * v + 1], mont_lazy(r[4 * v + 1], kv.y, p, pinv), p);
+          acc[pt][4 * v + 2] = add_lazy(acc[pt][4 * v + 2], mont_lazy(r[4 * v + 2], kv.z, p, pinv), p);
+          acc[pt][4 * v + 3] = add_lazy(acc[pt][4 * v + 3], mont_lazy(r[4 * v + 3], kv.w, p, pinv), p);
+        }
+      }
+    }
+  }
+  // sum over the NG groups (each covered other columns) in the tile buffer, group by group; store
+  // [..][pt][k], k = 16 tid + e
+  uint32_t *red = reinterpret_cast<uint32_t *>(tile);  // 2N words <= N * TILE bytes
+  for (int gg = 0; gg < NG; gg++) {
+    __syncthreads();
+    if (grp == gg) {
+#pragma unroll
+      for (int pt = 0; pt < 2; pt++)
+#pragma unroll
+        for (int e = 0; e < 16; e++) {
+          uint32_t *o = &red[pt * N + 16 * tid + e];
+          *o = gg ? add_lazy(*o, acc[pt][e], p) : acc[pt][e];
+        }
+    }
+  }
+  __syncthreads();
+  uint32_t *out = a.part + (((s * a.T + tau) * a.G + g) * NPR + q) * 2 * (int64_t)N;
+  for (int k = threadIdx.x; k < 2 * N; k += NTH) {
+    const uint32_t v = red[k];
+    out[k] = min(v, v - p);
+  }
+}
+
+// Per (token, group): sum the K-split partials, inverse NTTs, CRT, mod 2^q_in.
+__global__ void __launch_bounds__(1024)
+ks_finalize_kernel(KParams kp, const uint2 *__restrict__ tabs, const uint32_t *__restrict__ part, int S,
+                   int64_t TG, uint32_t z0, uint32_t z1, uint32_t z2, unsigned long long *__restrict__ acc) {
+  extern __shared__ uint32_t xs[];  // [3][2][N]
+  const int N = kp.N;
+  const int64_t tg = blockIdx.x;
+  for (int k = threadIdx.x; k < NPR * 2 * N; k += blockDim.x) {
+    const int q = k / (2 * N);
+    uint64_t v = 0;
+    for (int s = 0; s < S; s++) v += part[((s * TG + tg) * NPR) * 2 * (int64_t)N + k];
+    xs[k] = (uint32_t)(v % prime_h(q));
+  }
+  __syncthreads();
+  for (int q = 0; q < NPR; q++)
+    for (int pt = 0; pt < 2; pt++) intt_smem(xs + (q * 2 + pt) * N, tabs + (int64_t)(NPR + q) * N, kp.log2N, prime_h(q));
+  // Garner: v = x0 + p0 h1 + p0 p1 h2 = sum + Z in [0, p0 p1 p2); Z = 0 mod 2^q_in
+  constexpr uint32_t I01 = pw(P0, P1 - 2, P1);                           // p0^-1 mod p1
+  constexpr uint32_t I012 = pw((uint64_t)P0 * P1 % P2, P2 - 2, P2);      // (p0 p1)^-1 mod p2
+  constexpr uint64_t P01 = (uint64_t)P0 * P1;
+  for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) {
+    const int pt = k / N, c = k % N;
+    const uint64_t r0 = (xs[(0 * 2 + pt) * N + c] + (uint64_t)z0) % P0;
+    const uint64_t r1 = (xs[(1 * 2 + pt) * N + c] + (uint64_t)z1) % P1;
+    const uint64_t r2 = (xs[(2 * 2 + pt) * N + c] + (uint64_t)z2) % P2;
+    const uint64_t h1 = (r1 + P1 - r0 % P1) % P1 * I01 % P1;
+    const uint64_t x01 = r0 + (uint64_t)P0 * h1;                         // < p0 p1 < 2^60
+    const uint64_t h2 = (r2 + P2 - x01 % P2) % P2 * I012 % P2;
+    const uint64_t v = x01 + P01 * h2;                                   // mod 2^64
+    acc[(tg * 2 + pt) * N + c] = v & kp.qmask;
+  }
+}
+
+template <int LOGN>
+int launch_ks(const KsArgs &a, int64_t grid, cudaStream_t st) {
+  constexpr int smem = ks_smem<LOGN>();
+  cudaError_t e = cudaFuncSetAttribute(ks_ntt_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return phe_set_cuda_error(e);
+  ks_ntt_kernel<LOGN><<<(unsigned)grid, ks_ng<LOGN>() * ks_nt<LOGN>(), smem, st>>>(a);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+}  // namespace nks
+
+// ---------------------------------------------------------------- launchers (host)
+static uint32_t ks_psi(uint32_t p, int N) { return nks::pw(3, (p - 1) / (2 * (uint32_t)N), p); }
+static uint32_t ks_ninv_mont(uint32_t p, int N) {  // N^-1 2^32 mod p
+  return (uint32_t)((uint64_t)nks::pw(N, p - 2, p) * ((1ull << 32) % p) % p);
+}
+
+size_t ntt_ks_bytes(const KParams &kp) { return nks::tables_bytes(kp.N) + nks::khat_bytes(kp.N); }
+
+// CRT range: |sum| <= 4N * N * 2^7 * 2^(q_in-1) = 2^(q_in + 2 log2 N + 8) =: B; Z = B (a multiple
+// of 2^q_in) puts sum + Z in [0, 2B], unique below p0 p1 p2 iff 2B < p0 p1 p2.
+bool ntt_ks_supported(const KParams &kp) {
+  if (kp.log2N < 8 || kp.log2N > 13 || kp.q_in < KS_BITS) return false;
+  const int bb = kp.q_in + 2 * kp.log2N + 8;
+  const long double M = (long double)nks::P0 * nks::P1 * nks::P2;
+  return bb + 1 < 88 && (long double)2 * ((unsigned __int128)1 << bb) < M;
+}
+
+int launch_ntt_ks_prepare(const KParams &kp, const uint64_t *ksk, void *buf, cudaStream_t st) {
+  const int N = kp.N, NT = N / 16;
+  uint2 *tabs = static_cast<uint2 *>(buf);
+  const int ntab = 2 * nks::NPR * N + nks::NPR * 15 * NT;
+  nks::ks_tables_kernel<<<(ntab + 255) / 256, 256, 0, st>>>(kp.log2N, ks_psi(nks::P0, N), ks_psi(nks::P1, N),
+                                                           ks_psi(nks::P2, N), tabs);
+  PHE_CUDA_CHECK_LAUNCH();
+  uint32_t *khat = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(buf) + nks::tables_bytes(N));
+  const size_t smem = (size_t)N * 4;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(nks::ks_khat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return phe_set_cuda_error(e);
+  }
+  const int64_t blocks = (int64_t)nks::NPR * KS_LEVELS * N * 2;
+  nks::ks_khat_kernel<<<(unsigned)blocks, nks::PREP_THREADS, smem, st>>>(
+      kp, ksk, tabs, ks_ninv_mont(nks::P0, N), ks_ninv_mont(nks::P1, N), ks_ninv_mont(nks::P2, N), khat);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+// K-splits: enough CTAs for two waves of one CTA per SM; a power of two dividing the 4N/16 tiles
+int ntt_ks_splits(const KParams &kp, int64_t T, int64_t G) {
+  const int64_t tiles = (int64_t)KS_LEVELS * kp.N / nks::TILE;
+  int64_t S = 1;
+  while (S < tiles && nks::NPR * T * G * S < 2 * 148) S *= 2;
+  return (int)S;
+}
+size_t ntt_ks_ws_bytes(const KParams &kp, int64_t T, int64_t G) {
+  const size_t partb = (size_t)ntt_ks_splits(kp, T, G) * T * G * nks::NPR * 2 * kp.N * 4;
+  return (partb + 255) / 256 * 256 + (size_t)T * G * 2 * kp.N * 8;
+}
+
+// acc (uint64 [T][G][2][N]) = sum_{l,i} D_{l,i} * KSK_{l,i} mod 2^q_in, the tensor-core packing
+// GEMM's accumulator (Eq. 7 + Eq. 8 before (0, b) - acc and the switch)
+int launch_ntt_ks(const KParams &kp, const void *buf, const int8_t *digits, int64_t T, int64_t R, void *ws,
+                  void *acc_out, cudaStream_t st) {
+  const int N = kp.N;
+  const int64_t G = (R + N - 1) / N, R256 = (R + 255) / 256 * 256;
+  const int S = ntt_ks_splits(kp, T, G);
+  uint32_t *part = static_cast<uint32_t *>(ws);
+  unsigned long long *acc = acc_out ? static_cast<unsigned long long *>(acc_out)
+      : reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(ws) +
+          ((size_t)S * T * G * nks::NPR * 2 * N * 4 + 255) / 256 * 256);
+  nks::KsArgs a{};
+  a.tabs = static_cast<const uint2 *>(buf);
+  a.khat = reinterpret_cast<const uint32_t *>(static_cast<const uint8_t *>(buf) + nks::tables_bytes(N));
+  a.digits = digits;
+  a.T = T; a.R256 = R256; a.G = G; a.S = S;
+  a.tiles_per_split = (int)((int64_t)KS_LEVELS * N / nks::TILE / S);
+  a.part = part;
+  const int64_t grid = (int64_t)nks::NPR * T * G * S;
+  int rc;
+  switch (kp.log2N) {
+    case 8: rc = nks::launch_ks<8>(a, grid, st); break;
+    case 9: rc = nks::launch_ks<9>(a, grid, st); break;
+    case 10: rc = nks::launch_ks<10>(a, grid, st); break;
+    case 11: rc = nks::launch_ks<11>(a, grid, st); break;
+    case 12: rc = nks::launch_ks<12>(a, grid, st); break;
+    case 13: rc = nks::launch_ks<13>(a, grid, st); break;
+    default: return PHE_EUNSUPPORTED;
+  }
+  if (rc) return rc;
+  const int bb = kp.q_in + 2 * kp.log2N + 8;
+  const unsigned __int128 Z = (unsigned __int128)1 << bb;
+  const size_t smem = (size_t)nks::NPR * 2 * N * 4;
+  cudaError_t e = cudaFuncSetAttribute(nks::ks_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return phe_set_cuda_error(e);
+  nks::ks_finalize_kernel<<<(unsigned)(T * G), 1024, smem, st>>>(
+      kp, static_cast<const uint2 *>(buf), part, S, T * G, (uint32_t)(Z % nks::P0), (uint32_t)(Z % nks::P1),
+      (uint32_t)(Z % nks::P2), acc);
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
+}  // namespace phe

@@ -1025,6 +1025,56 @@ int phe_matmul_clear_digits_ntt(const phe_params *p, const void *d_tables, const
   return PHE_OK;
 }
 
+// NEXT #1 stage 2 in the NTT domain (ntt_keyswitch.cu)
+static int check_ntt_ks(const phe_params *p, KParams *kp) {
+  int rc = check_pack(p, kp);
+  if (rc) return rc;
+  return phe::ntt_ks_supported(*kp) ? PHE_OK : PHE_EUNSUPPORTED;
+}
+
+size_t phe_ntt_ksk_bytes(const phe_params *p) {
+  KParams kp;
+  if (!p || check_ntt_ks(p, &kp)) return 0;
+  return phe::ntt_ks_bytes(kp);
+}
+
+int phe_ntt_ksk_prepare(const phe_params *p, const void *d_ksk, void *d_nksk, size_t bytes, void *stream) {
+  KParams kp;
+  int rc = check_ntt_ks(p, &kp);
+  if (rc) return rc;
+  if (!d_ksk || !d_nksk) return PHE_EINVAL;
+  if (bytes < phe::ntt_ks_bytes(kp)) return PHE_ENOMEM;
+  return phe::launch_ntt_ks_prepare(kp, static_cast<const uint64_t *>(d_ksk), d_nksk, S(stream));
+}
+
+size_t phe_pack_ntt_ws_bytes(const phe_params *p, int64_t rows, int64_t T) {
+  KParams kp;
+  if (!p || rows < 1 || T < 0 || check_ntt_ks(p, &kp)) return 0;
+  return phe::ntt_ks_ws_bytes(kp, T, (rows + p->N - 1) / p->N);
+}
+
+int phe_pack_ntt(const phe_params *p, const void *d_digits, const uint64_t *d_body, int64_t T, int64_t rows,
+                 const void *d_nksk, void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_ntt_ks(p, &kp);
+  if (rc) return rc;
+  if (rows < 1 || T < 0) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_digits || !d_body || !d_nksk || !d_ws || !d_out_packed) return PHE_EINVAL;
+  if (ws_bytes < phe_pack_ntt_ws_bytes(p, rows, T)) return PHE_ENOMEM;
+  const int64_t G = (rows + p->N - 1) / p->N;
+  // the CRT-recovered sum, then the packing GEMM path's own finish ((0, b) - acc, switch)
+  const size_t partb = phe::ntt_ks_ws_bytes(kp, T, G) - (size_t)T * G * 2 * p->N * 8;
+  void *acc = static_cast<uint8_t *>(d_ws) + partb;
+  rc = phe::launch_ntt_ks(kp, d_nksk, static_cast<const int8_t *>(d_digits), T, rows, d_ws, acc, S(stream));
+  if (rc) return rc;
+  rc = phe::launch_pack_finalize(kp, acc, d_body, T, rows, (int)G, d_out_packed, S(stream));
+  if (rc) return rc;
+  g_last_launches = 3;
+  return PHE_OK;
+}
+
 int phe_matmul_clear_ntt(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
                          int64_t d_in, int64_t row_begin, int64_t row_end, const void *d_operand,
                          int64_t T, int32_t out_bits, void *d_out_mask, void *d_out_body, void *stream) {

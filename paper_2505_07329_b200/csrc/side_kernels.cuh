@@ -58,6 +58,16 @@ int launch_ntt_mask(const KParams &kp, const void *tables, const uint32_t *what,
                     int64_t T, int out_bits, void *out, cudaStream_t st, int64_t digit_rows = 0,
                     int64_t out_rows = 0);
 
+// ntt_keyswitch.cu (NEXT #1 stage 2 in the NTT domain): sum_{l,i} D_{l,i} * KSK_{l,i} mod 2^q_in
+// through three 30-bit primes + CRT, written as the packing GEMM's accumulator.
+size_t ntt_ks_bytes(const KParams &kp);
+bool ntt_ks_supported(const KParams &kp);
+int launch_ntt_ks_prepare(const KParams &kp, const uint64_t *ksk, void *buf, cudaStream_t st);
+int ntt_ks_splits(const KParams &kp, int64_t T, int64_t G);
+size_t ntt_ks_ws_bytes(const KParams &kp, int64_t T, int64_t G);
+int launch_ntt_ks(const KParams &kp, const void *buf, const int8_t *digits, int64_t T, int64_t R, void *ws,
+                  void *acc_out, cudaStream_t st);
+
 // limb_gemm.cu: the tcgen05 int8 limb GEMM (mask = Hankel operand, body = plain operand).
 struct GemmArgs {
   KParams kp;

@@ -1,0 +1,111 @@
+"""GPU parity of stage 2 of the packed primitive in the NTT domain (phe_pack_ntt: Eq. 7 + Eq. 8,
+P:187-191, exchanged into sum_{l,i} D_{l,i}(X) * KSK_{l,i}(X)) against the CPU
+oracle's literal Eq. 7 and against the tensor-core packing GEMM (phe_pack), bit-exactly."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import phe_oracle as O
+from oracle.phe_oracle import Params
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _setup(phe, over, d_out, d_in, T, eta, transpose=False, seed=0):
+    p = phe.params(phe.PRESET_PAPER, noise_eta=eta, **over)
+    W = synth.weights_int8(d_out, d_in, seed=d_out + d_in + seed)
+    cols = d_out if transpose else d_in
+    x = synth.activations_int8(T, cols, seed=T + cols + seed)
+    S = phe.keygen(p, 5)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).to(DEV), 77, 3)
+    w = phe.Weights(p, torch.from_numpy(W).to(DEV), transpose=transpose)
+    opnd = phe.ct_prepare(p, seeds, body)
+    ksk = phe.ksk_gen(p, S, 1234)
+    return p, W, x, S, w, opnd, ksk
+
+
+@pytest.mark.parametrize("over,d_out,d_in,T,eta", [
+    (dict(N=256), 512, 300, 3, 0),          # G = 2 groups, ragged input block
+    (dict(N=256), 300, 256, 2, 21),         # rows not a multiple of 256 (zeroed pad rows), noisy KSK
+    (dict(N=512), 700, 512, 2, 0),          # G = 2, second group ragged (rows beyond R256)
+])
+def test_pack_ntt_bit_exact_vs_oracle(phe, coracle, over, d_out, d_in, T, eta):
+    p, W, x, S, w, opnd, ksk = _setup(phe, over, d_out, d_in, T, eta)
+    dig, bod = phe.matmul_clear_digits(p, w, opnd, T)
+    got_t = phe.pack_ntt(p, dig, bod, phe.NttKeySwitchKey(p, ksk))
+    ref_t = phe.pack(p, dig, bod, phe.KeySwitchKey(p, ksk))
+    torch.cuda.synchronize()
+    assert torch.equal(got_t, ref_t)
+    op = Params(N=p.N, q_in=p.q_in, q_out=p.q_out, beta=p.beta, gamma=p.gamma, eta=eta)
+    So = O.keygen(5, op.N)
+    KA, KB = coracle.ksk_gen(op, So, 1234, eta=eta, nthreads=os.cpu_count())
+    seeds_o = O.block_seeds(77, T, op.L(d_in))
+    E = O.noise(op, 3, T, op.L(d_in))
+    got = got_t.cpu().numpy().astype(np.uint32).astype(np.uint64)
+    for tau in range(T):
+        A, B = O.encrypt(op, So, x[tau], seeds_o[tau], E[tau])
+        m, b = coracle.matmul_clear_literal(op, W, A, B, nthreads=os.cpu_count())
+        PA, PB = coracle.pack(op, m, b, KA, KB, nthreads=os.cpu_count())
+        assert np.array_equal(got[tau, :, 0], O.modswitch(PA, op.q_in, op.q_out))
+        assert np.array_equal(got[tau, :, 1], O.modswitch(PB, op.q_in, op.q_out))
+    wx = (W.astype(np.int64) @ x.astype(np.int64).T).T
+    y = phe.decrypt_packed(p, S, got_t, d_out).cpu().numpy().astype(np.int64)
+    assert np.all(np.abs(y - wx) < 2 ** 15)  # top gamma = 12 of beta = 27 bits
+
+
+@pytest.mark.parametrize("over,d_out,d_in,T,transpose", [
+    (dict(N=1024), 1100, 1024, 3, False),
+    (dict(N=2048), 2048, 2048, 3, False),   # Table 1 ring, q_proj rows
+    (dict(N=2048), 700, 2100, 2, True),     # W^T (backward), ragged
+    (dict(N=4096), 300, 4096, 1, False),
+    (dict(N=8192), 256, 8192, 1, False),
+])
+def test_pack_ntt_identical_to_tensor_core(phe, over, d_out, d_in, T, transpose):
+    """Every log2 N the kernel is instantiated for: phe_pack_ntt == phe_pack word for word (Eq. 7
+    defines the words uniquely; phe_pack is oracle-pinned in test_gpu_pack.py)."""
+    p, W, x, S, w, opnd, ksk = _setup(phe, over, d_out, d_in, T, 0, transpose)
+    dig, bod = phe.matmul_clear_digits(p, w, opnd, T)
+    got = phe.pack_ntt(p, dig, bod, phe.NttKeySwitchKey(p, ksk))
+    ref = phe.pack(p, dig, bod, phe.KeySwitchKey(p, ksk))
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+
+
+@pytest.mark.parametrize("dval,kval", [(-128, 1 << 38), (127, (1 << 38) - 1)])
+def test_pack_ntt_crt_range_adversarial(phe, dval, kval):
+    """Every digit at an extreme and every KSK word at the largest centred magnitude: the exact
+    sums reach 4N * N * 128 * 2^38 in magnitude, the top of the CRT range the launch admits."""
+    p = phe.params(phe.PRESET_PAPER, N=256)
+    N, T, R = p.N, 2, 256
+    dig = torch.full((T, R, 4, N), dval, dtype=torch.int8, device=DEV)
+    bod = torch.zeros((T, R), dtype=torch.int64, device=DEV)
+    ksk = torch.full((2, 4 * N, N), kval, dtype=torch.int64, device=DEV)
+    got = phe.pack_ntt(p, dig, bod, phe.NttKeySwitchKey(p, ksk))
+    ref = phe.pack(p, dig, bod, phe.KeySwitchKey(p, ksk))
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    # closed form: D_{l,i} = d * sum_r X^r and K = k * sum_c X^c for every (l, i), so coefficient
+    # c of the negacyclic product is d k (#{r + s = c} - #{r + s = c + N}) = d k (2c + 2 - N)
+    c = np.arange(N, dtype=np.int64)
+    acc = (4 * N * dval * (2 * c + 2 - N)).astype(object) * ((kval - (1 << 39)) if kval >= 1 << 38 else kval)
+    A = np.array([(-v) % (1 << 39) for v in acc], dtype=np.uint64)
+    exp = O.modswitch(A, 39, 26)
+    assert np.array_equal(got[0, 0, 0].cpu().numpy().astype(np.uint32).astype(np.uint64), exp)
+
+
+def test_pack_ntt_empty_and_errors(phe):
+    p = phe.params(phe.PRESET_PAPER, N=256)
+    ksk = torch.zeros((2, 4 * 256, 256), dtype=torch.int64, device=DEV)
+    nk = phe.NttKeySwitchKey(p, ksk)
+    dig = torch.zeros((0, 256, 4, 256), dtype=torch.int8, device=DEV)
+    bod = torch.zeros((0, 256), dtype=torch.int64, device=DEV)
+    out = phe.pack_ntt(p, dig, bod, nk)
+    assert out.shape == (0, 1, 2, 256)
+    with pytest.raises(phe.PheError):
+        phe.pack_ntt(p, torch.zeros((1, 256, 4, 256), dtype=torch.int8, device=DEV),
+                     torch.zeros((1, 256), dtype=torch.int64, device=DEV), nk,
+                     ws=torch.empty(16, dtype=torch.uint8, device=DEV))
