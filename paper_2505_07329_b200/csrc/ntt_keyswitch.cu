@@ -89,37 +89,41 @@ __host__ __device__ __forceinline__ uint32_t brev_n(uint32_t k, int logN) {
 #endif
 }
 
-// Storage order of the K_hat rows (N words per (prime, row, part)): transform index k = 16 t + 4 v
-// + c (thread t of the hot kernel's last phase) at word 4 (v NT + t) + c, so each of a thread's four
-// 16-byte loads is one contiguous 512-byte warp access.
+// The hot kernel runs N/8 threads per transform with V = 8 values each (3-bit phases).
+constexpr int VB = 3, V = 1 << VB;
+// Storage order of the K_hat rows (N words per (prime, row, part)): transform index k = 8 t + 4 v
+// + c (thread t of the hot kernel's last phase) at word 4 (v NT + t) + c, NT = N/8, so each of a
+// thread's two 16-byte loads per part is one contiguous 512-byte warp access.
 __host__ __device__ __forceinline__ int tpos(int k, int N) {
-  return 4 * (((k >> 2) & 3) * (N / 16) + (k >> 4)) + (k & 3);
+  return 4 * (((k >> 2) & 1) * (N / V) + (k >> VB)) + (k & 3);
 }
-__host__ __device__ constexpr int p1off(int s) { return s == 0 ? 0 : s == 1 ? 8 : s == 2 ? 12 : 14; }
+// last forward phase (stages 2, 1, 0): thread t's m-th twiddle of stage s sits at [P1OFF[s] + m][t]
+__host__ __device__ constexpr int p1off(int s) { return s == 0 ? 0 : s == 1 ? 4 : 6; }
+constexpr int P1N = 7;
 
 // ---------------------------------------------------------------- buffer layout (d_khat)
-// uint2 fwd[3][N], inv[3][N], p1[3][15][N/16]; then (256-byte aligned) uint32 K_hat
+// uint2 fwd[3][N], inv[3][N], p1[3][7][N/8]; then (256-byte aligned) uint32 K_hat
 // [3][4N rows][2 parts][N] in tpos order.  Row = l N + i as in phe_ksk_gen (Eq. 8's K-index).
 __host__ __device__ inline size_t tables_bytes(int N) {
-  return ((size_t)NPR * (2 * N + 15 * (N / 16)) * 8 + 255) / 256 * 256;
+  return ((size_t)NPR * (2 * N + P1N * (N / V)) * 8 + 255) / 256 * 256;
 }
 __host__ __device__ inline size_t khat_bytes(int N) { return (size_t)NPR * KS_LEVELS * N * 2 * (size_t)N * 4; }
 
 __global__ void ks_tables_kernel(int logN, uint32_t psi0, uint32_t psi1, uint32_t psi2, uint2 *__restrict__ tab) {
-  const int N = 1 << logN, NT = N / 16;
+  const int N = 1 << logN, NT = N / V;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int nf = 2 * NPR * N;
-  if (idx >= nf + NPR * 15 * NT) return;
+  if (idx >= nf + NPR * P1N * NT) return;
   int q, k, dir;
   if (idx < nf) {
     dir = idx / (NPR * N); q = (idx / N) % NPR; k = idx % N;
-  } else {  // phase (0,4) of the forward NTT: [P1OFF[s] + m][t] = fwd[(N >> (s+1)) + t 2^(3-s) + m]
+  } else {  // phase (0,3) of the forward NTT: [P1OFF[s] + m][t] = fwd[(N >> (s+1)) + t 2^(2-s) + m]
     const int r = idx - nf;
-    q = r / (15 * NT);
-    const int slot = (r / NT) % 15, t = r % NT;
-    const int s = slot >= 14 ? 3 : slot >= 12 ? 2 : slot >= 8 ? 1 : 0;
+    q = r / (P1N * NT);
+    const int slot = (r / NT) % P1N, t = r % NT;
+    const int s = slot >= 6 ? 2 : slot >= 4 ? 1 : 0;
     dir = 0;
-    k = (N >> (s + 1)) + t * (1 << (3 - s)) + (slot - p1off(s));
+    k = (N >> (s + 1)) + t * (1 << (2 - s)) + (slot - p1off(s));
   }
   const uint32_t p = prime_h(q), psi = q == 0 ? psi0 : q == 1 ? psi1 : psi2;
   const uint32_t e = brev_n((uint32_t)k, logN);
@@ -193,117 +197,134 @@ struct KsArgs {
   const int8_t *digits;    // [T][R256][4][N]
   int64_t T, R256, G;
   int S;                   // K-splits
-  int tiles_per_split;     // 16-row tiles of the 4N (l, i) rows per split
+  int tiles_per_split;     // digit tiles (ks_tile columns each) of the 4N (l, i) rows per split
   uint32_t *part;          // [S][T][G][3][2][N], natural transform index
 };
 
-// Thread/element mapping (as ntt_path.cu): N/16 threads per NTT, 16 values each; phase (S0, B)
-// makes index bits [S0, S0+B) thread-local.
+// Thread/element mapping: N/8 threads per transform, 8 values each; phase (S0, B) makes index
+// bits [S0, S0+B) thread-local.  Forward phases run (3(P-1), .), ..., (3, 3), (0, 3).
 template <int LOGN, int S0, int B>
 __device__ __forceinline__ int eidx(int tid, int e) {
   const int el = e & ((1 << B) - 1), g = e >> B;
-  const int o = tid | (g << (LOGN - 4));
+  const int o = tid | (g << (LOGN - VB));
   return (o & ((1 << S0) - 1)) | (el << S0) | ((o >> S0) << (S0 + B));
 }
-// exchange layout, keyed by the stage the reading phase starts at (tools/ntt_ks_model.py)
-template <int S0R>
-__device__ __forceinline__ int lay(int j) { return S0R == 0 ? j + (j >> 4) : S0R == 4 ? j + 16 * (j >> 8) : j; }
-template <int LOGN>
-__host__ __device__ constexpr int xwords() { return (1 << LOGN) + (1 << LOGN) / 16; }
-template <int LOGN>
-__host__ __device__ constexpr int ks_nt() { return (1 << LOGN) / 16; }
-template <int LOGN>
-__host__ __device__ constexpr int ks_ng() { return 512 / ks_nt<LOGN>() < 16 ? 512 / ks_nt<LOGN>() : 16; }
-// first forward phase = last inverse phase
-template <int LOGN>
-struct FirstPhase {
-  static constexpr int S0 = LOGN > 12 ? 12 : LOGN > 8 ? 8 : 4;
-  static constexpr int B = LOGN > 12 ? 1 : LOGN > 8 ? LOGN - 8 : 4;
+template <int LOGN, int K>
+struct Ph {  // inverse-order phase K: stages [3K, 3K + B)
+  static constexpr int S0 = 3 * K;
+  static constexpr int B = LOGN - 3 * K < 3 ? LOGN - 3 * K : 3;
 };
-constexpr int TILE = 16;  // (l, i) columns per digit tile
+template <int LOGN>
+__host__ __device__ constexpr int ks_nph() { return (LOGN + 2) / 3; }
+// exchange layout, keyed by the stage the reading phase starts at (32-bit words, bank-conflict
+// free for both access patterns of every exchange, log2 N = 8..13; tools/ntt_ks_model.py)
+template <int S0R>
+__device__ __forceinline__ int lay(int j) { return S0R == 0 ? j + (j >> 3) : S0R == 3 ? j + 4 * (j >> 5) : j; }
+template <int LOGN>
+__host__ __device__ constexpr int xwords() { return (1 << LOGN) + (1 << LOGN) / 8; }
+template <int LOGN>
+__host__ __device__ constexpr int ks_nt() { return (1 << LOGN) / V; }
+template <int LOGN>
+__host__ __device__ constexpr int ks_ng() { return 1024 / ks_nt<LOGN>() < 16 ? 1024 / ks_nt<LOGN>() : 16; }
+// digit tile: (l, i) columns per tile = bytes per staged row (8 at N = 8192: smem budget)
+__host__ __device__ constexpr int ks_tile(int logN) { return logN >= 13 ? 8 : 16; }
+template <int LOGN>
+__host__ __device__ constexpr int ks_ntb() { return LOGN >= 12 ? 1 : 2; }  // tile + staging buffer
+template <int LOGN>
+__host__ __device__ constexpr int ks_nxb() { return LOGN >= 13 ? 1 : 2; }  // exchange buffers per group
+template <int LOGN>
+__host__ __device__ constexpr int ks_smem() {
+  return V * ks_nt<LOGN>() * 8                                   // twiddles: tw1 [7][NT] + twl [NT]
+         + ks_ng<LOGN>() * ks_nxb<LOGN>() * xwords<LOGN>() * 4   // exchange buffers
+         + ks_ntb<LOGN>() * (1 << LOGN) * ks_tile(LOGN);         // digit tile (+ staging)
+}
+
+// Barrier over one transform group (named barrier 1 + grp); all-CTA when groups run in lockstep.
+template <int LOGN>
+__device__ __forceinline__ void gsync(int grp) {
+  if constexpr (ks_ng<LOGN>() >= 16) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(ks_nt<LOGN>()) : "memory");
+  }
+}
 
 // Cooley-Tukey stages S0+B-1 .. S0 (half-distance 2^s), values lazily in [0, 4p).
 template <int LOGN, int S0, int B>
-__device__ __forceinline__ void ct_phase(uint32_t (&r)[16], const uint2 *tw1, const uint2 *twl, uint32_t p,
+__device__ __forceinline__ void ct_phase(uint32_t (&r)[V], const uint2 *tw1, const uint2 *twl, uint32_t p,
                                          int tid) {
-  constexpr int N = 1 << LOGN, NT = N / 16;
+  constexpr int N = 1 << LOGN, NT = N / V;
   const int jt = eidx<LOGN, S0, B>(tid, 0);
 #pragma unroll
   for (int s = S0 + B - 1; s >= S0; s--) {
     const int d = 1 << (s - S0);
     const int tb = (N >> (s + 1)) + (jt >> (s + 1));
 #pragma unroll
-    for (int e = 0; e < 16; e++) {
+    for (int e = 0; e < V; e++) {
       if (e & d) continue;
       const uint2 w = S0 == 0 ? tw1[(p1off(s) + (e >> (s + 1))) * NT + tid]
                               : twl[tb + (eidx<LOGN, S0, B>(0, e) >> (s + 1))];
       uint32_t U = r[e];
       U = min(U, U - 2 * p);
-      const uint32_t V = shoup_lazy(r[e | d], w.x, w.y, p);
-      r[e] = U + V;
-      r[e | d] = U - V + 2 * p;
+      const uint32_t W = shoup_lazy(r[e | d], w.x, w.y, p);
+      r[e] = U + W;
+      r[e | d] = U - W + 2 * p;
     }
   }
 }
-template <int LOGN, int S0, int B, int S0R>
-__device__ __forceinline__ void xstore(const uint32_t (&r)[16], uint32_t *xb, int tid) {
-  const int base = lay<S0R>(eidx<LOGN, S0, B>(tid, 0));
-#pragma unroll
-  for (int e = 0; e < 16; e++) xb[base + lay<S0R>(eidx<LOGN, S0, B>(0, e))] = r[e];
-}
-template <int LOGN, int S0, int B>
-__device__ __forceinline__ void xload(uint32_t (&r)[16], const uint32_t *xb, int tid) {
-  const int base = lay<S0>(eidx<LOGN, S0, B>(tid, 0));
-#pragma unroll
-  for (int e = 0; e < 16; e++) r[e] = xb[base + lay<S0>(eidx<LOGN, S0, B>(0, e))];
-}
-// one exchange between phases (S0, B) and (S0N, BN); the buffer is reused, so a barrier on both
-// sides of the store
+// one exchange between phases (S0, B) -> (S0N, BN) through the group's buffer `cur`: NXB = 2
+// buffers alternate globally (buffer b is rewritten two exchanges later, after the barrier of the
+// exchange in between, which every reader of b has passed) -> one barrier per exchange; NXB = 1
+// -> a barrier on both sides of the store.
 template <int LOGN, int S0, int B, int S0N, int BN>
-__device__ __forceinline__ void xchg(uint32_t (&r)[16], uint32_t *xb, int tid) {
-  __syncthreads();
-  xstore<LOGN, S0, B, S0N>(r, xb, tid);
-  __syncthreads();
-  xload<LOGN, S0N, BN>(r, xb, tid);
+__device__ __forceinline__ void xchg(uint32_t (&r)[V], uint32_t *xb, int &cur, int tid, int grp) {
+  uint32_t *x = xb + cur * xwords<LOGN>();
+  if constexpr (ks_nxb<LOGN>() == 1) gsync<LOGN>(grp);
+  else cur ^= 1;
+  const int wb = lay<S0N>(eidx<LOGN, S0, B>(tid, 0));
+#pragma unroll
+  for (int e = 0; e < V; e++) x[wb + lay<S0N>(eidx<LOGN, S0, B>(0, e))] = r[e];
+  gsync<LOGN>(grp);
+  const int rb = lay<S0N>(eidx<LOGN, S0N, BN>(tid, 0));
+#pragma unroll
+  for (int e = 0; e < V; e++) r[e] = x[rb + lay<S0N>(eidx<LOGN, S0N, BN>(0, e))];
 }
-// forward negacyclic NTT (natural in, bit-reversed out: thread t ends with k = 16 t + e)
-template <int LOGN>
-__device__ __forceinline__ void fntt_regs(uint32_t (&r)[16], const uint2 *tw1, const uint2 *twl, uint32_t p,
-                                          uint32_t *xb, int tid) {
-  if constexpr (LOGN == 13) {
-    ct_phase<13, 12, 1>(r, tw1, twl, p, tid);
-    xchg<13, 12, 1, 8, 4>(r, xb, tid);
-    ct_phase<13, 8, 4>(r, tw1, twl, p, tid);
-    xchg<13, 8, 4, 4, 4>(r, xb, tid);
-  } else if constexpr (LOGN >= 9) {
-    ct_phase<LOGN, 8, LOGN - 8>(r, tw1, twl, p, tid);
-    xchg<LOGN, 8, LOGN - 8, 4, 4>(r, xb, tid);
+// forward negacyclic NTT from phase K down to phase 0 (natural in, bit-reversed out: thread t ends
+// with k = 8 t + e)
+template <int LOGN, int K>
+__device__ __forceinline__ void fntt_regs(uint32_t (&r)[V], const uint2 *tw1, const uint2 *twl, uint32_t p,
+                                          uint32_t *xb, int &cur, int tid, int grp) {
+  ct_phase<LOGN, Ph<LOGN, K>::S0, Ph<LOGN, K>::B>(r, tw1, twl, p, tid);
+  if constexpr (K > 0) {
+    xchg<LOGN, Ph<LOGN, K>::S0, Ph<LOGN, K>::B, Ph<LOGN, K - 1>::S0, Ph<LOGN, K - 1>::B>(r, xb, cur, tid, grp);
+    fntt_regs<LOGN, K - 1>(r, tw1, twl, p, xb, cur, tid, grp);
   }
-  ct_phase<LOGN, 4, 4>(r, tw1, twl, p, tid);
-  xchg<LOGN, 4, 4, 0, 4>(r, xb, tid);
-  ct_phase<LOGN, 0, 4>(r, tw1, twl, p, tid);
 }
-template <int LOGN>
-__host__ __device__ constexpr int ks_smem() {
-  return 16 * ks_nt<LOGN>() * 8                  // twiddles: tw1 [15][NT] + twl [NT]
-         + ks_ng<LOGN>() * xwords<LOGN>() * 4    // exchange buffers
-         + (1 << LOGN) * TILE;                   // digit tile [N rows][16 bytes]
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 template <int LOGN>
 __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kernel(KsArgs a) {
   constexpr int N = 1 << LOGN, NT = ks_nt<LOGN>(), NG = ks_ng<LOGN>(), NTH = NG * NT;
-  constexpr int COLS = TILE / NG;             // columns of a tile per group
-  constexpr int FS0 = FirstPhase<LOGN>::S0, FB = FirstPhase<LOGN>::B;
-  constexpr int SWS = LOGN == 8 ? 2 : 3;      // tile swizzle bits (r >> SWS) & 3
+  constexpr int TILE = ks_tile(LOGN), WPR = TILE / 4;  // bytes / 4-byte words per tile row
+  constexpr int COLS = TILE / NG;                     // columns of a tile per group
+  constexpr int KF = ks_nph<LOGN>() - 1;              // first forward phase
+  constexpr int FS0 = Ph<LOGN, KF>::S0, FB = Ph<LOGN, KF>::B;
+  constexpr int SWS = WPR == 4 ? 3 : 4;               // row swizzle: word w at w ^ ((r >> SWS) & (WPR-1))
   static_assert(TILE % NG == 0, "groups divide the tile");
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint2 *tw1 = reinterpret_cast<uint2 *>(smem_raw);
-  uint2 *twl = tw1 + 15 * NT;
+  uint2 *twl = tw1 + P1N * NT;
   uint32_t *xall = reinterpret_cast<uint32_t *>(twl + NT);
-  uint8_t *tile = reinterpret_cast<uint8_t *>(xall + NG * xwords<LOGN>());
+  uint8_t *tile = reinterpret_cast<uint8_t *>(xall + NG * ks_nxb<LOGN>() * xwords<LOGN>());
+  uint8_t *stage = tile + N * TILE;
   const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
-  uint32_t *xb = xall + grp * xwords<LOGN>();
+  uint32_t *xb = xall + grp * ks_nxb<LOGN>() * xwords<LOGN>();
+  int cur = 0;
 
   // blockIdx = (s * T G + tg) * 3 + q: the three primes of one token run side by side (shared
   // digit tiles in L2), and concurrent CTAs sweep the same K_hat rows
@@ -316,51 +337,81 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
 
   {  // twiddles of prime q
     const uint2 *fwd = a.tabs + (int64_t)q * N;
-    const uint2 *p1 = a.tabs + 2 * NPR * N + (int64_t)q * 15 * NT;
-    for (int k = threadIdx.x; k < 15 * NT; k += NTH) tw1[k] = p1[k];
+    const uint2 *p1 = a.tabs + 2 * NPR * N + (int64_t)q * P1N * NT;
+    for (int k = threadIdx.x; k < P1N * NT; k += NTH) tw1[k] = p1[k];
     for (int k = threadIdx.x; k < NT; k += NTH) twl[k] = fwd[k];
   }
-  uint32_t acc[2][16];
+  uint32_t acc[2][V];
 #pragma unroll
-  for (int e = 0; e < 16; e++) acc[0][e] = acc[1][e] = 0;
+  for (int e = 0; e < V; e++) acc[0][e] = acc[1][e] = 0;
 
-  const int jt = eidx<LOGN, FS0, FB>(tid, 0);
-  const int swt = (jt >> SWS) & 3;
+  const int jt = eidx<LOGN, FS0, FB>(tid, 0);  // row bits SWS.. of the first phase come from tid
+  const int swt = (jt >> SWS) & (WPR - 1);
   const int64_t row_base = ((tau * a.R256 + g * N) * KS_LEVELS) * (int64_t)N;  // digits of row gN, plane 0
   const int64_t rmax = a.R256 - g * N;       // rows of this group present in the digit tensor
   const int tile0 = s * a.tiles_per_split;
+  // Digit tile it: N rows of TILE bytes (columns i0.. of plane l), stored swizzled so that column
+  // reads across rows are bank-conflict free.  NTB = 2: 16-byte cp.async of tile it+1 into an
+  // unswizzled staging buffer while tile it is processed, then LDS.128 + 4 STS per row into the
+  // tile; NTB = 1: direct loads (smem budget, N >= 4096).
+  auto tile_src = [&](int it, int r) {
+    const int row0 = (tile0 + it) * TILE;
+    return a.digits + row_base + ((int64_t)r * KS_LEVELS + row0 / N) * N + row0 % N;
+  };
+  auto put_row = [&](int r, const uint32_t *v) {
+    uint32_t *trow = reinterpret_cast<uint32_t *>(tile + r * TILE);
+    const int sw = (r >> SWS) & (WPR - 1);
+#pragma unroll
+    for (int w = 0; w < WPR; w++) trow[w ^ sw] = v[w];
+  };
+  auto stage_tile = [&](int it) {
+    for (int r = threadIdx.x; r < N; r += NTH) {
+      const bool ok = r < rmax;
+      cp_async16(stage + r * TILE, ok ? tile_src(it, r) : a.digits, ok);
+    }
+    cp_async_commit();
+  };
+  if constexpr (ks_ntb<LOGN>() == 2) stage_tile(0);
   for (int it = 0; it < a.tiles_per_split; it++) {
     const int row0 = (tile0 + it) * TILE;    // (l, i) row l N + i of Eq. 8's K-index
-    const int l = row0 / N, i0 = row0 % N;
-    __syncthreads();  // every group is done with the previous tile
-    for (int r = threadIdx.x; r < N; r += NTH) {
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (r < rmax)
-        v = __ldg(reinterpret_cast<const uint4 *>(a.digits + row_base + ((int64_t)r * KS_LEVELS + l) * N + i0));
-      uint32_t *trow = reinterpret_cast<uint32_t *>(tile + r * TILE);
-      const int sw = (r >> SWS) & 3;
-      trow[0 ^ sw] = v.x; trow[1 ^ sw] = v.y; trow[2 ^ sw] = v.z; trow[3 ^ sw] = v.w;
+    if constexpr (ks_ntb<LOGN>() == 2) {
+      cp_async_wait_all();
+      __syncthreads();                       // staging complete; previous tile consumed
+      for (int r = threadIdx.x; r < N; r += NTH) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(stage + r * TILE);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        put_row(r, w);
+      }
+      __syncthreads();                       // tile ready; staging free
+      if (it + 1 < a.tiles_per_split) stage_tile(it + 1);
+    } else {
+      __syncthreads();
+      for (int r = threadIdx.x; r < N; r += NTH) {
+        uint32_t w[WPR];
+        if constexpr (WPR == 4) {
+          const uint4 v = r < rmax ? __ldg(reinterpret_cast<const uint4 *>(tile_src(it, r))) : make_uint4(0u, 0u, 0u, 0u);
+          w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        } else {
+          const uint2 v = r < rmax ? __ldg(reinterpret_cast<const uint2 *>(tile_src(it, r))) : make_uint2(0u, 0u);
+          w[0] = v.x; w[1] = v.y;
+        }
+        put_row(r, w);
+      }
+      __syncthreads();
     }
-    __syncthreads();
 #pragma unroll 1
     for (int cc = 0; cc < COLS; cc++) {
       const int c = grp * COLS + cc;
-      const uint8_t *cb = tile + jt * TILE + (c & 3);
-      const int cx = (c >> 2) ^ swt;
-      uint32_t r[16];
+      const int8_t *cb = reinterpret_cast<const int8_t *>(tile) + jt * TILE + 4 * ((c >> 2) ^ swt) + (c & 3);
+      uint32_t r[V];
 #pragma unroll
-      for (int e = 0; e < 16; e++) {
-        const int je = eidx<LOGN, FS0, FB>(0, e);
-        const int swe = (je >> SWS) & 3;  // 0 for LOGN >= 9 (thread bits carry the swizzle)
-        const int8_t d = reinterpret_cast<const int8_t *>(cb)[je * TILE + 4 * (cx ^ swe)];
-        r[e] = (uint32_t)((int32_t)d + (int32_t)p);
-      }
-      fntt_regs<LOGN>(r, tw1, twl, p, xb, tid);
+      for (int e = 0; e < V; e++) r[e] = (uint32_t)((int32_t)cb[eidx<LOGN, FS0, FB>(0, e) * TILE] + (int32_t)p);
+      fntt_regs<LOGN, KF>(r, tw1, twl, p, xb, cur, tid, grp);
       const uint4 *kr = reinterpret_cast<const uint4 *>(a.khat + (((int64_t)q * KS_LEVELS * N + row0 + c) * 2) * N) + tid;
 #pragma unroll
       for (int pt = 0; pt < 2; pt++) {
 #pragma unroll
-        for (int v = 0; v < 4; v++) {
+        for (int v = 0; v < 2; v++) {
           const uint4 kv = __ldg(kr + pt * (N / 4) + v * NT);
           acc[pt][4 * v + 0] = add_lazy(acc[pt][4 * v + 0], mont_lazy(r[4 * v + 0], kv.x, p, pinv), p);
           acc[pt][4 * v + 1] = add_lazy(acc[pt][4 * v + 1], mont_lazy(r[4 * v + 1], kv.y, p, pinv), p);
@@ -371,7 +422,7 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
     }
   }
   // sum over the NG groups (each covered other columns) in the tile buffer, group by group; store
-  // [..][pt][k], k = 16 tid + e
+  // [..][pt][k], k = 8 tid + e
   uint32_t *red = reinterpret_cast<uint32_t *>(tile);  // 2N words <= N * TILE bytes
   for (int gg = 0; gg < NG; gg++) {
     __syncthreads();
@@ -379,8 +430,8 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
 #pragma unroll
       for (int pt = 0; pt < 2; pt++)
 #pragma unroll
-        for (int e = 0; e < 16; e++) {
-          uint32_t *o = &red[pt * N + 16 * tid + e];
+        for (int e = 0; e < V; e++) {
+          uint32_t *o = &red[pt * N + V * tid + e];
           *o = gg ? add_lazy(*o, acc[pt][e], p) : acc[pt][e];
         }
     }
@@ -477,7 +528,7 @@ int launch_ntt_ks_prepare(const KParams &kp, const uint64_t *ksk, void *buf, cud
 
 // K-splits: enough CTAs for two waves of one CTA per SM; a power of two dividing the 4N/16 tiles
 int ntt_ks_splits(const KParams &kp, int64_t T, int64_t G) {
-  const int64_t tiles = (int64_t)KS_LEVELS * kp.N / nks::TILE;
+  const int64_t tiles = (int64_t)KS_LEVELS * kp.N / nks::ks_tile(kp.log2N);
   int64_t S = 1;
   while (S < tiles && nks::NPR * T * G * S < 2 * 148) S *= 2;
   return (int)S;
@@ -503,7 +554,7 @@ int launch_ntt_ks(const KParams &kp, const void *buf, const int8_t *digits, int6
   a.khat = reinterpret_cast<const uint32_t *>(static_cast<const uint8_t *>(buf) + nks::tables_bytes(N));
   a.digits = digits;
   a.T = T; a.R256 = R256; a.G = G; a.S = S;
-  a.tiles_per_split = (int)((int64_t)KS_LEVELS * N / nks::TILE / S);
+  a.tiles_per_split = (int)((int64_t)KS_LEVELS * N / nks::ks_tile(kp.log2N) / S);
   a.part = part;
   const int64_t grid = (int64_t)nks::NPR * T * G * S;
   int rc;

@@ -2,7 +2,10 @@
 KeySwitch (phe_pack_ntt) on q_proj-shaped digits (Table 1, rows = 2048), CUDA events."""
 import sys
 import torch
+import os
 import paper_2505_07329_b200 as phe
+if os.environ.get("PHE_LIB"):
+    phe.load(os.environ["PHE_LIB"])
 import synth
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 256
