@@ -6,24 +6,25 @@
 // O(N) multiply-adds per (l, i, output coefficient).  Exchanging the sums gives the same value as
 //   sum_{l,i} D_{l,i}(X) * KSK_{l,i}(X),        D_{l,i}(X) = sum_r d_{gN+r,i,l} X^r
 // a sum of 4N negacyclic polynomial products (X^N = -1), computed here EXACTLY in the NTT
-// domain: |sum| <= 4N * N * 2^7 * 2^(q_in-1) (< 2^70 at Table 1), so three 30-bit primes
-// (p0 p1 p2 ~ 2^88.6) and a Garner CRT with an offset Z = 0 mod 2^q_in recover it; the result
-// mod 2^q_in is the accumulator the tensor-core path (pack_gemm_2sm_kernel) writes, and
+// domain.  With the centred KSK words split as K = K_hi 2^SPLIT + K_lo (|K_half| <= 2^19 at
+// Table 1), each half-sum is below 4N * N * 2^7 * 2^19 = 2^50, so two 30-bit primes (p0 p1 ~
+// 2^59.8) and a CRT recover it exactly; sum_hi 2^SPLIT + sum_lo mod 2^q_in is the accumulator
+// the tensor-core path (pack_gemm_2sm_kernel) writes, and
 // pack_finalize_kernel finishes both identically ((0, b) - acc, ModulusSwitch).  Work per
-// (l, i, coefficient): (log2 N)/2 butterflies + 2 pointwise products per prime, O(log N)
+// (l, i, coefficient): (log2 N)/2 butterflies + 4 pointwise products per prime (2 primes), O(log N)
 // instead of O(N).
 //
 // Kernels:
-//   ks_tables_kernel    psi^{+-bitrev(k)} with Shoup companions for the three primes, and the
+//   ks_tables_kernel    psi^{+-bitrev(k)} with Shoup companions for the two primes, and the
 //                       per-thread regrouped table of the register NTT's last phase
-//   ks_khat_kernel      K_hat = NTT(centred KSK row) * N^-1 * 2^32 (Montgomery), thread order
+//   ks_khat_kernel      K_hat = NTT(hi / lo half of the centred KSK row) * N^-1 * 2^32, thread order
 //                       [server, once per key]
 //   ks_ntt_kernel<LOGN> the hot kernel: one CTA per (token, group g, prime, K-split); NG groups
 //                       of N/16 threads each take columns (l, i) of a 16-column digit tile staged
 //                       in shared memory, run the forward NTT of D_{l,i} in registers (16 values
 //                       per thread, exchanges through conflict-free layouts, tools/ntt_ks_model.py)
-//                       and accumulate D_hat o K_hat_A, D_hat o K_hat_B (Montgomery, lazy)
-//   ks_finalize_kernel  sum of the K-split partials, inverse NTTs (3 primes x A/B), Garner CRT,
+//                       and accumulate D_hat o K_hat_{A,B}{hi,lo} (Montgomery, lazy)
+//   ks_finalize_kernel  sum of the K-split partials, inverse NTTs (2 primes x 4 parts), CRT,
 //                       mod 2^q_in -> the uint64 accumulator of pack_finalize_kernel
 #include <cstdint>
 #include <cstdio>
@@ -34,11 +35,16 @@
 namespace phe {
 namespace nks {
 
-constexpr int NPR = 3;
+constexpr int NPR = 2;
 // p = c 2^k + 1 with k >= 21 (negacyclic NTTs up to N = 8192 need 2N | p - 1), p < 2^30 so that
-// lazy values in [0, 4p) fit 32 bits; generator 3 for all three.
-constexpr uint32_t P0 = 998244353u, P1 = 1004535809u, P2 = 469762049u;
-__host__ __device__ constexpr uint32_t prime_h(int q) { return q == 0 ? P0 : q == 1 ? P1 : P2; }
+// lazy values in [0, 4p) fit 32 bits; generator 3 for both.
+constexpr uint32_t P0 = 998244353u, P1 = 1004535809u;
+__host__ __device__ constexpr uint32_t prime_h(int q) { return q == 0 ? P0 : P1; }
+// The KSK words are split K = K_hi 2^SPLIT + K_lo (centred halves, SPLIT = ceil(q_in / 2)) so that
+// each of the four sums (A_hi, A_lo, B_hi, B_lo) stays below p0 p1 / 2: two primes instead of
+// three for the forward transforms of the digit polynomials, the dominant work.
+constexpr int NKP = 4;  // K_hat parts per (prime, row): A_hi, A_lo, B_hi, B_lo
+__host__ __device__ constexpr int ks_split(int q_in) { return (q_in + 1) / 2; }
 
 __host__ __device__ constexpr uint32_t neg_inv32(uint32_t p) {
   uint32_t x = p;
@@ -56,7 +62,7 @@ __host__ __device__ constexpr uint32_t pw(uint64_t b, uint64_t e, uint32_t p) {
   return (uint32_t)r;
 }
 static_assert((uint64_t)4 * P0 < (1ull << 32) && (uint64_t)4 * P1 < (1ull << 32), "lazy range");
-static_assert((P0 - 1) % (1u << 14) == 0 && (P1 - 1) % (1u << 14) == 0 && (P2 - 1) % (1u << 14) == 0,
+static_assert((P0 - 1) % (1u << 14) == 0 && (P1 - 1) % (1u << 14) == 0,
               "2N | p - 1 up to N = 8192");
 
 __device__ __forceinline__ uint32_t mul_shoup(uint32_t x, uint32_t w, uint32_t wq, uint32_t p) {
@@ -107,9 +113,9 @@ constexpr int P1N = 7;
 __host__ __device__ inline size_t tables_bytes(int N) {
   return ((size_t)NPR * (2 * N + P1N * (N / V)) * 8 + 255) / 256 * 256;
 }
-__host__ __device__ inline size_t khat_bytes(int N) { return (size_t)NPR * KS_LEVELS * N * 2 * (size_t)N * 4; }
+__host__ __device__ inline size_t khat_bytes(int N) { return (size_t)NPR * KS_LEVELS * N * NKP * (size_t)N * 4; }
 
-__global__ void ks_tables_kernel(int logN, uint32_t psi0, uint32_t psi1, uint32_t psi2, uint2 *__restrict__ tab) {
+__global__ void ks_tables_kernel(int logN, uint32_t psi0, uint32_t psi1, uint2 *__restrict__ tab) {
   const int N = 1 << logN, NT = N / V;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int nf = 2 * NPR * N;
@@ -125,7 +131,7 @@ __global__ void ks_tables_kernel(int logN, uint32_t psi0, uint32_t psi1, uint32_
     dir = 0;
     k = (N >> (s + 1)) + t * (1 << (2 - s)) + (slot - p1off(s));
   }
-  const uint32_t p = prime_h(q), psi = q == 0 ? psi0 : q == 1 ? psi1 : psi2;
+  const uint32_t p = prime_h(q), psi = q == 0 ? psi0 : psi1;
   const uint32_t e = brev_n((uint32_t)k, logN);
   const uint32_t ex = dir ? (uint32_t)((2 * N - e) % (2 * N)) : e;
   const uint32_t w = pw(psi, ex, p);
@@ -164,28 +170,34 @@ __device__ void intt_smem(uint32_t *x, const uint2 *__restrict__ inv, int logN, 
 
 constexpr int PREP_THREADS = 256;
 
-// K_hat for (prime q, row, part): centred K = KSK - 2^q_in [KSK >= 2^(q_in-1)] (same value mod
-// 2^q_in, half the CRT range), mod p, forward NTT, * N^-1 2^32 (Montgomery, inverse scaling folded).
+// K_hat for (prime q, row, part j): j = 2 * (A/B) + (hi/lo) of the centred KSK word
+// K = KSK - 2^q_in [KSK >= 2^(q_in-1)] = K_hi 2^SPLIT + K_lo, K_lo in [-2^(SPLIT-1), 2^(SPLIT-1));
+// mod p, forward NTT, * N^-1 2^32 (Montgomery, the inverse transform's scaling folded in).
 __global__ void __launch_bounds__(PREP_THREADS)
 ks_khat_kernel(KParams kp, const uint64_t *__restrict__ ksk, const uint2 *__restrict__ tabs,
-               uint32_t c0, uint32_t c1, uint32_t c2, uint32_t *__restrict__ khat) {
+               uint32_t c0, uint32_t c1, uint32_t *__restrict__ khat) {
   extern __shared__ uint32_t xs[];
   const int N = kp.N;
   const int64_t rows = (int64_t)KS_LEVELS * N;
-  const int64_t b = blockIdx.x;  // (q * rows + row) * 2 + part
-  const int part = (int)(b & 1);
-  const int64_t row = (b >> 1) % rows;
-  const int q = (int)((b >> 1) / rows);
+  const int64_t b = blockIdx.x;  // (q * rows + row) * NKP + j
+  const int j = (int)(b % NKP);
+  const int64_t row = (b / NKP) % rows;
+  const int q = (int)(b / NKP / rows);
+  const int part = j >> 1, hi = (j & 1) == 0;
   const uint32_t p = prime_h(q);
   const uint64_t *src = ksk + ((int64_t)part * rows + row) * N;
-  const uint64_t half = 1ull << (kp.q_in - 1);
+  const int sp = ks_split(kp.q_in);
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
     const uint64_t v = src[k] & kp.qmask;
-    xs[k] = v >= half ? (uint32_t)((p - (uint32_t)(((1ull << kp.q_in) - v) % p)) % p) : (uint32_t)(v % p);
+    const int64_t kc = v >= (1ull << (kp.q_in - 1)) ? (int64_t)v - (int64_t)(1ull << kp.q_in) : (int64_t)v;
+    const int64_t lo = ((kc + (1ll << (sp - 1))) & ((1ll << sp) - 1)) - (1ll << (sp - 1));
+    const int64_t h = hi ? (kc - lo) >> sp : lo;
+    const int64_t m = h % (int64_t)p;
+    xs[k] = (uint32_t)(m < 0 ? m + p : m);
   }
   __syncthreads();
   fntt_smem(xs, tabs + (int64_t)q * N, kp.log2N, p);
-  const uint32_t c = q == 0 ? c0 : q == 1 ? c1 : c2;
+  const uint32_t c = q == 0 ? c0 : c1;
   uint32_t *o = khat + b * N;
   for (int k = threadIdx.x; k < N; k += blockDim.x) o[tpos(k, N)] = (uint32_t)((uint64_t)xs[k] * c % p);
 }
@@ -193,12 +205,12 @@ ks_khat_kernel(KParams kp, const uint64_t *__restrict__ ksk, const uint2 *__rest
 // ---------------------------------------------------------------- the hot kernel
 struct KsArgs {
   const uint2 *tabs;       // table section (fwd [3][N] first, p1 after inv)
-  const uint32_t *khat;    // [3][4N][2][N]
+  const uint32_t *khat;    // [2 primes][4N rows][NKP][N]
   const int8_t *digits;    // [T][R256][4][N]
   int64_t T, R256, G;
   int S;                   // K-splits
   int tiles_per_split;     // digit tiles (ks_tile columns each) of the 4N (l, i) rows per split
-  uint32_t *part;          // [S][T][G][3][2][N], natural transform index
+  uint32_t *part;          // [S][T][G][2 primes][NKP][N], natural transform index
 };
 
 // Thread/element mapping: N/8 threads per transform, 8 values each; phase (S0, B) makes index
@@ -326,7 +338,7 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
   uint32_t *xb = xall + grp * ks_nxb<LOGN>() * xwords<LOGN>();
   int cur = 0;
 
-  // blockIdx = (s * T G + tg) * 3 + q: the three primes of one token run side by side (shared
+  // blockIdx = (s * T G + tg) * 2 + q: the two primes of one token run side by side (shared
   // digit tiles in L2), and concurrent CTAs sweep the same K_hat rows
   const int64_t b = blockIdx.x;
   const int q = (int)(b % NPR);
@@ -341,9 +353,11 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
     for (int k = threadIdx.x; k < P1N * NT; k += NTH) tw1[k] = p1[k];
     for (int k = threadIdx.x; k < NT; k += NTH) twl[k] = fwd[k];
   }
-  uint32_t acc[2][V];
+  uint32_t acc[NKP][V];
 #pragma unroll
-  for (int e = 0; e < V; e++) acc[0][e] = acc[1][e] = 0;
+  for (int j = 0; j < NKP; j++)
+#pragma unroll
+    for (int e = 0; e < V; e++) acc[j][e] = 0;
 
   const int jt = eidx<LOGN, FS0, FB>(tid, 0);  // row bits SWS.. of the first phase come from tid
   const int swt = (jt >> SWS) & (WPR - 1);
@@ -407,9 +421,9 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
 #pragma unroll
       for (int e = 0; e < V; e++) r[e] = (uint32_t)((int32_t)cb[eidx<LOGN, FS0, FB>(0, e) * TILE] + (int32_t)p);
       fntt_regs<LOGN, KF>(r, tw1, twl, p, xb, cur, tid, grp);
-      const uint4 *kr = reinterpret_cast<const uint4 *>(a.khat + (((int64_t)q * KS_LEVELS * N + row0 + c) * 2) * N) + tid;
+      const uint4 *kr = reinterpret_cast<const uint4 *>(a.khat + (((int64_t)q * KS_LEVELS * N + row0 + c) * NKP) * N) + tid;
 #pragma unroll
-      for (int pt = 0; pt < 2; pt++) {
+      for (int pt = 0; pt < NKP; pt++) {
 #pragma unroll
         for (int v = 0; v < 2; v++) {
           const uint4 kv = __ldg(kr + pt * (N / 4) + v * NT);
@@ -422,58 +436,70 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
     }
   }
   // sum over the NG groups (each covered other columns) in the tile buffer, group by group; store
-  // [..][pt][k], k = 8 tid + e
-  uint32_t *red = reinterpret_cast<uint32_t *>(tile);  // 2N words <= N * TILE bytes
-  for (int gg = 0; gg < NG; gg++) {
-    __syncthreads();
-    if (grp == gg) {
+  // [..][part][k], k = 8 tid + e
+  uint32_t *out = a.part + (((s * a.T + tau) * a.G + g) * NPR + q) * NKP * (int64_t)N;
+  if constexpr (NG == 1) {
 #pragma unroll
-      for (int pt = 0; pt < 2; pt++)
+    for (int pt = 0; pt < NKP; pt++)
 #pragma unroll
-        for (int e = 0; e < V; e++) {
-          uint32_t *o = &red[pt * N + V * tid + e];
-          *o = gg ? add_lazy(*o, acc[pt][e], p) : acc[pt][e];
-        }
+      for (int e = 0; e < V; e++) out[pt * N + V * tid + e] = min(acc[pt][e], acc[pt][e] - p);
+  } else {
+    static_assert(NKP * (1 << LOGN) * 4 <= (1 << LOGN) * TILE, "reduction fits the tile buffer");
+    uint32_t *red = reinterpret_cast<uint32_t *>(tile);
+    for (int gg = 0; gg < NG; gg++) {
+      __syncthreads();
+      if (grp == gg) {
+#pragma unroll
+        for (int pt = 0; pt < NKP; pt++)
+#pragma unroll
+          for (int e = 0; e < V; e++) {
+            uint32_t *o = &red[pt * N + V * tid + e];
+            *o = gg ? add_lazy(*o, acc[pt][e], p) : acc[pt][e];
+          }
+      }
     }
-  }
-  __syncthreads();
-  uint32_t *out = a.part + (((s * a.T + tau) * a.G + g) * NPR + q) * 2 * (int64_t)N;
-  for (int k = threadIdx.x; k < 2 * N; k += NTH) {
-    const uint32_t v = red[k];
-    out[k] = min(v, v - p);
+    __syncthreads();
+    for (int k = threadIdx.x; k < NKP * N; k += NTH) {
+      const uint32_t v = red[k];
+      out[k] = min(v, v - p);
+    }
   }
 }
 
-// Per (token, group): sum the K-split partials, inverse NTTs, CRT, mod 2^q_in.
+// Per (token, group) and part (A, B): sum the K-split partials, inverse NTTs (2 primes x hi/lo),
+// CRT of each half (v = sum + Z in [0, p0 p1), Z = 2^bb >= max |sum|), acc = sum_hi 2^SPLIT + sum_lo.
 __global__ void __launch_bounds__(1024)
 ks_finalize_kernel(KParams kp, const uint2 *__restrict__ tabs, const uint32_t *__restrict__ part, int S,
-                   int64_t TG, uint32_t z0, uint32_t z1, uint32_t z2, unsigned long long *__restrict__ acc) {
-  extern __shared__ uint32_t xs[];  // [3][2][N]
+                   int64_t TG, int bb, unsigned long long *__restrict__ acc) {
+  extern __shared__ uint32_t xs[];  // [2 primes][2 halves][N]
   const int N = kp.N;
   const int64_t tg = blockIdx.x;
-  for (int k = threadIdx.x; k < NPR * 2 * N; k += blockDim.x) {
-    const int q = k / (2 * N);
-    uint64_t v = 0;
-    for (int s = 0; s < S; s++) v += part[((s * TG + tg) * NPR) * 2 * (int64_t)N + k];
-    xs[k] = (uint32_t)(v % prime_h(q));
-  }
-  __syncthreads();
-  for (int q = 0; q < NPR; q++)
-    for (int pt = 0; pt < 2; pt++) intt_smem(xs + (q * 2 + pt) * N, tabs + (int64_t)(NPR + q) * N, kp.log2N, prime_h(q));
-  // Garner: v = x0 + p0 h1 + p0 p1 h2 = sum + Z in [0, p0 p1 p2); Z = 0 mod 2^q_in
-  constexpr uint32_t I01 = pw(P0, P1 - 2, P1);                           // p0^-1 mod p1
-  constexpr uint32_t I012 = pw((uint64_t)P0 * P1 % P2, P2 - 2, P2);      // (p0 p1)^-1 mod p2
-  constexpr uint64_t P01 = (uint64_t)P0 * P1;
-  for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) {
-    const int pt = k / N, c = k % N;
-    const uint64_t r0 = (xs[(0 * 2 + pt) * N + c] + (uint64_t)z0) % P0;
-    const uint64_t r1 = (xs[(1 * 2 + pt) * N + c] + (uint64_t)z1) % P1;
-    const uint64_t r2 = (xs[(2 * 2 + pt) * N + c] + (uint64_t)z2) % P2;
-    const uint64_t h1 = (r1 + P1 - r0 % P1) % P1 * I01 % P1;
-    const uint64_t x01 = r0 + (uint64_t)P0 * h1;                         // < p0 p1 < 2^60
-    const uint64_t h2 = (r2 + P2 - x01 % P2) % P2 * I012 % P2;
-    const uint64_t v = x01 + P01 * h2;                                   // mod 2^64
-    acc[(tg * 2 + pt) * N + c] = v & kp.qmask;
+  constexpr uint32_t I01 = pw(P0, P1 - 2, P1);  // p0^-1 mod p1
+  const uint64_t Z = 1ull << bb;
+  const uint32_t z0 = (uint32_t)(Z % P0), z1 = (uint32_t)(Z % P1);
+  const int sp = ks_split(kp.q_in);
+  for (int pt = 0; pt < 2; pt++) {
+    for (int k = threadIdx.x; k < NPR * 2 * N; k += blockDim.x) {
+      const int q = k / (2 * N), h = (k / N) & 1, c = k % N;
+      uint64_t v = 0;
+      for (int s = 0; s < S; s++) v += part[(((s * TG + tg) * NPR + q) * NKP + 2 * pt + h) * (int64_t)N + c];
+      xs[k] = (uint32_t)(v % prime_h(q));
+    }
+    __syncthreads();
+    for (int q = 0; q < NPR; q++)
+      for (int h = 0; h < 2; h++) intt_smem(xs + (q * 2 + h) * N, tabs + (int64_t)(NPR + q) * N, kp.log2N, prime_h(q));
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+      int64_t sum[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const uint64_t r0 = (xs[(0 * 2 + h) * N + c] + (uint64_t)z0) % P0;
+        const uint64_t r1 = (xs[(1 * 2 + h) * N + c] + (uint64_t)z1) % P1;
+        const uint64_t h1 = (r1 + P1 - r0 % P1) % P1 * I01 % P1;
+        sum[h] = (int64_t)(r0 + (uint64_t)P0 * h1 - Z);  // the exact sum
+      }
+      acc[(tg * 2 + pt) * N + c] = ((uint64_t)sum[0] * (1ull << sp) + (uint64_t)sum[1]) & kp.qmask;
+    }
+    __syncthreads();
   }
 }
 
@@ -497,21 +523,24 @@ static uint32_t ks_ninv_mont(uint32_t p, int N) {  // N^-1 2^32 mod p
 
 size_t ntt_ks_bytes(const KParams &kp) { return nks::tables_bytes(kp.N) + nks::khat_bytes(kp.N); }
 
-// CRT range: |sum| <= 4N * N * 2^7 * 2^(q_in-1) = 2^(q_in + 2 log2 N + 8) =: B; Z = B (a multiple
-// of 2^q_in) puts sum + Z in [0, 2B], unique below p0 p1 p2 iff 2B < p0 p1 p2.
+// CRT range per part: |K_half| <= 2^hb with hb = max(SPLIT - 1, q_in - SPLIT), so |sum| <=
+// 4N * N * 2^7 * 2^hb = 2^(2 log2 N + 9 + hb) =: 2^bb; Z = 2^bb puts sum + Z in [0, 2^(bb+1)],
+// unique below p0 p1 iff 2^(bb+1) < p0 p1 (Table 1: bb = 50 at N = 2048).
+static int ks_bb(const KParams &kp) {
+  const int sp = nks::ks_split(kp.q_in);
+  const int hb = sp - 1 > kp.q_in - sp ? sp - 1 : kp.q_in - sp;
+  return 2 * kp.log2N + 9 + hb;
+}
 bool ntt_ks_supported(const KParams &kp) {
-  if (kp.log2N < 8 || kp.log2N > 13 || kp.q_in < KS_BITS) return false;
-  const int bb = kp.q_in + 2 * kp.log2N + 8;
-  const long double M = (long double)nks::P0 * nks::P1 * nks::P2;
-  return bb + 1 < 88 && (long double)2 * ((unsigned __int128)1 << bb) < M;
+  if (kp.log2N < 8 || kp.log2N > 13 || kp.q_in < KS_BITS || kp.q_in > 63) return false;
+  return (long double)2 * (long double)(1ull << ks_bb(kp)) < (long double)nks::P0 * nks::P1;
 }
 
 int launch_ntt_ks_prepare(const KParams &kp, const uint64_t *ksk, void *buf, cudaStream_t st) {
-  const int N = kp.N, NT = N / 16;
+  const int N = kp.N, NT = N / nks::V;
   uint2 *tabs = static_cast<uint2 *>(buf);
-  const int ntab = 2 * nks::NPR * N + nks::NPR * 15 * NT;
-  nks::ks_tables_kernel<<<(ntab + 255) / 256, 256, 0, st>>>(kp.log2N, ks_psi(nks::P0, N), ks_psi(nks::P1, N),
-                                                           ks_psi(nks::P2, N), tabs);
+  const int ntab = 2 * nks::NPR * N + nks::NPR * nks::P1N * NT;
+  nks::ks_tables_kernel<<<(ntab + 255) / 256, 256, 0, st>>>(kp.log2N, ks_psi(nks::P0, N), ks_psi(nks::P1, N), tabs);
   PHE_CUDA_CHECK_LAUNCH();
   uint32_t *khat = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(buf) + nks::tables_bytes(N));
   const size_t smem = (size_t)N * 4;
@@ -519,9 +548,9 @@ int launch_ntt_ks_prepare(const KParams &kp, const uint64_t *ksk, void *buf, cud
     cudaError_t e = cudaFuncSetAttribute(nks::ks_khat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return phe_set_cuda_error(e);
   }
-  const int64_t blocks = (int64_t)nks::NPR * KS_LEVELS * N * 2;
+  const int64_t blocks = (int64_t)nks::NPR * KS_LEVELS * N * nks::NKP;
   nks::ks_khat_kernel<<<(unsigned)blocks, nks::PREP_THREADS, smem, st>>>(
-      kp, ksk, tabs, ks_ninv_mont(nks::P0, N), ks_ninv_mont(nks::P1, N), ks_ninv_mont(nks::P2, N), khat);
+      kp, ksk, tabs, ks_ninv_mont(nks::P0, N), ks_ninv_mont(nks::P1, N), khat);
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
 }
@@ -534,7 +563,7 @@ int ntt_ks_splits(const KParams &kp, int64_t T, int64_t G) {
   return (int)S;
 }
 size_t ntt_ks_ws_bytes(const KParams &kp, int64_t T, int64_t G) {
-  const size_t partb = (size_t)ntt_ks_splits(kp, T, G) * T * G * nks::NPR * 2 * kp.N * 4;
+  const size_t partb = (size_t)ntt_ks_splits(kp, T, G) * T * G * nks::NPR * nks::NKP * kp.N * 4;
   return (partb + 255) / 256 * 256 + (size_t)T * G * 2 * kp.N * 8;
 }
 
@@ -548,7 +577,7 @@ int launch_ntt_ks(const KParams &kp, const void *buf, const int8_t *digits, int6
   uint32_t *part = static_cast<uint32_t *>(ws);
   unsigned long long *acc = acc_out ? static_cast<unsigned long long *>(acc_out)
       : reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(ws) +
-          ((size_t)S * T * G * nks::NPR * 2 * N * 4 + 255) / 256 * 256);
+          ((size_t)S * T * G * nks::NPR * nks::NKP * N * 4 + 255) / 256 * 256);
   nks::KsArgs a{};
   a.tabs = static_cast<const uint2 *>(buf);
   a.khat = reinterpret_cast<const uint32_t *>(static_cast<const uint8_t *>(buf) + nks::tables_bytes(N));
@@ -568,14 +597,11 @@ int launch_ntt_ks(const KParams &kp, const void *buf, const int8_t *digits, int6
     default: return PHE_EUNSUPPORTED;
   }
   if (rc) return rc;
-  const int bb = kp.q_in + 2 * kp.log2N + 8;
-  const unsigned __int128 Z = (unsigned __int128)1 << bb;
   const size_t smem = (size_t)nks::NPR * 2 * N * 4;
   cudaError_t e = cudaFuncSetAttribute(nks::ks_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return phe_set_cuda_error(e);
-  nks::ks_finalize_kernel<<<(unsigned)(T * G), 1024, smem, st>>>(
-      kp, static_cast<const uint2 *>(buf), part, S, T * G, (uint32_t)(Z % nks::P0), (uint32_t)(Z % nks::P1),
-      (uint32_t)(Z % nks::P2), acc);
+  nks::ks_finalize_kernel<<<(unsigned)(T * G), 1024, smem, st>>>(kp, static_cast<const uint2 *>(buf), part, S,
+                                                                   T * G, ks_bb(kp), acc);
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
 }
