@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["q_proj", "ffn", "stack", "q_proj_packed", "stack_packed"],
                     default="q_proj")
+    ap.add_argument("--pack", choices=["tc", "ntt"], default="ntt",
+                    help="packed workloads, stage 2 (KeySwitch Eq. 8 + rotate-sum Eq. 7): tc = int8 packing GEMM "
+                         "on tcgen05, ntt = sum_{l,i} D_{l,i} * KSK_{l,i} in the NTT domain (ntt_keyswitch.cu)")
     ap.add_argument("--contraction", choices=["tc", "ntt", "hybrid"], default="tc",
                     help="mask contraction a5: tc = int8 limb GEMM on tcgen05 (north_star), ntt = NTT domain "
                          "(NEXT #4, CUDA cores), hybrid = ntt for multi-block (L >= 2) linears, tc otherwise")
@@ -193,7 +196,9 @@ def run_ours(args):
     S = phe.keygen(p, synth.MASTER_SEED + 17)
     packed = args.workload.endswith("_packed")
     if packed:  # NEXT #1: KeySwitch key (client keygen, server registration), untimed setup
-        K = phe.KeySwitchKey(p, phe.ksk_gen(p, S, synth.MASTER_SEED + 23))
+        ksk = phe.ksk_gen(p, S, synth.MASTER_SEED + 23)
+        K = phe.KeySwitchKey(p, ksk) if args.pack == "tc" else phe.NttKeySwitchKey(p, ksk)
+        del ksk
     # input ciphertexts: one per distinct (shape, role) -- layers reuse the resident synthetic
     # ciphertexts of the same shape, but every call still expands (ct_prepare) and contracts its own
     inputs = {}
@@ -222,7 +227,8 @@ def run_ours(args):
         Gm = (max_rows + p.N - 1) // p.N
         dig_flat = torch.empty(chunk * r256m * phe.KS_LEVELS * p.N, dtype=torch.int8, device=dev)
         bod_flat = torch.empty(chunk * max_rows, dtype=torch.int64, device=dev)
-        acc_buf = torch.empty(max(phe.load().phe_pack_acc_bytes(__import__("ctypes").byref(p), w.rows, chunk)
+        acc_fn = phe.load().phe_pack_acc_bytes if args.pack == "tc" else phe.load().phe_pack_ntt_ws_bytes
+        acc_buf = torch.empty(max(acc_fn(__import__("ctypes").byref(p), w.rows, chunk)
                                   for _, w, _ in regs), dtype=torch.uint8, device=dev)
         pk_flat = torch.empty(chunk * Gm * 2 * p.N, dtype=torch.int32, device=dev)
         out_mask = torch.empty(1, dtype=torch.int32, device=dev)  # unused: no LWE-form outputs
@@ -267,7 +273,11 @@ def run_ours(args):
                         phe.matmul_clear_digits(p, w, operand, n, digits=dig, body=bod)
                     launches[0] += phe.last_launch_count()
                     e[2].record(stream)
-                    phe.pack(p, dig, bod, K, out=pk_flat[: n * G * 2 * p.N].view(n, G, 2, p.N), acc=acc_buf)
+                    pko = pk_flat[: n * G * 2 * p.N].view(n, G, 2, p.N)
+                    if args.pack == "tc":
+                        phe.pack(p, dig, bod, K, out=pko, acc=acc_buf)
+                    else:
+                        phe.pack_ntt(p, dig, bod, K, out=pko, ws=acc_buf)
                     launches[0] += phe.last_launch_count()
                     e[3].record(stream)
                     evs.append((name, e))
@@ -396,17 +406,30 @@ def run_ours(args):
             traffic = None
     total_ops = sum(alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "mask") +
                     alg_int8_ops(p, rr[n_][1] - rr[n_][0], w.cols, T, "body") for n_, w, _ in regs) + pack_ops
-    if ntt_ms > mask_ms:  # NTT kernel dominates: ALU (integer-multiply pipe) roofline
+    smax = (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak_imad = 148 * 4 * 16 * smax * 1e6 / 1e12  # T IMAD/s: 148 SMs x 4 SMSPs x 16 lanes/clk
+    imad_src = ("IMAD issue rate from B300_MICROARCH.md (fma pipe, rt_SMSP = 2 -> 16 lanes/clk/SMSP) x 148 SMs "
+                "x sm_max clock (DESIGN.md §6)")
+    if packed and args.pack == "ntt":  # stage 2 in the NTT domain dominates: integer-multiply roofline
+        lg = p.N.bit_length() - 1
+        per_col = 1.5 * p.N * lg + 12 * p.N  # forward NTT (3 per Shoup product) + 4 Montgomery products
+        imad = sum(T * ((w.rows + p.N - 1) // p.N) * 2 * phe.KS_LEVELS * p.N * per_col for _, w, _ in regs)
+        ach = imad / (mask_ms / 1e3) / 1e12
+        roofline = {"bound": "alu", "achieved": round(ach, 3), "peak": round(peak_imad, 3), "unit": "T IMAD/s",
+                    "frac": round(ach / peak_imad, 4), "traffic": None,
+                    "kernel": "ks_ntt_kernel<11> + ks_finalize_kernel + pack_finalize_kernel (NTT-domain "
+                              "KeySwitch packing, Eq. 7/8)",
+                    "ops": "algorithmic 32-bit multiplies: per (l, i) row, prime and packed ciphertext "
+                           "1.5 N log2 N (forward NTT) + 12 N (4 Montgomery products); 4N rows x 2 primes",
+                    "peak_source": imad_src}
+    elif ntt_ms > mask_ms:  # NTT kernel dominates: ALU (integer-multiply pipe) roofline
         imad = sum(alg_imad_ops(p, rr[n_][1] - rr[n_][0], w.cols, T) for n_, w, _ in regs if is_ntt[n_])
-        smax = (clocks or {}).get("sm_max_mhz") or 1965.0
-        peak_imad = 148 * 4 * 16 * smax * 1e6 / 1e12  # T IMAD/s: 148 SMs x 4 SMSPs x 16 lanes/clk
         ach = imad / (ntt_ms / 1e3) / 1e12
         roofline = {"bound": "alu", "achieved": round(ach, 3), "peak": round(peak_imad, 3), "unit": "T IMAD/s",
                     "frac": round(ach / peak_imad, 4), "traffic": None,
                     "kernel": "ntt_mask_kernel<11,SW,1,1> (NTT-domain mask contraction, NEXT #4)",
                     "ops": "algorithmic 32-bit multiplies: (2*(3*log2(N)/2 + 3L) + 4) per output coefficient",
-                    "peak_source": "IMAD issue rate from B300_MICROARCH.md (fma pipe, rt_SMSP = 2 -> 16 lanes/clk"
-                                   "/SMSP) x 148 SMs x sm_max clock (DESIGN.md §6)"}
+                    "peak_source": imad_src}
     else:
         roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
                     "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -427,11 +450,12 @@ def run_ours(args):
         hi = phe.wire_serialize_inputs(p, seeds, body).cpu().pin_memory()
         G0 = (w.rows + p.N - 1) // p.N
         ho = torch.empty((T, G0, phe.wire_output_bytes(p)), dtype=torch.uint8, pin_memory=True)
-        phe.server_wire_host(p, w, K, hi, ho, chunk_tokens=255)
+        swh = phe.server_wire_host if args.pack == "tc" else phe.server_wire_host_ntt
+        swh(p, w, K, hi, ho, chunk_tokens=255)
         wall = []
         for _ in range(max(2, min(args.steps, 3))):
             t0 = time.perf_counter()
-            phe.server_wire_host(p, w, K, hi, ho, chunk_tokens=255)
+            swh(p, w, K, hi, ho, chunk_tokens=255)
             wall.append(time.perf_counter() - t0)
         e2e_s = statistics.mean(wall)
         te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -440,7 +464,8 @@ def run_ours(args):
         e2e = {"value": round(world * T / float(te.item()), 2), "unit": "tokens/s",
                "h2d_bytes_per_step": int(hi.numel()), "d2h_bytes_per_step": int(ho.numel()),
                "ms_per_step": round(float(te.item()) * 1e3, 2),
-               "api": "phe_server_wire_host (wire-format bytes in/out, pinned host buffers, 255-token chunks)"}
+               "api": ("phe_server_wire_host" if args.pack == "tc" else "phe_server_wire_host_ntt") +
+                      " (wire-format bytes in/out, pinned host buffers, 255-token chunks)"}
     if (not args.no_e2e and not args.profile and args.workload == "q_proj" and not rows_mode
             and args.contraction == "tc"):
         name, w, _ = regs[0]
@@ -516,7 +541,8 @@ def run_ours(args):
             "clocks": clocks,
             "breakdown_ms": ({"ct_prepare": round(statistics.mean(parts_ms["ct_prepare"]), 3),
                               "lwe_digits_gemms": round(statistics.mean(parts_ms["body_gemm"]), 3),
-                              "pack_gemm_finalize": round(statistics.mean(parts_ms["mask_gemm"]), 3)} if packed else
+                              ("pack_gemm_finalize" if args.pack == "tc" else "pack_ntt_finalize"):
+                                  round(statistics.mean(parts_ms["mask_gemm"]), 3)} if packed else
                              {k: round(statistics.mean(v), 3) for k, v in parts_ms.items()}),
         }
         if len(regs) > 1:
@@ -541,8 +567,12 @@ def config_dict(args, world, T, rows_mode=False):
     if args.contraction != "tc":
         wl += {"ntt": "; mask contraction in the NTT domain (NEXT #4, CUDA cores)",
                "hybrid": "; NTT-domain mask contraction for L >= 2 linears (NEXT #4), tcgen05 otherwise"}[args.contraction]
+    if args.workload.endswith("_packed"):
+        wl += {"tc": "; packing stage (Eq. 8 MatMul + rotate-sum) on tcgen05",
+               "ntt": "; packing stage as sum_{l,i} D_{l,i} * KSK_{l,i} in the NTT domain"}[args.pack]
     B, C = (1, T) if args.workload == "stack_packed" else (8, T // 8)
-    return {"workload": wl, "contraction": args.contraction, "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": B, "C": C, "N": 2048, "q_in": 39, "q_out": 26,
+    return {"workload": wl, "contraction": args.contraction,
+            **({"pack": args.pack} if args.workload.endswith("_packed") else {}), "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": B, "C": C, "N": 2048, "q_in": 39, "q_out": 26,
             "beta": 27,
             "parallelism": (f"row-sharded x{world}" if rows_mode else f"token-sharded x{world}") if world > 1
             else "single GPU",

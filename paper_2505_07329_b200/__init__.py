@@ -39,6 +39,7 @@ EXPORTS = [
     "phe_ntt_weights_bytes", "phe_ntt_weights_prepare", "phe_ntt_operand_bytes", "phe_ntt_ct_prepare",
     "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T", "phe_matmul_clear_ct", "phe_encrypt_pack_ntt",
     "phe_ntt_ksk_bytes", "phe_ntt_ksk_prepare", "phe_pack_ntt_ws_bytes", "phe_pack_ntt",
+    "phe_packed_ntt_ws_bytes", "phe_matmul_clear_packed_ntt", "phe_server_wire_host_ntt",
     "phe_wire_lwe_bytes", "phe_wire_serialize_lwe", "phe_wire_deserialize_lwe", "phe_server_matvec_wire_host",
     "phe_matmul_clear_digits_ntt", "phe_matmul_clear_into", "phe_matmul_clear_ntt_into",
 ]
@@ -149,6 +150,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_ntt_ksk_prepare": ([_P, _vp, _vp, _sz, _vp], ctypes.c_int),
         "phe_pack_ntt_ws_bytes": ([_P, _i64, _i64], _sz),
         "phe_pack_ntt": ([_P, _vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
+        "phe_packed_ntt_ws_bytes": ([_P, _i64, _i64], _sz),
+        "phe_matmul_clear_packed_ntt": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp, _vp, _sz, _vp, _vp],
+                                        ctypes.c_int),
+        "phe_server_wire_host_ntt": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp],
+                                     ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -531,6 +537,32 @@ def server_wire_host(p: Params, w: Weights, ksk: KeySwitchKey, h_wire_in: torch.
     _check(load().phe_server_wire_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
                                        _ptr(ksk.buf), _ptr(h_wire_in), h_wire_in.shape[0], chunk_tokens,
                                        _ptr(h_wire_out), _stream()), "phe_server_wire_host")
+
+
+def matmul_clear_packed_ntt(p: Params, w: Weights, operand: torch.Tensor, T: int, nksk: "NttKeySwitchKey",
+                            out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """matmul_clear_packed with stage 2 (Eq. 7/8) in the NTT domain: same output."""
+    G = (w.rows + p.N - 1) // p.N
+    if out is None:
+        out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=operand.device)
+    nbytes = load().phe_packed_ntt_ws_bytes(ctypes.byref(p), w.rows, T)
+    if ws is None:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=operand.device)
+    _check(load().phe_matmul_clear_packed_ntt(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
+                                              _ptr(operand), T, _ptr(nksk.buf), _ptr(ws), ws.numel(), _ptr(out),
+                                              _stream()), "phe_matmul_clear_packed_ntt")
+    return out
+
+
+def server_wire_host_ntt(p: Params, w: Weights, nksk: "NttKeySwitchKey", h_wire_in: torch.Tensor,
+                         h_wire_out: torch.Tensor, chunk_tokens: int = 255) -> None:
+    """server_wire_host with the packing stage in the NTT domain (phe_server_wire_host_ntt)."""
+    for t, n in [(h_wire_in, "h_wire_in"), (h_wire_out, "h_wire_out")]:
+        if t.is_cuda or not t.is_contiguous():
+            raise PheError(f"{n} must be a contiguous host tensor")
+    _check(load().phe_server_wire_host_ntt(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
+                                           _ptr(nksk.buf), _ptr(h_wire_in), h_wire_in.shape[0], chunk_tokens,
+                                           _ptr(h_wire_out), _stream()), "phe_server_wire_host_ntt")
 
 
 # ------------------------------------------------------------------ NEXT #4: NTT-domain contraction

@@ -649,12 +649,13 @@ int phe_wire_deserialize_packed(const phe_params *p, const uint8_t *d_wire, int6
 
 // The server step as the network sees it (Fig. 1): wire-format input blocks in (9992 B each at
 // Table 1), wire-format packed ciphertexts out (13312 B each).  Chunked, two streams.
-int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
-                         const void *d_kprep, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
-                         uint8_t *h_wire_out, void *stream) {
+static int server_wire_host_impl(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                                 int transpose, const void *d_kprep, const uint8_t *h_wire_in, int64_t T,
+                                 int64_t chunk_tokens, uint8_t *h_wire_out, void *stream, bool ntt_pack) {
   KParams kp;
   int rc = check_pack(p, &kp);
   if (!rc) rc = check_wire(p, &kp);
+  if (!rc && ntt_pack && !phe::ntt_ks_supported(kp)) rc = PHE_EUNSUPPORTED;
   if (rc) return rc;
   const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
   if (rows < 1 || cols < 1 || T < 0 || chunk_tokens < 1) return PHE_EINVAL;
@@ -666,7 +667,8 @@ int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out
   const size_t b_win = round_up(C * L * bin, 256), b_seeds = round_up(C * L * 8, 256);
   const size_t b_body = round_up(C * L * N * 8, 256);
   const size_t b_op = round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256);
-  const size_t b_ws = round_up((int64_t)phe_packed_ws_bytes(p, rows, C), 256);
+  const size_t b_ws = round_up((int64_t)(ntt_pack ? phe_packed_ntt_ws_bytes(p, rows, C)
+                                                   : phe_packed_ws_bytes(p, rows, C)), 256);
   const size_t b_pk = round_up(C * G * 2 * N * 4, 256), b_wout = round_up(C * G * bout, 256);
   const size_t slot = b_win + b_seeds + b_body + b_op + b_ws + b_pk + b_wout;
   if (g_ws.bytes < 2 * slot) {
@@ -700,7 +702,10 @@ int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out
     cudaMemcpyAsync(d_win, h_wire_in + t0 * L * bin, n * L * bin, cudaMemcpyHostToDevice, st);
     rc = phe_wire_deserialize_inputs(p, d_win, n, L, d_seeds, d_bod, st);
     if (!rc) rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
-    if (!rc) rc = phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws, d_pk, st);
+    if (!rc)
+      rc = ntt_pack ? phe_matmul_clear_packed_ntt(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws,
+                                                  d_pk, st)
+                    : phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws, d_pk, st);
     if (!rc) rc = phe_wire_serialize_packed(p, d_pk, n * G, d_wout, st);
     if (rc) return rc;
     cudaMemcpyAsync(h_wire_out + t0 * G * bout, d_wout, n * G * bout, cudaMemcpyDeviceToHost, st);
@@ -714,6 +719,18 @@ int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out
   return PHE_OK;
 }
 
+int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
+                         const void *d_kprep, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
+                         uint8_t *h_wire_out, void *stream) {
+  return server_wire_host_impl(p, d_wprep, d_out, d_in, transpose, d_kprep, h_wire_in, T, chunk_tokens, h_wire_out,
+                               stream, false);
+}
+int phe_server_wire_host_ntt(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
+                             const void *d_nksk, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
+                             uint8_t *h_wire_out, void *stream) {
+  return server_wire_host_impl(p, d_wprep, d_out, d_in, transpose, d_nksk, h_wire_in, T, chunk_tokens, h_wire_out,
+                               stream, true);
+}
 
 // ================================================================ LWE outputs on the wire
 static inline int64_t lwe_seg_words(const phe_params *p) { return (int64_t)p->N * p->q_out / 64; }
@@ -1072,6 +1089,40 @@ int phe_pack_ntt(const phe_params *p, const void *d_digits, const uint64_t *d_bo
   rc = phe::launch_pack_finalize(kp, acc, d_body, T, rows, (int)G, d_out_packed, S(stream));
   if (rc) return rc;
   g_last_launches = 3;
+  return PHE_OK;
+}
+
+size_t phe_packed_ntt_ws_bytes(const phe_params *p, int64_t rows, int64_t T) {
+  KParams kp;
+  if (!p || rows < 1 || T < 0 || check_ntt_ks(p, &kp)) return 0;
+  const int64_t N = p->N, rp = round_up(rows, 256);
+  return (size_t)(round_up(T * rp * phe::KS_LEVELS * N, 256) + round_up(T * rows * 8, 256)) +
+         phe_pack_ntt_ws_bytes(p, rows, T);
+}
+
+int phe_matmul_clear_packed_ntt(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
+                                int transpose, const void *d_operand, int64_t T, const void *d_nksk,
+                                void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_ntt_ks(p, &kp);
+  if (rc) return rc;
+  if (d_out < 1 || d_in < 1 || T < 0 || (transpose != 0 && transpose != 1)) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_wprep || !d_operand || !d_nksk || !d_ws || !d_out_packed) return PHE_EINVAL;
+  const int64_t rows = transpose ? d_in : d_out;
+  if (ws_bytes < phe_packed_ntt_ws_bytes(p, rows, T)) return PHE_ENOMEM;
+  const int64_t N = p->N, rp = round_up(rows, 256);
+  uint8_t *digits = static_cast<uint8_t *>(d_ws);
+  uint64_t *body = reinterpret_cast<uint64_t *>(digits + round_up(T * rp * phe::KS_LEVELS * N, 256));
+  void *ws2 = reinterpret_cast<uint8_t *>(body) + round_up(T * rows * 8, 256);
+  // (1) Eq. 6 on the tensor cores, masks written as Decomp digits; (2) Eq. 7/8 in the NTT domain
+  rc = phe_matmul_clear_digits(p, d_wprep, d_out, d_in, transpose, d_operand, T, digits, body, stream);
+  if (rc) return rc;
+  const int l1 = g_last_launches;
+  rc = phe_pack_ntt(p, digits, body, T, rows, d_nksk, ws2, phe_pack_ntt_ws_bytes(p, rows, T), d_out_packed, stream);
+  if (rc) return rc;
+  g_last_launches += l1;
   return PHE_OK;
 }
 

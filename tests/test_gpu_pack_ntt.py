@@ -109,3 +109,22 @@ def test_pack_ntt_empty_and_errors(phe):
         phe.pack_ntt(p, torch.zeros((1, 256, 4, 256), dtype=torch.int8, device=DEV),
                      torch.zeros((1, 256), dtype=torch.int64, device=DEV), nk,
                      ws=torch.empty(16, dtype=torch.uint8, device=DEV))
+
+
+def test_packed_ntt_primitive_and_wire_host(phe):
+    """phe_matmul_clear_packed_ntt == phe_matmul_clear_packed (whole primitive), and the wire-byte
+    host pipeline with the NTT packing stage == the tensor-core one, byte for byte."""
+    p, W, x, S, w, opnd, ksk = _setup(phe, dict(N=2048), 2048, 2048, 5, 0)
+    K, NK = phe.KeySwitchKey(p, ksk), phe.NttKeySwitchKey(p, ksk)
+    ref = phe.matmul_clear_packed(p, w, opnd, 5, K)
+    got = phe.matmul_clear_packed_ntt(p, w, opnd, 5, NK)
+    assert torch.equal(got, ref)
+    T = 5
+    s2, b2 = phe.encrypt_pack(p, S, torch.from_numpy(x).to(DEV), 77, 3)  # the ciphertexts behind opnd
+    hi = phe.wire_serialize_inputs(p, s2, b2).cpu().pin_memory()
+    ho_ref = torch.empty((T, 1, phe.wire_output_bytes(p)), dtype=torch.uint8).pin_memory()
+    ho_ntt = torch.empty_like(ho_ref).pin_memory()
+    phe.server_wire_host(p, w, K, hi, ho_ref, chunk_tokens=2)
+    phe.server_wire_host_ntt(p, w, NK, hi, ho_ntt, chunk_tokens=2)
+    assert torch.equal(ho_ref, ho_ntt)
+    assert torch.equal(phe.wire_deserialize_packed(p, ho_ntt.to(DEV)).view(T, 1, 2, p.N), ref)
