@@ -120,3 +120,18 @@ def test_ntt_kernel_index_scheme():
         h = ntt_model.shoup((res[1][k] - res[0][k]) % ntt_model.P[1], cinv, ntt_model.P[1])
         v = res[0][k] + ntt_model.P[0] * h
         assert (v - M if v >= M // 2 else v) == exact[k]
+
+
+def test_ntt_keyswitch_index_scheme_and_split_crt():
+    """tools/ntt_ks_model.py (the NTT-domain KeySwitch kernel's scheme, ntt_keyswitch.cu): every
+    exchange and digit-tile access bank-conflict free for log2 N = 8..13, and the kernel-order
+    forward NTTs + Montgomery pointwise products + KSK hi/lo split + two-prime CRT reproduce the
+    exact negacyclic sum of Eq. 7/8 mod 2^39 on a small ring (brute-force schoolbook reference)."""
+    import ntt_ks_model as m
+    for logN in range(8, 14):
+        assert m.bank_check(logN) is None, logN
+    import io, contextlib
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        m.main()
+    assert "logN=8: kernel-scheme" in buf.getvalue()

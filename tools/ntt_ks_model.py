@@ -1,14 +1,16 @@
 """Integer model of the NTT-domain KeySwitch packing kernel (stage 2 of the packed primitive,
 ntt_keyswitch.cu), used to check its index scheme on the host before running it: the forward
-Cooley-Tukey NTT by reversed phases in registers, 32-bit-word exchange layouts (bank-conflict
-freedom), the swizzled digit tile, lazy Harvey/Montgomery arithmetic bounds, and the 3-prime
-Garner CRT with an offset Z = 0 mod 2^q_in.  Development tool only (not the oracle, not the
-product).  Run: python tools/ntt_ks_model.py
+Cooley-Tukey NTT by reversed 3-bit phases in registers (V = 8 values per thread), 32-bit-word
+exchange layouts (bank-conflict freedom), the swizzled digit tile, lazy Harvey/Montgomery
+arithmetic bounds, the KSK hi/lo split and the two-prime CRT with an offset Z.  Development tool
+only (not the oracle, not the product).  Run: python tools/ntt_ks_model.py
 """
 import random
 
-P = [998244353, 1004535809, 469762049]
-GEN = [3, 3, 3]
+P = [998244353, 1004535809]
+GEN = [3, 3]
+VB = 3
+V = 1 << VB
 
 
 def bitrev(x, bits):
@@ -43,50 +45,53 @@ def mont_lazy(a, b, p):
     return u
 
 
-def phases(logN):  # inverse (GS) phase list of the hot kernels; forward runs it reversed
+def phases(logN):  # inverse-order phase list (3-bit phases); the forward transform runs it reversed
     out = []; s0 = 0
     while s0 < logN:
-        b = min(4, logN - s0); out.append((s0, b)); s0 += b
+        b = min(VB, logN - s0); out.append((s0, b)); s0 += b
     return out
 
 
 def elem_index(tid, e, s0, b, logN):
     el = e & ((1 << b) - 1)
     g = e >> b
-    o = tid | (g << (logN - 4))
+    o = tid | (g << (logN - VB))
     return (o & ((1 << s0) - 1)) | (el << s0) | ((o >> s0) << (s0 + b))
 
 
 def lay(s0_read, j):
     """word address of element j in the exchange buffer read by the phase starting at stage
     s0_read (found by search: conflict-free for both access patterns of that exchange, 32-bit
-    words, logN 9..13; additive in disjoint index bits)"""
-    return j + (j >> 4) if s0_read == 0 else j + 16 * (j >> 8) if s0_read == 4 else j
+    words, logN 8..13; additive in disjoint index bits)"""
+    return j + (j >> 3) if s0_read == 0 else j + 4 * (j >> 5) if s0_read == 3 else j
 
 
-SWS = {8: 2}
+def tile_bytes(logN):
+    return 8 if logN >= 13 else 16
 
 
 def tile_addr(r, c, logN):
-    sws = SWS.get(logN, 3)
+    tb = tile_bytes(logN)
+    wpr = tb // 4
+    sws = 3 if wpr == 4 else 4
     w, byte = c >> 2, c & 3
-    return r * 16 + 4 * (w ^ ((r >> sws) & 3)) + byte
+    return r * tb + 4 * (w ^ ((r >> sws) & (wpr - 1))) + byte
 
 
 def bank_check(logN):
-    nthr = (1 << logN) // 16
+    nthr = (1 << logN) // V
     rev = phases(logN)[::-1]
     for x in range(len(rev) - 1):
         for (s0, b) in (rev[x], rev[x + 1]):
             for w0 in range(0, nthr, 32):
-                for e in range(16):
+                for e in range(V):
                     banks = [lay(rev[x + 1][0], elem_index(t, e, s0, b, logN)) % 32 for t in range(w0, min(w0 + 32, nthr))]
                     if len(set(banks)) != len(banks):
                         return f"exchange {x} phase {(s0, b)} e={e}: {len(banks) - len(set(banks))} conflicts"
     s0, b = rev[0]
     for w0 in range(0, nthr, 32):
-        for e in range(16):
-            for c in range(16):
+        for e in range(V):
+            for c in range(tile_bytes(logN)):
                 banks = [tile_addr(elem_index(t, e, s0, b, logN), c, logN) // 4 % 32
                          for t in range(w0, min(w0 + 32, nthr))]
                 if len(set(banks)) != len(banks):
@@ -96,41 +101,41 @@ def bank_check(logN):
 
 def fwd_kernel_model(a, p, fwd, logN):
     """CT forward NTT (natural in -> bit-reversed out), values lazily in [0, 4p)."""
-    N = 1 << logN; nthr = N // 16
+    N = 1 << logN; nthr = N // V
     rev = phases(logN)[::-1]
     s0, b = rev[0]
-    regs = [[a[elem_index(t, e, s0, b, logN)] for e in range(16)] for t in range(nthr)]
+    regs = [[a[elem_index(t, e, s0, b, logN)] for e in range(V)] for t in range(nthr)]
     for pi, (s0, b) in enumerate(rev):
         if pi > 0:
-            regs = [[smem[lay(s0, elem_index(t, e, s0, b, logN))] for e in range(16)] for t in range(nthr)]
+            regs = [[smem[lay(s0, elem_index(t, e, s0, b, logN))] for e in range(V)] for t in range(nthr)]
         for t in range(nthr):
             r = regs[t]
             for s in range(s0 + b - 1, s0 - 1, -1):
                 d = 1 << (s - s0)
-                for e in range(16):
+                for e in range(V):
                     if e & d:
                         continue
                     j = elem_index(t, e, s0, b, logN)
                     assert elem_index(t, e | d, s0, b, logN) == j + (1 << s)
                     w = fwd[(N >> (s + 1)) + (j >> (s + 1))]
-                    U, V = r[e], r[e | d]
-                    assert U < 4 * p and V < 4 * p
+                    U, Y = r[e], r[e | d]
+                    assert U < 4 * p and Y < 4 * p
                     U = min(U, (U - 2 * p) % 2**32)
-                    Vp = shoup_lazy(V, w, p)
+                    Vp = shoup_lazy(Y, w, p)
                     r[e] = U + Vp
                     r[e | d] = U - Vp + 2 * p
         if pi < len(rev) - 1:
             smem = {}
             for t in range(nthr):
-                for e in range(16):
+                for e in range(V):
                     smem[lay(rev[pi + 1][0], elem_index(t, e, s0, b, logN))] = regs[t][e]
     s0, b = rev[-1]
-    assert (s0, b) == (0, 4)
+    assert (s0, b) == (0, VB)
     out = [None] * N
     for t in range(nthr):
-        for e in range(16):
-            assert elem_index(t, e, 0, 4, logN) == 16 * t + e
-            out[16 * t + e] = regs[t][e]
+        for e in range(V):
+            assert elem_index(t, e, 0, VB, logN) == V * t + e
+            out[V * t + e] = regs[t][e]
     return out
 
 
@@ -186,31 +191,41 @@ def main():
         exact = [0] * N
         for r in range(rows):
             for k, v in enumerate(negacyclic(D[r], K[r])): exact[k] += v
-        bound_bits = q_in - 1 + 2 * logN + 2 + 7
-        Z = 1 << bound_bits
-        res = []
-        for p, g in zip(P, GEN):
-            fwd, inv = tables(p, g, N)
-            ninv_r = pow(N, -1, p) * 2**32 % p
-            acc = [0] * N
-            for r in range(rows):
-                Dh = fwd_kernel_model([d + p for d in D[r]], p, fwd, logN)
-                assert [x % p for x in Dh] == ntt_fwd_ref(D[r], p, fwd)
-                Kh = [x * ninv_r % p for x in ntt_fwd_ref(Kc[r], p, fwd)]
-                for k in range(N):
-                    s = acc[k] + mont_lazy(Dh[k], Kh[k], p)
-                    acc[k] = min(s, (s - 2 * p) % 2**32)
-            res.append([x % p for x in ntt_inv_ref([a % p for a in acc], p, inv)])
-        p0, p1, p2 = P
+        sp = (q_in + 1) // 2                      # K = K_hi 2^sp + K_lo, centred halves
+        lo = [[((k + (1 << (sp - 1))) % (1 << sp)) - (1 << (sp - 1)) for k in Kr] for Kr in Kc]
+        hi = [[(k - l) >> sp for k, l in zip(Kr, Lr)] for Kr, Lr in zip(Kc, lo)]
+        hb = max(sp - 1, q_in - sp)
+        assert all(abs(v) <= 1 << hb for Hr in hi + lo for v in Hr)
+        bb = 2 * logN + 9 + hb                    # |half-sum| <= 4N N 2^7 2^hb
+        assert 2 ** (bb + 1) < P[0] * P[1]
+        Z = 1 << bb
+        sums = []
+        for half in (hi, lo):
+            res = []
+            for p, g in zip(P, GEN):
+                fwd, inv = tables(p, g, N)
+                ninv_r = pow(N, -1, p) * 2**32 % p
+                acc = [0] * N
+                for r in range(rows):
+                    Dh = fwd_kernel_model([d + p for d in D[r]], p, fwd, logN)
+                    assert [x % p for x in Dh] == ntt_fwd_ref(D[r], p, fwd)
+                    Kh = [x * ninv_r % p for x in ntt_fwd_ref(half[r], p, fwd)]
+                    for k in range(N):
+                        s_ = acc[k] + mont_lazy(Dh[k], Kh[k], p)
+                        acc[k] = min(s_, (s_ - 2 * p) % 2**32)
+                res.append([x % p for x in ntt_inv_ref([a % p for a in acc], p, inv)])
+            p0, p1 = P
+            out = []
+            for k in range(N):
+                r0, r1 = (res[0][k] + Z) % p0, (res[1][k] + Z) % p1
+                h1 = (r1 - r0) * pow(p0, -1, p1) % p1
+                out.append(r0 + p0 * h1 - Z)      # the exact half-sum
+            sums.append(out)
         for k in range(N):
-            r = [(res[i][k] + Z) % P[i] for i in range(3)]
-            x0 = r[0]
-            h1 = (r[1] - x0) * pow(p0, -1, p1) % p1
-            h2 = (r[2] - x0 - p0 * h1) * pow(p0 * p1, -1, p2) % p2
-            v = (x0 + p0 * h1 + (p0 * p1 % 2**64) * h2) % 2**64
+            v = (sums[0][k] * 2**sp + sums[1][k]) % 2**64
             assert v % 2**q_in == exact[k] % 2**q_in, (logN, k)
-        print(f"logN={logN}: kernel-scheme forward NTTs + Montgomery pointwise + 3-prime CRT == "
-              f"exact negacyclic KeySwitch sum mod 2^{q_in}")
+        print(f"logN={logN}: kernel-scheme forward NTTs + Montgomery pointwise + hi/lo split + 2-prime CRT "
+              f"== exact negacyclic KeySwitch sum mod 2^{q_in}")
 
 
 if __name__ == "__main__":
