@@ -128,3 +128,42 @@ def test_packed_ntt_primitive_and_wire_host(phe):
     phe.server_wire_host_ntt(p, w, NK, hi, ho_ntt, chunk_tokens=2)
     assert torch.equal(ho_ref, ho_ntt)
     assert torch.equal(phe.wire_deserialize_packed(p, ho_ntt.to(DEV)).view(T, 1, 2, p.N), ref)
+
+
+@pytest.mark.slow
+def test_full_size_q_proj_packed_bench_config(phe, coracle):
+    """bench.py --workload q_proj_packed in its launch configuration (q_proj 2048x2048, T = 2048,
+    Table 1): (i) every packed word of all 2048 tokens through phe_matmul_clear_packed_ntt equals
+    the tensor-core primitive's; (ii) two sampled tokens against the oracle's own keygen, KSK,
+    encryption, literal Eq. 6 and literal Eq. 7/8; (iii) all 4.2M packed outputs decrypt to W.x
+    within the gamma-MSB contract."""
+    p = phe.params(phe.PRESET_PAPER)
+    d, T = 2048, 2048
+    W = synth.weights_int8(d, d)
+    x = synth.activations_int8(T, d)
+    S = phe.keygen(p, 5)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).to(DEV), 77)
+    w = phe.Weights(p, torch.from_numpy(W).to(DEV))
+    opnd = phe.ct_prepare(p, seeds, body)
+    ksk = phe.ksk_gen(p, S, 1234)
+    got = phe.matmul_clear_packed_ntt(p, w, opnd, T, phe.NttKeySwitchKey(p, ksk))
+    torch.cuda.synchronize()
+    ref = phe.matmul_clear_packed(p, w, opnd, T, phe.KeySwitchKey(p, ksk))
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    del ref
+    phe._ws_cache.clear()
+    op = Params(N=p.N, q_in=p.q_in, q_out=p.q_out, beta=p.beta, gamma=p.gamma)
+    So = O.keygen(5, op.N)
+    KA, KB = coracle.ksk_gen(op, So, 1234, nthreads=os.cpu_count())
+    seeds_o = O.block_seeds(77, T, 1)
+    g = got.cpu().numpy().astype(np.uint32).astype(np.uint64)
+    for tau in (0, 1733):
+        A, B = O.encrypt(op, So, x[tau], seeds_o[tau])
+        m, b = coracle.matmul_clear_literal(op, W, A, B, nthreads=os.cpu_count())
+        PA, PB = coracle.pack(op, m, b, KA, KB, nthreads=os.cpu_count())
+        assert np.array_equal(g[tau, :, 0], O.modswitch(PA, op.q_in, op.q_out))
+        assert np.array_equal(g[tau, :, 1], O.modswitch(PB, op.q_in, op.q_out))
+    y = phe.decrypt_packed(p, S, got, d).double()
+    wx = torch.from_numpy(x).to(DEV).double() @ torch.from_numpy(W).to(DEV).double().T
+    assert (y - wx).abs().max().item() < 2 ** 15
