@@ -556,11 +556,21 @@ int launch_ntt_ks_prepare(const KParams &kp, const uint64_t *ksk, void *buf, cud
 }
 
 // K-splits: enough CTAs for two waves of one CTA per SM; a power of two dividing the 4N/16 tiles
+// K-splits: a power of two dividing the 4N / TILE tiles, the smallest whose grid fills its last
+// wave of one CTA per SM to >= 90% (long CTAs: the tail wave is what small T loses), else the
+// best fill down to 4 tiles per CTA.
 int ntt_ks_splits(const KParams &kp, int64_t T, int64_t G) {
+  constexpr int64_t SMS = 148;
   const int64_t tiles = (int64_t)KS_LEVELS * kp.N / nks::ks_tile(kp.log2N);
-  int64_t S = 1;
-  while (S < tiles && nks::NPR * T * G * S < 2 * 148) S *= 2;
-  return (int)S;
+  int64_t best = 1;
+  double best_eff = 0.0;
+  for (int64_t S = 1; S <= tiles && tiles / S >= 4; S *= 2) {
+    const int64_t ctas = nks::NPR * T * G * S;
+    const double waves = (double)ctas / SMS, eff = waves / (double)((ctas + SMS - 1) / SMS);
+    if (eff >= 0.9 && ctas >= 2 * SMS) return (int)S;
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = S; }
+  }
+  return (int)best;
 }
 size_t ntt_ks_ws_bytes(const KParams &kp, int64_t T, int64_t G) {
   const size_t partb = (size_t)ntt_ks_splits(kp, T, G) * T * G * nks::NPR * nks::NKP * kp.N * 4;
