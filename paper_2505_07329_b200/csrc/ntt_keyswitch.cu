@@ -244,9 +244,16 @@ template <int LOGN>
 __host__ __device__ constexpr int ks_ntb() { return LOGN >= 12 ? 1 : 2; }  // tile + staging buffer
 template <int LOGN>
 __host__ __device__ constexpr int ks_nxb() { return LOGN >= 13 ? 1 : 2; }  // exchange buffers per group
-template <int LOGN>
+// Both primes in one CTA (half the groups each, sharing every digit tile) when it has >= 2 groups;
+// N = 8192 (one group) runs one CTA per prime.
+// Small grids (few tokens) keep one prime per CTA: twice the CTAs, so fewer K-splits are needed.
+template <int LOGN, bool MRG>
+__host__ __device__ constexpr int ks_npc() { return MRG && ks_ng<LOGN>() >= 2 ? NPR : 1; }
+__host__ __device__ inline bool ks_merge(int64_t T, int64_t G) { return NPR * T * G >= 2 * 148; }
+__host__ __device__ inline int ks_primes_per_cta(int logN, bool mrg) { return mrg && logN < 13 ? NPR : 1; }
+template <int LOGN, bool MRG>
 __host__ __device__ constexpr int ks_smem() {
-  return V * ks_nt<LOGN>() * 8                                   // twiddles: tw1 [7][NT] + twl [NT]
+  return ks_npc<LOGN, MRG>() * V * ks_nt<LOGN>() * 8             // twiddles: tw1 [7][NT] + twl [NT] per prime
          + ks_ng<LOGN>() * ks_nxb<LOGN>() * xwords<LOGN>() * 4   // exchange buffers
          + ks_ntb<LOGN>() * (1 << LOGN) * ks_tile(LOGN);         // digit tile (+ staging)
 }
@@ -319,39 +326,46 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src, bool vali
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-template <int LOGN>
+template <int LOGN, bool MRG>
 __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kernel(KsArgs a) {
   constexpr int N = 1 << LOGN, NT = ks_nt<LOGN>(), NG = ks_ng<LOGN>(), NTH = NG * NT;
   constexpr int TILE = ks_tile(LOGN), WPR = TILE / 4;  // bytes / 4-byte words per tile row
-  constexpr int COLS = TILE / NG;                     // columns of a tile per group
+  constexpr int NPC = ks_npc<LOGN, MRG>();            // primes per CTA
+  constexpr int GPP = NG / NPC;                       // groups per prime
+  constexpr int COLS = TILE / GPP;                    // columns of a tile per group
   constexpr int KF = ks_nph<LOGN>() - 1;              // first forward phase
   constexpr int FS0 = Ph<LOGN, KF>::S0, FB = Ph<LOGN, KF>::B;
   constexpr int SWS = WPR == 4 ? 3 : 4;               // row swizzle: word w at w ^ ((r >> SWS) & (WPR-1))
-  static_assert(TILE % NG == 0, "groups divide the tile");
+  static_assert(TILE % GPP == 0 && NG % NPC == 0, "groups divide the tile");
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint2 *tw1 = reinterpret_cast<uint2 *>(smem_raw);
+  const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
+  const int qg = grp / GPP, gq = grp % GPP;          // this group's prime slot, rank among its prime's groups
+  uint2 *tw_all = reinterpret_cast<uint2 *>(smem_raw);
+  uint2 *tw1 = tw_all + qg * V * NT;
   uint2 *twl = tw1 + P1N * NT;
-  uint32_t *xall = reinterpret_cast<uint32_t *>(twl + NT);
+  uint32_t *xall = reinterpret_cast<uint32_t *>(tw_all + NPC * V * NT);
   uint8_t *tile = reinterpret_cast<uint8_t *>(xall + NG * ks_nxb<LOGN>() * xwords<LOGN>());
   uint8_t *stage = tile + N * TILE;
-  const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
   uint32_t *xb = xall + grp * ks_nxb<LOGN>() * xwords<LOGN>();
   int cur = 0;
 
-  // blockIdx = (s * T G + tg) * 2 + q: the two primes of one token run side by side (shared
-  // digit tiles in L2), and concurrent CTAs sweep the same K_hat rows
+  // blockIdx = ((s * T G + tg) * NPR / NPC + q-slot): concurrent CTAs sweep the same K_hat rows;
+  // with NPC = 2 both primes of a token share each digit tile, else they run side by side
   const int64_t b = blockIdx.x;
-  const int q = (int)(b % NPR);
-  const int64_t tg = (b / NPR) % (a.T * a.G);
-  const int s = (int)(b / NPR / (a.T * a.G));
+  constexpr int NQB = NPR / NPC;                      // prime slots across CTAs
+  const int q = (int)(b % NQB) * NPC + qg;
+  const int64_t tg = (b / NQB) % (a.T * a.G);
+  const int s = (int)(b / NQB / (a.T * a.G));
   const int64_t tau = tg / a.G, g = tg % a.G;
   const uint32_t p = prime_h(q), pinv = neg_inv32(p);
 
-  {  // twiddles of prime q
-    const uint2 *fwd = a.tabs + (int64_t)q * N;
-    const uint2 *p1 = a.tabs + 2 * NPR * N + (int64_t)q * P1N * NT;
-    for (int k = threadIdx.x; k < P1N * NT; k += NTH) tw1[k] = p1[k];
-    for (int k = threadIdx.x; k < NT; k += NTH) twl[k] = fwd[k];
+  for (int qq = 0; qq < NPC; qq++) {  // twiddles of the CTA's primes
+    const int qc = (int)(b % NQB) * NPC + qq;
+    const uint2 *fwd = a.tabs + (int64_t)qc * N;
+    const uint2 *p1 = a.tabs + 2 * NPR * N + (int64_t)qc * P1N * NT;
+    uint2 *t1 = tw_all + qq * V * NT;
+    for (int k = threadIdx.x; k < P1N * NT; k += NTH) t1[k] = p1[k];
+    for (int k = threadIdx.x; k < NT; k += NTH) t1[P1N * NT + k] = fwd[k];
   }
   uint32_t acc[NKP][V];
 #pragma unroll
@@ -415,7 +429,7 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
     }
 #pragma unroll 1
     for (int cc = 0; cc < COLS; cc++) {
-      const int c = grp * COLS + cc;
+      const int c = gq * COLS + cc;
       const int8_t *cb = reinterpret_cast<const int8_t *>(tile) + jt * TILE + 4 * ((c >> 2) ^ swt) + (c & 3);
       uint32_t r[V];
 #pragma unroll
@@ -437,8 +451,10 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
   }
   // sum over the NG groups (each covered other columns) in the tile buffer, group by group; store
   // [..][part][k], k = 8 tid + e
-  uint32_t *out = a.part + (((s * a.T + tau) * a.G + g) * NPR + q) * NKP * (int64_t)N;
-  if constexpr (NG == 1) {
+  // sum over the GPP groups of each prime (they covered other columns) in the tile buffer, group by
+  // group, one prime at a time; store [..][part][k], k = 8 tid + e
+  if constexpr (GPP == 1 && NPC == 1) {
+    uint32_t *out = a.part + (((s * a.T + tau) * a.G + g) * NPR + q) * NKP * (int64_t)N;
 #pragma unroll
     for (int pt = 0; pt < NKP; pt++)
 #pragma unroll
@@ -446,22 +462,27 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
   } else {
     static_assert(NKP * (1 << LOGN) * 4 <= (1 << LOGN) * TILE, "reduction fits the tile buffer");
     uint32_t *red = reinterpret_cast<uint32_t *>(tile);
-    for (int gg = 0; gg < NG; gg++) {
-      __syncthreads();
-      if (grp == gg) {
+    for (int qq = 0; qq < NPC; qq++) {
+      for (int gg = 0; gg < GPP; gg++) {
+        __syncthreads();
+        if (qg == qq && gq == gg) {
 #pragma unroll
-        for (int pt = 0; pt < NKP; pt++)
+          for (int pt = 0; pt < NKP; pt++)
 #pragma unroll
-          for (int e = 0; e < V; e++) {
-            uint32_t *o = &red[pt * N + V * tid + e];
-            *o = gg ? add_lazy(*o, acc[pt][e], p) : acc[pt][e];
-          }
+            for (int e = 0; e < V; e++) {
+              uint32_t *o = &red[pt * N + V * tid + e];
+              *o = gg ? add_lazy(*o, acc[pt][e], p) : acc[pt][e];
+            }
+        }
       }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < NKP * N; k += NTH) {
-      const uint32_t v = red[k];
-      out[k] = min(v, v - p);
+      __syncthreads();
+      const int qc = (int)(b % NQB) * NPC + qq;
+      const uint32_t pc = prime_h(qc);
+      uint32_t *out = a.part + (((s * a.T + tau) * a.G + g) * NPR + qc) * NKP * (int64_t)N;
+      for (int k = threadIdx.x; k < NKP * N; k += NTH) {
+        const uint32_t v = red[k];
+        out[k] = min(v, v - pc);
+      }
     }
   }
 }
@@ -503,14 +524,18 @@ ks_finalize_kernel(KParams kp, const uint2 *__restrict__ tabs, const uint32_t *_
   }
 }
 
-template <int LOGN>
-int launch_ks(const KsArgs &a, int64_t grid, cudaStream_t st) {
-  constexpr int smem = ks_smem<LOGN>();
-  cudaError_t e = cudaFuncSetAttribute(ks_ntt_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+template <int LOGN, bool MRG>
+int launch_ks_cfg(const KsArgs &a, int64_t grid, cudaStream_t st) {
+  constexpr int smem = ks_smem<LOGN, MRG>();
+  cudaError_t e = cudaFuncSetAttribute(ks_ntt_kernel<LOGN, MRG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return phe_set_cuda_error(e);
-  ks_ntt_kernel<LOGN><<<(unsigned)grid, ks_ng<LOGN>() * ks_nt<LOGN>(), smem, st>>>(a);
+  ks_ntt_kernel<LOGN, MRG><<<(unsigned)grid, ks_ng<LOGN>() * ks_nt<LOGN>(), smem, st>>>(a);
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
+}
+template <int LOGN>
+int launch_ks(const KsArgs &a, int64_t grid, bool mrg, cudaStream_t st) {
+  return mrg ? launch_ks_cfg<LOGN, true>(a, grid, st) : launch_ks_cfg<LOGN, false>(a, grid, st);
 }
 
 }  // namespace nks
@@ -565,7 +590,7 @@ int ntt_ks_splits(const KParams &kp, int64_t T, int64_t G) {
   int64_t best = 1;
   double best_eff = 0.0;
   for (int64_t S = 1; S <= tiles && tiles / S >= 4; S *= 2) {
-    const int64_t ctas = nks::NPR * T * G * S;
+    const int64_t ctas = (nks::NPR / nks::ks_primes_per_cta(kp.log2N, nks::ks_merge(T, G))) * T * G * S;
     const double waves = (double)ctas / SMS, eff = waves / (double)((ctas + SMS - 1) / SMS);
     if (eff >= 0.9 && ctas >= 2 * SMS) return (int)S;
     if (eff > best_eff + 1e-9) { best_eff = eff; best = S; }
@@ -595,15 +620,16 @@ int launch_ntt_ks(const KParams &kp, const void *buf, const int8_t *digits, int6
   a.T = T; a.R256 = R256; a.G = G; a.S = S;
   a.tiles_per_split = (int)((int64_t)KS_LEVELS * N / nks::ks_tile(kp.log2N) / S);
   a.part = part;
-  const int64_t grid = (int64_t)nks::NPR * T * G * S;
+  const bool mrg = nks::ks_merge(T, G);
+  const int64_t grid = (int64_t)(nks::NPR / nks::ks_primes_per_cta(kp.log2N, mrg)) * T * G * S;
   int rc;
   switch (kp.log2N) {
-    case 8: rc = nks::launch_ks<8>(a, grid, st); break;
-    case 9: rc = nks::launch_ks<9>(a, grid, st); break;
-    case 10: rc = nks::launch_ks<10>(a, grid, st); break;
-    case 11: rc = nks::launch_ks<11>(a, grid, st); break;
-    case 12: rc = nks::launch_ks<12>(a, grid, st); break;
-    case 13: rc = nks::launch_ks<13>(a, grid, st); break;
+    case 8: rc = nks::launch_ks<8>(a, grid, mrg, st); break;
+    case 9: rc = nks::launch_ks<9>(a, grid, mrg, st); break;
+    case 10: rc = nks::launch_ks<10>(a, grid, mrg, st); break;
+    case 11: rc = nks::launch_ks<11>(a, grid, mrg, st); break;
+    case 12: rc = nks::launch_ks<12>(a, grid, mrg, st); break;
+    case 13: rc = nks::launch_ks<13>(a, grid, mrg, st); break;
     default: return PHE_EUNSUPPORTED;
   }
   if (rc) return rc;

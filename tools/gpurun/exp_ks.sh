@@ -1,2 +1,4 @@
-echo "== base"; PYTHONPATH=. timeout 300 python tools/probe_pack_ntt.py 256 2>&1 | grep "pack_ntt\|ident"
-for v in F1 F2 F4; do echo "== $v"; PHE_LIB=$PWD/paper_2505_07329_b200/libphe_$v.so PYTHONPATH=. timeout 300 python tools/probe_pack_ntt.py 256 2>&1 | grep "pack_ntt\|ident"; done
+timeout 900 python -m pytest tests/test_gpu_pack_ntt.py -x -q 2>&1 | tail -1
+PYTHONPATH=. timeout 300 python tools/probe_pack_ntt.py 256 2>&1 | grep "pack_ntt"
+PYTHONPATH=. timeout 300 python tools/probe_pack_ntt.py 16 2>&1 | grep "pack_ntt"
+PYTHONPATH=. timeout 300 python tools/probe_pack_ntt.py 2048 2>&1 | grep "pack_ntt\|ident"
