@@ -416,7 +416,8 @@ def run_ours(args):
         imad = sum(T * ((w.rows + p.N - 1) // p.N) * 2 * phe.KS_LEVELS * p.N * per_col for _, w, _ in regs)
         ach = imad / (mask_ms / 1e3) / 1e12
         roofline = {"bound": "alu", "achieved": round(ach, 3), "peak": round(peak_imad, 3), "unit": "T IMAD/s",
-                    "frac": round(ach / peak_imad, 4), "traffic": None,
+                    "frac": round(ach / peak_imad, 4),
+                    "traffic": traffic if args.workload == "q_proj_packed" and T == 2048 else None,
                     "kernel": "ks_ntt_kernel<11> + ks_finalize_kernel + pack_finalize_kernel (NTT-domain "
                               "KeySwitch packing, Eq. 7/8)",
                     "ops": "algorithmic 32-bit multiplies: per (l, i) row, prime and packed ciphertext "
@@ -432,7 +433,7 @@ def run_ours(args):
                     "peak_source": imad_src}
     else:
         roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
-                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "frac": round(achieved / peak, 4), "traffic": None if packed else traffic,
                     "kernel": ("pack_gemm_2sm_kernel<5> (KeySwitch GEMM Eq. 8 + rotate-sum Eq. 7)" if packed else
                                "limb_gemm_2sm_kernel<5,SW,13> (mask contraction, tcgen05 cta_group::2)"),
                     "ops": "int8 tensor ops (2 per MAC), algorithmic: 2*ell*d_out*d_in*N per token",
