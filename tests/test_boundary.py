@@ -113,3 +113,31 @@ def test_wire_sizes_match_paper(lib):
     p = phe.params(phe.PRESET_PAPER)
     assert phe.wire_input_bytes(p) == 9992
     assert phe.wire_output_bytes(p) == 13312
+
+
+def test_ntt_keyswitch_sizes_and_support(lib):
+    """NEXT #1 stage 2 in the NTT domain (R24): buffer sizes and the CRT-range support rule are
+    host-side; unsupported parameter sets report 0 bytes / EUNSUPPORTED without a launch."""
+    import paper_2505_07329_b200 as phe
+    p = phe.params(phe.PRESET_PAPER)
+    P = ctypes.byref(p)
+    N = 2048
+    tables = (2 * 2 * N + 2 * 7 * (N // 8)) * 8           # fwd + inv + last-phase twiddles, 2 primes
+    tables = (tables + 255) // 256 * 256
+    khat = 2 * 4 * N * 4 * N * 4                          # [2 primes][4N rows][4 parts][N] u32
+    assert lib.phe_ntt_ksk_bytes(P) == tables + khat
+    # T = 2048, one ciphertext group: one K-split (the grid fills its waves), partials + accumulator
+    assert lib.phe_pack_ntt_ws_bytes(P, 2048, 2048) == 2048 * 2 * 4 * N * 4 + 2048 * 2 * N * 8
+    ws_small = lib.phe_pack_ntt_ws_bytes(P, 2048, 16)      # small T: K-split partials
+    assert ws_small > 16 * 2 * 4 * N * 4 and (ws_small - 16 * 2 * N * 8) % (16 * 2 * 4 * N * 4) == 0
+    assert lib.phe_packed_ntt_ws_bytes(P, 2048, 16) >= ws_small + 16 * 2048 * 4 * N
+    # q_in = 24 < 32 bits of the 4-level gadget (R18): not supported
+    q = phe.params(phe.PRESET_PAPER, q_in=24, q_out=20, beta=20, gamma=8)
+    assert lib.phe_ntt_ksk_bytes(ctypes.byref(q)) == 0
+    assert lib.phe_ntt_ksk_prepare(ctypes.byref(q), ctypes.c_void_p(16), ctypes.c_void_p(16), 1 << 30,
+                                   None) == phe.PHE_EUNSUPPORTED
+    # too-small buffers -> ENOMEM, T == 0 -> no-op, all before any launch
+    assert lib.phe_ntt_ksk_prepare(P, ctypes.c_void_p(16), ctypes.c_void_p(16), 16, None) == phe.PHE_ENOMEM
+    assert lib.phe_pack_ntt(P, ctypes.c_void_p(16), ctypes.c_void_p(16), 4, 2048, ctypes.c_void_p(16),
+                            ctypes.c_void_p(16), 16, ctypes.c_void_p(16), None) == phe.PHE_ENOMEM
+    assert lib.phe_pack_ntt(P, None, None, 0, 2048, None, None, 0, None, None) == phe.PHE_OK
