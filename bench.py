@@ -44,9 +44,11 @@ def parse():
     ap.add_argument("--pack", choices=["tc", "ntt"], default="ntt",
                     help="packed workloads, stage 2 (KeySwitch Eq. 8 + rotate-sum Eq. 7): tc = int8 packing GEMM "
                          "on tcgen05, ntt = sum_{l,i} D_{l,i} * KSK_{l,i} in the NTT domain (ntt_keyswitch.cu)")
-    ap.add_argument("--contraction", choices=["tc", "ntt", "hybrid"], default="tc",
-                    help="mask contraction a5: tc = int8 limb GEMM on tcgen05 (north_star), ntt = NTT domain "
-                         "(NEXT #4, CUDA cores), hybrid = ntt for multi-block (L >= 2) linears, tc otherwise")
+    ap.add_argument("--contraction", choices=["tc", "ntt", "hybrid"], default=None,
+                    help="mask contraction a5: tc = int8 limb GEMM on tcgen05 (north_star; the default), ntt = NTT "
+                         "domain (NEXT #4, CUDA cores), hybrid = ntt for multi-block (L >= 2) linears, tc otherwise; "
+                         "packed workloads below 512 tokens default to ntt (a 16-token batch fills a third of a "
+                         "51-token tensor-core tile)")
     ap.add_argument("--tokens", type=int, default=None,
                     help="tokens per rank (default B*C = 8*256 = 2048; stack_packed: the paper's training "
                          "step, B*C = 1*16)")
@@ -59,7 +61,12 @@ def parse():
                     help="rows mode (q_proj): nccl = time an NCCL send/recv gather to rank 0 after the step; "
                          "p2p = fused gather: every rank's kernels write their row block straight into rank "
                          "0's buffer (CUDA IPC / NVLink peer stores) inside the timed step")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.tokens is None:  # B*C = 8*256; the paper's training step (P:432-435) is B = 1, C = 16
+        args.tokens = 16 if args.workload == "stack_packed" else 2048
+    if args.contraction is None:
+        args.contraction = "ntt" if args.workload.endswith("_packed") and args.tokens < 512 else "tc"
+    return args
 
 
 # ----------------------------------------------------------------------------- environment
@@ -669,8 +676,6 @@ def run_reference(args):
 
 def main():
     args = parse()
-    if args.tokens is None:  # B*C = 8*256; the paper's training step (P:432-435) is B = 1, C = 16
-        args.tokens = 16 if args.workload == "stack_packed" else 2048
     if args.impl == "reference":
         run_reference(args)
     else:
