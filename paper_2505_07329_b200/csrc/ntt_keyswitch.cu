@@ -7,8 +7,8 @@
 //   sum_{l,i} D_{l,i}(X) * KSK_{l,i}(X),        D_{l,i}(X) = sum_r d_{gN+r,i,l} X^r
 // a sum of 4N negacyclic polynomial products (X^N = -1), computed here EXACTLY in the NTT
 // domain.  With the centred KSK words split as K = K_hi 2^SPLIT + K_lo (|K_half| <= 2^19 at
-// Table 1), each half-sum is below 4N * N * 2^7 * 2^19 = 2^50, so two 30-bit primes (p0 p1 ~
-// 2^59.8) and a CRT recover it exactly; sum_hi 2^SPLIT + sum_lo mod 2^q_in is the accumulator
+// Table 1), each half-sum is below 4N * N * 2^7 * 2^19 = 2^50, so two 28-bit primes (p0 p1 ~
+// 2^56) and a CRT recover it exactly; sum_hi 2^SPLIT + sum_lo mod 2^q_in is the accumulator
 // the tensor-core path (pack_gemm_2sm_kernel) writes, and
 // pack_finalize_kernel finishes both identically ((0, b) - acc, ModulusSwitch).  Work per
 // (l, i, coefficient): (log2 N)/2 butterflies + 4 pointwise products per prime (2 primes), O(log N)
@@ -36,9 +36,11 @@ namespace phe {
 namespace nks {
 
 constexpr int NPR = 2;
-// p = c 2^k + 1 with k >= 21 (negacyclic NTTs up to N = 8192 need 2N | p - 1), p < 2^30 so that
-// lazy values in [0, 4p) fit 32 bits; generator 3 for both.
-constexpr uint32_t P0 = 998244353u, P1 = 1004535809u;
+// The two largest primes p < 2^28 with 2^14 | p - 1 (negacyclic NTTs up to N = 8192): 16p < 2^32,
+// so butterfly values may grow lazily to [0, 16p) and the transform reduces only once (ct_phase);
+// p0 p1 ~ 2^56 still covers every half-sum (< 2^54 at N = 8192).  Generators 23 and 5.
+constexpr uint32_t P0 = 268369921u, P1 = 268271617u;
+constexpr uint32_t GEN0 = 23u, GEN1 = 5u;
 __host__ __device__ constexpr uint32_t prime_h(int q) { return q == 0 ? P0 : P1; }
 // The KSK words are split K = K_hi 2^SPLIT + K_lo (centred halves, SPLIT = ceil(q_in / 2)) so that
 // each of the four sums (A_hi, A_lo, B_hi, B_lo) stays below p0 p1 / 2: two primes instead of
@@ -61,7 +63,7 @@ __host__ __device__ constexpr uint32_t pw(uint64_t b, uint64_t e, uint32_t p) {
   }
   return (uint32_t)r;
 }
-static_assert((uint64_t)4 * P0 < (1ull << 32) && (uint64_t)4 * P1 < (1ull << 32), "lazy range");
+static_assert((uint64_t)16 * P0 < (1ull << 32) && (uint64_t)16 * P1 < (1ull << 32), "lazy range");
 static_assert((P0 - 1) % (1u << 14) == 0 && (P1 - 1) % (1u << 14) == 0,
               "2N | p - 1 up to N = 8192");
 
@@ -73,7 +75,7 @@ __device__ __forceinline__ uint32_t shoup_lazy(uint32_t x, uint32_t w, uint32_t 
   return x * w - __umulhi(x, wq) * p;  // any x < 2^32: [0, 2p)
 }
 __device__ __forceinline__ uint32_t mont_lazy(uint32_t a, uint32_t b, uint32_t p, uint32_t pi) {
-  const uint64_t t = (uint64_t)a * b;  // a < 4p, b < p: (t + m p) / 2^32 < 2p
+  const uint64_t t = (uint64_t)a * b;  // a < 16p, b < p, 16p < 2^32: (t + m p) / 2^32 < 2p
   const uint32_t m = (uint32_t)t * pi;
   return (uint32_t)((t + (uint64_t)m * p) >> 32);
 }
@@ -268,7 +270,10 @@ __device__ __forceinline__ void gsync(int grp) {
   }
 }
 
-// Cooley-Tukey stages S0+B-1 .. S0 (half-distance 2^s), values lazily in [0, 4p).
+// Cooley-Tukey stages S0+B-1 .. S0 (half-distance 2^s).  Lazy bounds (units of p): inputs < 2p; a
+// butterfly maps U < b, any V to U + W, U - W + 2p < b + 2 (W = Shoup product < 2p), so seven stages
+// run without reductions (2 -> 16 < 2^32 / p); the eighth first brings U below 4p (two conditional
+// subtractions) and at most five more follow (N <= 8192): outputs < 14p, fine for mont_lazy.
 template <int LOGN, int S0, int B>
 __device__ __forceinline__ void ct_phase(uint32_t (&r)[V], const uint2 *tw1, const uint2 *twl, uint32_t p,
                                          int tid) {
@@ -284,7 +289,10 @@ __device__ __forceinline__ void ct_phase(uint32_t (&r)[V], const uint2 *tw1, con
       const uint2 w = S0 == 0 ? tw1[(p1off(s) + (e >> (s + 1))) * NT + tid]
                               : twl[tb + (eidx<LOGN, S0, B>(0, e) >> (s + 1))];
       uint32_t U = r[e];
-      U = min(U, U - 2 * p);
+      if (LOGN - 1 - s == 7) {  // stage index 7: U < 16p -> < 4p
+        U = min(U, U - 8 * p);
+        U = min(U, U - 4 * p);
+      }
       const uint32_t W = shoup_lazy(r[e | d], w.x, w.y, p);
       r[e] = U + W;
       r[e | d] = U - W + 2 * p;
@@ -541,7 +549,7 @@ int launch_ks(const KsArgs &a, int64_t grid, bool mrg, cudaStream_t st) {
 }  // namespace nks
 
 // ---------------------------------------------------------------- launchers (host)
-static uint32_t ks_psi(uint32_t p, int N) { return nks::pw(3, (p - 1) / (2 * (uint32_t)N), p); }
+static uint32_t ks_psi(uint32_t p, uint32_t g, int N) { return nks::pw(g, (p - 1) / (2 * (uint32_t)N), p); }
 static uint32_t ks_ninv_mont(uint32_t p, int N) {  // N^-1 2^32 mod p
   return (uint32_t)((uint64_t)nks::pw(N, p - 2, p) * ((1ull << 32) % p) % p);
 }
@@ -565,7 +573,8 @@ int launch_ntt_ks_prepare(const KParams &kp, const uint64_t *ksk, void *buf, cud
   const int N = kp.N, NT = N / nks::V;
   uint2 *tabs = static_cast<uint2 *>(buf);
   const int ntab = 2 * nks::NPR * N + nks::NPR * nks::P1N * NT;
-  nks::ks_tables_kernel<<<(ntab + 255) / 256, 256, 0, st>>>(kp.log2N, ks_psi(nks::P0, N), ks_psi(nks::P1, N), tabs);
+  nks::ks_tables_kernel<<<(ntab + 255) / 256, 256, 0, st>>>(kp.log2N, ks_psi(nks::P0, nks::GEN0, N),
+                                                           ks_psi(nks::P1, nks::GEN1, N), tabs);
   PHE_CUDA_CHECK_LAUNCH();
   uint32_t *khat = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(buf) + nks::tables_bytes(N));
   const size_t smem = (size_t)N * 4;

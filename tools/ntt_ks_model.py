@@ -7,8 +7,8 @@ only (not the oracle, not the product).  Run: python tools/ntt_ks_model.py
 """
 import random
 
-P = [998244353, 1004535809]
-GEN = [3, 3]
+P = [268369921, 268271617]   # the two largest primes < 2^28 with 2^14 | p - 1 (16p < 2^32)
+GEN = [23, 5]
 VB = 3
 V = 1 << VB
 
@@ -119,11 +119,14 @@ def fwd_kernel_model(a, p, fwd, logN):
                     assert elem_index(t, e | d, s0, b, logN) == j + (1 << s)
                     w = fwd[(N >> (s + 1)) + (j >> (s + 1))]
                     U, Y = r[e], r[e | d]
-                    assert U < 4 * p and Y < 4 * p
-                    U = min(U, (U - 2 * p) % 2**32)
+                    assert U < 16 * p and Y < 16 * p
+                    if logN - 1 - s == 7:   # the kernel's only reduction: U < 16p -> < 4p
+                        U = min(U, (U - 8 * p) % 2**32)
+                        U = min(U, (U - 4 * p) % 2**32)
                     Vp = shoup_lazy(Y, w, p)
                     r[e] = U + Vp
                     r[e | d] = U - Vp + 2 * p
+                    assert r[e] < 16 * p and r[e | d] < 16 * p
         if pi < len(rev) - 1:
             smem = {}
             for t in range(nthr):
@@ -179,6 +182,15 @@ def main():
     for logN in range(8, 14):
         msg = bank_check(logN)
         print(f"logN={logN}: exchanges/tile", "conflict-free" if msg is None else msg)
+    for logN in range(8, 14):  # lazy bounds (units of p) of the kernel's reduction schedule
+        b = 2
+        for k in range(logN):
+            if k == 7:
+                b = 4
+            b += 2
+            assert b <= 16, (logN, k)
+        assert b <= 16 and 16 * max(P) < 2**32
+    print("lazy butterfly bounds < 16p < 2^32 for logN 8..13 (one reduction, at stage 7)")
     rng = random.Random(5)
     q_in = 39
     for logN in (8, 9):
