@@ -17,13 +17,15 @@
 // Kernels:
 //   ks_tables_kernel    psi^{+-bitrev(k)} with Shoup companions for the two primes, and the
 //                       per-thread regrouped table of the register NTT's last phase
-//   ks_khat_kernel      K_hat = NTT(hi / lo half of the centred KSK row) * N^-1 * 2^32, thread order
-//                       [server, once per key]
-//   ks_ntt_kernel<LOGN> the hot kernel: one CTA per (token, group g, prime, K-split); NG groups
-//                       of N/16 threads each take columns (l, i) of a 16-column digit tile staged
-//                       in shared memory, run the forward NTT of D_{l,i} in registers (16 values
-//                       per thread, exchanges through conflict-free layouts, tools/ntt_ks_model.py)
-//                       and accumulate D_hat o K_hat_{A,B}{hi,lo} (Montgomery, lazy)
+//   ks_khat_kernel      K_hat = NTT(hi / lo half of the centred KSK row) * N^-1 * 2^32 (Montgomery),
+//                       thread order [server, once per key]
+//   ks_ntt_kernel<LOGN, MRG> the hot kernel: one CTA per (token, ciphertext g, K-split) holding both
+//                       primes (MRG, large grids) or per prime (small grids); groups of N/8 threads
+//                       take columns (l, i) of a 16-column digit tile (cp.async-staged, swizzled in
+//                       shared memory), run the forward NTT of D_{l,i} in registers (8 values per
+//                       thread, 3-bit phases, conflict-free exchanges with one named barrier each,
+//                       values lazily < 16p with a single reduction; tools/ntt_ks_model.py) and
+//                       accumulate D_hat o K_hat_{A,B}{hi,lo} (Montgomery, lazy)
 //   ks_finalize_kernel  sum of the K-split partials, inverse NTTs (2 primes x 4 parts), CRT,
 //                       mod 2^q_in -> the uint64 accumulator of pack_finalize_kernel
 #include <cstdint>
@@ -206,7 +208,7 @@ ks_khat_kernel(KParams kp, const uint64_t *__restrict__ ksk, const uint2 *__rest
 
 // ---------------------------------------------------------------- the hot kernel
 struct KsArgs {
-  const uint2 *tabs;       // table section (fwd [3][N] first, p1 after inv)
+  const uint2 *tabs;       // table section: fwd [2][N], inv [2][N], last-phase twiddles [2][7][N/8]
   const uint32_t *khat;    // [2 primes][4N rows][NKP][N]
   const int8_t *digits;    // [T][R256][4][N]
   int64_t T, R256, G;
