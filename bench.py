@@ -173,10 +173,19 @@ def run_ours(args):
     import synth
 
     rank, world, local = dist_env()
+    # PHE_BENCH_SHARED_GPU=1 (test hook, tests/test_gpu_torchrun.py): every rank on the box's one
+    # GPU with gloo plumbing, so the N > 1 path (sharding, max-over-ranks, gathers) runs under
+    # torchrun on a 1-GPU box.  The driver's runs leave it unset: one GPU per rank, NCCL.
+    shared = os.environ.get("PHE_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(dev))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(dev))
     phe.load()
     p = phe.params(phe.PRESET_PAPER)
     T = args.tokens
