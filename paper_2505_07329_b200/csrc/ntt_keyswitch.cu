@@ -444,8 +444,21 @@ __global__ void __launch_bounds__(ks_ng<LOGN>() * ks_nt<LOGN>(), 1) ks_ntt_kerne
       uint32_t r[V];
 #pragma unroll
       for (int e = 0; e < V; e++) r[e] = (uint32_t)((int32_t)cb[eidx<LOGN, FS0, FB>(0, e) * TILE] + (int32_t)p);
+      // KS_EXP_* are timing-only builds (outputs wrong by construction) behind the cost split in
+      // profiles/r1_summary.md: forward NTT dropped / K_hat loads made L1-hot / pointwise dropped
+#ifndef KS_EXP_NO_NTT
       fntt_regs<LOGN, KF>(r, tw1, twl, p, xb, cur, tid, grp);
+#endif
+#ifdef KS_EXP_KHAT_FIXED
+      const uint4 *kr = reinterpret_cast<const uint4 *>(a.khat + (((int64_t)q * KS_LEVELS * N) * NKP) * N) + tid;
+#else
       const uint4 *kr = reinterpret_cast<const uint4 *>(a.khat + (((int64_t)q * KS_LEVELS * N + row0 + c) * NKP) * N) + tid;
+#endif
+#ifdef KS_EXP_NO_POINTWISE
+#pragma unroll
+      for (int e = 0; e < V; e++) acc[e & 3][e] += r[e];
+      continue;
+#endif
 #pragma unroll
       for (int pt = 0; pt < NKP; pt++) {
 #pragma unroll
