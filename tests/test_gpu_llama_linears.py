@@ -10,6 +10,8 @@ oracle's own ChaCha20 re-expansion of the seeds; every (tau, j) output through t
 decryption invariant b - <a, S> = Delta (M v)_j; the tc and NTT paths
 word-identical; and the fused 39 -> 26 switch against the oracle's modswitch on the
 sampled words."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -82,3 +84,50 @@ def test_llama_linear_full_size(phe, coracle, name, d_out, d_in, transpose):
     assert np.array_equal(sw, O.modswitch(got, 39, 26))
     y26 = phe.decrypt_unpack(p, S, m26, b26, 26).double()
     assert (y26 - mv).abs().max().item() <= 1 + int(S.sum().item())
+
+
+@pytest.mark.parametrize("transpose", [False, True], ids=["fwd", "bwd_T"])
+@pytest.mark.parametrize("name,d_out,d_in", SHAPES, ids=[s[0] for s in SHAPES])
+def test_llama_linear_packed_training_step_config(phe, coracle, name, d_out, d_in, transpose):
+    """The packed primitive (Eq. 6 -> Decomp digits -> Eq. 8 KeySwitch -> Eq. 7 rotate-sum ->
+    switch; NEXT #1) per linear in bench.py's `stack_packed` launch configuration: T = 16 (the
+    paper's training step, B = 1, C = 16), stage 1 in the NTT domain, stage 2 in the NTT
+    domain.  Checked: the NTT stages == the tensor-core stages word for word (G = d_out / N groups,
+    up to 4); one token against the oracle's own keygen, KSK, literal Eq. 6 and literal Eq. 7/8;
+    every output decrypts to M v within the gamma-MSB contract."""
+    p = phe.params(phe.PRESET_PAPER)
+    T = 16
+    W = synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED + d_out + 3 * d_in)
+    M = np.ascontiguousarray(W.T) if transpose else W
+    v_len, r_out = M.shape[1], M.shape[0]
+    v = synth.gradients_int8(T, v_len) if transpose else synth.activations_int8(T, v_len)
+    S = phe.keygen(p, 5)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(v).to(DEV), 77)
+    ksk = phe.ksk_gen(p, S, 1234)
+    tabs = phe.NttTables(p)
+    wn = phe.NttWeights(p, tabs, torch.from_numpy(W).to(DEV), transpose=transpose)
+    dig, bod = phe.matmul_clear_digits_ntt(p, wn, phe.ntt_ct_prepare(p, tabs, seeds, body), T)
+    got = phe.pack_ntt(p, dig, bod, phe.NttKeySwitchKey(p, ksk))
+    w = phe.Weights(p, torch.from_numpy(W).to(DEV), transpose=transpose)
+    dig_t, bod_t = phe.matmul_clear_digits(p, w, phe.ct_prepare(p, seeds, body), T)
+    assert torch.equal(dig, dig_t) and torch.equal(bod, bod_t)
+    ref = phe.pack(p, dig_t, bod_t, phe.KeySwitchKey(p, ksk))
+    torch.cuda.synchronize()
+    G = (r_out + p.N - 1) // p.N
+    assert got.shape == (T, G, 2, p.N) and torch.equal(got, ref)
+    # one token through the oracle (O(rows L N^2) + O(rows 4 N^2) in C/OpenMP)
+    op = Params(N=p.N, q_in=p.q_in, q_out=p.q_out, beta=p.beta, gamma=p.gamma)
+    So = O.keygen(5, op.N)
+    KA, KB = coracle.ksk_gen(op, So, 1234, nthreads=os.cpu_count())
+    seeds_o = O.block_seeds(77, T, op.L(v_len))
+    assert np.array_equal(_u64(seeds), seeds_o)
+    g = got.cpu().numpy().astype(np.uint32).astype(np.uint64)
+    tau = 11
+    A, B = O.encrypt(op, So, v[tau], seeds_o[tau])
+    m, b = coracle.matmul_clear_literal(op, M, A, B, nthreads=os.cpu_count())
+    PA, PB = coracle.pack(op, m, b, KA, KB, nthreads=os.cpu_count())
+    assert np.array_equal(g[tau, :, 0], O.modswitch(PA, op.q_in, op.q_out))
+    assert np.array_equal(g[tau, :, 1], O.modswitch(PB, op.q_in, op.q_out))
+    y = phe.decrypt_packed(p, S, got, r_out).double()
+    mv = torch.from_numpy(v).to(DEV).double() @ torch.from_numpy(M).to(DEV).double().T
+    assert (y - mv).abs().max().item() < 2 ** 15
