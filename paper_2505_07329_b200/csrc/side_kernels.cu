@@ -635,6 +635,85 @@ __global__ void wire_u32_kernel(uint32_t *__restrict__ vals, int64_t nseg, int s
   }
 }
 
+// Staged variants (one CTA per segment, grid-strided; segments up to 48 KB): the segment is first
+// copied to shared memory by every thread at once (16-byte loads of the values / 8-byte loads of
+// the stream words), so each thread has several independent loads in flight instead of a chain of
+// 2-4 overlapping ones; the gather / extract then reads shared memory.  Same words as above.
+constexpr int WIRE_THREADS = 256;
+constexpr int WIRE_SMEM_MAX = 48 * 1024;
+// BITS > 0: the coefficient width as a compile-time constant (Table 1's 39 and 26: the word ->
+// coefficient divisions become multiplies); 0: runtime `bits`.
+template <typename WordT, int BITS>
+__global__ void __launch_bounds__(WIRE_THREADS)
+wire_ser_staged_kernel(const WordT *__restrict__ vals, int nvals, int bits_rt, int64_t nseg,
+                       const uint64_t *__restrict__ head, uint64_t *__restrict__ wire) {
+  const int bits = BITS > 0 ? BITS : bits_rt;
+  extern __shared__ __align__(16) uint8_t wsm[];
+  WordT *sv = reinterpret_cast<WordT *>(wsm);
+  const int hw = head != nullptr, nw = (int)(((int64_t)nvals * bits + 63) / 64);
+  const int n16 = nvals * (int)sizeof(WordT) / 16;
+  for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(vals + sg * nvals);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n16; i += WIRE_THREADS) reinterpret_cast<uint4 *>(sv)[i] = __ldcs(src + i);
+    __syncthreads();
+    uint64_t *out = wire + sg * (hw + nw);
+    if (hw && threadIdx.x == 0) out[0] = head[sg];
+    for (int w = threadIdx.x; w < nw; w += WIRE_THREADS) out[hw + w] = gather_word<WordT>(sv, nvals, bits, w);
+    __syncthreads();
+  }
+}
+template <typename WordT, int BITS>
+__global__ void __launch_bounds__(WIRE_THREADS)
+wire_de_staged_kernel(WordT *__restrict__ vals, int nvals, int bits_rt, int64_t nseg, uint64_t *__restrict__ head,
+                      const uint64_t *__restrict__ wire) {
+  const int bits = BITS > 0 ? BITS : bits_rt;
+  extern __shared__ __align__(16) uint8_t wsm[];
+  uint64_t *sw = reinterpret_cast<uint64_t *>(wsm);
+  const int hw = head != nullptr, nw = (int)(((int64_t)nvals * bits + 63) / 64);
+  for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    const uint64_t *src = wire + sg * (hw + nw);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < nw; i += WIRE_THREADS) sw[i] = __ldcs(src + hw + i);
+    if (hw && threadIdx.x == 0) head[sg] = src[0];
+    __syncthreads();
+    WordT *dst = vals + sg * nvals;
+    for (int k = 4 * threadIdx.x; k < nvals; k += 4 * WIRE_THREADS) {
+      if constexpr (sizeof(WordT) == 8) {
+        ulonglong2 *d2 = reinterpret_cast<ulonglong2 *>(dst + k);
+        d2[0] = make_ulonglong2(extract_bits(sw, k, bits), extract_bits(sw, k + 1, bits));
+        d2[1] = make_ulonglong2(extract_bits(sw, k + 2, bits), extract_bits(sw, k + 3, bits));
+      } else {
+        *reinterpret_cast<uint4 *>(dst + k) =
+            make_uint4((uint32_t)extract_bits(sw, k, bits), (uint32_t)extract_bits(sw, k + 1, bits),
+                       (uint32_t)extract_bits(sw, k + 2, bits), (uint32_t)extract_bits(sw, k + 3, bits));
+      }
+    }
+    __syncthreads();
+  }
+}
+// grid: 8 resident 256-thread CTAs per SM x 148 SMs, grid-strided over the segments
+template <typename WordT>
+static int launch_wire_staged(WordT *vals, int nvals, int bits, int64_t nseg, uint64_t *head, uint64_t *wire,
+                              int dir, cudaStream_t st) {
+  const int64_t nw = ((int64_t)nvals * bits + 63) / 64;
+  const size_t smem = dir == 0 ? (size_t)nvals * sizeof(WordT) : (size_t)nw * 8;
+  const unsigned grid = (unsigned)(nseg < 148 * 8 ? nseg : 148 * 8);
+#define PHE_WIRE_LAUNCH(B)                                                                             \
+  do {                                                                                                 \
+    if (dir == 0)                                                                                      \
+      wire_ser_staged_kernel<WordT, B><<<grid, WIRE_THREADS, smem, st>>>(vals, nvals, bits, nseg, head, wire); \
+    else                                                                                               \
+      wire_de_staged_kernel<WordT, B><<<grid, WIRE_THREADS, smem, st>>>(vals, nvals, bits, nseg, head, wire);  \
+  } while (0)
+  if (bits == 39) PHE_WIRE_LAUNCH(39);
+  else if (bits == 26) PHE_WIRE_LAUNCH(26);
+  else PHE_WIRE_LAUNCH(0);
+#undef PHE_WIRE_LAUNCH
+  PHE_CUDA_CHECK_LAUNCH();
+  return PHE_OK;
+}
+
 int launch_wire_u32(uint32_t *vals, int64_t nseg, int seglen, int bits, uint8_t *wire, int64_t seg_words,
                     int64_t per_group, int64_t group_words, int64_t off_words, int dir, cudaStream_t st) {
   if (nseg == 0) return PHE_OK;
@@ -649,6 +728,8 @@ int launch_wire_u32(uint32_t *vals, int64_t nseg, int seglen, int bits, uint8_t 
 int launch_wire_inputs(const KParams &kp, uint64_t *seeds, uint64_t *body, int64_t nblk, uint8_t *wire,
                        int dir, cudaStream_t st) {
   if (nblk == 0) return PHE_OK;
+  if ((size_t)kp.N * 8 <= WIRE_SMEM_MAX)
+    return launch_wire_staged<uint64_t>(body, kp.N, kp.q_in, nblk, seeds, reinterpret_cast<uint64_t *>(wire), dir, st);
   const int nx = dir == 0 ? 1 + kp.N * kp.q_in / 64 : kp.N / 4 + 1;
   const dim3 grid((unsigned)((nx + 255) / 256), (unsigned)(nblk < 65535 ? nblk : 65535));
   wire_inputs_kernel<<<grid, 256, 0, st>>>(kp.N, kp.q_in, seeds, body, nblk, reinterpret_cast<uint64_t *>(wire), dir);
@@ -658,6 +739,8 @@ int launch_wire_inputs(const KParams &kp, uint64_t *seeds, uint64_t *body, int64
 
 int launch_wire_packed(const KParams &kp, uint32_t *packed, int64_t nct, uint8_t *wire, int dir, cudaStream_t st) {
   if (nct == 0) return PHE_OK;
+  if ((size_t)2 * kp.N * 4 <= WIRE_SMEM_MAX)
+    return launch_wire_staged<uint32_t>(packed, 2 * kp.N, kp.q_out, nct, nullptr, reinterpret_cast<uint64_t *>(wire), dir, st);
   const int nx = dir == 0 ? 2 * kp.N * kp.q_out / 64 : 2 * kp.N / 4;
   const dim3 grid((unsigned)((nx + 255) / 256), (unsigned)(nct < 65535 ? nct : 65535));
   wire_packed_kernel<<<grid, 256, 0, st>>>(kp.N, kp.q_out, packed, nct, reinterpret_cast<uint64_t *>(wire), dir);
