@@ -47,8 +47,9 @@ def parse():
     ap.add_argument("--contraction", choices=["tc", "ntt", "hybrid"], default=None,
                     help="mask contraction a5: tc = int8 limb GEMM on tcgen05 (north_star; the default), ntt = NTT "
                          "domain (NEXT #4, CUDA cores), hybrid = ntt for multi-block (L >= 2) linears, tc otherwise; "
-                         "packed workloads below 512 tokens default to ntt (a 16-token batch fills a third of a "
-                         "51-token tensor-core tile)")
+                         "packed workloads default to ntt for stage 1 (T = 16: a 16-token batch fills a third of a "
+                         "51-token tensor-core tile; T = 2048: 45 vs 50 ms, and the step then stays at the "
+                         "uncapped clock for the NTT KeySwitch: 6.85k vs 6.40k tok/s)")
     ap.add_argument("--tokens", type=int, default=None,
                     help="tokens per rank (default B*C = 8*256 = 2048; stack_packed: the paper's training "
                          "step, B*C = 1*16)")
@@ -65,7 +66,7 @@ def parse():
     if args.tokens is None:  # B*C = 8*256; the paper's training step is B = 1, C = 16
         args.tokens = 16 if args.workload == "stack_packed" else 2048
     if args.contraction is None:
-        args.contraction = "ntt" if args.workload.endswith("_packed") and args.tokens < 512 else "tc"
+        args.contraction = "ntt" if args.workload.endswith("_packed") else "tc"
     return args
 
 
@@ -467,8 +468,22 @@ def run_ours(args):
         hi = phe.wire_serialize_inputs(p, seeds, body).cpu().pin_memory()
         G0 = (w.rows + p.N - 1) // p.N
         ho = torch.empty((T, G0, phe.wire_output_bytes(p)), dtype=torch.uint8, pin_memory=True)
-        swh = phe.server_wire_host if args.pack == "tc" else phe.server_wire_host_ntt
+        if isinstance(w, phe.NttWeights) and args.pack == "ntt":   # both stages in the NTT domain
+            swh, api = phe.server_wire_host_nttw, "phe_server_wire_host_nttw"
+        else:  # tensor-core stage 1: the registration the host pipeline takes
+            if isinstance(w, phe.NttWeights):
+                W0 = synth.weights_int8_torch(w.d_out, w.d_in, seed=synth.MASTER_SEED, device=dev)
+                w = phe.Weights(p, W0, transpose=w.transpose)
+                del W0
+            swh, api = ((phe.server_wire_host, "phe_server_wire_host") if args.pack == "tc" else
+                        (phe.server_wire_host_ntt, "phe_server_wire_host_ntt"))
         swh(p, w, K, hi, ho, chunk_tokens=255)
+        verified = None
+        if chunk >= T:  # the device step's packed outputs for the same inputs are still in pk_flat
+            dev_wire = phe.wire_serialize_packed(p, pk_flat[: T * G0 * 2 * p.N].view(T, G0, 2, p.N)).cpu()
+            verified = bool(torch.equal(dev_wire.view(-1), ho.view(-1)))
+            if not verified:
+                raise RuntimeError(f"e2e: {api} output differs from the device step's packed ciphertexts")
         wall = []
         for _ in range(max(2, min(args.steps, 3))):
             t0 = time.perf_counter()
@@ -481,8 +496,8 @@ def run_ours(args):
         e2e = {"value": round(world * T / float(te.item()), 2), "unit": "tokens/s",
                "h2d_bytes_per_step": int(hi.numel()), "d2h_bytes_per_step": int(ho.numel()),
                "ms_per_step": round(float(te.item()) * 1e3, 2),
-               "api": ("phe_server_wire_host" if args.pack == "tc" else "phe_server_wire_host_ntt") +
-                      " (wire-format bytes in/out, pinned host buffers, 255-token chunks)"}
+               "api": api + " (wire-format bytes in/out, pinned host buffers, 255-token chunks)",
+               "output_equals_device_step": verified}
     if (not args.no_e2e and not args.profile and args.workload == "q_proj" and not rows_mode
             and args.contraction == "tc"):
         name, w, _ = regs[0]

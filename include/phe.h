@@ -364,7 +364,14 @@ int phe_pack_ntt(const phe_params *p, const void *d_digits, const uint64_t *d_bo
 /* phe_matmul_clear_packed_ntt: the whole primitive as phe_matmul_clear_packed (same contract and
  *   output), stage 1 (Eq. 6 -> Decomp digits) on the tensor cores, stage 2 through phe_pack_ntt;
  *   d_nksk from phe_ntt_ksk_prepare, d_ws of phe_packed_ntt_ws_bytes(p, rows, T) bytes.
- * phe_server_wire_host_ntt: phe_server_wire_host with phe_matmul_clear_packed_ntt inside.      */
+ * phe_server_wire_host_ntt: phe_server_wire_host with phe_matmul_clear_packed_ntt inside.
+ * phe_matmul_clear_packed_nttw: the same primitive with stage 1 in the NTT domain as well
+ *   (phe_matmul_clear_digits_ntt on d_nttw from phe_ntt_weights_prepare and d_operand from
+ *   phe_ntt_ct_prepare, d_tables from phe_ntt_tables_init), then phe_pack_ntt; same output, d_ws
+ *   of phe_packed_ntt_ws_bytes(p, rows, T) bytes; errors as phe_matmul_clear_packed_ntt, and
+ *   EUNSUPPORTED where phe_matmul_clear_digits_ntt is (q_in < 32, L above phe_ntt_max_blocks).
+ * phe_server_wire_host_nttw: phe_server_wire_host with phe_ntt_ct_prepare +
+ *   phe_matmul_clear_packed_nttw inside (NTT weights and tables instead of d_wprep).            */
 size_t phe_packed_ntt_ws_bytes(const phe_params *p, int64_t rows, int64_t T);
 int phe_matmul_clear_packed_ntt(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
                                 int transpose, const void *d_operand, int64_t T, const void *d_nksk,
@@ -372,6 +379,12 @@ int phe_matmul_clear_packed_ntt(const phe_params *p, const void *d_wprep, int64_
 int phe_server_wire_host_ntt(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
                              const void *d_nksk, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
                              uint8_t *h_wire_out, void *stream);
+int phe_matmul_clear_packed_nttw(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                                 int64_t d_in, int transpose, const void *d_operand, int64_t T, const void *d_nksk,
+                                 void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream);
+int phe_server_wire_host_nttw(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                              int64_t d_in, int transpose, const void *d_nksk, const uint8_t *h_wire_in, int64_t T,
+                              int64_t chunk_tokens, uint8_t *h_wire_out, void *stream);
 
 /* ---- introspection (tests / bench) -------------------------------------------------- */
 /* Number of kernel launches the last phe_matmul_clear[_T] on this thread enqueued. */

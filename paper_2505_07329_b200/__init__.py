@@ -40,6 +40,7 @@ EXPORTS = [
     "phe_matmul_clear_ntt", "phe_matmul_clear_ntt_T", "phe_matmul_clear_ct", "phe_encrypt_pack_ntt",
     "phe_ntt_ksk_bytes", "phe_ntt_ksk_prepare", "phe_pack_ntt_ws_bytes", "phe_pack_ntt",
     "phe_packed_ntt_ws_bytes", "phe_matmul_clear_packed_ntt", "phe_server_wire_host_ntt",
+    "phe_matmul_clear_packed_nttw", "phe_server_wire_host_nttw",
     "phe_wire_lwe_bytes", "phe_wire_serialize_lwe", "phe_wire_deserialize_lwe", "phe_server_matvec_wire_host",
     "phe_matmul_clear_digits_ntt", "phe_matmul_clear_into", "phe_matmul_clear_ntt_into",
 ]
@@ -155,6 +156,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                                         ctypes.c_int),
         "phe_server_wire_host_ntt": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp],
                                      ctypes.c_int),
+        "phe_matmul_clear_packed_nttw": ([_P, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp, _vp, _sz, _vp,
+                                          _vp], ctypes.c_int),
+        "phe_server_wire_host_nttw": ([_P, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp],
+                                      ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -563,6 +568,33 @@ def server_wire_host_ntt(p: Params, w: Weights, nksk: "NttKeySwitchKey", h_wire_
     _check(load().phe_server_wire_host_ntt(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
                                            _ptr(nksk.buf), _ptr(h_wire_in), h_wire_in.shape[0], chunk_tokens,
                                            _ptr(h_wire_out), _stream()), "phe_server_wire_host_ntt")
+
+
+def matmul_clear_packed_nttw(p: Params, w: "NttWeights", operand: torch.Tensor, T: int, nksk: "NttKeySwitchKey",
+                             out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """matmul_clear_packed with both stages in the NTT domain (operand from ntt_ct_prepare): same
+    output (phe_matmul_clear_packed_nttw)."""
+    G = (w.rows + p.N - 1) // p.N
+    if out is None:
+        out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=operand.device)
+    nbytes = load().phe_packed_ntt_ws_bytes(ctypes.byref(p), w.rows, T)
+    if ws is None:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=operand.device)
+    _check(load().phe_matmul_clear_packed_nttw(ctypes.byref(p), _ptr(w.tables.buf), _ptr(w.buf), w.d_out, w.d_in,
+                                               int(w.transpose), _ptr(operand), T, _ptr(nksk.buf), _ptr(ws),
+                                               ws.numel(), _ptr(out), _stream()), "phe_matmul_clear_packed_nttw")
+    return out
+
+
+def server_wire_host_nttw(p: Params, w: "NttWeights", nksk: "NttKeySwitchKey", h_wire_in: torch.Tensor,
+                          h_wire_out: torch.Tensor, chunk_tokens: int = 255) -> None:
+    """server_wire_host with both stages in the NTT domain (phe_server_wire_host_nttw)."""
+    for t, n in [(h_wire_in, "h_wire_in"), (h_wire_out, "h_wire_out")]:
+        if t.is_cuda or not t.is_contiguous():
+            raise PheError(f"{n} must be a contiguous host tensor")
+    _check(load().phe_server_wire_host_nttw(ctypes.byref(p), _ptr(w.tables.buf), _ptr(w.buf), w.d_out, w.d_in,
+                                            int(w.transpose), _ptr(nksk.buf), _ptr(h_wire_in), h_wire_in.shape[0],
+                                            chunk_tokens, _ptr(h_wire_out), _stream()), "phe_server_wire_host_nttw")
 
 
 # ------------------------------------------------------------------ NEXT #4: NTT-domain contraction

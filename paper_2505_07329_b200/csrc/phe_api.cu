@@ -649,9 +649,13 @@ int phe_wire_deserialize_packed(const phe_params *p, const uint8_t *d_wire, int6
 
 // The server step as the network sees it (Fig. 1): wire-format input blocks in (9992 B each at
 // Table 1), wire-format packed ciphertexts out (13312 B each).  Chunked, two streams.
-static int server_wire_host_impl(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
-                                 int transpose, const void *d_kprep, const uint8_t *h_wire_in, int64_t T,
-                                 int64_t chunk_tokens, uint8_t *h_wire_out, void *stream, bool ntt_pack) {
+// mode 0: tensor-core stage 1 + packing GEMM; 1: tensor-core stage 1 + NTT-domain packing;
+// 2: NTT-domain stage 1 (d_tables, NTT weights, NTT operand) + NTT-domain packing.
+static int server_wire_host_impl(const phe_params *p, const void *d_tables, const void *d_wprep, int64_t d_out,
+                                 int64_t d_in, int transpose, const void *d_kprep, const uint8_t *h_wire_in,
+                                 int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *stream, int mode) {
+  const bool ntt_pack = mode >= 1, ntt_s1 = mode == 2;
+  if (ntt_s1 && !d_tables) return PHE_EINVAL;
   KParams kp;
   int rc = check_pack(p, &kp);
   if (!rc) rc = check_wire(p, &kp);
@@ -666,7 +670,8 @@ static int server_wire_host_impl(const phe_params *p, const void *d_wprep, int64
   const int64_t C = chunk_tokens < T ? chunk_tokens : T;
   const size_t b_win = round_up(C * L * bin, 256), b_seeds = round_up(C * L * 8, 256);
   const size_t b_body = round_up(C * L * N * 8, 256);
-  const size_t b_op = round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256);
+  const size_t b_op = round_up((int64_t)(ntt_s1 ? phe_ntt_operand_bytes(p, C, L) : phe_ct_operand_bytes(p, C, L)), 256);
+  if (b_op == 0) return PHE_EUNSUPPORTED;
   const size_t b_ws = round_up((int64_t)(ntt_pack ? phe_packed_ntt_ws_bytes(p, rows, C)
                                                    : phe_packed_ws_bytes(p, rows, C)), 256);
   const size_t b_pk = round_up(C * G * 2 * N * 4, 256), b_wout = round_up(C * G * bout, 256);
@@ -701,11 +706,15 @@ static int server_wire_host_impl(const phe_params *p, const void *d_wprep, int64
     uint8_t *d_wout = base + b_win + b_seeds + b_body + b_op + b_ws + b_pk;
     cudaMemcpyAsync(d_win, h_wire_in + t0 * L * bin, n * L * bin, cudaMemcpyHostToDevice, st);
     rc = phe_wire_deserialize_inputs(p, d_win, n, L, d_seeds, d_bod, st);
-    if (!rc) rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
     if (!rc)
-      rc = ntt_pack ? phe_matmul_clear_packed_ntt(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws,
-                                                  d_pk, st)
-                    : phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws, d_pk, st);
+      rc = ntt_s1 ? phe_ntt_ct_prepare(p, d_tables, d_seeds, d_bod, n, L, d_op, b_op, st)
+                  : phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
+    if (!rc)
+      rc = ntt_s1 ? phe_matmul_clear_packed_nttw(p, d_tables, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp,
+                                                 b_ws, d_pk, st)
+           : ntt_pack ? phe_matmul_clear_packed_ntt(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws,
+                                                    d_pk, st)
+                      : phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws, d_pk, st);
     if (!rc) rc = phe_wire_serialize_packed(p, d_pk, n * G, d_wout, st);
     if (rc) return rc;
     cudaMemcpyAsync(h_wire_out + t0 * G * bout, d_wout, n * G * bout, cudaMemcpyDeviceToHost, st);
@@ -722,14 +731,20 @@ static int server_wire_host_impl(const phe_params *p, const void *d_wprep, int64
 int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
                          const void *d_kprep, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
                          uint8_t *h_wire_out, void *stream) {
-  return server_wire_host_impl(p, d_wprep, d_out, d_in, transpose, d_kprep, h_wire_in, T, chunk_tokens, h_wire_out,
-                               stream, false);
+  return server_wire_host_impl(p, nullptr, d_wprep, d_out, d_in, transpose, d_kprep, h_wire_in, T, chunk_tokens,
+                               h_wire_out, stream, 0);
 }
 int phe_server_wire_host_ntt(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
                              const void *d_nksk, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
                              uint8_t *h_wire_out, void *stream) {
-  return server_wire_host_impl(p, d_wprep, d_out, d_in, transpose, d_nksk, h_wire_in, T, chunk_tokens, h_wire_out,
-                               stream, true);
+  return server_wire_host_impl(p, nullptr, d_wprep, d_out, d_in, transpose, d_nksk, h_wire_in, T, chunk_tokens,
+                               h_wire_out, stream, 1);
+}
+int phe_server_wire_host_nttw(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                              int64_t d_in, int transpose, const void *d_nksk, const uint8_t *h_wire_in, int64_t T,
+                              int64_t chunk_tokens, uint8_t *h_wire_out, void *stream) {
+  return server_wire_host_impl(p, d_tables, d_nttw, d_out, d_in, transpose, d_nksk, h_wire_in, T, chunk_tokens,
+                               h_wire_out, stream, 2);
 }
 
 // ================================================================ LWE outputs on the wire
@@ -1118,6 +1133,32 @@ int phe_matmul_clear_packed_ntt(const phe_params *p, const void *d_wprep, int64_
   void *ws2 = reinterpret_cast<uint8_t *>(body) + round_up(T * rows * 8, 256);
   // (1) Eq. 6 on the tensor cores, masks written as Decomp digits; (2) Eq. 7/8 in the NTT domain
   rc = phe_matmul_clear_digits(p, d_wprep, d_out, d_in, transpose, d_operand, T, digits, body, stream);
+  if (rc) return rc;
+  const int l1 = g_last_launches;
+  rc = phe_pack_ntt(p, digits, body, T, rows, d_nksk, ws2, phe_pack_ntt_ws_bytes(p, rows, T), d_out_packed, stream);
+  if (rc) return rc;
+  g_last_launches += l1;
+  return PHE_OK;
+}
+
+int phe_matmul_clear_packed_nttw(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
+                                 int64_t d_in, int transpose, const void *d_operand, int64_t T, const void *d_nksk,
+                                 void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_ntt_ks(p, &kp);
+  if (rc) return rc;
+  if (d_out < 1 || d_in < 1 || T < 0 || (transpose != 0 && transpose != 1)) return PHE_EINVAL;
+  if (T == 0) return PHE_OK;
+  if (!d_tables || !d_nttw || !d_operand || !d_nksk || !d_ws || !d_out_packed) return PHE_EINVAL;
+  const int64_t rows = transpose ? d_in : d_out;
+  if (ws_bytes < phe_packed_ntt_ws_bytes(p, rows, T)) return PHE_ENOMEM;
+  const int64_t N = p->N, rp = round_up(rows, 256);
+  uint8_t *digits = static_cast<uint8_t *>(d_ws);
+  uint64_t *body = reinterpret_cast<uint64_t *>(digits + round_up(T * rp * phe::KS_LEVELS * N, 256));
+  void *ws2 = reinterpret_cast<uint8_t *>(body) + round_up(T * rows * 8, 256);
+  // (1) Eq. 6 in the NTT domain, masks written as Decomp digits; (2) Eq. 7/8 in the NTT domain
+  rc = phe_matmul_clear_digits_ntt(p, d_tables, d_nttw, d_out, d_in, transpose, d_operand, T, digits, body, stream);
   if (rc) return rc;
   const int l1 = g_last_launches;
   rc = phe_pack_ntt(p, digits, body, T, rows, d_nksk, ws2, phe_pack_ntt_ws_bytes(p, rows, T), d_out_packed, stream);

@@ -128,6 +128,14 @@ def test_packed_ntt_primitive_and_wire_host(phe):
     phe.server_wire_host_ntt(p, w, NK, hi, ho_ntt, chunk_tokens=2)
     assert torch.equal(ho_ref, ho_ntt)
     assert torch.equal(phe.wire_deserialize_packed(p, ho_ntt.to(DEV)).view(T, 1, 2, p.N), ref)
+    # both stages in the NTT domain (NTT weights + NTT operand): the same words and wire bytes
+    tabs = phe.NttTables(p)
+    wn = phe.NttWeights(p, tabs, torch.from_numpy(W).to(DEV))
+    got_w = phe.matmul_clear_packed_nttw(p, wn, phe.ntt_ct_prepare(p, tabs, s2, b2), T, NK)
+    assert torch.equal(got_w, ref)
+    ho_w = torch.empty_like(ho_ref).pin_memory()
+    phe.server_wire_host_nttw(p, wn, NK, hi, ho_w, chunk_tokens=2)
+    assert torch.equal(ho_w, ho_ref)
 
 
 @pytest.mark.slow
