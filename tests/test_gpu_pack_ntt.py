@@ -109,6 +109,18 @@ def test_pack_ntt_empty_and_errors(phe):
         phe.pack_ntt(p, torch.zeros((1, 256, 4, 256), dtype=torch.int8, device=DEV),
                      torch.zeros((1, 256), dtype=torch.int64, device=DEV), nk,
                      ws=torch.empty(16, dtype=torch.uint8, device=DEV))
+    # both stages in the NTT domain (its smallest ring, N = 512): T = 0 is a no-op, a short
+    # workspace is refused
+    p5 = phe.params(phe.PRESET_PAPER, N=512)
+    nk5 = phe.NttKeySwitchKey(p5, torch.zeros((2, 4 * 512, 512), dtype=torch.int64, device=DEV))
+    tabs = phe.NttTables(p5)
+    wn = phe.NttWeights(p5, tabs, torch.from_numpy(synth.weights_int8(700, 512, seed=9)).to(DEV))
+    opnd = torch.empty(phe.load().phe_ntt_operand_bytes(__import__("ctypes").byref(p5), 1, 1), dtype=torch.uint8,
+                       device=DEV)
+    out0 = phe.matmul_clear_packed_nttw(p5, wn, opnd, 0, nk5)
+    assert out0.shape == (0, 2, 2, 512)
+    with pytest.raises(phe.PheError):
+        phe.matmul_clear_packed_nttw(p5, wn, opnd, 1, nk5, ws=torch.empty(16, dtype=torch.uint8, device=DEV))
 
 
 def test_packed_ntt_primitive_and_wire_host(phe):
