@@ -97,7 +97,10 @@ int phe_encrypt_pack(const phe_params *p, const uint8_t *d_S, const int8_t *d_x,
  *   [rows][Lc][2N][16] int8  "16-shift expansion" of wext_{j,i}[m] = M[j,iN+m] (m < N),
  *                            -M[j,iN+m-N] (N <= m < 2N), 0 beyond cols/2N; Lc = ceil(cols/N)
  *   [rows][Lc*N]       int8  M, zero-padded to Lc*N columns (body GEMM operand)
- * Errors: EINVAL on dims, ENOMEM if bytes is too small.  |w| <= 127 is the caller's contract.  */
+ * Errors: EINVAL on dims, ENOMEM if bytes is too small, ERANGE if some weight is -128: symmetric
+ *   quantization gives w in [-127, 127], and encode_weights refuses out-of-range
+ *   weights.  The range check runs on the device and SYNCHRONISES `stream` (once per
+ *   model); on ERANGE nothing else was enqueued and d_wprep's contents are unspecified.       */
 size_t phe_weights_bytes(const phe_params *p, int64_t rows, int64_t cols);
 int phe_weights_prepare(const phe_params *p, const int8_t *d_W, int64_t d_out, int64_t d_in,
                         int transpose, void *d_wprep, size_t bytes, void *stream);
@@ -286,7 +289,9 @@ int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out
  *               [op_rows][L*N] uint8 body limb planes (the second half of phe_ct_prepare's layout)
  *             NTT-domain vectors: element k of the bit-reversed transform output is stored at
  *             word 4*(((k>>2)&3)*(N/16) + (k>>4)) + (k&3) (the hot kernel's thread order).
- * Errors as phe_matmul_clear; EUNSUPPORTED for N or L outside the range above.              */
+ * Errors as phe_matmul_clear; EUNSUPPORTED for N or L outside the range above; ERANGE (after a
+ * synchronising device-side check, as phe_weights_prepare) if some weight is -128 (P:150-164,
+ * S:253-255): both contractions accept exactly the same weights.                             */
 int phe_ntt_primes(uint32_t *out2);
 int64_t phe_ntt_max_blocks(const phe_params *p);
 size_t phe_ntt_tables_bytes(const phe_params *p);

@@ -45,6 +45,8 @@ class COracle:
         L.oracle_mask_entries.argtypes = [ctypes.c_int, ctypes.c_int, _i8p, ctypes.c_int64,
                                           _u64p, _i64p, _i64p, ctypes.c_int64, _u64p]
         L.oracle_modswitch.argtypes = [_u64p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _u64p]
+        L.oracle_mask_projection.argtypes = [ctypes.c_int, ctypes.c_int, _i8p, ctypes.c_int64, ctypes.c_int64,
+                                             _u64p, ctypes.c_int64, _u64p, ctypes.c_int, _u64p, ctypes.c_int]
         L.oracle_ksk_gen.argtypes = [ctypes.c_int, ctypes.c_int, _u8p, ctypes.c_uint64, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, _u64p, _u64p, ctypes.c_int]
         L.oracle_decompose.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -86,6 +88,20 @@ class COracle:
         self.lib.oracle_mask_entries(params.N, params.q_in, _p(W, _i8p), W.shape[1],
                                      _p(A, _u64p), _p(js, _i64p), _p(ts, _i64p), len(js),
                                      _p(out, _u64p))
+        return out
+
+    def mask_projection(self, params, W: np.ndarray, A: np.ndarray, r: np.ndarray, nthreads: int = 1):
+        """Freivalds projections sum_t a_{tau,j}[t] r_e[t] mod 2^q_in of Eq. 6's masks for matrix W,
+        masks A [T][L][N], vectors r [nr][N]: returns [T][d_out][nr] (see phe_oracle.c)."""
+        W = np.ascontiguousarray(W, dtype=np.int8)
+        A = np.ascontiguousarray(A, dtype=np.uint64)
+        r = np.ascontiguousarray(r, dtype=np.uint64)
+        d_out, d_in = W.shape
+        T = A.shape[0]
+        assert A.shape == (T, params.L(d_in), params.N) and r.shape[1] == params.N
+        out = np.zeros((T, d_out, r.shape[0]), np.uint64)
+        self.lib.oracle_mask_projection(params.N, params.q_in, _p(W, _i8p), d_out, d_in, _p(A, _u64p), T,
+                                        _p(r, _u64p), r.shape[0], _p(out, _u64p), nthreads)
         return out
 
     def modswitch(self, v: np.ndarray, q_from: int, q_to: int) -> np.ndarray:

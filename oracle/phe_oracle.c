@@ -141,6 +141,47 @@ void oracle_mask_entries(int N, int q_in, const int8_t *W, int64_t d_in, const u
   }
 }
 
+/* Freivalds projection of Eq. 6's LWE masks (a TEST PIN over all outputs, not a step of the method).
+ * For r in Z_Q^N:  sum_t a_j[t] r[t] = sum_c W[j,c] sum_t At_i[m,t] r[t]   (c = iN + m; the closed
+ * form above, At_i[m,t] = A_i[m-t] (m >= t), -A_i[m-t+N] (m < t))
+ *                                    = sum_c W[j,c] (A_i * r)[m]            (negacyclic product, P:90:
+ * (A*r)[m] = sum_{t<=m} A[m-t] r[t] - sum_{t>m} A[m-t+N] r[t]).  One product per (token, block, r),
+ * then a plain matvec, so every output (tau, j) of a full-size run is checked against nr random
+ * projections without evaluating the N^2 closed-form entries.
+ * A: [T][L][N] residues; r: [nr][N] residues (< 2^63); out: [T][d_out][nr] mod 2^q_in. */
+void oracle_mask_projection(int N, int q_in, const int8_t *W, int64_t d_out, int64_t d_in, const uint64_t *A,
+                            int64_t T, const uint64_t *r, int nr, uint64_t *out, int nthreads) {
+  int L = (int)((d_in + N - 1) / N);
+  uint64_t qm = (q_in >= 64) ? ~0ull : ((1ull << q_in) - 1);
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel
+#endif
+  {
+    int64_t *rv = (int64_t *)malloc(sizeof(int64_t) * (size_t)N);
+    uint64_t *u = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)L * N * nr); /* [nr][L*N] */
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+    for (int64_t tau = 0; tau < T; tau++) {
+      for (int e = 0; e < nr; e++) {
+        for (int k = 0; k < N; k++) rv[k] = (int64_t)r[(int64_t)e * N + k];
+        for (int i = 0; i < L; i++)
+          negacyclic_mul(A + (tau * L + i) * (int64_t)N, rv, N, u + ((int64_t)e * L + i) * N);
+      }
+      for (int64_t j = 0; j < d_out; j++)
+        for (int e = 0; e < nr; e++) {
+          const uint64_t *ue = u + (int64_t)e * L * N;
+          uint64_t acc = 0;
+          for (int64_t c = 0; c < d_in; c++) acc += (uint64_t)(int64_t)W[j * d_in + c] * ue[c];
+          out[(tau * d_out + j) * nr + e] = acc & qm;
+        }
+    }
+    free(rv);
+    free(u);
+  }
+}
+
 /* ModulusSwitch, round half up (R8): floor((v + 2^(s-1)) / 2^s) mod 2^q_to. */
 void oracle_modswitch(const uint64_t *v, int64_t n, int q_from, int q_to, uint64_t *out) {
   int s = q_from - q_to;

@@ -329,6 +329,25 @@ def body_closed_form(params: Params, W: np.ndarray, B: np.ndarray) -> np.ndarray
     return out
 
 
+def body_projection(params: Params, W: np.ndarray, B: np.ndarray, rp: np.ndarray) -> np.ndarray:
+    """Freivalds projection of the bodies (a TEST PIN over all outputs, not a method step):
+    sum_j rp[j] b_{tau,j} mod Q for B [T][L][N], with b_j = body_closed_form (the N-1 coefficient
+    of B*w_hat):  sum_j rp[j] sum_c W[j,c] B[c] = sum_c (sum_j rp[j] W[j,c]) B[c].
+    uint64 wrap-around arithmetic is exact mod Q = 2^q (R3).  Returns [T] uint64."""
+    d_out, d_in = W.shape
+    T = B.shape[0]
+    with np.errstate(over="ignore"):
+        Wu = W.astype(np.int64).astype(U64)                      # two's complement mod 2^64
+        v = np.zeros(d_in, dtype=U64)
+        for j in range(d_out):                                   # v = rp^T W
+            v += U64(int(rp[j])) * Wu[j]
+        flat = B.reshape(T, -1)[:, :d_in].astype(U64)
+        out = np.zeros(T, dtype=U64)
+        for tau in range(T):
+            out[tau] = np.sum(flat[tau] * v, dtype=U64)
+    return out & U64(params.Q - 1)
+
+
 # --------------------------------------------------------------------------------------
 # a8: ModulusSwitch q_from -> q_to  (P:88, P:185); round half up (R8, S:53)
 # --------------------------------------------------------------------------------------

@@ -28,12 +28,28 @@ def deps():
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc -c per translation unit (in parallel), then one nvcc -shared link."""
+    from concurrent.futures import ThreadPoolExecutor
     stale = force or not os.path.exists(OUT) or any(
         os.path.getmtime(d) > os.path.getmtime(OUT) for d in deps())
     if stale:
-        cmd = [NVCC, *FLAGS, "-o", OUT, *sources()]
+        objdir = os.path.join(HERE, "build")
+        os.makedirs(objdir, exist_ok=True)
+        cflags = [f for f in FLAGS if f != "-shared"]
+
+        def compile_one(src):
+            obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+            cmd = [NVCC, *cflags, "-c", "-o", obj, src]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.check_call(cmd)
+            return obj
+
+        with ThreadPoolExecutor(max_workers=len(sources())) as ex:
+            objs = list(ex.map(compile_one, sources()))
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs]
         if verbose:
-            print(" ".join(cmd))
+            print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
     return OUT
 

@@ -128,6 +128,8 @@ int phe_weights_prepare(const phe_params *p, const int8_t *d_W, int64_t d_out, i
     return PHE_EINVAL;
   int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
   if (bytes < phe_weights_bytes(p, rows, cols)) return PHE_ENOMEM;
+  rc = phe::check_weights_range(d_W, d_out * d_in, static_cast<unsigned *>(d_wprep), S(stream));
+  if (rc) return rc;
   return phe::launch_weights_prepare(kp, d_W, d_out, d_in, transpose, d_wprep, S(stream));
 }
 
@@ -920,6 +922,8 @@ int phe_ntt_weights_prepare(const phe_params *p, const void *d_tables, const int
     return PHE_EINVAL;
   const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
   if (bytes < phe_ntt_weights_bytes(p, rows, cols)) return PHE_ENOMEM;
+  rc = phe::check_weights_range(d_W, d_out * d_in, static_cast<unsigned *>(d_nttw), S(stream));
+  if (rc) return rc;
   const int64_t Lc = phe_num_blocks(p, cols);
   uint32_t *what = static_cast<uint32_t *>(d_nttw);
   rc = phe::launch_ntt_weights(kp, d_tables, d_W, d_out, d_in, transpose, what, S(stream));

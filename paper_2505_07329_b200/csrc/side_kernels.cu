@@ -120,6 +120,34 @@ __global__ void weights_expand_kernel(const int8_t *__restrict__ W, int64_t d_in
   exp16[idx] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
 }
 
+// Symmetric int8 weights lie in [-127, 127] (symmetric quantization, zero-point 0;
+// encode_weights refuses out-of-range weights).  The one int8 value outside that range,
+// -128, has no negation in int8 (the Hankel operand stores -w for the negacyclic wrap), so
+// registration refuses it: *flag != 0 iff some byte of W is 0x80.  One grid-stride pass with
+// 16-byte loads (bytes before a 16-byte boundary / after the last full vector byte-wise).
+__global__ void weights_range_kernel(const int8_t *__restrict__ W, int64_t n, unsigned *__restrict__ flag) {
+  const uint8_t *b = reinterpret_cast<const uint8_t *>(W);
+  const int64_t head = (int64_t)((16 - (reinterpret_cast<uintptr_t>(b) & 15)) & 15);
+  const int64_t h = head < n ? head : n;
+  const int64_t nvec = (n - h) / 16;
+  const uint4 *v = reinterpret_cast<const uint4 *>(b + h);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned bad = 0;
+  for (int64_t k = tid; k < nvec; k += stride) {
+    uint4 q = v[k];
+    uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      uint32_t x = w[c] ^ 0x80808080u;  // byte == 0x80  <=>  byte of x == 0
+      bad |= (x - 0x01010101u) & ~x & 0x80808080u;
+    }
+  }
+  for (int64_t k = tid; k < h; k += stride) bad |= (b[k] == 0x80u);
+  for (int64_t k = h + nvec * 16 + tid; k < n; k += stride) bad |= (b[k] == 0x80u);
+  if (__any_sync(0xffffffffu, bad != 0) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 __global__ void weights_plain_kernel(const int8_t *__restrict__ W, int64_t d_in, int transpose,
                                      int64_t rows, int64_t rows_pad, int64_t cols, int64_t K,
                                      int8_t *__restrict__ plain) {
@@ -320,6 +348,22 @@ int launch_weights_prepare(const KParams &kp, const int8_t *W, int64_t d_out, in
       W, d_in, transpose, rows, rows_pad, cols, Lc * N, reinterpret_cast<int8_t *>(base + n_exp * 16));
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
+}
+
+// Device-side check of the symmetric weight range (see weights_range_kernel); synchronises `st`
+// (registration is a once-per-model call).  flag: 4 bytes of device scratch (the caller's output
+// buffer, overwritten afterwards).  PHE_OK, PHE_ERANGE (some w == -128) or PHE_ECUDA.
+int check_weights_range(const int8_t *W, int64_t n, unsigned *flag, cudaStream_t st) {
+  if (cudaMemsetAsync(flag, 0, sizeof(unsigned), st) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+  int64_t blocks = (n / 16 + 255) / 256;
+  blocks = blocks < 1 ? 1 : (blocks > 148 * 8 ? 148 * 8 : blocks);
+  weights_range_kernel<<<(unsigned)blocks, 256, 0, st>>>(W, n, flag);
+  PHE_CUDA_CHECK_LAUNCH();
+  unsigned h = 0;
+  cudaError_t e = cudaMemcpyAsync(&h, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return phe_set_cuda_error(e);
+  return h ? PHE_ERANGE : PHE_OK;
 }
 
 int launch_weights_plain(const KParams &kp, const int8_t *W, int64_t d_out, int64_t d_in, int transpose,

@@ -38,6 +38,7 @@ int launch_wire_packed(const KParams &kp, uint32_t *packed, int64_t nct, uint8_t
 int launch_wire_u32(uint32_t *vals, int64_t nseg, int seglen, int bits, uint8_t *wire, int64_t seg_words,
                     int64_t per_group, int64_t group_words, int64_t off_words, int dir, cudaStream_t st);
 
+int check_weights_range(const int8_t *W, int64_t n, unsigned *flag, cudaStream_t st);
 int launch_weights_plain(const KParams &kp, const int8_t *W, int64_t d_out, int64_t d_in, int transpose,
                          int8_t *plain, cudaStream_t st);
 

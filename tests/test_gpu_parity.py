@@ -161,6 +161,61 @@ def test_extreme_limbs_and_weights(phe, coracle):
         assert np.array_equal(u64(m[tau]), mo) and np.array_equal(u64(b[tau]), bo)
 
 
+@pytest.mark.parametrize("pos", ["first", "last", "middle", "unaligned_tail"])
+def test_weight_minus_128_refused_on_both_paths(phe, pos):
+    """w = -128 lies outside symmetric int8 quantization's [-127, 127] and
+    encode_weights refuses out-of-range weights: both registrations (tensor-core and
+    NTT, forward and W^T) return PHE_ERANGE instead of computing with it.  Positions cover the
+    range kernel's unaligned head, 16-byte body and tail."""
+    p = phe.params(phe.PRESET_PAPER)
+    d_out, d_in = 37, 2100
+    W = synth.weights_int8(d_out, d_in, seed=3)
+    flat = torch.from_numpy(W.reshape(-1).copy())
+    buf = torch.zeros(flat.numel() + 1, dtype=torch.int8)
+    off = 1 if pos == "unaligned_tail" else 0   # W starting 1 byte past a 16-byte boundary
+    k = {"first": 0, "last": flat.numel() - 1, "middle": flat.numel() // 2 + 5,
+         "unaligned_tail": flat.numel() - 3}[pos]
+    flat[k] = -128
+    buf[off: off + flat.numel()] = flat
+    Wd = buf.to(DEV)[off: off + flat.numel()].view(d_out, d_in)
+    tabs = phe.NttTables(p)
+    for tr in (False, True):
+        with pytest.raises(phe.PheError, match="out of range"):
+            phe.Weights(p, Wd, transpose=tr)
+        with pytest.raises(phe.PheError, match="out of range"):
+            phe.NttWeights(p, tabs, Wd, transpose=tr)
+    flat[k] = -127                               # the same matrix inside the range registers
+    buf[off: off + flat.numel()] = flat
+    Wd = buf.to(DEV)[off: off + flat.numel()].view(d_out, d_in)
+    phe.Weights(p, Wd)
+    phe.NttWeights(p, tabs, Wd)
+
+
+def test_full_int8_range_both_paths_vs_oracle(phe, coracle):
+    """Every weight value the paths accept, [-127, 127], with the extremes on both halves of the
+    Hankel operand (the negacyclic wrap stores -w): tensor-core and NTT paths bit-exact vs the
+    oracle's literal Eq. 6, forward and W^T."""
+    p = phe.params(phe.PRESET_PAPER)
+    op = oparams(p)
+    W = synth.uniform_int8((70, 2100), 31, -127, 127)
+    W[0, :] = -127
+    W[1, :] = 127
+    W[2, ::2] = -127
+    for tr in (False, True):
+        M = np.ascontiguousarray(W.T) if tr else W
+        x = synth.uniform_int8((3, M.shape[1]), 5 + tr, -127, 127)
+        S, seeds, body, w, opnd, (m, b) = run_gpu(phe, p, W, x, transpose=tr, out_bits=39)
+        tabs = phe.NttTables(p)
+        wn = phe.NttWeights(p, tabs, torch.from_numpy(W).to(DEV), transpose=tr)
+        mn, bn = phe.matmul_clear_ntt(p, wn, phe.ntt_ct_prepare(p, tabs, seeds, body), 3, out_bits=39)
+        sd, bd = u64(seeds), u64(body)
+        for tau in range(3):
+            A = np.stack([coracle.expand_mask(int(s_), op.N, op.q_in) for s_ in sd[tau]])
+            mo, bo = coracle.matmul_clear_literal(op, M, A, bd[tau], nthreads=os.cpu_count())
+            assert np.array_equal(u64(m[tau]), mo) and np.array_equal(u64(b[tau]), bo)
+            assert np.array_equal(u64(mn[tau]), mo) and np.array_equal(u64(bn[tau]), bo)
+
+
 def test_matmul_clear_ct_one_call(phe):
     """phe_matmul_clear_ct (north_star's matmul_clear(W, ct)) == ct_prepare + matmul_clear[_T]."""
     p = phe.params(phe.PRESET_PAPER)
@@ -272,6 +327,15 @@ def test_full_size_q_proj_bench_config(phe, coracle):
     y = phe.decrypt_unpack(p, S, m39, b39, 39)
     wx = (torch.from_numpy(x).to(DEV).double() @ torch.from_numpy(W).to(DEV).double().T)
     assert torch.equal(y.double(), wx)
+    # (iv) all 8.6e9 mask words: NR Freivalds projections per (tau, j) vs the oracle's
+    # (A_tau * r) . W with the oracle's own mask expansion (tests/test_gpu_freivalds.py)
+    from freivalds_util import NR, projections, r_limbs
+    seeds_o = O.block_seeds(12345, T, 1)
+    assert np.array_equal(sd, seeds_o)
+    A_all = np.stack([coracle.expand_mask(int(s_), op.N, op.q_in)[None] for s_ in seeds_o[:, 0]])
+    r = rng.integers(0, op.Q, size=(NR, op.N), dtype=np.uint64)
+    got = projections(m39, r_limbs(r, DEV)) & np.uint64(op.Q - 1)
+    assert np.array_equal(got, coracle.mask_projection(op, W, A_all, r, nthreads=os.cpu_count()))
     del m39
     m26, b26 = phe.matmul_clear(p, w, opnd, T)
     y26 = phe.decrypt_unpack(p, S, m26, b26, 26).double()

@@ -356,3 +356,44 @@ def test_c_oracle_decryption_invariant_paper_params(coracle):
 def test_c_oracle_modswitch(coracle):
     v = synth.uniform_u64(1000, 3, 39)
     assert np.array_equal(coracle.modswitch(v, 39, 26), O.modswitch(v, 39, 26))
+
+
+@pytest.mark.parametrize("N,d_out,d_in,q", [(16, 5, 37, 39), (8, 3, 8, 16), (256, 4, 600, 39)])
+def test_mask_projection_is_the_literal_masks_projected(coracle, N, d_out, d_in, q):
+    """oracle_mask_projection (the Freivalds check the GPU suites run over every output) equals
+    sum_t a_j[t] r[t] mod 2^q computed with Python integers from the literal Eq. 6 masks
+    (Python oracle for tiny N; the C literal path for N = 256), ragged last block included."""
+    prm = Params(N=N, q_in=q, q_out=min(q, 26) - 4, beta=min(q, 26) - 4, gamma=4, eta=0)
+    rng = np.random.default_rng(N + d_in)
+    W = rng.integers(-127, 128, size=(d_out, d_in)).astype(np.int8)
+    T, L = 3, prm.L(d_in)
+    A = rng.integers(0, 2 ** 62, size=(T, L, N), dtype=np.uint64) & np.uint64(prm.Q - 1)
+    r = rng.integers(0, 2 ** 62, size=(2, N), dtype=np.uint64) & np.uint64(prm.Q - 1)
+    got = coracle.mask_projection(prm, W, A, r)
+    for tau in range(T):
+        if N <= 16:
+            mask, _ = O.matmul_clear_literal(prm, W, A[tau], np.zeros((L, N), np.uint64))
+        else:
+            mask, _ = coracle.matmul_clear_literal(prm, W, A[tau], np.zeros((L, N), np.uint64))
+        for j in range(d_out):
+            for e in range(2):
+                want = sum(int(mask[j, t]) * int(r[e, t]) for t in range(N)) % prm.Q
+                assert int(got[tau, j, e]) == want
+    # a single flipped top bit in one mask word changes the projection for odd r[t]
+    r1 = np.ones((1, N), np.uint64)
+    base = coracle.mask_projection(prm, W, A, r1)
+    mask, _ = coracle.matmul_clear_literal(prm, W, A[0], np.zeros((L, N), np.uint64))
+    assert int(base[0, 0, 0]) == sum(int(v) for v in mask[0]) % prm.Q
+
+
+def test_body_projection_is_the_closed_form_bodies_projected():
+    """body_projection == sum_j rp[j] * body_closed_form(...)[j] mod Q in Python integers."""
+    prm = Params(N=16, q_in=39, q_out=26, beta=27, gamma=12, eta=0)
+    rng = np.random.default_rng(7)
+    W = rng.integers(-127, 128, size=(6, 37)).astype(np.int8)
+    B = rng.integers(0, 2 ** 39, size=(4, 3, 16), dtype=np.uint64)
+    rp = rng.integers(0, 2 ** 39, size=6, dtype=np.uint64)
+    got = O.body_projection(prm, W, B, rp)
+    for tau in range(4):
+        b = O.body_closed_form(prm, W, B[tau])
+        assert int(got[tau]) == sum(int(rp[j]) * int(b[j]) for j in range(6)) % prm.Q
