@@ -1,19 +1,27 @@
 #!/usr/bin/env python
-"""bench.py — encrypted tokens/s through the W.[x]_HE hot path on B200 (BASELINE.json metric).
+"""bench.py — encrypted tokens/s through all Llama-3.2-1B linears on B200 (BASELINE.json metric).
 
-Default workload = BASELINE configs[1]: Llama-3.2-1B q_proj 2048x2048 forward, B=8 x C=256 =
-2048 tokens per GPU, Table 1 parameters (N=2048, q 2^39 -> 2^26).  One step = one pass of the
-whole server hot path over one batch:
+Default workload = BASELINE configs[3]: the full 16-layer Llama-3.2-1B linear stack, forward
+(qkv fused 3072x2048, o 2048x2048, gate_up fused 16384x2048, down 2048x8192) plus backward W^T
+(q/k/v/o, gate/up/down transposes, GQA k/v 512x2048), B=8 x C=256 = 2048 tokens, Table 1
+parameters (N=2048, q 2^39 -> 2^26).  This is the per-token HE work of the paper's training step
+("invokes the W.[x]_HE primitive for the various weight matrices in each transformer
+layer ... forward and backward").  One step = one pass of the whole server hot path over the
+batch, for every linear call of the stack:
     ct_prepare   seed expansion (ChaCha20) + limb split of masks and bodies      (a3, a4)
     body GEMM    b = W . B  (tcgen05 limb GEMM, plain operand)                    (a6-a8)
     mask GEMM    a = Hankel(W) . A-limbs (tcgen05 limb GEMM) + recombine + switch (a5, a7, a8)
 Inputs are resident in HBM when the timed region starts (client-side keygen/encrypt_pack run
 untimed); L2 is flushed (256 MiB write) between timed steps, outside the per-step events.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload q_proj|ffn]
-Multi-GPU (torchrun, one rank per GPU): tokens are sharded (each rank its own 2048-token
-batch, "scaling": "weak"); no collective on the data path; the NCCL all-reduce only takes
-the max step time over ranks.  --impl reference times the CPU oracle (oracle/) on host cores.
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                  [--workload stack|q_proj|ffn|q_proj_packed|stack_packed]
+Multi-GPU (torchrun, one rank per GPU): LWE workloads are row-sharded by default (north_star:
+rank r owns rows shard_range(R, N, r) of every linear for the same tokens, "scaling": "strong";
+no collective on the data path), and the gather of the output ciphertexts to rank 0 (26-bit wire
+form, NCCL P2P on a side stream, overlapped with the next chunk's GEMMs) is timed in a separate
+pass and reported under "gather".  --shard tokens gives the paper's "S identical HE servers"
+(weak scaling).  --impl reference times the CPU oracle (oracle/) on host cores.
 """
 from __future__ import annotations
 
@@ -31,6 +39,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "encrypted tokens/sec through all Llama-3.2-1B linears; % int8 TC peak"
 NOMINAL_INT8_TOPS = 4500.0
+LWE_WORKLOADS = ("stack", "q_proj", "ffn")
 
 
 def parse():
@@ -39,8 +48,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["q_proj", "ffn", "stack", "q_proj_packed", "stack_packed"],
-                    default="q_proj")
+    ap.add_argument("--workload", choices=["stack", "q_proj", "ffn", "q_proj_packed", "stack_packed"],
+                    default="stack")
+    ap.add_argument("--layers", type=int, default=16,
+                    help="stack workloads: transformer layers (Llama-3.2-1B has 16; fewer only for tests)")
     ap.add_argument("--pack", choices=["tc", "ntt"], default="ntt",
                     help="packed workloads, stage 2 (KeySwitch Eq. 8 + rotate-sum Eq. 7): tc = int8 packing GEMM "
                          "on tcgen05, ntt = sum_{l,i} D_{l,i} * KSK_{l,i} in the NTT domain (ntt_keyswitch.cu)")
@@ -48,20 +59,24 @@ def parse():
                     help="mask contraction a5: tc = int8 limb GEMM on tcgen05 (north_star; the default), ntt = NTT "
                          "domain (NEXT #4, CUDA cores), hybrid = ntt for multi-block (L >= 2) linears, tc otherwise; "
                          "packed workloads default to ntt for stage 1 (T = 16: a 16-token batch fills a third of a "
-                         "51-token tensor-core tile; T = 2048: 45 vs 50 ms, and the step then stays at the "
-                         "uncapped clock for the NTT KeySwitch: 6.85k vs 6.40k tok/s)")
+                         "51-token tensor-core tile)")
     ap.add_argument("--tokens", type=int, default=None,
-                    help="tokens per rank (default B*C = 8*256 = 2048; stack_packed: the paper's training "
+                    help="tokens per step (default B*C = 8*256 = 2048; stack_packed: the paper's training "
                          "step, B*C = 1*16)")
+    ap.add_argument("--e2e-tokens", type=int, default=None,
+                    help="tokens of the e2e pass (host buffers, PCIe-bound); default 102 for the stack, T otherwise")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e/cpu/clocks)")
-    ap.add_argument("--shard", choices=["tokens", "rows"], default="tokens",
-                    help="N>1: tokens = each rank its own batch (weak); rows = W rows split (strong)")
-    ap.add_argument("--gather", nargs="?", const="nccl", default="none", choices=["none", "nccl", "p2p"],
-                    help="rows mode (q_proj): nccl = time an NCCL send/recv gather to rank 0 after the step; "
-                         "p2p = fused gather: every rank's kernels write their row block straight into rank "
-                         "0's buffer (CUDA IPC / NVLink peer stores) inside the timed step")
+    ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e/cpu/clocks/gather)")
+    ap.add_argument("--shard", choices=["tokens", "rows"], default=None,
+                    help="N>1: rows = W rows split, same tokens (strong; default for LWE workloads); "
+                         "tokens = each rank its own batch (weak; default for packed workloads)")
+    ap.add_argument("--gather", choices=["none", "nccl", "p2p"], default=None,
+                    help="rows mode: nccl (default) = a separately timed pass in which every (chunk, linear)'s "
+                         "row shards are serialized to the 26-bit wire form and sent to rank 0 over NCCL P2P on a "
+                         "side stream, overlapped with the next GEMMs; p2p (q_proj) = fused gather: every rank's "
+                         "kernels store their row block straight into rank 0's buffer (CUDA IPC / NVLink) inside "
+                         "the timed step; none")
     args = ap.parse_args()
     if args.tokens is None:  # B*C = 8*256; the paper's training step is B = 1, C = 16
         args.tokens = 16 if args.workload == "stack_packed" else 2048
@@ -125,7 +140,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workloads
-def linears(workload: str):
+def linears(workload: str, layers: int = 16):
     """Calls one step makes: (name, d_out, d_in, transpose, input_key).  Llama-3.2-1B:
     d = 2048, m = 8192, GQA k/v 512x2048, 16 layers.  Linears that share an input ciphertext
     are registered fused (qkv 3072x2048, gate_up 16384x2048), so the input is expanded once and
@@ -138,7 +153,7 @@ def linears(workload: str):
                 ("gate_T", 8192, 2048, True, "g_gate"), ("up_T", 8192, 2048, True, "g_up"),
                 ("down_T", 2048, 8192, True, "g_down")]
     calls = []                # configs[3]: the full 16-layer stack, forward + backward
-    for l in range(16):
+    for l in range(layers):
         calls += [(f"L{l}.qkv", 3072, 2048, False, f"L{l}.x"), (f"L{l}.o", 2048, 2048, False, f"L{l}.a"),
                   (f"L{l}.gate_up", 16384, 2048, False, f"L{l}.h"), (f"L{l}.down", 2048, 8192, False, f"L{l}.m"),
                   (f"L{l}.q_T", 2048, 2048, True, f"L{l}.gq"), (f"L{l}.k_T", 512, 2048, True, f"L{l}.gk"),
@@ -146,6 +161,11 @@ def linears(workload: str):
                   (f"L{l}.gate_T", 8192, 2048, True, f"L{l}.gg"), (f"L{l}.up_T", 8192, 2048, True, f"L{l}.gu"),
                   (f"L{l}.down_T", 2048, 8192, True, f"L{l}.gd")]
     return calls
+
+
+def rows_cols(d_out, d_in, tr):
+    """Output rows and contracted width of one call (W^T for the backward calls)."""
+    return (d_in, d_out) if tr else (d_out, d_in)
 
 
 def alg_imad_ops(p, rows, cols, T):
@@ -164,9 +184,13 @@ def alg_int8_ops(p, rows, cols, T, part):
     return 2.0 * p.ell * macs * T
 
 
+def tile_round(n, tpt):
+    """Largest multiple of the 51-token tensor-core tile <= n (at least one tile)."""
+    return max(tpt, n // tpt * tpt)
+
+
 # ----------------------------------------------------------------------------- our arm
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -190,10 +214,15 @@ def run_ours(args):
     phe.load()
     p = phe.params(phe.PRESET_PAPER)
     T = args.tokens
-    lins = linears(args.workload)
-    # ---------------- untimed setup: weights (server registration) and client encryption
-    from paper_2505_07329_b200.dist import PeerGather, gather_rows, shard_range
+    packed = args.workload.endswith("_packed")
+    if args.shard is None:
+        args.shard = "tokens" if packed else "rows"
     rows_mode = args.shard == "rows" and world > 1
+    if args.gather is None:
+        args.gather = "nccl" if rows_mode and not packed else "none"
+    lins = linears(args.workload, args.layers)
+    # ---------------- untimed setup: weights (server registration) and client encryption
+    from paper_2505_07329_b200.dist import PeerGather, gather_wire_shards, shard_range
     regs = []   # (name, Weights | NttWeights, input_key)
     tabs = phe.NttTables(p, device=dev) if args.contraction != "tc" else None
 
@@ -211,7 +240,6 @@ def run_ours(args):
     # this rank's output rows of each linear (all rows unless row-sharded)
     rr = {name: (shard_range(w.rows, world, rank) if rows_mode else (0, w.rows)) for name, w, _ in regs}
     S = phe.keygen(p, synth.MASTER_SEED + 17)
-    packed = args.workload.endswith("_packed")
     if packed:  # NEXT #1: KeySwitch key (client keygen, server registration), untimed setup
         ksk = phe.ksk_gen(p, S, synth.MASTER_SEED + 23)
         K = phe.KeySwitchKey(p, ksk) if args.pack == "tc" else phe.NttKeySwitchKey(p, ksk)
@@ -232,11 +260,11 @@ def run_ours(args):
     # 4 levels x 1 B) stay <= ~34 GB (gate_up: 275 GB at T=2048) and a chunk is a whole number
     # of 51-token tiles (no extra tile-padding waste)
     tpt = 256 // p.ell
-    per_row = (phe.KS_LEVELS if args.workload.endswith("_packed") else 4) * p.N
-    rows_for_chunk = (max_rows + 255) // 256 * 256 if args.workload.endswith("_packed") else max_rows
+    per_row = (phe.KS_LEVELS if packed else 4) * p.N
+    rows_for_chunk = (max_rows + 255) // 256 * 256 if packed else max_rows
     cap = 34_400_000_000 // (rows_for_chunk * per_row)
-    chunk = T if T <= cap else max(tpt, cap // tpt * tpt)  # chunk only when the output does not fit
-    if not args.workload.endswith("_packed"):
+    chunk = T if T <= cap else tile_round(cap, tpt)  # chunk only when the output does not fit
+    if not packed:
         out_mask = torch.empty((chunk, max_rows, p.N), dtype=torch.int32, device=dev)
         out_body = torch.empty((chunk, max_rows), dtype=torch.int32, device=dev)
     if packed:  # flat buffers sized for the largest linear, viewed per linear
@@ -245,8 +273,12 @@ def run_ours(args):
         dig_flat = torch.empty(chunk * r256m * phe.KS_LEVELS * p.N, dtype=torch.int8, device=dev)
         bod_flat = torch.empty(chunk * max_rows, dtype=torch.int64, device=dev)
         acc_fn = phe.load().phe_pack_acc_bytes if args.pack == "tc" else phe.load().phe_pack_ntt_ws_bytes
-        acc_buf = torch.empty(max(acc_fn(__import__("ctypes").byref(p), w.rows, chunk)
-                                  for _, w, _ in regs), dtype=torch.uint8, device=dev)
+        # the workspace need is not monotone in T (the K-split follows wave fill): size it for
+        # the full chunk and for the ragged last chunk
+        tail = T % chunk
+        acc_buf = torch.empty(max(acc_fn(__import__("ctypes").byref(p), w.rows, n_)
+                                  for _, w, _ in regs for n_ in {chunk, tail} if n_ > 0),
+                              dtype=torch.uint8, device=dev)
         pk_flat = torch.empty(chunk * Gm * 2 * p.N, dtype=torch.int32, device=dev)
         out_mask = torch.empty(1, dtype=torch.int32, device=dev)  # unused: no LWE-form outputs
     max_L = max(p.L(w.cols) for _, w, _ in regs)
@@ -256,7 +288,9 @@ def run_ours(args):
     ntt_operand = (torch.empty(phe.load().phe_ntt_operand_bytes(__import__("ctypes").byref(p), chunk, ntt_L),
                                dtype=torch.uint8, device=dev) if ntt_L else None)
     peer = None
-    if rows_mode and args.gather == "p2p" and args.workload == "q_proj" and not packed:
+    if rows_mode and args.gather == "p2p":
+        if args.workload != "q_proj":
+            raise SystemExit("--gather p2p needs the whole [T][R][N] output resident on rank 0: q_proj only")
         peer = PeerGather(T, regs[0][1].rows, p.N, dtype=torch.int32, root=0)  # 34 GB on rank 0
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
@@ -265,10 +299,12 @@ def run_ours(args):
     parts_ms = {"ct_prepare": [], "body_gemm": [], "mask_gemm": []}
     launches = [0]
 
-    def step(record):
+    def step(chunk_=chunk, after=None):
+        """One pass over all calls.  `after(name, w, t0, n, mask_view, body_view)` runs after each
+        (chunk, linear)'s GEMMs on the compute stream (the gather pass hooks in here)."""
         evs = []
-        for t0 in range(0, T, chunk):
-            n = min(chunk, T - t0)
+        for t0 in range(0, T, chunk_):
+            n = min(chunk_, T - t0)
             for name, w, ikey in regs:
                 seeds, body = inputs[(w.cols, w.transpose)]
                 e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -322,11 +358,13 @@ def run_ours(args):
                 launches[0] += phe.last_launch_count()
                 e[3].record(stream)
                 evs.append((name, e))
+                if after is not None:
+                    after(name, w, t0, n, mview, bview)
         return evs
 
     # ---------------- warmup
     for _ in range(args.warmup):
-        step(False)
+        step()
     torch.cuda.synchronize()
     # ---------------- timed region (re-measured once if the clock record shows a thermal /
     # HW slowdown or SM clocks stuck well below max with no reason: the run would be rejected)
@@ -343,7 +381,7 @@ def run_ours(args):
             parts_ms[k] = []
         launches[0] = 0
         for _ in range(args.steps):
-            evs = step(True)
+            evs = step()
             torch.cuda.synchronize()
             step_ms.append(sum(e[0].elapsed_time(e[3]) for _, e in evs))
             parts_ms["ct_prepare"].append(sum(e[0].elapsed_time(e[1]) for _, e in evs))
@@ -370,6 +408,7 @@ def run_ours(args):
             if clocks is not None:
                 clocks["remeasured"] = attempt == 1
             break
+    launches_total = launches[0]
     ms = statistics.mean(step_ms)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -377,28 +416,16 @@ def run_ours(args):
     ms_max = float(t.item())
     value = (T if rows_mode else world * T) / (ms_max / 1e3)
 
-    # ---------------- optional: NCCL gather of the row-sharded output ciphertexts to rank 0
+    # ---------------- gather of the output ciphertexts to rank 0 (rows mode)
     gather = None
     if peer is not None:
         peer.complete()
         gather = {"mode": "p2p: fused into the kernels' stores (dist.PeerGather, phe_matmul_clear_into); "
                           "included in ms_per_step",
                   "bytes": int(T * regs[0][1].rows * (p.N + 1) * 4)}
-    if rows_mode and args.gather == "nccl" and args.workload == "q_proj":
-        name, w, _ = regs[0]
-        r0, r1 = rr[name]
-        dist.barrier()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
-        nr = r1 - r0
-        gather_rows(out_mask.view(-1)[: T * nr * p.N].view(T, nr, p.N), out_body.view(-1)[: T * nr].view(T, nr),
-                    w.rows, world, rank)
-        g1.record(stream)
-        torch.cuda.synchronize()
-        tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
-        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
-        gather = {"ms": round(float(tg.item()), 2), "bytes": int(T * w.rows * (p.N + 1) * 4),
-                  "api": "paper_2505_07329_b200.dist.gather_rows (NCCL send/recv to rank 0)"}
+    if rows_mode and args.gather == "nccl" and not args.profile:
+        gather = gather_pass(args, p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, shared,
+                             gather_wire_shards, shard_range, ms_max)
 
     # ---------------- roofline of the dominant kernel (mask limb GEMM, or the NTT kernel if the
     # NTT-domain contraction takes more of the step)
@@ -453,114 +480,28 @@ def run_ours(args):
                     "frac": round(achieved / peak, 4), "traffic": None if packed else traffic,
                     "kernel": ("pack_gemm_2sm_kernel<5> (KeySwitch GEMM Eq. 8 + rotate-sum Eq. 7)" if packed else
                                "limb_gemm_2sm_kernel<5,SW,13> (mask contraction, tcgen05 cta_group::2)"),
-                    "ops": "int8 tensor ops (2 per MAC), algorithmic: 2*ell*d_out*d_in*N per token",
+                    "ops": ("int8 tensor ops (2 per MAC), algorithmic: 2*ell*d_out*d_in*N per token per call, "
+                            "summed over every call of the step; achieved = that / the summed mask-GEMM time"),
                     "peak_source": f"{src}: 2 x bf16_tflops (burst) of MEASURED_PEAKS.json",
                     "frac_of_nominal_4500": round(achieved / NOMINAL_INT8_TOPS, 4),
                     "step_frac": round(total_ops / (ms_max / 1e3) / 1e12 / peak, 4)}
+        if traffic is not None and not packed:
+            roofline["traffic_note"] = ("dram bytes of one mask-GEMM launch from ncu --set full "
+                                        "(profiles/ncu_traffic.json); per launch, see _source there")
 
     # ---------------- e2e through the C ABI with host buffers
     e2e = None
     if not args.no_e2e and not args.profile and args.workload == "q_proj_packed" and not rows_mode:
-        # the server step as the network sees it: wire-format input blocks (9992 B) in,
-        # wire-format packed RLWE ciphertexts (13312 B) out, through host buffers
-        name, w, _ = regs[0]
-        seeds, body = inputs[(w.cols, w.transpose)]
-        hi = phe.wire_serialize_inputs(p, seeds, body).cpu().pin_memory()
-        G0 = (w.rows + p.N - 1) // p.N
-        ho = torch.empty((T, G0, phe.wire_output_bytes(p)), dtype=torch.uint8, pin_memory=True)
-        if isinstance(w, phe.NttWeights) and args.pack == "ntt":   # both stages in the NTT domain
-            swh, api = phe.server_wire_host_nttw, "phe_server_wire_host_nttw"
-        else:  # tensor-core stage 1: the registration the host pipeline takes
-            if isinstance(w, phe.NttWeights):
-                W0 = synth.weights_int8_torch(w.d_out, w.d_in, seed=synth.MASTER_SEED, device=dev)
-                w = phe.Weights(p, W0, transpose=w.transpose)
-                del W0
-            swh, api = ((phe.server_wire_host, "phe_server_wire_host") if args.pack == "tc" else
-                        (phe.server_wire_host_ntt, "phe_server_wire_host_ntt"))
-        swh(p, w, K, hi, ho, chunk_tokens=255)
-        verified = None
-        if chunk >= T:  # the device step's packed outputs for the same inputs are still in pk_flat
-            dev_wire = phe.wire_serialize_packed(p, pk_flat[: T * G0 * 2 * p.N].view(T, G0, 2, p.N)).cpu()
-            verified = bool(torch.equal(dev_wire.view(-1), ho.view(-1)))
-            if not verified:
-                raise RuntimeError(f"e2e: {api} output differs from the device step's packed ciphertexts")
-        wall = []
-        for _ in range(max(2, min(args.steps, 3))):
-            t0 = time.perf_counter()
-            swh(p, w, K, hi, ho, chunk_tokens=255)
-            wall.append(time.perf_counter() - t0)
-        e2e_s = statistics.mean(wall)
-        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(world * T / float(te.item()), 2), "unit": "tokens/s",
-               "h2d_bytes_per_step": int(hi.numel()), "d2h_bytes_per_step": int(ho.numel()),
-               "ms_per_step": round(float(te.item()) * 1e3, 2),
-               "api": api + " (wire-format bytes in/out, pinned host buffers, 255-token chunks)",
-               "output_equals_device_step": verified}
-    if (not args.no_e2e and not args.profile and args.workload == "q_proj" and not rows_mode
-            and args.contraction == "tc"):
-        name, w, _ = regs[0]
-        seeds, body = inputs[(w.cols, w.transpose)]
-        # pinned host memory: 28 GB (wire) [+ 34 GB uint32 variant] per rank; with several ranks on
-        # one host measure the wire form only, and over fewer tokens if host RAM is short
-        # (tokens/s is per-chunk throughput: 256-token chunks either way)
-        lwe_b = phe.wire_lwe_bytes(p, w.rows)
-        Te = T
-        try:
-            import psutil
-            avail = psutil.virtual_memory().available
-            while Te > 256 and world * Te * (lwe_b + (0 if world > 1 else w.rows * p.N * 4)) > 0.5 * avail:
-                Te //= 2
-        except Exception:
-            pass
-        e2e_u32 = None
-        if world == 1:
-            hs = seeds[:Te].cpu().pin_memory()
-            hb = body[:Te].cpu().pin_memory()
-            hm = torch.empty((Te, w.rows, p.N), dtype=torch.int32, pin_memory=True)
-            hbo = torch.empty((Te, w.rows), dtype=torch.int32, pin_memory=True)
-            phe.server_matvec_host(p, w, hs, hb, hm, hbo, chunk_tokens=256)  # warm
-            wall = []
-            for _ in range(max(2, min(args.steps, 3))):
-                t0 = time.perf_counter()
-                phe.server_matvec_host(p, w, hs, hb, hm, hbo, chunk_tokens=256)
-                wall.append(time.perf_counter() - t0)
-            e2e_u32 = {"value": round(Te / statistics.mean(wall), 2), "unit": "tokens/s",
-                       "h2d_bytes_per_step": int(hs.numel() * 8 + hb.numel() * 8),
-                       "d2h_bytes_per_step": int(hm.numel() * 4 + hbo.numel() * 4),
-                       "ms_per_step": round(statistics.mean(wall) * 1e3, 2),
-                       "api": "phe_server_matvec_host (uint64 inputs / uint32 outputs, pinned, 256-token chunks)"}
-            del hm, hbo, hs, hb
-        # the same step on wire bytes: 39-bit input blocks (9992 B) in, LWE outputs at
-        # q_out = 26 bits out (0.8125 of the uint32 bytes) -- the D2H-bound headline
-        hi = phe.wire_serialize_inputs(p, seeds[:Te], body[:Te]).cpu().pin_memory()
-        ho = torch.empty((Te, lwe_b), dtype=torch.uint8, pin_memory=True)
-        phe.server_matvec_wire_host(p, w, hi, ho, chunk_tokens=256)  # warm
-        if world > 1:
-            dist.barrier()
-        wall = []
-        for _ in range(max(2, min(args.steps, 3))):
-            t0 = time.perf_counter()
-            phe.server_matvec_wire_host(p, w, hi, ho, chunk_tokens=256)
-            wall.append(time.perf_counter() - t0)
-        te = torch.tensor([statistics.mean(wall)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(world * Te / float(te.item()), 2), "unit": "tokens/s",
-               "h2d_bytes_per_step": int(hi.numel()), "d2h_bytes_per_step": int(ho.numel()),
-               "ms_per_step": round(float(te.item()) * 1e3, 2), "tokens_per_rank": Te,
-               "api": "phe_server_matvec_wire_host (wire bytes in/out: 9992 B input blocks, LWE outputs at "
-                      "26 bits; pinned host buffers, 256-token chunks, 2 streams)",
-               "uint32_outputs": e2e_u32}
-        del ho
+        e2e = e2e_packed(args, p, phe, synth, regs, inputs, K, pk_flat, chunk, T, world, dev)
+    elif (not args.no_e2e and not args.profile and args.workload in LWE_WORKLOADS
+          and all(not is_ntt[n_] for n_, _, _ in regs)):
+        e2e = e2e_lwe(args, p, phe, regs, rr, inputs, T, world, dev)
 
     # ---------------- CPU baseline: the oracle on host cores, bounded sample (rank 0, N=1)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
-        cpu = cpu_baseline(args, lins[0], budget_s=12.0)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile and not packed:
+        cpu = oracle_sample(lins, budget_s=15.0)
 
-    launches_total = launches[0]
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
@@ -579,6 +520,14 @@ def run_ours(args):
         }
         if len(regs) > 1:
             line["per_linear_ms"] = {k: round(sum(v) / args.steps, 3) for k, v in per_kind.items()}
+        if args.workload == "stack" and "o" in per_kind and not rows_mode:
+            # configs[1]'s shape inside the stack: o is 2048x2048 forward, exactly q_proj's GEMM
+            o_ms = sum(per_kind["o"]) / args.steps / args.layers
+            o_ops = alg_int8_ops(p, 2048, 2048, T, "mask") + alg_int8_ops(p, 2048, 2048, T, "body")
+            line["sub"] = {"q_proj_shape": {
+                "what": "the 2048x2048 forward calls of the stack (o_proj; q_proj's shape, BASELINE configs[1])",
+                "tokens_per_s": round(T / (o_ms / 1e3), 1), "ms_per_call": round(o_ms, 3),
+                "frac_of_peak": round(o_ops / (o_ms / 1e3) / 1e12 / peak, 4)}}
         if gather is not None:
             line["gather"] = gather
         print(json.dumps(line), flush=True)
@@ -586,15 +535,189 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def gather_pass(args, p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, shared, gather_wire_shards,
+                shard_range, ms_compute):
+    """One extra step with the gather to rank 0: after each (chunk, linear)'s
+    GEMMs every rank serializes its row shard to the 26-bit wire form (phe_wire_serialize_lwe,
+    0.8125 of the uint32 bytes) into one of two slots, and a side stream sends it to rank 0 with
+    NCCL P2P (rank 0 receives each peer's shard straight into its destination block), so the
+    transfer of call c overlaps the GEMMs of call c+1.  Rank 0 double-buffers its receive blocks.
+    Chunks are smaller than in the compute-only step so that two receive slots of the widest
+    linear (gate_up, 16384 rows) stay <= 2 x 16 GB on rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    def shard_bytes(w, k):
+        a, b = shard_range(w.rows, world, k)
+        return phe.wire_lwe_bytes(p, b - a)
+    per_tok_full = max(sum(shard_bytes(w, k) for k in range(world)) for _, w, _ in regs)
+    gchunk = min(T, tile_round(16_000_000_000 // per_tok_full, tpt))
+    send_max = gchunk * max(shard_bytes(w, rank) for _, w, _ in regs)
+    recv_max = gchunk * per_tok_full if rank == 0 else 0
+    slots = [torch.empty(send_max, dtype=torch.uint8, device=dev) for _ in range(2)]
+    recv = [torch.empty(recv_max, dtype=torch.uint8, device=dev) for _ in range(2)] if rank == 0 else None
+    comm = torch.cuda.Stream(device=dev)
+    ev_ready = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
+    used = [False, False]
+    count = [0]
+    sent = [0]
+
+    def after(name, w, t0, n, mview, bview):
+        s = count[0] % 2
+        count[0] += 1
+        if used[s]:
+            stream.wait_event(ev_free[s])  # the transfer that last used slot s has completed
+        used[s] = True
+        nb = [shard_bytes(w, k) for k in range(world)]
+        shard = slots[s][: n * nb[rank]].view(n, nb[rank])
+        phe.wire_serialize_lwe(p, mview, bview, out=shard)
+        ev_ready[s].record(stream)
+        blocks = None
+        if rank == 0:
+            blocks, off = [], 0
+            for k in range(world):
+                blocks.append(recv[s][off: off + n * nb[k]].view(n, nb[k]))
+                off += n * nb[k]
+        sent[0] += sum(n * nb[k] for k in range(world) if k != 0)
+        with torch.cuda.stream(comm):
+            comm.wait_event(ev_ready[s])
+            if rank == 0:  # rank 0's own shard joins the gathered set with a local D2D copy
+                blocks[0].copy_(shard)
+            works = gather_wire_shards(shard, blocks, world, rank, 0, staged=shared)
+            for wk in works:
+                wk.wait()  # the comm stream waits for the NCCL transfer
+            ev_free[s].record(comm)
+
+    # untimed: one small exchange per peer pair first (NCCL builds its P2P connections lazily)
+    warm = torch.zeros((1, 8), dtype=torch.uint8, device=dev)
+    wblocks = [torch.empty((1, 8), dtype=torch.uint8, device=dev) for _ in range(world)] if rank == 0 else None
+    for wk in gather_wire_shards(warm, wblocks, world, rank, 0, staged=shared):
+        wk.wait()
+    dist.barrier()
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    step(gchunk, after)
+    stream.wait_stream(comm)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+    ms_g = float(tg.item())
+    return {"mode": "nccl: 26-bit wire shards (phe_wire_serialize_lwe), P2P to rank 0 on a side stream, "
+                    "overlapped with the next call's GEMMs; separate pass, not in ms_per_step",
+            "ms_step_with_gather": round(ms_g, 2), "ms_step_compute_only": round(ms_compute, 2),
+            "exposed_ms": round(ms_g - ms_compute, 2), "bytes_to_rank0": int(sent[0]),
+            "rank0_ingress_GBps": round(sent[0] / (ms_g / 1e3) / 1e9, 1), "chunk_tokens": gchunk,
+            "transport": "gloo via host (shared-GPU test hook)" if shared else "NCCL batch_isend_irecv"}
+
+
+def e2e_lwe(args, p, phe, regs, rr, inputs, T, world, dev):
+    """The step as a client sees it, through the C ABI with HOST buffers: for every call of the
+    workload, phe_server_matvec_wire_host takes the wire-format input blocks (9992 B) from
+    pinned host memory and returns the switched LWE outputs at 26 bits into pinned host memory
+    (chunked H2D / GEMM / D2H on two streams).  PCIe-bound: the stack returns 4.69 GB of
+    ciphertext per token, so the pass runs over a stated token subset."""
+    import torch
+    import torch.distributed as dist
+    Te = args.e2e_tokens or (102 if args.workload == "stack" else T)
+    Te = min(Te, T)
+    max_out = max(phe.wire_lwe_bytes(p, rr[n_][1] - rr[n_][0]) for n_, _, _ in regs)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+        while Te > 51 and world * Te * max_out > 0.4 * avail:
+            Te //= 2
+    except Exception:
+        pass
+    wire_in = {}
+    for name, w, _ in regs:
+        key = (w.cols, w.transpose)
+        if key not in wire_in:
+            seeds, body = inputs[key]
+            wire_in[key] = phe.wire_serialize_inputs(p, seeds[:Te], body[:Te]).cpu().pin_memory()
+    ho = torch.empty(Te * max_out, dtype=torch.uint8, pin_memory=True)
+    h2d = sum(wire_in[(w.cols, w.transpose)].numel() for _, w, _ in regs)
+    d2h = sum(Te * phe.wire_lwe_bytes(p, rr[n_][1] - rr[n_][0]) for n_, _, _ in regs)
+    chunk_e = 51 if Te >= 102 else Te
+
+    def run():
+        for name, w, _ in regs:
+            r0, r1 = rr[name]
+            out = ho[: Te * phe.wire_lwe_bytes(p, r1 - r0)].view(Te, -1)
+            phe.server_matvec_wire_host(p, w, wire_in[(w.cols, w.transpose)], out, chunk_tokens=chunk_e,
+                                        row_begin=r0, row_end=r1)
+    run()  # warm
+    if world > 1:
+        dist.barrier()
+    wall = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        run()
+        wall.append(time.perf_counter() - t0)
+    te = torch.tensor([statistics.mean(wall)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    s = float(te.item())
+    return {"value": round(Te / s, 3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(s * 1e3, 1), "tokens_per_step": Te,
+            "api": "phe_server_matvec_wire_host per call (wire bytes in/out: 9992 B input blocks, LWE outputs at "
+                   f"26 bits; pinned host buffers, {chunk_e}-token chunks, 2 streams)",
+            "note": f"a {Te}-token subset of the step's batch (D2H-bound: the outputs cross PCIe)"}
+
+
+def e2e_packed(args, p, phe, synth, regs, inputs, K, pk_flat, chunk, T, world, dev):
+    """q_proj_packed: wire-format input blocks (9992 B) in, wire-format packed RLWE
+    ciphertexts (13312 B) out, through host buffers; checked equal to the device step."""
+    import torch
+    import torch.distributed as dist
+    name, w, _ = regs[0]
+    seeds, body = inputs[(w.cols, w.transpose)]
+    hi = phe.wire_serialize_inputs(p, seeds, body).cpu().pin_memory()
+    G0 = (w.rows + p.N - 1) // p.N
+    ho = torch.empty((T, G0, phe.wire_output_bytes(p)), dtype=torch.uint8, pin_memory=True)
+    if isinstance(w, phe.NttWeights) and args.pack == "ntt":   # both stages in the NTT domain
+        swh, api = phe.server_wire_host_nttw, "phe_server_wire_host_nttw"
+    else:  # tensor-core stage 1: the registration the host pipeline takes
+        if isinstance(w, phe.NttWeights):
+            W0 = synth.weights_int8_torch(w.d_out, w.d_in, seed=synth.MASTER_SEED, device=dev)
+            w = phe.Weights(p, W0, transpose=w.transpose)
+            del W0
+        swh, api = ((phe.server_wire_host, "phe_server_wire_host") if args.pack == "tc" else
+                    (phe.server_wire_host_ntt, "phe_server_wire_host_ntt"))
+    swh(p, w, K, hi, ho, chunk_tokens=255)
+    verified = None
+    if chunk >= T:  # the device step's packed outputs for the same inputs are still in pk_flat
+        dev_wire = phe.wire_serialize_packed(p, pk_flat[: T * G0 * 2 * p.N].view(T, G0, 2, p.N)).cpu()
+        verified = bool(torch.equal(dev_wire.view(-1), ho.view(-1)))
+        if not verified:
+            raise RuntimeError(f"e2e: {api} output differs from the device step's packed ciphertexts")
+    wall = []
+    for _ in range(max(2, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        swh(p, w, K, hi, ho, chunk_tokens=255)
+        wall.append(time.perf_counter() - t0)
+    te = torch.tensor([statistics.mean(wall)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    return {"value": round(world * T / float(te.item()), 2), "unit": "tokens/s",
+            "h2d_bytes_per_step": int(hi.numel()), "d2h_bytes_per_step": int(ho.numel()),
+            "ms_per_step": round(float(te.item()) * 1e3, 2),
+            "api": api + " (wire-format bytes in/out, pinned host buffers, 255-token chunks)",
+            "output_equals_device_step": verified}
+
+
 def config_dict(args, world, T, rows_mode=False):
     wl = {"q_proj": "Llama-3.2-1B q_proj 2048x2048 forward W.[x]_HE (BASELINE configs[1])",
           "ffn": "Llama-3.2-1B FFN gate/up 8192x2048 + down 2048x8192, fwd + W^T bwd (configs[2])",
           "q_proj_packed": "Llama-3.2-1B q_proj 2048x2048 forward, full primitive: Eq. 6 + KeySwitch packing "
                            "Eq. 7/8 -> RLWE(Wx), 39->26 switch (configs[1] + SURVEY NEXT #1)",
-          "stack": "Llama-3.2-1B all linears x 16 layers (qkv fused 3072x2048, o, gate_up fused 16384x2048, "
-                   "down; bwd W^T incl. GQA k/v 512x2048), fwd + bwd (configs[3])",
-          "stack_packed": "Llama-3.2-1B all linears x 16 layers fwd + bwd, full primitive (Eq. 6 + KeySwitch "
-                          "packing Eq. 7/8 + switch): the HE server work of the paper's training step "
+          "stack": f"Llama-3.2-1B all linears x {args.layers} layers (qkv fused 3072x2048, o 2048x2048, gate_up "
+                   "fused 16384x2048, down 2048x8192; bwd W^T of q/k/v/o/gate/up/down incl. GQA k/v 512x2048), "
+                   "fwd + bwd (BASELINE configs[3])",
+          "stack_packed": f"Llama-3.2-1B all linears x {args.layers} layers fwd + bwd, full primitive (Eq. 6 + "
+                          "KeySwitch packing Eq. 7/8 + switch): the HE server work of the paper's training step "
                           "(P:432-435, B=1, C=16 by default)"}[args.workload]
     if args.contraction != "tc":
         wl += {"ntt": "; mask contraction in the NTT domain (NEXT #4, CUDA cores)",
@@ -603,97 +726,118 @@ def config_dict(args, world, T, rows_mode=False):
         wl += {"tc": "; packing stage (Eq. 8 MatMul + rotate-sum) on tcgen05",
                "ntt": "; packing stage as sum_{l,i} D_{l,i} * KSK_{l,i} in the NTT domain"}[args.pack]
     B, C = (1, T) if args.workload == "stack_packed" else (8, T // 8)
-    return {"workload": wl, "contraction": args.contraction,
-            **({"pack": args.pack} if args.workload.endswith("_packed") else {}), "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": B, "C": C, "N": 2048, "q_in": 39, "q_out": 26,
-            "beta": 27,
-            "parallelism": (f"row-sharded x{world}" if rows_mode else f"token-sharded x{world}") if world > 1
-            else "single GPU",
-            "l2": ("flushed between steps (256 MiB write)" if args.workload.endswith("_packed") else
-                   "flushed between steps (256 MiB write), outputs 34 GB/step >> L2"),
-            "output": ("packed RLWE ciphertexts (Eq. 7), uint32 A', B' after the 39->26 switch"
-                       if args.workload.endswith("_packed") else
-                       "LWE ciphertexts, uint32 per coefficient after 39->26 modulus switch")}
+    cfg = {"workload": wl, "contraction": args.contraction,
+           **({"pack": args.pack} if args.workload.endswith("_packed") else {}),
+           "tokens_per_gpu": T if not rows_mode else None, "tokens": T, "B": B, "C": C,
+           "N": 2048, "q_in": 39, "q_out": 26, "beta": 27,
+           "parallelism": (f"row-sharded x{world}" if rows_mode else f"token-sharded x{world}") if world > 1
+           else "single GPU",
+           "l2": ("flushed between steps (256 MiB write)" if args.workload.endswith("_packed") else
+                  "flushed between steps (256 MiB write); outputs >= 8.6 GB per call >> L2"),
+           "output": ("packed RLWE ciphertexts (Eq. 7), uint32 A', B' after the 39->26 switch"
+                      if args.workload.endswith("_packed") else
+                      "LWE ciphertexts, uint32 per coefficient after 39->26 modulus switch")}
+    if args.workload.startswith("stack"):
+        cfg["layers"] = args.layers
+        cfg["calls_per_step"] = 11 * args.layers
+    return cfg
 
 
-def cpu_baseline(args, lin, budget_s=12.0):
-    """Times the oracle (oracle/phe_oracle.py + the C literal path) as it stands on the host's
-    cores: server-side expansion + literal Eq. 6 + modswitch, on a bounded token sample."""
+def oracle_sample(lins, budget_s=15.0, nthreads=None):
+    """Times the oracle as it stands (oracle/phe_oracle.py: ChaCha20 expansion + the C literal
+    Eq. 6 path with OpenMP over output rows + modswitch) on the host's cores, on a bounded sample
+    of the workload: for each distinct contracted width (2048, 8192 and the 512-wide k/v
+    transposes) token(s) through row subsets of that width's first matrix.  The oracle's cost per
+    call is a + b * rows (a: expanding the token's masks; b: L schoolbook N x N negacyclic
+    products per row + the switch), linear in tokens and identical across layers, so tokens/s of
+    the whole workload is 1 / sum_calls (a + b rows_call)  (SURVEY §8(d) "Oracle timing")."""
     import numpy as np
 
     import synth
     from oracle import c_oracle
     from oracle import phe_oracle as O
 
-    name, d_out, d_in, tr, _ = lin
     lib = c_oracle.load()
     op = O.PAPER
-    W = synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED)
-    M = np.ascontiguousarray(W.T) if tr else W
-    cols = M.shape[1]
+    cores = nthreads or os.cpu_count() or 1
     S = O.keygen(synth.MASTER_SEED + 17, op.N)
-    cores = os.cpu_count() or 1
+    first = {}
+    for idx, (name, d_out, d_in, tr, _) in enumerate(lins):
+        rows, cols = rows_cols(d_out, d_in, tr)
+        first.setdefault(cols, (idx, name, d_out, d_in, tr))
+    fit, desc = {}, []
+    share = budget_s / len(first)
+    for cols, (idx, name, d_out, d_in, tr) in sorted(first.items()):
+        W = synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED + idx)
+        M = np.ascontiguousarray(W.T) if tr else W
 
-    def sample(n):
-        x = synth.activations_int8(n, cols, seed=synth.MASTER_SEED + 5)
-        seeds = O.block_seeds(synth.seed_base(99), n, op.L(cols))
-        bodies = np.stack([O.encrypt(op, S, x[t], seeds[t])[1] for t in range(n)])
-        t0 = time.perf_counter()
-        O.server_matmul(op, M, seeds, bodies, out_bits=op.q_out, lib=lib, nthreads=cores)
-        return time.perf_counter() - t0
-
-    t1 = sample(1)
-    n = int(max(1, min(64, budget_s // max(t1, 1e-3))))
-    tn = sample(n) if n > 1 else t1
-    return {"value": round(n / tn, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
-            "sample": f"{n} tokens of {name} {d_out}x{d_in} (seed expansion + literal Eq.6 in C/OpenMP + "
-                      f"modswitch), {tn:.1f} s wall"}
+        def run(r, n):
+            xs = (synth.gradients_int8 if tr else synth.activations_int8)(n, cols, seed=synth.MASTER_SEED + 5)
+            sd = O.block_seeds(synth.seed_base(99), n, op.L(cols))
+            bd = np.stack([O.encrypt(op, S, xs[i], sd[i])[1] for i in range(n)])
+            t0 = time.perf_counter()
+            O.server_matmul(op, M[:r], sd, bd, out_bits=op.q_out, lib=lib, nthreads=cores)
+            return time.perf_counter() - t0
+        # grow the row count until the sample fills its share of the budget (or the matrix),
+        # then fit t(r) = a + b r over the last two sizes: a = the per-call work (mask expansion
+        # of the token's blocks), b = the per-row work (L schoolbook products + switch)
+        r, n = min(M.shape[0], cores), 1
+        pts = [(r, run(r, n))]
+        while pts[-1][1] < 0.5 * share and r < M.shape[0]:
+            r = int(min(M.shape[0], max(2 * r, r * 0.6 * share / max(pts[-1][1], 1e-4))))
+            pts.append((r, run(r, n)))
+        (r1, t1), (r2, t2) = (pts[-2], pts[-1]) if len(pts) > 1 else ((0, 0.0), pts[-1])
+        b = (t2 - t1) / (r2 - r1)
+        a = max(0.0, t2 - b * r2)
+        if r == M.shape[0] and t2 < 0.5 * share:  # whole matrix in well under the share: more tokens
+            n = int(min(64, share / max(t2, 1e-4)))
+            if n > 1:
+                tn = run(r, n)
+                a, b = a * tn / (n * t2), b * tn / (n * t2)
+        fit[cols] = (a, b)
+        desc.append(f"{n} token(s) x {r} rows of {name.split('.')[-1]} (width {cols}) in {pts[-1][1]:.2f} s "
+                    f"(per call {a * 1e3:.1f} ms + per row {b * 1e3:.3f} ms)")
+    per_token = 0.0
+    for _, d_out, d_in, tr, _ in lins:
+        rows, cols = rows_cols(d_out, d_in, tr)
+        per_token += fit[cols][0] + fit[cols][1] * rows
+    return {"value": round(1.0 / per_token, 6), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": ("; ".join(desc) + f" (seed expansion + literal Eq. 6 in C/OpenMP "
+                       f"+ modswitch, {cores} threads); extrapolated over all {len(lins)} calls of the step "
+                       "as sum_calls (a + b rows) per width (the oracle's cost is linear in rows and "
+                       "identical across layers)"),
+            "s_per_token": round(per_token, 3)}
 
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The base contract's reference arm for this tier: the CPU oracle as it stands, on this
+    arm's config and metric.  Each step times oracle_sample (a bounded sample: token(s) through a
+    row subset of each distinct width) and converts it to tokens/s of the whole workload;
+    ms_per_step is the wall time of one such sample, value the mean extrapolated tokens/s."""
     rank, world, local = dist_env()
     if rank != 0:
         return  # rank 0 alone runs the CPU oracle; other ranks exit 0 without work
-    import numpy as np
-
-    import synth
-    from oracle import c_oracle
-    from oracle import phe_oracle as O
-
-    lib = c_oracle.load()
-    op = O.PAPER
+    lins = linears(args.workload, args.layers)
     cores = os.cpu_count() or 1
-    lin = linears(args.workload)[0]
-    name, d_out, d_in, tr, _ = lin
-    W = synth.weights_int8(d_out, d_in, seed=synth.MASTER_SEED)
-    M = np.ascontiguousarray(W.T) if tr else W
-    cols = M.shape[1]
-    S = O.keygen(synth.MASTER_SEED + 17, op.N)
-    per_step = 2  # tokens per step: a bounded sample of the workload
-    x = synth.activations_int8(per_step, cols, seed=synth.MASTER_SEED + 5)
-    seeds = O.block_seeds(synth.seed_base(7), per_step, op.L(cols))
-    bodies = np.stack([O.encrypt(op, S, x[t], seeds[t])[1] for t in range(per_step)])
-
-    def step():
-        O.server_matmul(op, M, seeds, bodies, out_bits=op.q_out, lib=lib, nthreads=cores)
-
+    budget = 2.0 if len({rows_cols(d, e, t)[1] for _, d, e, t, _ in lins}) > 1 else 1.0
     for _ in range(args.warmup):
-        step()
-    ts = []
+        oracle_sample(lins, budget_s=budget)
+    vals, walls, last = [], [], None
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        step()
-        ts.append(time.perf_counter() - t0)
-    ms = statistics.mean(ts) * 1e3
-    value = per_step / (ms / 1e3)
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "uint64",
-            "data": "synthetic", "config": config_dict(args, world, args.tokens),
-            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{per_step} tokens of {name} {d_out}x{d_in} per step (literal Eq. 6, "
-                                       f"C/OpenMP, {cores} threads)"},
-            "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+        last = oracle_sample(lins, budget_s=budget)
+        walls.append(time.perf_counter() - t0)
+        vals.append(last["value"])
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(statistics.mean(walls) * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "uint64", "data": "synthetic",
+            "config": config_dict(args, world, args.tokens),
+            "cpu_baseline": {"value": round(value, 6), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": last["sample"], "wall_s_per_sample": round(statistics.mean(walls), 2)},
+            "e2e": {"value": round(value, 6), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

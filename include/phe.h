@@ -7,8 +7,13 @@
  *
  * Conventions (all calls):
  *  - Pointers prefixed d_ are DEVICE pointers (cudaMalloc / torch CUDA tensors) owned by the
- *    caller.  The library never allocates device memory except in phe_server_matvec_host,
- *    which documents it.  Host pointers are prefixed h_.
+ *    caller.  The library never allocates device memory: every scratch buffer is a caller
+ *    workspace sized by a *_bytes / *_ws_bytes query.  Host pointers are prefixed h_.
+ *  - The host-buffer pipelines (phe_server_*_host) take a caller device workspace d_ws of two
+ *    chunk slots (their *_ws_bytes query, same shape arguments; ENOMEM if smaller), create two
+ *    streams + one event on the current device for the call, order after the caller's stream,
+ *    and return only after both streams drained (also on an error: no copy still touches the
+ *    caller's host buffers).  They are synchronous, re-entrant and hold no state between calls.
  *  - Every call is asynchronous on the caller's `stream` (a cudaStream_t passed as void*;
  *    NULL = legacy default stream).  Argument validation is synchronous: on a non-zero
  *    return nothing was enqueued.
@@ -182,14 +187,17 @@ int phe_decrypt_unpack(const phe_params *p, const uint8_t *d_S, const void *d_ma
  * h_seeds [T][L] uint64, h_body [T][L][N] uint64 (pinned host memory recommended);
  * result (switched to q_out, uint32) streamed back into h_out_mask [T][R][N], h_out_body
  * [T][R].  Tokens are processed in chunks of `chunk_tokens`: H2D of chunk c+1 and D2H of
- * chunk c-1 overlap the GEMM of chunk c on internal streams.  d_wprep is device-resident
- * (registered once).  Allocates and frees its own device workspace (documented exception
- * to the ownership rule).  Synchronous: returns after all copies completed.              */
+ * chunk c-1 overlap the GEMM of chunk c on two per-call streams.  d_wprep is device-resident
+ * (registered once).  d_ws: caller workspace of phe_server_matvec_host_ws_bytes(...) bytes
+ * (same p, d_out, d_in, transpose, rows, T, chunk_tokens; 0 = invalid arguments).
+ * Synchronous: returns after all copies completed.                                        */
+size_t phe_server_matvec_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose,
+                                       int64_t row_begin, int64_t row_end, int64_t T, int64_t chunk_tokens);
 int phe_server_matvec_host(const phe_params *p, const void *d_wprep, int64_t d_out,
                            int64_t d_in, int transpose, int64_t row_begin, int64_t row_end,
                            const uint64_t *h_seeds, const uint64_t *h_body, int64_t T,
                            int64_t chunk_tokens, uint32_t *h_out_mask, uint32_t *h_out_body,
-                           void *stream);
+                           void *d_ws, size_t ws_bytes, void *stream);
 
 /* ---- NEXT #1: KeySwitch packing of the LWE outputs into RLWE (Eq. 7; Eq. 8,
  * P:233-249) --------------------------------------------------------------------------------
@@ -232,12 +240,16 @@ int phe_matmul_clear_packed(const phe_params *p, const void *d_wprep, int64_t d_
                             int transpose, const void *d_operand, int64_t T, const void *d_kprep,
                             void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream);
 /* phe_server_matvec_packed_host: phe_server_matvec_host for the packed primitive: host seeds /
- * bodies in, h_out_packed uint32 [T][G][2][N] out (chunked, copies overlapped; allocates its
- * own device workspace).                                                                    */
+ * bodies in, h_out_packed uint32 [T][G][2][N] out (chunked, copies overlapped; caller workspace
+ * of phe_server_matvec_packed_host_ws_bytes(...) bytes, sized for the full and the ragged last
+ * chunk).                                                                                   */
+size_t phe_server_matvec_packed_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose,
+                                              int64_t T, int64_t chunk_tokens);
 int phe_server_matvec_packed_host(const phe_params *p, const void *d_wprep, int64_t d_out,
                                   int64_t d_in, int transpose, const void *d_kprep,
                                   const uint64_t *h_seeds, const uint64_t *h_body, int64_t T,
-                                  int64_t chunk_tokens, uint32_t *h_out_packed, void *stream);
+                                  int64_t chunk_tokens, uint32_t *h_out_packed, void *d_ws, size_t ws_bytes,
+                                  void *stream);
 /* phe_decrypt_packed (client): d_y int32 [T][rows] = decode(B' - A'S) coefficient-wise. */
 int phe_decrypt_packed(const phe_params *p, const uint8_t *d_S, const uint32_t *d_packed, int64_t T,
                        int64_t rows, int32_t q_bits, int32_t *d_y, void *stream);
@@ -261,10 +273,14 @@ int phe_wire_serialize_packed(const phe_params *p, const uint32_t *d_packed, int
 int phe_wire_deserialize_packed(const phe_params *p, const uint8_t *d_wire, int64_t n_ct,
                                 uint32_t *d_packed, void *stream);
 /* The server step as the network sees it: h_wire_in [T][L] input blocks -> h_wire_out [T][G]
- * packed ciphertexts (host buffers; chunked; allocates its own device workspace).           */
+ * packed ciphertexts (host buffers; chunked; caller workspace of phe_server_wire_host_ws_bytes
+ * bytes, sized for the full and the ragged last chunk: the packing workspace is not monotone
+ * in T).                                                                                    */
+size_t phe_server_wire_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose, int64_t T,
+                                     int64_t chunk_tokens);
 int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
                          int transpose, const void *d_kprep, const uint8_t *h_wire_in, int64_t T,
-                         int64_t chunk_tokens, uint8_t *h_wire_out, void *stream);
+                         int64_t chunk_tokens, uint8_t *h_wire_out, void *d_ws, size_t ws_bytes, void *stream);
 
 /* ---- NEXT #4: the mask contraction a5 in the NTT domain ---------
  * Same contract and bit-identical results as phe_matmul_clear(_T): Eq. 6 defines the
@@ -341,10 +357,13 @@ int phe_wire_deserialize_lwe(const phe_params *p, const uint8_t *d_wire, int64_t
 /* The LWE server step as the network sees it: h_wire_in [T][L] wire input blocks (9992 B each)
  * -> h_wire_out [T][phe_wire_lwe_bytes(p, R)], R = row_end - row_begin; chunked H2D, deserialize,
  * ct_prepare, matmul_clear(_T) with the fused switch, serialize, D2H on two internal streams
- * (same workspace exception as phe_server_matvec_host).  Synchronous.                       */
+ * (caller workspace of phe_server_matvec_wire_host_ws_bytes bytes).  Synchronous.           */
+size_t phe_server_matvec_wire_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose,
+                                            int64_t row_begin, int64_t row_end, int64_t T, int64_t chunk_tokens);
 int phe_server_matvec_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
                                 int transpose, int64_t row_begin, int64_t row_end, const uint8_t *h_wire_in,
-                                int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *stream);
+                                int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *d_ws, size_t ws_bytes,
+                                void *stream);
 
 /* ---- NEXT #1 stage 2 in the NTT domain (Eq. 7 + Eq. 8) ---------------
  * Exchanging Eq. 7's sum over outputs j with Eq. 4's sum over KSK rows gives, for packed
@@ -381,15 +400,19 @@ size_t phe_packed_ntt_ws_bytes(const phe_params *p, int64_t rows, int64_t T);
 int phe_matmul_clear_packed_ntt(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
                                 int transpose, const void *d_operand, int64_t T, const void *d_nksk,
                                 void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream);
+size_t phe_server_wire_host_ntt_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose, int64_t T,
+                                         int64_t chunk_tokens);
 int phe_server_wire_host_ntt(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
                              const void *d_nksk, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
-                             uint8_t *h_wire_out, void *stream);
+                             uint8_t *h_wire_out, void *d_ws, size_t ws_bytes, void *stream);
 int phe_matmul_clear_packed_nttw(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
                                  int64_t d_in, int transpose, const void *d_operand, int64_t T, const void *d_nksk,
                                  void *d_ws, size_t ws_bytes, uint32_t *d_out_packed, void *stream);
+size_t phe_server_wire_host_nttw_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose, int64_t T,
+                                          int64_t chunk_tokens);
 int phe_server_wire_host_nttw(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
                               int64_t d_in, int transpose, const void *d_nksk, const uint8_t *h_wire_in, int64_t T,
-                              int64_t chunk_tokens, uint8_t *h_wire_out, void *stream);
+                              int64_t chunk_tokens, uint8_t *h_wire_out, void *d_ws, size_t ws_bytes, void *stream);
 
 /* ---- introspection (tests / bench) -------------------------------------------------- */
 /* Number of kernel launches the last phe_matmul_clear[_T] on this thread enqueued. */

@@ -43,6 +43,9 @@ EXPORTS = [
     "phe_matmul_clear_packed_nttw", "phe_server_wire_host_nttw",
     "phe_wire_lwe_bytes", "phe_wire_serialize_lwe", "phe_wire_deserialize_lwe", "phe_server_matvec_wire_host",
     "phe_matmul_clear_digits_ntt", "phe_matmul_clear_into", "phe_matmul_clear_ntt_into",
+    "phe_server_matvec_host_ws_bytes", "phe_server_matvec_packed_host_ws_bytes", "phe_server_wire_host_ws_bytes",
+    "phe_server_wire_host_ntt_ws_bytes", "phe_server_wire_host_nttw_ws_bytes",
+    "phe_server_matvec_wire_host_ws_bytes",
 ]
 
 
@@ -100,7 +103,13 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_modswitch": ([_vp, _vp, _i64, _i32, _i32, _vp], ctypes.c_int),
         "phe_decrypt_unpack": ([_P, _vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp], ctypes.c_int),
         "phe_server_matvec_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64,
-                                    _i64, _vp, _vp, _vp], ctypes.c_int),
+                                    _i64, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
+        "phe_server_matvec_host_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64, _i64, _i64], _sz),
+        "phe_server_matvec_wire_host_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64, _i64, _i64], _sz),
+        "phe_server_matvec_packed_host_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64], _sz),
+        "phe_server_wire_host_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64], _sz),
+        "phe_server_wire_host_ntt_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64], _sz),
+        "phe_server_wire_host_nttw_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64], _sz),
         "phe_ksk_bytes": ([_P], _sz),
         "phe_ksk_gen": ([_P, _vp, _u64, _vp, _sz, _vp], ctypes.c_int),
         "phe_ksk_prep_bytes": ([_P], _sz),
@@ -113,14 +122,15 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_pack_acc_bytes": ([_P, _i64, _i64], _sz),
         "phe_pack": ([_P, _vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
         "phe_server_matvec_packed_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _i64, _i64, _vp,
-                                           _vp], ctypes.c_int),
+                                           _vp, _sz, _vp], ctypes.c_int),
         "phe_wire_input_bytes": ([_P], _sz),
         "phe_wire_output_bytes": ([_P], _sz),
         "phe_wire_serialize_inputs": ([_P, _vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
         "phe_wire_deserialize_inputs": ([_P, _vp, _i64, _i64, _vp, _vp, _vp], ctypes.c_int),
         "phe_wire_serialize_packed": ([_P, _vp, _i64, _vp, _vp], ctypes.c_int),
         "phe_wire_deserialize_packed": ([_P, _vp, _i64, _vp, _vp], ctypes.c_int),
-        "phe_server_wire_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
+        "phe_server_wire_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp],
+                                 ctypes.c_int),
         "phe_matmul_clear_ct": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _sz,
                                  _vp, _vp, _vp], ctypes.c_int),
         "phe_ntt_primes": ([_vp], ctypes.c_int),
@@ -133,8 +143,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_wire_lwe_bytes": ([_P, _i64], _sz),
         "phe_wire_serialize_lwe": ([_P, _vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
         "phe_wire_deserialize_lwe": ([_P, _vp, _i64, _i64, _vp, _vp, _vp], ctypes.c_int),
-        "phe_server_matvec_wire_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _i64, _i64, _vp, _vp],
-                                        ctypes.c_int),
+        "phe_server_matvec_wire_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _i64, _i64, _vp, _vp,
+                                         _sz, _vp], ctypes.c_int),
         "phe_encrypt_pack_ntt": ([_P, _vp, _vp, _vp, _i64, _i64, _u64, _u64, _vp, _vp, _vp], ctypes.c_int),
         "phe_ntt_max_blocks": ([_P], _i64),
         "phe_ntt_tables_bytes": ([_P], _sz),
@@ -154,12 +164,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_packed_ntt_ws_bytes": ([_P, _i64, _i64], _sz),
         "phe_matmul_clear_packed_ntt": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp, _vp, _sz, _vp, _vp],
                                         ctypes.c_int),
-        "phe_server_wire_host_ntt": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp],
+        "phe_server_wire_host_ntt": ([_P, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp],
                                      ctypes.c_int),
         "phe_matmul_clear_packed_nttw": ([_P, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp, _vp, _sz, _vp,
                                           _vp], ctypes.c_int),
-        "phe_server_wire_host_nttw": ([_P, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp],
-                                      ctypes.c_int),
+        "phe_server_wire_host_nttw": ([_P, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp,
+                                       _sz, _vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -197,6 +207,25 @@ def _dev(t: torch.Tensor, dtype=None, name="tensor"):
 
 
 # ------------------------------------------------------------------ params
+def _need(t: torch.Tensor, dtype, shape, name: str) -> torch.Tensor:
+    """A caller-supplied device tensor the C ABI reads or writes without a size argument:
+    CUDA, `dtype`, contiguous, exactly `shape` (no silent out-of-bounds access)."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+        raise PheError(f"{name} must be a contiguous CUDA {dtype} tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise PheError(f"{name} has shape {tuple(t.shape)}, the call needs {tuple(shape)}")
+    return t
+
+
+def _need_bytes(t: torch.Tensor, nbytes: int, name: str) -> torch.Tensor:
+    """A caller-supplied device buffer of at least `nbytes` bytes (operands, workspaces)."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous():
+        raise PheError(f"{name} must be a contiguous CUDA tensor")
+    if t.numel() * t.element_size() < nbytes:
+        raise PheError(f"{name} holds {t.numel() * t.element_size()} bytes, the call reads {nbytes}")
+    return t
+
+
 def params(preset: int = PRESET_PAPER, **override) -> Params:
     p = Params()
     _check(load().phe_params_init(ctypes.byref(p), preset), "phe_params_init")
@@ -354,16 +383,37 @@ def modswitch(x: torch.Tensor, from_bits: int, to_bits: int, out: torch.Tensor |
 def server_matvec_host(p: Params, w: Weights, h_seeds: torch.Tensor, h_body: torch.Tensor,
                        h_out_mask: torch.Tensor, h_out_body: torch.Tensor, chunk_tokens: int = 256,
                        row_begin: int = 0, row_end: int | None = None) -> None:
-    """End-to-end with HOST buffers (pinned CPU tensors): H2D, prepare, GEMM, D2H pipelined."""
-    for t, n in [(h_seeds, "h_seeds"), (h_body, "h_body"), (h_out_mask, "h_out_mask"), (h_out_body, "h_out_body")]:
-        if t.is_cuda or not t.is_contiguous():
-            raise PheError(f"{n} must be a contiguous host tensor")
+    """End-to-end with HOST buffers (pinned CPU tensors): H2D, prepare, GEMM, D2H pipelined.
+    The device workspace (two chunk slots, phe_server_matvec_host_ws_bytes) comes from torch's
+    allocator on the weights' device; the call is synchronous, so it is free again on return."""
     T = h_seeds.shape[0]
     row_end = w.rows if row_end is None else row_end
+    R, L = row_end - row_begin, p.L(w.cols)
+    _host(h_seeds, "h_seeds", T * L * 8); _host(h_body, "h_body", T * L * p.N * 8)
+    _host(h_out_mask, "h_out_mask", T * R * p.N * 4); _host(h_out_body, "h_out_body", T * R * 4)
+    if T == 0 or R == 0:
+        return
+    ws = _host_ws(load().phe_server_matvec_host_ws_bytes(ctypes.byref(p), w.d_out, w.d_in, int(w.transpose),
+                                                         row_begin, row_end, T, chunk_tokens), w.buf.device)
     _check(load().phe_server_matvec_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
                                          row_begin, row_end, _ptr(h_seeds), _ptr(h_body), T, chunk_tokens,
-                                         _ptr(h_out_mask), _ptr(h_out_body), _stream()),
+                                         _ptr(h_out_mask), _ptr(h_out_body), _ptr(ws), ws.numel(), _stream()),
            "phe_server_matvec_host")
+
+
+def _host(t: torch.Tensor, name: str, nbytes: int) -> None:
+    """A host-buffer argument: contiguous CPU memory of exactly `nbytes` bytes."""
+    if t.is_cuda or not t.is_contiguous():
+        raise PheError(f"{name} must be a contiguous host tensor")
+    if t.numel() * t.element_size() != nbytes:
+        raise PheError(f"{name} holds {t.numel() * t.element_size()} bytes, the call needs {nbytes}")
+
+
+def _host_ws(nbytes: int, device) -> torch.Tensor:
+    """Device workspace of a host pipeline (its *_ws_bytes query; 0 = arguments it rejects)."""
+    if nbytes == 0:
+        raise PheError("host pipeline: invalid arguments (workspace query returned 0)")
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
 
 
 def last_launch_count() -> int:
@@ -399,8 +449,10 @@ def matmul_clear_packed(p: Params, w: Weights, operand: torch.Tensor, T: int, ks
                         out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
     """RLWE(Wx) (Eq. 7 + Eq. 8): int32 [T][G][2][N] (A', B' at q_out), G = ceil(rows / N)."""
     G = (w.rows + p.N - 1) // p.N
+    _need_bytes(operand, load().phe_ct_operand_bytes(ctypes.byref(p), T, p.L(w.cols)), "operand")
     if out is None:
         out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=operand.device)
+    _need(out, torch.int32, (T, G, 2, p.N), "out")
     nbytes = load().phe_packed_ws_bytes(ctypes.byref(p), w.rows, T)
     if ws is None:
         ws = _ws_cache.get(operand.device)
@@ -427,10 +479,13 @@ def matmul_clear_digits(p: Params, w: Weights, operand: torch.Tensor, T: int, di
     """Stage 1 of the packed primitive: Eq. 6 with masks as Decomp digits (int8 [T][R256][4][N],
     KS_LEVELS = 4) and bodies uint64 [T][R] (int64 storage)."""
     r256 = (w.rows + 255) // 256 * 256
+    _need_bytes(operand, load().phe_ct_operand_bytes(ctypes.byref(p), T, p.L(w.cols)), "operand")
     if digits is None:
         digits = torch.empty((T, r256, KS_LEVELS, p.N), dtype=torch.int8, device=operand.device)
     if body is None:
         body = torch.empty((T, w.rows), dtype=torch.int64, device=operand.device)
+    _need(digits, torch.int8, (T, r256, KS_LEVELS, p.N), "digits")
+    _need(body, torch.int64, (T, w.rows), "body")
     _check(load().phe_matmul_clear_digits(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
                                           _ptr(operand), T, _ptr(digits), _ptr(body), _stream()),
            "phe_matmul_clear_digits")
@@ -441,8 +496,11 @@ def pack(p: Params, digits: torch.Tensor, body: torch.Tensor, ksk: KeySwitchKey,
     """Stage 2: Eq. 8 + Eq. 7 (KeySwitch GEMM, Rotate, sum) + ModulusSwitch."""
     T, rows = body.shape
     G = (rows + p.N - 1) // p.N
+    _need(body, torch.int64, (T, rows), "body")
+    _need(digits, torch.int8, (T, (rows + 255) // 256 * 256, KS_LEVELS, p.N), "digits")
     if out is None:
         out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=body.device)
+    _need(out, torch.int32, (T, G, 2, p.N), "out")
     nbytes = load().phe_pack_acc_bytes(ctypes.byref(p), rows, T)
     if acc is None:
         acc = torch.empty(nbytes, dtype=torch.uint8, device=body.device)
@@ -469,8 +527,11 @@ def pack_ntt(p: Params, digits: torch.Tensor, body: torch.Tensor, nksk: NttKeySw
     """Stage 2 in the NTT domain: same contract and bit-identical output as pack()."""
     T, rows = body.shape
     G = (rows + p.N - 1) // p.N
+    _need(body, torch.int64, (T, rows), "body")
+    _need(digits, torch.int8, (T, (rows + 255) // 256 * 256, KS_LEVELS, p.N), "digits")
     if out is None:
         out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=body.device)
+    _need(out, torch.int32, (T, G, 2, p.N), "out")
     nbytes = load().phe_pack_ntt_ws_bytes(ctypes.byref(p), rows, T)
     if ws is None:
         ws = torch.empty(nbytes, dtype=torch.uint8, device=body.device)
@@ -482,12 +543,16 @@ def pack_ntt(p: Params, digits: torch.Tensor, body: torch.Tensor, nksk: NttKeySw
 def server_matvec_packed_host(p: Params, w: Weights, ksk: KeySwitchKey, h_seeds: torch.Tensor,
                               h_body: torch.Tensor, h_out: torch.Tensor, chunk_tokens: int = 256) -> None:
     """End to end with HOST buffers for the packed primitive: h_out int32 [T][G][2][N]."""
-    for t, n in [(h_seeds, "h_seeds"), (h_body, "h_body"), (h_out, "h_out")]:
-        if t.is_cuda or not t.is_contiguous():
-            raise PheError(f"{n} must be a contiguous host tensor")
+    T, L, G = h_seeds.shape[0], p.L(w.cols), (w.rows + p.N - 1) // p.N
+    _host(h_seeds, "h_seeds", T * L * 8); _host(h_body, "h_body", T * L * p.N * 8)
+    _host(h_out, "h_out", T * G * 2 * p.N * 4)
+    if T == 0:
+        return
+    ws = _host_ws(load().phe_server_matvec_packed_host_ws_bytes(ctypes.byref(p), w.d_out, w.d_in, int(w.transpose),
+                                                                T, chunk_tokens), w.buf.device)
     _check(load().phe_server_matvec_packed_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
-                                                _ptr(ksk.buf), _ptr(h_seeds), _ptr(h_body), h_seeds.shape[0],
-                                                chunk_tokens, _ptr(h_out), _stream()),
+                                                _ptr(ksk.buf), _ptr(h_seeds), _ptr(h_body), T,
+                                                chunk_tokens, _ptr(h_out), _ptr(ws), ws.numel(), _stream()),
            "phe_server_matvec_packed_host")
 
 
@@ -536,20 +601,31 @@ def wire_deserialize_packed(p: Params, wire: torch.Tensor) -> torch.Tensor:
 def server_wire_host(p: Params, w: Weights, ksk: KeySwitchKey, h_wire_in: torch.Tensor, h_wire_out: torch.Tensor,
                      chunk_tokens: int = 255) -> None:
     """The server step on wire bytes (host buffers): [T][L][9992] in -> [T][G][13312] out."""
-    for t, n in [(h_wire_in, "h_wire_in"), (h_wire_out, "h_wire_out")]:
-        if t.is_cuda or not t.is_contiguous():
-            raise PheError(f"{n} must be a contiguous host tensor")
-    _check(load().phe_server_wire_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
-                                       _ptr(ksk.buf), _ptr(h_wire_in), h_wire_in.shape[0], chunk_tokens,
-                                       _ptr(h_wire_out), _stream()), "phe_server_wire_host")
+    _wire_host(p, w, ksk, h_wire_in, h_wire_out, chunk_tokens, "phe_server_wire_host")
+
+
+def _wire_host(p, w, key, h_wire_in, h_wire_out, chunk_tokens, api):
+    T, L, G = h_wire_in.shape[0], p.L(w.cols), (w.rows + p.N - 1) // p.N
+    _host(h_wire_in, "h_wire_in", T * L * wire_input_bytes(p))
+    _host(h_wire_out, "h_wire_out", T * G * wire_output_bytes(p))
+    if T == 0:
+        return
+    lib = load()
+    ws = _host_ws(getattr(lib, api + "_ws_bytes")(ctypes.byref(p), w.d_out, w.d_in, int(w.transpose), T,
+                                                  chunk_tokens), w.buf.device)
+    head = [ctypes.byref(p)] + ([_ptr(w.tables.buf)] if api.endswith("_nttw") else [])
+    _check(getattr(lib, api)(*head, _ptr(w.buf), w.d_out, w.d_in, int(w.transpose), _ptr(key.buf), _ptr(h_wire_in),
+                             T, chunk_tokens, _ptr(h_wire_out), _ptr(ws), ws.numel(), _stream()), api)
 
 
 def matmul_clear_packed_ntt(p: Params, w: Weights, operand: torch.Tensor, T: int, nksk: "NttKeySwitchKey",
                             out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
     """matmul_clear_packed with stage 2 (Eq. 7/8) in the NTT domain: same output."""
     G = (w.rows + p.N - 1) // p.N
+    _need_bytes(operand, load().phe_ct_operand_bytes(ctypes.byref(p), T, p.L(w.cols)), "operand")
     if out is None:
         out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=operand.device)
+    _need(out, torch.int32, (T, G, 2, p.N), "out")
     nbytes = load().phe_packed_ntt_ws_bytes(ctypes.byref(p), w.rows, T)
     if ws is None:
         ws = torch.empty(nbytes, dtype=torch.uint8, device=operand.device)
@@ -562,12 +638,7 @@ def matmul_clear_packed_ntt(p: Params, w: Weights, operand: torch.Tensor, T: int
 def server_wire_host_ntt(p: Params, w: Weights, nksk: "NttKeySwitchKey", h_wire_in: torch.Tensor,
                          h_wire_out: torch.Tensor, chunk_tokens: int = 255) -> None:
     """server_wire_host with the packing stage in the NTT domain (phe_server_wire_host_ntt)."""
-    for t, n in [(h_wire_in, "h_wire_in"), (h_wire_out, "h_wire_out")]:
-        if t.is_cuda or not t.is_contiguous():
-            raise PheError(f"{n} must be a contiguous host tensor")
-    _check(load().phe_server_wire_host_ntt(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
-                                           _ptr(nksk.buf), _ptr(h_wire_in), h_wire_in.shape[0], chunk_tokens,
-                                           _ptr(h_wire_out), _stream()), "phe_server_wire_host_ntt")
+    _wire_host(p, w, nksk, h_wire_in, h_wire_out, chunk_tokens, "phe_server_wire_host_ntt")
 
 
 def matmul_clear_packed_nttw(p: Params, w: "NttWeights", operand: torch.Tensor, T: int, nksk: "NttKeySwitchKey",
@@ -575,8 +646,10 @@ def matmul_clear_packed_nttw(p: Params, w: "NttWeights", operand: torch.Tensor, 
     """matmul_clear_packed with both stages in the NTT domain (operand from ntt_ct_prepare): same
     output (phe_matmul_clear_packed_nttw)."""
     G = (w.rows + p.N - 1) // p.N
+    _need_bytes(operand, load().phe_ntt_operand_bytes(ctypes.byref(p), T, p.L(w.cols)), "operand")
     if out is None:
         out = torch.empty((T, G, 2, p.N), dtype=torch.int32, device=operand.device)
+    _need(out, torch.int32, (T, G, 2, p.N), "out")
     nbytes = load().phe_packed_ntt_ws_bytes(ctypes.byref(p), w.rows, T)
     if ws is None:
         ws = torch.empty(nbytes, dtype=torch.uint8, device=operand.device)
@@ -589,12 +662,7 @@ def matmul_clear_packed_nttw(p: Params, w: "NttWeights", operand: torch.Tensor, 
 def server_wire_host_nttw(p: Params, w: "NttWeights", nksk: "NttKeySwitchKey", h_wire_in: torch.Tensor,
                           h_wire_out: torch.Tensor, chunk_tokens: int = 255) -> None:
     """server_wire_host with both stages in the NTT domain (phe_server_wire_host_nttw)."""
-    for t, n in [(h_wire_in, "h_wire_in"), (h_wire_out, "h_wire_out")]:
-        if t.is_cuda or not t.is_contiguous():
-            raise PheError(f"{n} must be a contiguous host tensor")
-    _check(load().phe_server_wire_host_nttw(ctypes.byref(p), _ptr(w.tables.buf), _ptr(w.buf), w.d_out, w.d_in,
-                                            int(w.transpose), _ptr(nksk.buf), _ptr(h_wire_in), h_wire_in.shape[0],
-                                            chunk_tokens, _ptr(h_wire_out), _stream()), "phe_server_wire_host_nttw")
+    _wire_host(p, w, nksk, h_wire_in, h_wire_out, chunk_tokens, "phe_server_wire_host_nttw")
 
 
 # ------------------------------------------------------------------ NEXT #4: NTT-domain contraction
@@ -682,11 +750,20 @@ def wire_lwe_bytes(p: Params, R: int) -> int:
     return int(load().phe_wire_lwe_bytes(ctypes.byref(p), R))
 
 
-def wire_serialize_lwe(p: Params, mask: torch.Tensor, body: torch.Tensor) -> torch.Tensor:
-    """uint32 LWE outputs [T][R][N], [T][R] -> bytes [T][wire_lwe_bytes(p, R)] at q_out bits."""
+def wire_serialize_lwe(p: Params, mask: torch.Tensor, body: torch.Tensor, out: torch.Tensor | None = None
+                       ) -> torch.Tensor:
+    """uint32 LWE outputs [T][R][N], [T][R] -> bytes [T][wire_lwe_bytes(p, R)] at q_out bits
+    (`out`: a contiguous uint8 CUDA tensor of exactly that shape, 8-byte aligned)."""
     _dev(mask, torch.int32, "mask"); _dev(body, torch.int32, "body")
     T, R = body.shape
-    out = torch.empty((T, wire_lwe_bytes(p, R)), dtype=torch.uint8, device=mask.device)
+    if tuple(mask.shape) != (T, R, p.N):
+        raise PheError("mask must be [T][R][N] matching body [T][R]")
+    nb = wire_lwe_bytes(p, R)
+    if out is None:
+        out = torch.empty((T, nb), dtype=torch.uint8, device=mask.device)
+    elif (not out.is_cuda or out.dtype != torch.uint8 or not out.is_contiguous() or tuple(out.shape) != (T, nb)
+          or out.data_ptr() % 8):
+        raise PheError(f"out must be a contiguous, 8-byte aligned uint8 CUDA tensor of shape {(T, nb)}")
     _check(load().phe_wire_serialize_lwe(ctypes.byref(p), _ptr(mask), _ptr(body), T, R, _ptr(out), _stream()),
            "phe_wire_serialize_lwe")
     return out
@@ -706,23 +783,31 @@ def server_matvec_wire_host(p: Params, w: Weights, h_wire_in: torch.Tensor, h_wi
                             chunk_tokens: int = 256, row_begin: int = 0, row_end: int | None = None) -> None:
     """End to end on wire bytes with HOST buffers: input blocks [T][L][9992] -> switched LWE outputs
     at q_out bits [T][wire_lwe_bytes(p, R)] (phe_server_matvec_wire_host)."""
-    for t, n in [(h_wire_in, "h_wire_in"), (h_wire_out, "h_wire_out")]:
-        if t.is_cuda or not t.is_contiguous():
-            raise PheError(f"{n} must be a contiguous host tensor")
     T = h_wire_in.shape[0]
     row_end = w.rows if row_end is None else row_end
+    R, L = row_end - row_begin, p.L(w.cols)
+    _host(h_wire_in, "h_wire_in", T * L * wire_input_bytes(p))
+    _host(h_wire_out, "h_wire_out", T * (wire_lwe_bytes(p, R) if R > 0 else 0))
+    if T == 0 or R == 0:
+        return
+    ws = _host_ws(load().phe_server_matvec_wire_host_ws_bytes(ctypes.byref(p), w.d_out, w.d_in, int(w.transpose),
+                                                              row_begin, row_end, T, chunk_tokens), w.buf.device)
     _check(load().phe_server_matvec_wire_host(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose),
                                               row_begin, row_end, _ptr(h_wire_in), T, chunk_tokens,
-                                              _ptr(h_wire_out), _stream()), "phe_server_matvec_wire_host")
+                                              _ptr(h_wire_out), _ptr(ws), ws.numel(), _stream()),
+           "phe_server_matvec_wire_host")
 
 
 def matmul_clear_digits_ntt(p: Params, w: "NttWeights", operand: torch.Tensor, T: int, digits=None, body=None):
     """matmul_clear_digits through the NTT-domain contraction (bit-identical); feeds phe.pack."""
     r256 = (w.rows + 255) // 256 * 256
+    _need_bytes(operand, load().phe_ntt_operand_bytes(ctypes.byref(p), T, p.L(w.cols)), "operand")
     if digits is None:
         digits = torch.empty((T, r256, KS_LEVELS, p.N), dtype=torch.int8, device=operand.device)
     if body is None:
         body = torch.empty((T, w.rows), dtype=torch.int64, device=operand.device)
+    _need(digits, torch.int8, (T, r256, KS_LEVELS, p.N), "digits")
+    _need(body, torch.int64, (T, w.rows), "body")
     _check(load().phe_matmul_clear_digits_ntt(ctypes.byref(p), _ptr(w.tables.buf), _ptr(w.buf), w.d_out, w.d_in,
                                               int(w.transpose), _ptr(operand), T, _ptr(digits), _ptr(body),
                                               _stream()), "phe_matmul_clear_digits_ntt")

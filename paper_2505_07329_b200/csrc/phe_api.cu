@@ -277,21 +277,85 @@ int phe_decrypt_unpack(const phe_params *p, const uint8_t *d_S, const void *d_ma
 }
 
 // ------------------------------------------------------------------ host end-to-end
-// Chunked pipeline over two device slots and two streams: chunk c runs H2D -> ct_prepare ->
-// limb GEMM -> D2H on stream c%2, so chunk c+1's copies overlap chunk c's GEMM.
-struct HostWs {
-  void *buf = nullptr;
-  size_t bytes = 0;
+// Chunked pipelines over two workspace slots and two streams: chunk c runs H2D -> compute -> D2H
+// on stream c%2 in slot c%2, so chunk c+1's copies overlap chunk c's kernels.  The device memory
+// is the caller's (d_ws: two slots, sized by the matching *_ws_bytes query; SURVEY §8(b)
+// ownership rule); the two streams and the ordering event are created per call on the current
+// device and destroyed before returning, after both streams drained -- also on an error, so no
+// copy touches the caller's host buffers once the call has returned.
+struct HostPipe {
   cudaStream_t st[2] = {nullptr, nullptr};
   cudaEvent_t ev = nullptr;
+  int start(cudaStream_t caller) {
+    for (int s = 0; s < 2; s++)
+      if (cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking) != cudaSuccess)
+        return phe_set_cuda_error(cudaGetLastError());
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+      return phe_set_cuda_error(cudaGetLastError());
+    // order after work already queued on the caller's stream (weight registration, the
+    // workspace allocation of a stream-ordered allocator)
+    if (cudaEventRecord(ev, caller) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+    cudaStreamWaitEvent(st[0], ev, 0);
+    cudaStreamWaitEvent(st[1], ev, 0);
+    return PHE_OK;
+  }
+  // drain both streams (always), release them, and report the first failure
+  int finish(int rc) {
+    cudaError_t e0 = st[0] ? cudaStreamSynchronize(st[0]) : cudaSuccess;
+    cudaError_t e1 = st[1] ? cudaStreamSynchronize(st[1]) : cudaSuccess;
+    release();
+    if (rc) return rc;
+    if (e0 != cudaSuccess) return phe_set_cuda_error(e0);
+    if (e1 != cudaSuccess) return phe_set_cuda_error(e1);
+    cudaError_t e = cudaGetLastError();
+    return e != cudaSuccess ? phe_set_cuda_error(e) : PHE_OK;
+  }
+  void release() {
+    for (int s = 0; s < 2; s++)
+      if (st[s]) { cudaStreamDestroy(st[s]); st[s] = nullptr; }
+    if (ev) { cudaEventDestroy(ev); ev = nullptr; }
+  }
+  ~HostPipe() { release(); }
 };
-static thread_local HostWs g_ws;
+
+// sequential carving of one workspace slot
+struct Carve {
+  uint8_t *base;
+  size_t off = 0;
+  void *take(size_t bytes) {
+    void *r = base + off;
+    off += bytes;
+    return r;
+  }
+};
+
+static inline int64_t host_chunk(int64_t T, int64_t chunk_tokens) { return chunk_tokens < T ? chunk_tokens : T; }
+
+// slot of phe_server_matvec_host: seeds, bodies, operand, uint32 mask and body outputs
+struct MatvecSlot {
+  size_t seeds, body, op, om, ob;
+  size_t total() const { return seeds + body + op + om + ob; }
+};
+static MatvecSlot matvec_slot(const phe_params *p, int64_t L, int64_t R, int64_t C) {
+  const int64_t N = p->N;
+  return {(size_t)round_up(C * L * 8, 256), (size_t)round_up(C * L * N * 8, 256),
+          (size_t)round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256), (size_t)round_up(C * R * N * 4, 256),
+          (size_t)round_up(C * R * 4, 256)};
+}
+
+size_t phe_server_matvec_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose,
+                                       int64_t row_begin, int64_t row_end, int64_t T, int64_t chunk_tokens) {
+  if (!p || phe_params_validate(p) || d_out < 1 || d_in < 1 || T < 1 || chunk_tokens < 1) return 0;
+  const int64_t cols = transpose ? d_out : d_in, R = row_end - row_begin;
+  if (R < 1) return 0;
+  return 2 * matvec_slot(p, phe_num_blocks(p, cols), R, host_chunk(T, chunk_tokens)).total();
+}
 
 int phe_server_matvec_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
                            int transpose, int64_t row_begin, int64_t row_end,
                            const uint64_t *h_seeds, const uint64_t *h_body, int64_t T,
                            int64_t chunk_tokens, uint32_t *h_out_mask, uint32_t *h_out_body,
-                           void *stream) {
+                           void *d_ws, size_t ws_bytes, void *stream) {
   KParams kp;
   int rc = check_gpu(p, &kp);
   if (rc) return rc;
@@ -299,56 +363,33 @@ int phe_server_matvec_host(const phe_params *p, const void *d_wprep, int64_t d_o
   if (rows < 1 || cols < 1 || T < 0 || chunk_tokens < 1) return PHE_EINVAL;
   if (row_begin < 0 || row_end > rows || row_begin > row_end) return PHE_EINVAL;
   if (T == 0 || row_end == row_begin) return PHE_OK;
-  if (!d_wprep || !h_seeds || !h_body || !h_out_mask || !h_out_body) return PHE_EINVAL;
+  if (!d_wprep || !h_seeds || !h_body || !h_out_mask || !h_out_body || !d_ws) return PHE_EINVAL;
   const int64_t N = p->N, L = phe_num_blocks(p, cols), R = row_end - row_begin;
-  const int64_t C = chunk_tokens < T ? chunk_tokens : T;
-  const size_t b_seeds = round_up(C * L * 8, 256), b_body = round_up(C * L * N * 8, 256);
-  const size_t b_op = round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256);
-  const size_t b_om = round_up(C * R * N * 4, 256), b_ob = round_up(C * R * 4, 256);
-  const size_t slot = b_seeds + b_body + b_op + b_om + b_ob;
-  if (g_ws.bytes < 2 * slot) {
-    if (g_ws.buf) cudaFree(g_ws.buf);
-    g_ws.buf = nullptr; g_ws.bytes = 0;
-    if (cudaMalloc(&g_ws.buf, 2 * slot) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
-    g_ws.bytes = 2 * slot;
-  }
-  if (!g_ws.st[0]) {
-    for (int s = 0; s < 2; s++)
-      if (cudaStreamCreateWithFlags(&g_ws.st[s], cudaStreamNonBlocking) != cudaSuccess)
-        return phe_set_cuda_error(cudaGetLastError());
-    if (cudaEventCreateWithFlags(&g_ws.ev, cudaEventDisableTiming) != cudaSuccess)
-      return phe_set_cuda_error(cudaGetLastError());
-  }
-  // order after work already queued on the caller's stream (e.g. weight registration)
-  cudaEventRecord(g_ws.ev, S(stream));
-  cudaStreamWaitEvent(g_ws.st[0], g_ws.ev, 0);
-  cudaStreamWaitEvent(g_ws.st[1], g_ws.ev, 0);
+  const int64_t C = host_chunk(T, chunk_tokens);
+  const MatvecSlot sl = matvec_slot(p, L, R, C);
+  const size_t slot = sl.total();
+  if (ws_bytes < 2 * slot) return PHE_ENOMEM;
+  HostPipe pipe;
+  rc = pipe.start(S(stream));
   int64_t c = 0;
-  for (int64_t t0 = 0; t0 < T; t0 += C, c++) {
+  for (int64_t t0 = 0; !rc && t0 < T; t0 += C, c++) {
     const int64_t n = (T - t0) < C ? (T - t0) : C;
-    cudaStream_t st = g_ws.st[c & 1];
-    uint8_t *base = static_cast<uint8_t *>(g_ws.buf) + (c & 1) * slot;
-    uint64_t *d_seeds = reinterpret_cast<uint64_t *>(base);
-    uint64_t *d_bod = reinterpret_cast<uint64_t *>(base + b_seeds);
-    void *d_op = base + b_seeds + b_body;
-    uint32_t *d_om = reinterpret_cast<uint32_t *>(base + b_seeds + b_body + b_op);
-    uint32_t *d_ob = reinterpret_cast<uint32_t *>(base + b_seeds + b_body + b_op + b_om);
+    cudaStream_t st = pipe.st[c & 1];
+    Carve cv{static_cast<uint8_t *>(d_ws) + (c & 1) * slot};
+    uint64_t *d_seeds = static_cast<uint64_t *>(cv.take(sl.seeds));
+    uint64_t *d_bod = static_cast<uint64_t *>(cv.take(sl.body));
+    void *d_op = cv.take(sl.op);
+    uint32_t *d_om = static_cast<uint32_t *>(cv.take(sl.om));
+    uint32_t *d_ob = static_cast<uint32_t *>(cv.take(sl.ob));
     cudaMemcpyAsync(d_seeds, h_seeds + t0 * L, n * L * 8, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(d_bod, h_body + t0 * L * N, n * L * N * 8, cudaMemcpyHostToDevice, st);
-    rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
-    if (rc) return rc;
-    rc = matmul_common(p, d_wprep, rows, cols, row_begin, row_end, d_op, n, p->q_out, d_om, d_ob, st);
-    if (rc) return rc;
+    rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, sl.op, st);
+    if (!rc) rc = matmul_common(p, d_wprep, rows, cols, row_begin, row_end, d_op, n, p->q_out, d_om, d_ob, st);
+    if (rc) break;
     cudaMemcpyAsync(h_out_mask + t0 * R * N, d_om, n * R * N * 4, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(h_out_body + t0 * R, d_ob, n * R * 4, cudaMemcpyDeviceToHost, st);
   }
-  cudaError_t e0 = cudaStreamSynchronize(g_ws.st[0]);
-  cudaError_t e1 = cudaStreamSynchronize(g_ws.st[1]);
-  if (e0 != cudaSuccess) return phe_set_cuda_error(e0);
-  if (e1 != cudaSuccess) return phe_set_cuda_error(e1);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return phe_set_cuda_error(e);
-  return PHE_OK;
+  return pipe.finish(rc);
 }
 
 }  // extern "C"
@@ -526,65 +567,66 @@ int phe_decrypt_packed(const phe_params *p, const uint8_t *d_S, const uint32_t *
 
 }  // extern "C"
 
+// slot of phe_server_matvec_packed_host: seeds, bodies, operand, packing workspace, packed outputs.
+// The packing workspace is not monotone in T (the K-split follows wave fill), so it is sized for
+// both the full chunk and the ragged last one.
+struct PackedSlot {
+  size_t seeds, body, op, ws, out;
+  size_t total() const { return seeds + body + op + ws + out; }
+};
+static PackedSlot packed_slot(const phe_params *p, int64_t rows, int64_t L, int64_t C, int64_t tail) {
+  const int64_t N = p->N, G = (rows + N - 1) / N;
+  int64_t ws = (int64_t)phe_packed_ws_bytes(p, rows, C);
+  if (tail > 0 && (int64_t)phe_packed_ws_bytes(p, rows, tail) > ws) ws = (int64_t)phe_packed_ws_bytes(p, rows, tail);
+  return {(size_t)round_up(C * L * 8, 256), (size_t)round_up(C * L * N * 8, 256),
+          (size_t)round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256), (size_t)round_up(ws, 256),
+          (size_t)round_up(C * G * 2 * N * 4, 256)};
+}
+
+extern "C" size_t phe_server_matvec_packed_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in,
+                                                         int transpose, int64_t T, int64_t chunk_tokens) {
+  if (!p || phe_params_validate(p) || d_out < 1 || d_in < 1 || T < 1 || chunk_tokens < 1) return 0;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in, C = host_chunk(T, chunk_tokens);
+  return 2 * packed_slot(p, rows, phe_num_blocks(p, cols), C, T % C).total();
+}
+
 extern "C" int phe_server_matvec_packed_host(const phe_params *p, const void *d_wprep, int64_t d_out,
                                              int64_t d_in, int transpose, const void *d_kprep,
                                              const uint64_t *h_seeds, const uint64_t *h_body, int64_t T,
-                                             int64_t chunk_tokens, uint32_t *h_out_packed, void *stream) {
+                                             int64_t chunk_tokens, uint32_t *h_out_packed, void *d_ws,
+                                             size_t ws_bytes, void *stream) {
   KParams kp;
   int rc = check_pack(p, &kp);
   if (rc) return rc;
   const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
   if (rows < 1 || cols < 1 || T < 0 || chunk_tokens < 1) return PHE_EINVAL;
   if (T == 0) return PHE_OK;
-  if (!d_wprep || !d_kprep || !h_seeds || !h_body || !h_out_packed) return PHE_EINVAL;
+  if (!d_wprep || !d_kprep || !h_seeds || !h_body || !h_out_packed || !d_ws) return PHE_EINVAL;
   const int64_t N = p->N, L = phe_num_blocks(p, cols), G = (rows + N - 1) / N;
-  const int64_t C = chunk_tokens < T ? chunk_tokens : T;
-  const size_t b_seeds = round_up(C * L * 8, 256), b_body = round_up(C * L * N * 8, 256);
-  const size_t b_op = round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256);
-  const size_t b_ws = round_up((int64_t)phe_packed_ws_bytes(p, rows, C), 256);
-  const size_t b_out = round_up(C * G * 2 * N * 4, 256);
-  const size_t slot = b_seeds + b_body + b_op + b_ws + b_out;
-  if (g_ws.bytes < 2 * slot) {
-    if (g_ws.buf) cudaFree(g_ws.buf);
-    g_ws.buf = nullptr; g_ws.bytes = 0;
-    if (cudaMalloc(&g_ws.buf, 2 * slot) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
-    g_ws.bytes = 2 * slot;
-  }
-  if (!g_ws.st[0]) {
-    for (int s = 0; s < 2; s++)
-      if (cudaStreamCreateWithFlags(&g_ws.st[s], cudaStreamNonBlocking) != cudaSuccess)
-        return phe_set_cuda_error(cudaGetLastError());
-    if (cudaEventCreateWithFlags(&g_ws.ev, cudaEventDisableTiming) != cudaSuccess)
-      return phe_set_cuda_error(cudaGetLastError());
-  }
-  cudaEventRecord(g_ws.ev, S(stream));
-  cudaStreamWaitEvent(g_ws.st[0], g_ws.ev, 0);
-  cudaStreamWaitEvent(g_ws.st[1], g_ws.ev, 0);
+  const int64_t C = host_chunk(T, chunk_tokens);
+  const PackedSlot sl = packed_slot(p, rows, L, C, T % C);
+  const size_t slot = sl.total();
+  if (ws_bytes < 2 * slot) return PHE_ENOMEM;
+  HostPipe pipe;
+  rc = pipe.start(S(stream));
   int64_t c = 0;
-  for (int64_t t0 = 0; t0 < T; t0 += C, c++) {
+  for (int64_t t0 = 0; !rc && t0 < T; t0 += C, c++) {
     const int64_t n = (T - t0) < C ? (T - t0) : C;
-    cudaStream_t st = g_ws.st[c & 1];
-    uint8_t *base = static_cast<uint8_t *>(g_ws.buf) + (c & 1) * slot;
-    uint64_t *d_seeds = reinterpret_cast<uint64_t *>(base);
-    uint64_t *d_bod = reinterpret_cast<uint64_t *>(base + b_seeds);
-    void *d_op = base + b_seeds + b_body;
-    void *d_wsp = base + b_seeds + b_body + b_op;
-    uint32_t *d_o = reinterpret_cast<uint32_t *>(base + b_seeds + b_body + b_op + b_ws);
+    cudaStream_t st = pipe.st[c & 1];
+    Carve cv{static_cast<uint8_t *>(d_ws) + (c & 1) * slot};
+    uint64_t *d_seeds = static_cast<uint64_t *>(cv.take(sl.seeds));
+    uint64_t *d_bod = static_cast<uint64_t *>(cv.take(sl.body));
+    void *d_op = cv.take(sl.op);
+    void *d_wsp = cv.take(sl.ws);
+    uint32_t *d_o = static_cast<uint32_t *>(cv.take(sl.out));
     cudaMemcpyAsync(d_seeds, h_seeds + t0 * L, n * L * 8, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(d_bod, h_body + t0 * L * N, n * L * N * 8, cudaMemcpyHostToDevice, st);
-    rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
-    if (rc) return rc;
-    rc = phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws, d_o, st);
-    if (rc) return rc;
+    rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, sl.op, st);
+    if (!rc) rc = phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, sl.ws, d_o, st);
+    if (rc) break;
     cudaMemcpyAsync(h_out_packed + t0 * G * 2 * N, d_o, n * G * 2 * N * 4, cudaMemcpyDeviceToHost, st);
   }
-  cudaError_t e0 = cudaStreamSynchronize(g_ws.st[0]);
-  cudaError_t e1 = cudaStreamSynchronize(g_ws.st[1]);
-  if (e0 != cudaSuccess) return phe_set_cuda_error(e0);
-  if (e1 != cudaSuccess) return phe_set_cuda_error(e1);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return phe_set_cuda_error(e);
-  return PHE_OK;
+  return pipe.finish(rc);
 }
 
 // ------------------------------------------------------------------ NEXT #2: wire format
@@ -653,9 +695,35 @@ int phe_wire_deserialize_packed(const phe_params *p, const uint8_t *d_wire, int6
 // Table 1), wire-format packed ciphertexts out (13312 B each).  Chunked, two streams.
 // mode 0: tensor-core stage 1 + packing GEMM; 1: tensor-core stage 1 + NTT-domain packing;
 // 2: NTT-domain stage 1 (d_tables, NTT weights, NTT operand) + NTT-domain packing.
+struct WireSlot {
+  size_t win, seeds, body, op, ws, pk, wout;
+  size_t total() const { return win + seeds + body + op + ws + pk + wout; }
+};
+static size_t wire_pack_ws(const phe_params *p, int64_t rows, int64_t n, int mode) {
+  return mode >= 1 ? phe_packed_ntt_ws_bytes(p, rows, n) : phe_packed_ws_bytes(p, rows, n);
+}
+static WireSlot wire_slot(const phe_params *p, int64_t rows, int64_t L, int64_t C, int64_t tail, int mode) {
+  const int64_t N = p->N, G = (rows + N - 1) / N;
+  const int64_t bin = (int64_t)phe_wire_input_bytes(p), bout = (int64_t)phe_wire_output_bytes(p);
+  const size_t op = mode == 2 ? phe_ntt_operand_bytes(p, C, L) : phe_ct_operand_bytes(p, C, L);
+  size_t ws = wire_pack_ws(p, rows, C, mode);  // not monotone in T: full and ragged chunk
+  if (tail > 0 && wire_pack_ws(p, rows, tail, mode) > ws) ws = wire_pack_ws(p, rows, tail, mode);
+  return {(size_t)round_up(C * L * bin, 256), (size_t)round_up(C * L * 8, 256), (size_t)round_up(C * L * N * 8, 256),
+          op ? (size_t)round_up((int64_t)op, 256) : 0, (size_t)round_up((int64_t)ws, 256),
+          (size_t)round_up(C * G * 2 * N * 4, 256), (size_t)round_up(C * G * bout, 256)};
+}
+static size_t server_wire_host_ws(const phe_params *p, int64_t d_out, int64_t d_in, int transpose, int64_t T,
+                                  int64_t chunk_tokens, int mode) {
+  if (!p || phe_params_validate(p) || d_out < 1 || d_in < 1 || T < 1 || chunk_tokens < 1) return 0;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in, C = host_chunk(T, chunk_tokens);
+  const WireSlot sl = wire_slot(p, rows, phe_num_blocks(p, cols), C, T % C, mode);
+  return sl.op ? 2 * sl.total() : 0;
+}
+
 static int server_wire_host_impl(const phe_params *p, const void *d_tables, const void *d_wprep, int64_t d_out,
                                  int64_t d_in, int transpose, const void *d_kprep, const uint8_t *h_wire_in,
-                                 int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *stream, int mode) {
+                                 int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *d_ws, size_t ws_bytes,
+                                 void *stream, int mode) {
   const bool ntt_pack = mode >= 1, ntt_s1 = mode == 2;
   if (ntt_s1 && !d_tables) return PHE_EINVAL;
   KParams kp;
@@ -666,87 +734,76 @@ static int server_wire_host_impl(const phe_params *p, const void *d_tables, cons
   const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
   if (rows < 1 || cols < 1 || T < 0 || chunk_tokens < 1) return PHE_EINVAL;
   if (T == 0) return PHE_OK;
-  if (!d_wprep || !d_kprep || !h_wire_in || !h_wire_out) return PHE_EINVAL;
-  const int64_t N = p->N, L = phe_num_blocks(p, cols), G = (rows + N - 1) / N;
+  if (!d_wprep || !d_kprep || !h_wire_in || !h_wire_out || !d_ws) return PHE_EINVAL;
+  const int64_t L = phe_num_blocks(p, cols), G = (rows + p->N - 1) / p->N;
   const int64_t bin = (int64_t)phe_wire_input_bytes(p), bout = (int64_t)phe_wire_output_bytes(p);
-  const int64_t C = chunk_tokens < T ? chunk_tokens : T;
-  const size_t b_win = round_up(C * L * bin, 256), b_seeds = round_up(C * L * 8, 256);
-  const size_t b_body = round_up(C * L * N * 8, 256);
-  const size_t b_op = round_up((int64_t)(ntt_s1 ? phe_ntt_operand_bytes(p, C, L) : phe_ct_operand_bytes(p, C, L)), 256);
-  if (b_op == 0) return PHE_EUNSUPPORTED;
-  const size_t b_ws = round_up((int64_t)(ntt_pack ? phe_packed_ntt_ws_bytes(p, rows, C)
-                                                   : phe_packed_ws_bytes(p, rows, C)), 256);
-  const size_t b_pk = round_up(C * G * 2 * N * 4, 256), b_wout = round_up(C * G * bout, 256);
-  const size_t slot = b_win + b_seeds + b_body + b_op + b_ws + b_pk + b_wout;
-  if (g_ws.bytes < 2 * slot) {
-    if (g_ws.buf) cudaFree(g_ws.buf);
-    g_ws.buf = nullptr; g_ws.bytes = 0;
-    if (cudaMalloc(&g_ws.buf, 2 * slot) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
-    g_ws.bytes = 2 * slot;
-  }
-  if (!g_ws.st[0]) {
-    for (int s = 0; s < 2; s++)
-      if (cudaStreamCreateWithFlags(&g_ws.st[s], cudaStreamNonBlocking) != cudaSuccess)
-        return phe_set_cuda_error(cudaGetLastError());
-    if (cudaEventCreateWithFlags(&g_ws.ev, cudaEventDisableTiming) != cudaSuccess)
-      return phe_set_cuda_error(cudaGetLastError());
-  }
-  cudaEventRecord(g_ws.ev, S(stream));
-  cudaStreamWaitEvent(g_ws.st[0], g_ws.ev, 0);
-  cudaStreamWaitEvent(g_ws.st[1], g_ws.ev, 0);
+  const int64_t C = host_chunk(T, chunk_tokens);
+  const WireSlot sl = wire_slot(p, rows, L, C, T % C, mode);
+  if (sl.op == 0) return PHE_EUNSUPPORTED;
+  const size_t slot = sl.total();
+  if (ws_bytes < 2 * slot) return PHE_ENOMEM;
+  HostPipe pipe;
+  rc = pipe.start(S(stream));
   int64_t c = 0;
-  for (int64_t t0 = 0; t0 < T; t0 += C, c++) {
+  for (int64_t t0 = 0; !rc && t0 < T; t0 += C, c++) {
     const int64_t n = (T - t0) < C ? (T - t0) : C;
-    cudaStream_t st = g_ws.st[c & 1];
-    uint8_t *base = static_cast<uint8_t *>(g_ws.buf) + (c & 1) * slot;
-    uint8_t *d_win = base;
-    uint64_t *d_seeds = reinterpret_cast<uint64_t *>(base + b_win);
-    uint64_t *d_bod = reinterpret_cast<uint64_t *>(base + b_win + b_seeds);
-    void *d_op = base + b_win + b_seeds + b_body;
-    void *d_wsp = base + b_win + b_seeds + b_body + b_op;
-    uint32_t *d_pk = reinterpret_cast<uint32_t *>(base + b_win + b_seeds + b_body + b_op + b_ws);
-    uint8_t *d_wout = base + b_win + b_seeds + b_body + b_op + b_ws + b_pk;
+    cudaStream_t st = pipe.st[c & 1];
+    Carve cv{static_cast<uint8_t *>(d_ws) + (c & 1) * slot};
+    uint8_t *d_win = static_cast<uint8_t *>(cv.take(sl.win));
+    uint64_t *d_seeds = static_cast<uint64_t *>(cv.take(sl.seeds));
+    uint64_t *d_bod = static_cast<uint64_t *>(cv.take(sl.body));
+    void *d_op = cv.take(sl.op);
+    void *d_wsp = cv.take(sl.ws);
+    uint32_t *d_pk = static_cast<uint32_t *>(cv.take(sl.pk));
+    uint8_t *d_wout = static_cast<uint8_t *>(cv.take(sl.wout));
     cudaMemcpyAsync(d_win, h_wire_in + t0 * L * bin, n * L * bin, cudaMemcpyHostToDevice, st);
     rc = phe_wire_deserialize_inputs(p, d_win, n, L, d_seeds, d_bod, st);
     if (!rc)
-      rc = ntt_s1 ? phe_ntt_ct_prepare(p, d_tables, d_seeds, d_bod, n, L, d_op, b_op, st)
-                  : phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
+      rc = ntt_s1 ? phe_ntt_ct_prepare(p, d_tables, d_seeds, d_bod, n, L, d_op, sl.op, st)
+                  : phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, sl.op, st);
     if (!rc)
       rc = ntt_s1 ? phe_matmul_clear_packed_nttw(p, d_tables, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp,
-                                                 b_ws, d_pk, st)
-           : ntt_pack ? phe_matmul_clear_packed_ntt(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws,
+                                                 sl.ws, d_pk, st)
+           : ntt_pack ? phe_matmul_clear_packed_ntt(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, sl.ws,
                                                     d_pk, st)
-                      : phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, b_ws, d_pk, st);
+                      : phe_matmul_clear_packed(p, d_wprep, d_out, d_in, transpose, d_op, n, d_kprep, d_wsp, sl.ws,
+                                                d_pk, st);
     if (!rc) rc = phe_wire_serialize_packed(p, d_pk, n * G, d_wout, st);
-    if (rc) return rc;
+    if (rc) break;
     cudaMemcpyAsync(h_wire_out + t0 * G * bout, d_wout, n * G * bout, cudaMemcpyDeviceToHost, st);
   }
-  cudaError_t e0 = cudaStreamSynchronize(g_ws.st[0]);
-  cudaError_t e1 = cudaStreamSynchronize(g_ws.st[1]);
-  if (e0 != cudaSuccess) return phe_set_cuda_error(e0);
-  if (e1 != cudaSuccess) return phe_set_cuda_error(e1);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return phe_set_cuda_error(e);
-  return PHE_OK;
+  return pipe.finish(rc);
 }
 
+size_t phe_server_wire_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose, int64_t T,
+                                     int64_t chunk_tokens) {
+  return server_wire_host_ws(p, d_out, d_in, transpose, T, chunk_tokens, 0);
+}
+size_t phe_server_wire_host_ntt_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose, int64_t T,
+                                         int64_t chunk_tokens) {
+  return server_wire_host_ws(p, d_out, d_in, transpose, T, chunk_tokens, 1);
+}
+size_t phe_server_wire_host_nttw_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose, int64_t T,
+                                          int64_t chunk_tokens) {
+  return server_wire_host_ws(p, d_out, d_in, transpose, T, chunk_tokens, 2);
+}
 int phe_server_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
                          const void *d_kprep, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
-                         uint8_t *h_wire_out, void *stream) {
+                         uint8_t *h_wire_out, void *d_ws, size_t ws_bytes, void *stream) {
   return server_wire_host_impl(p, nullptr, d_wprep, d_out, d_in, transpose, d_kprep, h_wire_in, T, chunk_tokens,
-                               h_wire_out, stream, 0);
+                               h_wire_out, d_ws, ws_bytes, stream, 0);
 }
 int phe_server_wire_host_ntt(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
                              const void *d_nksk, const uint8_t *h_wire_in, int64_t T, int64_t chunk_tokens,
-                             uint8_t *h_wire_out, void *stream) {
+                             uint8_t *h_wire_out, void *d_ws, size_t ws_bytes, void *stream) {
   return server_wire_host_impl(p, nullptr, d_wprep, d_out, d_in, transpose, d_nksk, h_wire_in, T, chunk_tokens,
-                               h_wire_out, stream, 1);
+                               h_wire_out, d_ws, ws_bytes, stream, 1);
 }
 int phe_server_wire_host_nttw(const phe_params *p, const void *d_tables, const void *d_nttw, int64_t d_out,
                               int64_t d_in, int transpose, const void *d_nksk, const uint8_t *h_wire_in, int64_t T,
-                              int64_t chunk_tokens, uint8_t *h_wire_out, void *stream) {
+                              int64_t chunk_tokens, uint8_t *h_wire_out, void *d_ws, size_t ws_bytes, void *stream) {
   return server_wire_host_impl(p, d_tables, d_nttw, d_out, d_in, transpose, d_nksk, h_wire_in, T, chunk_tokens,
-                               h_wire_out, stream, 2);
+                               h_wire_out, d_ws, ws_bytes, stream, 2);
 }
 
 // ================================================================ LWE outputs on the wire
@@ -791,9 +848,30 @@ int phe_wire_deserialize_lwe(const phe_params *p, const uint8_t *d_wire, int64_t
   return phe::launch_wire_u32(d_body, T, (int)R, p->q_out, w, lwe_body_words(p, R), 1, tw, R * sw, 1, S(stream));
 }
 
+// slot of phe_server_matvec_wire_host: wire inputs, seeds, bodies, operand, uint32 outputs, wire outputs
+struct LweWireSlot {
+  size_t win, seeds, body, op, om, ob, wout;
+  size_t total() const { return win + seeds + body + op + om + ob + wout; }
+};
+static LweWireSlot lwe_wire_slot(const phe_params *p, int64_t L, int64_t R, int64_t C) {
+  const int64_t N = p->N, bin = (int64_t)phe_wire_input_bytes(p), bout = (int64_t)phe_wire_lwe_bytes(p, R);
+  return {(size_t)round_up(C * L * bin, 256), (size_t)round_up(C * L * 8, 256), (size_t)round_up(C * L * N * 8, 256),
+          (size_t)round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256), (size_t)round_up(C * R * N * 4, 256),
+          (size_t)round_up(C * R * 4, 256), (size_t)round_up(C * bout, 256)};
+}
+
+size_t phe_server_matvec_wire_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose,
+                                            int64_t row_begin, int64_t row_end, int64_t T, int64_t chunk_tokens) {
+  if (!p || phe_params_validate(p) || p->N % 64 || d_out < 1 || d_in < 1 || T < 1 || chunk_tokens < 1) return 0;
+  const int64_t cols = transpose ? d_out : d_in, R = row_end - row_begin;
+  if (R < 1) return 0;
+  return 2 * lwe_wire_slot(p, phe_num_blocks(p, cols), R, host_chunk(T, chunk_tokens)).total();
+}
+
 int phe_server_matvec_wire_host(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in,
                                 int transpose, int64_t row_begin, int64_t row_end, const uint8_t *h_wire_in,
-                                int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *stream) {
+                                int64_t T, int64_t chunk_tokens, uint8_t *h_wire_out, void *d_ws, size_t ws_bytes,
+                                void *stream) {
   KParams kp;
   int rc = check_wire(p, &kp);
   if (rc) return rc;
@@ -801,59 +879,36 @@ int phe_server_matvec_wire_host(const phe_params *p, const void *d_wprep, int64_
   if (rows < 1 || cols < 1 || T < 0 || chunk_tokens < 1) return PHE_EINVAL;
   if (row_begin < 0 || row_end > rows || row_begin > row_end) return PHE_EINVAL;
   if (T == 0 || row_end == row_begin) return PHE_OK;
-  if (!d_wprep || !h_wire_in || !h_wire_out) return PHE_EINVAL;
-  const int64_t N = p->N, L = phe_num_blocks(p, cols), R = row_end - row_begin;
-  const int64_t C = chunk_tokens < T ? chunk_tokens : T;
+  if (!d_wprep || !h_wire_in || !h_wire_out || !d_ws) return PHE_EINVAL;
+  const int64_t L = phe_num_blocks(p, cols), R = row_end - row_begin;
+  const int64_t C = host_chunk(T, chunk_tokens);
   const int64_t bin = (int64_t)phe_wire_input_bytes(p), bout = (int64_t)phe_wire_lwe_bytes(p, R);
-  const size_t b_win = round_up(C * L * bin, 256), b_seeds = round_up(C * L * 8, 256);
-  const size_t b_body = round_up(C * L * N * 8, 256);
-  const size_t b_op = round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256);
-  const size_t b_om = round_up(C * R * N * 4, 256), b_ob = round_up(C * R * 4, 256);
-  const size_t b_wout = round_up(C * bout, 256);
-  const size_t slot = b_win + b_seeds + b_body + b_op + b_om + b_ob + b_wout;
-  if (g_ws.bytes < 2 * slot) {
-    if (g_ws.buf) cudaFree(g_ws.buf);
-    g_ws.buf = nullptr; g_ws.bytes = 0;
-    if (cudaMalloc(&g_ws.buf, 2 * slot) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
-    g_ws.bytes = 2 * slot;
-  }
-  if (!g_ws.st[0]) {
-    for (int s = 0; s < 2; s++)
-      if (cudaStreamCreateWithFlags(&g_ws.st[s], cudaStreamNonBlocking) != cudaSuccess)
-        return phe_set_cuda_error(cudaGetLastError());
-    if (cudaEventCreateWithFlags(&g_ws.ev, cudaEventDisableTiming) != cudaSuccess)
-      return phe_set_cuda_error(cudaGetLastError());
-  }
-  cudaEventRecord(g_ws.ev, S(stream));
-  cudaStreamWaitEvent(g_ws.st[0], g_ws.ev, 0);
-  cudaStreamWaitEvent(g_ws.st[1], g_ws.ev, 0);
+  const LweWireSlot sl = lwe_wire_slot(p, L, R, C);
+  const size_t slot = sl.total();
+  if (ws_bytes < 2 * slot) return PHE_ENOMEM;
+  HostPipe pipe;
+  rc = pipe.start(S(stream));
   int64_t c = 0;
-  for (int64_t t0 = 0; t0 < T; t0 += C, c++) {
+  for (int64_t t0 = 0; !rc && t0 < T; t0 += C, c++) {
     const int64_t n = (T - t0) < C ? (T - t0) : C;
-    cudaStream_t st = g_ws.st[c & 1];
-    uint8_t *base = static_cast<uint8_t *>(g_ws.buf) + (c & 1) * slot;
-    uint8_t *d_win = base;
-    uint64_t *d_seeds = reinterpret_cast<uint64_t *>(base + b_win);
-    uint64_t *d_bod = reinterpret_cast<uint64_t *>(base + b_win + b_seeds);
-    void *d_op = base + b_win + b_seeds + b_body;
-    uint32_t *d_om = reinterpret_cast<uint32_t *>(base + b_win + b_seeds + b_body + b_op);
-    uint32_t *d_ob = reinterpret_cast<uint32_t *>(base + b_win + b_seeds + b_body + b_op + b_om);
-    uint8_t *d_wout = base + b_win + b_seeds + b_body + b_op + b_om + b_ob;
+    cudaStream_t st = pipe.st[c & 1];
+    Carve cv{static_cast<uint8_t *>(d_ws) + (c & 1) * slot};
+    uint8_t *d_win = static_cast<uint8_t *>(cv.take(sl.win));
+    uint64_t *d_seeds = static_cast<uint64_t *>(cv.take(sl.seeds));
+    uint64_t *d_bod = static_cast<uint64_t *>(cv.take(sl.body));
+    void *d_op = cv.take(sl.op);
+    uint32_t *d_om = static_cast<uint32_t *>(cv.take(sl.om));
+    uint32_t *d_ob = static_cast<uint32_t *>(cv.take(sl.ob));
+    uint8_t *d_wout = static_cast<uint8_t *>(cv.take(sl.wout));
     cudaMemcpyAsync(d_win, h_wire_in + t0 * L * bin, n * L * bin, cudaMemcpyHostToDevice, st);
     rc = phe_wire_deserialize_inputs(p, d_win, n, L, d_seeds, d_bod, st);
-    if (!rc) rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, b_op, st);
+    if (!rc) rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, sl.op, st);
     if (!rc) rc = matmul_common(p, d_wprep, rows, cols, row_begin, row_end, d_op, n, p->q_out, d_om, d_ob, st);
     if (!rc) rc = phe_wire_serialize_lwe(p, d_om, d_ob, n, R, d_wout, st);
-    if (rc) return rc;
+    if (rc) break;
     cudaMemcpyAsync(h_wire_out + t0 * bout, d_wout, n * bout, cudaMemcpyDeviceToHost, st);
   }
-  cudaError_t e0 = cudaStreamSynchronize(g_ws.st[0]);
-  cudaError_t e1 = cudaStreamSynchronize(g_ws.st[1]);
-  if (e0 != cudaSuccess) return phe_set_cuda_error(e0);
-  if (e1 != cudaSuccess) return phe_set_cuda_error(e1);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return phe_set_cuda_error(e);
-  return PHE_OK;
+  return pipe.finish(rc);
 }
 
 }  // extern "C"

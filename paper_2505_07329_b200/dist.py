@@ -6,8 +6,10 @@ collective on the data path:
     and every weight; weak scaling when each rank brings its own batch.
   * row sharding (north_star): rank r owns rows shard_range(R, W, r) of each linear for all
     tokens; the input ciphertexts (seeds + bodies, ~1.1 MB/token) are replicated.
-The only collective is the optional gather of output ciphertexts to one rank: either NCCL
-send/recv after the GEMM (`gather_rows`), or fused into the GEMM itself (`PeerGather`): rank 0's
+The only collective is the optional gather of output ciphertexts to one rank: NCCL P2P of the
+26-bit wire form of each row shard, chunk by chunk on a side stream so it overlaps the next
+chunk's GEMMs (`gather_wire_shards`, driven by bench.py), send/recv of the uint32 form after the
+GEMM (`gather_rows`), or fused into the GEMM itself (`PeerGather`): rank 0's
 gather buffer is mapped into every rank through CUDA IPC and each rank's mask kernel TMA-stores
 its row block straight into it (NVLink peer writes, overlapped with the contraction tile by
 tile; `phe_matmul_clear_into`).  This module is plumbing: the compute is libphe's.
@@ -82,6 +84,33 @@ def gather_tokens(mask: torch.Tensor, body: torch.Tensor, T: int, world: int, ra
             dist.recv(full_m[t0:t1], k, group=group)  # token slices are contiguous
             dist.recv(full_b[t0:t1], k, group=group)
     return full_m, full_b
+
+
+def gather_wire_shards(shard: torch.Tensor | None, recv: Sequence[torch.Tensor | None] | None, world: int,
+                       rank: int, dst: int = 0, group=None, staged: bool = False):
+    """One gather step of serialized row shards (phe_wire_serialize_lwe bytes, 26-bit LWE at
+    Table 1) to `dst`: rank k != dst sends its shard [n][bytes_k]; dst receives rank k's shard
+    straight into its destination recv[k] (no temporaries).  All point-to-point ops of the step
+    are issued as one batch (NCCL group: every peer's transfer is in flight at once, so dst's
+    NVLink ingress is the only limit).  Returns the works; the caller waits on them on the stream
+    that must observe completion.  `staged`: bounce device tensors through host memory (gloo
+    plumbing of the shared-GPU test hook only; gloo moves CPU tensors) -- completes before return."""
+    if staged:
+        if rank != dst:
+            dist.send(shard.cpu(), dst, group=group)
+        else:
+            for k in range(world):
+                if k != dst:
+                    h = torch.empty(recv[k].shape, dtype=recv[k].dtype)
+                    dist.recv(h, k, group=group)
+                    recv[k].copy_(h)
+        return []
+    ops = []
+    if rank != dst:
+        ops.append(dist.P2POp(dist.isend, shard, dst, group))
+    else:
+        ops += [dist.P2POp(dist.irecv, recv[k], k, group) for k in range(world) if k != dst]
+    return dist.batch_isend_irecv(ops) if ops else []
 
 
 class PeerGather:

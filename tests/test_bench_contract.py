@@ -65,5 +65,24 @@ def test_argument_defaults():
         a = bench.parse()
     finally:
         sys.argv = old
-    assert a.gpus == 1 and a.workload == "q_proj" and a.contraction == "tc" and a.impl == "ours"
+    # the default line is BASELINE configs[3]: every Llama-3.2-1B linear x 16 layers, fwd + W^T bwd,
+    # 2048 tokens, tensor-core contraction (north_star)
+    assert a.gpus == 1 and a.workload == "stack" and a.layers == 16 and a.tokens == 2048
+    assert a.contraction == "tc" and a.impl == "ours"
     assert a.warmup >= 3 and a.steps >= 1
+    calls = bench.linears("stack")
+    assert len(calls) == 16 * 11
+    macs = sum(d_out * d_in for _, d_out, d_in, _, _ in calls)
+    assert macs == 2 * 973_078_528          # sum d_out*d_in over 16 layers, fwd + bwd
+
+
+def test_reference_arm_runs_on_cpu():
+    """--impl reference: the oracle's bounded sample, on the same config/metric as our arm."""
+    import subprocess
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
+    assert d["config"]["workload"].startswith("Llama-3.2-1B all linears x 16 layers")
+    assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}

@@ -35,10 +35,11 @@ def _torchrun(extra, timeout=900):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("extra,tokens_total", [
-    (["--tokens", "256"], 512),                                           # weak: tokens per rank
-    (["--tokens", "256", "--contraction", "ntt", "--no-e2e"], 512),
-    (["--tokens", "256", "--shard", "rows", "--gather", "p2p", "--no-e2e"], 256),  # strong + fused gather
+    (["--workload", "q_proj", "--tokens", "256", "--shard", "tokens"], 512),          # weak: tokens per rank
+    (["--workload", "q_proj", "--tokens", "256", "--shard", "tokens", "--contraction", "ntt", "--no-e2e"], 512),
+    (["--workload", "q_proj", "--tokens", "256", "--gather", "p2p", "--no-e2e"], 256),  # rows + fused gather
     (["--workload", "q_proj_packed", "--tokens", "64"], 128),           # KeySwitch packing, wire e2e
+    (["--layers", "1", "--tokens", "8"], 8),                             # the default: rows-sharded stack
 ])
 def test_bench_two_ranks_one_gpu(extra, tokens_total):
     d = _torchrun(extra)
@@ -49,3 +50,19 @@ def test_bench_two_ranks_one_gpu(extra, tokens_total):
     assert d["gpu_launches"] > 0
     if "--no-e2e" not in extra:
         assert d["e2e"]["value"] > 0
+    if "--layers" in extra:
+        # default N > 1 stack line: row-sharded (strong) with the separately timed gather pass
+        assert d["scaling"] == "strong" and d["config"]["parallelism"] == "row-sharded x2"
+        g = d["gather"]
+        assert g["ms_step_with_gather"] > 0 and g["chunk_tokens"] >= 1
+        # rank 1's wire bytes of every call: its half of each linear's rows at 26 bits per word
+        import paper_2505_07329_b200 as phe
+        import bench
+        from paper_2505_07329_b200.dist import shard_range
+        p = phe.params(phe.PRESET_PAPER)
+        exp = 0
+        for _, d_out, d_in, tr, _ in bench.linears("stack", 1):
+            rows = d_in if tr else d_out
+            a, b = shard_range(rows, 2, 1)
+            exp += 8 * phe.wire_lwe_bytes(p, b - a)
+        assert g["bytes_to_rank0"] == exp
