@@ -150,6 +150,38 @@ def test_packed_ntt_primitive_and_wire_host(phe):
     assert torch.equal(ho_w, ho_ref)
 
 
+def test_wire_host_ragged_last_chunk(phe):
+    """ADVICE r1: the NTT packing workspace is not monotone in T (the K-split follows wave fill;
+    q_proj: T = 7 needs more than T = 8), so a host pipeline sized for the full chunk failed with
+    ENOMEM on a shorter last chunk.  T = 15 in chunks of 8: all three wire pipelines == the device
+    primitive; the workspace query covers both chunk sizes; a short workspace is refused."""
+    import ctypes
+    p, W, x, S, w, opnd, ksk = _setup(phe, dict(N=2048), 2048, 2048, 15, 0)
+    K, NK = phe.KeySwitchKey(p, ksk), phe.NttKeySwitchKey(p, ksk)
+    ref = phe.matmul_clear_packed(p, w, opnd, 15, K)
+    s2, b2 = phe.encrypt_pack(p, S, torch.from_numpy(x).to(DEV), 77, 3)
+    hi = phe.wire_serialize_inputs(p, s2, b2).cpu().pin_memory()
+    tabs = phe.NttTables(p)
+    wn = phe.NttWeights(p, tabs, torch.from_numpy(W).to(DEV))
+    lib = phe.load()
+    for fn, wt, key, api in [(phe.server_wire_host, w, K, "phe_server_wire_host"),
+                             (phe.server_wire_host_ntt, w, NK, "phe_server_wire_host_ntt"),
+                             (phe.server_wire_host_nttw, wn, NK, "phe_server_wire_host_nttw")]:
+        need = getattr(lib, api + "_ws_bytes")(ctypes.byref(p), 2048, 2048, 0, 15, 8)
+        ws_fn = lib.phe_packed_ntt_ws_bytes if api != "phe_server_wire_host" else lib.phe_packed_ws_bytes
+        assert need >= 2 * max(ws_fn(ctypes.byref(p), 2048, 8), ws_fn(ctypes.byref(p), 2048, 7))
+        ho = torch.empty((15, 1, phe.wire_output_bytes(p)), dtype=torch.uint8).pin_memory()
+        fn(p, wt, key, hi, ho, chunk_tokens=8)
+        assert torch.equal(phe.wire_deserialize_packed(p, ho.to(DEV)).view(15, 1, 2, p.N), ref), api
+    # the C ABI refuses a workspace one byte short (ENOMEM), before enqueueing anything
+    need = lib.phe_server_wire_host_ntt_ws_bytes(ctypes.byref(p), 2048, 2048, 0, 15, 8)
+    ws = torch.empty(need - 1, dtype=torch.uint8, device=DEV)
+    ho = torch.empty((15, 1, phe.wire_output_bytes(p)), dtype=torch.uint8).pin_memory()
+    rc = lib.phe_server_wire_host_ntt(ctypes.byref(p), w.buf.data_ptr(), 2048, 2048, 0, NK.buf.data_ptr(),
+                                      hi.data_ptr(), 15, 8, ho.data_ptr(), ws.data_ptr(), ws.numel(), None)
+    assert rc == phe.PHE_ENOMEM
+
+
 @pytest.mark.slow
 def test_full_size_q_proj_packed_bench_config(phe, coracle):
     """bench.py --workload q_proj_packed in its launch configuration (q_proj 2048x2048, T = 2048,
