@@ -75,6 +75,8 @@ struct KArgs {
   int N;
   int tpt;            // tokens per tile
   int n_mma;          // MMA N = round16(tpt * ell) (2-CTA kernel)
+  int n_mma_tail;     // MMA N of the last token tile (T % tpt tokens; == n_mma when it is full):
+                      // the ragged tile runs a narrower MMA instead of a full-width one
   int n_tiles;        // token tiles
   int tb_per_row;     // N / BM (HANKEL) or 1
   int64_t m_tiles;    // rows*tb_per_row (HANKEL) or ceil(rows/BM)
@@ -84,6 +86,9 @@ struct KArgs {
   int64_t Lc;
   int64_t cols;       // columns of the prepared matrix (d_in of the contraction)
   int full_k;         // no zero-padded K-blocks (or more than 64): no skipping
+  int jpair;          // 2-CTA mask kernel: the pair's CTAs take rows j, j+1 over the same 128 t
+                      // (tile = 128 t x 2 j) instead of 256 consecutive t of one j: the Hankel
+                      // K-window of a partial block is then V + 127 wide instead of V + 255
   int64_t row_begin;  // absolute first row
   int64_t R;          // rows in range
   int64_t out_rows;   // row stride of the output tensor [T][out_rows][N] (>= R; > R when the
@@ -536,19 +541,20 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
 // (bit kb = issue) is computed once per tile, identically by the producer and MMA warps, so
 // the smem ring stays in step.  Never empty for V >= 1.  Blocks kb >= 64 are never skipped.
 __device__ __forceinline__ uint64_t kblock_mask(const KArgs &ka, int tp) {
+  const int span = ka.jpair ? BM : 2 * BM;  // rows t of the tile: tp .. tp + span - 1
   if (ka.full_k || kdbg(ka) == 9) return ~0ull;
   // Closed form (checked against the per-block definition above for N in 256..4096, all
   // cols, all tp): only the last block il = Lc-1 can be partial (V < N); its needed kk are
   // [0, lo_end) U [hi_start, hi_end) with a = kk*BK + tp:
   //   a < V               <=> kk < ceil((V - tp) / BK)
-  //   a + 383 > N         <=> kk >= floor((N - tp - 383) / BK) + 1   (all kk if N - tp - 383 < 0)
+  //   a + span+127 > N    <=> kk >= floor((N - tp - span - 127) / BK) + 1   (all kk if < 0)
   //   a < N + V           <=> kk < ceil((N + V - tp) / BK)
   const int kbpb = ka.kb_per_block, N = ka.N, il = (int)ka.Lc - 1;
   const int V = (int)(ka.cols - (int64_t)il * N);
   auto cl = [kbpb](int v) { return v < 0 ? 0 : (v > kbpb ? kbpb : v); };
   auto rng = [](int a, int b) -> uint64_t { return b > a ? (((1ull << b) - 1ull) & ~((1ull << a) - 1ull)) : 0ull; };
   const int lo_end = V - tp > 0 ? cl((V - tp + BK - 1) / BK) : 0;
-  const int x = N - tp - (2 * BM + BK - 1);
+  const int x = N - tp - (span + BK - 1);
   const int hi_start = x >= 0 ? cl(x / BK + 1) : 0;
   const int hi_end = cl((N + V - tp + BK - 1) / BK);
   const uint64_t full_bits = il * kbpb >= 64 ? ~0ull : ((1ull << (il * kbpb)) - 1ull);
@@ -559,7 +565,7 @@ __device__ __forceinline__ bool kb_issue(uint64_t m, int kb) { return kb >= 64 |
 template <int ELL, int MODE, int SH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                     const __grid_constant__ CUtensorMap map_out,
+                     const __grid_constant__ CUtensorMap map_b_tail, const __grid_constant__ CUtensorMap map_out,
                      const __grid_constant__ CUtensorMap map_out_tail, KArgs ka) {
   using C2 = Cfg2<MODE>;
   using OutT = typename C2::OutT;
@@ -609,15 +615,28 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     // own half of B, bytes land on CTA 0's barrier =====
     int s = 0; uint32_t ph = 0;
     long long pw = 0;
-    const uint32_t tx = (uint32_t)(2 * ((kdbg(ka) == 5 ? 0 : A_BYTES_HANKEL) + (kdbg(ka) == 6 ? 0 : b_half)));
+    const int a_tx = kdbg(ka) == 5 ? 0 : A_BYTES_HANKEL;
+    const uint32_t tx_full = (uint32_t)(2 * (a_tx + (kdbg(ka) == 6 ? 0 : b_half)));
+    const uint32_t tx_tail = (uint32_t)(2 * (a_tx + (kdbg(ka) == 6 ? 0 : (ka.n_mma_tail / 2) * BK)));
     for (TileIter it(cid, ncl, ka.n_tiles); it.tile < total; it.next(ncl, ka.n_tiles)) {
       const int64_t m_tile = it.m;
       const int n_tile = it.n;
-      const int brow = n_tile * ka.tpt * ELL + (int)crank * (n_mma / 2);
+      const bool tl = n_tile == ka.n_tiles - 1;  // ragged last token tile: narrower B box
+      const uint32_t tx = tl ? tx_tail : tx_full;
+      const CUtensorMap *mbp = tl ? &map_b_tail : &map_b;
+      const int brow = n_tile * ka.tpt * ELL + (int)crank * ((tl ? ka.n_mma_tail : n_mma) / 2);
       const int jr_ = (int)((uint32_t)m_tile / (uint32_t)ka.tb_per_row);
-      const int64_t jrow = ka.row_begin + jr_;
-      const int tp = ((int)m_tile - jr_ * ka.tb_per_row) * (2 * BM);  // pair's first row t
-      const int64_t abase = jrow * ka.Lc * (2 * (int64_t)ka.N) + tp + (int)crank * BM;
+      int64_t jrow, abase;
+      int tp;  // the tile's first row t
+      if (ka.jpair) {  // CTA r: row j = 2 jr_ + r, rows t tp .. tp + 127
+        tp = ((int)m_tile - jr_ * ka.tb_per_row) * BM;
+        jrow = ka.row_begin + 2 * (int64_t)jr_ + (int)crank;
+        abase = jrow * ka.Lc * (2 * (int64_t)ka.N) + tp;
+      } else {         // CTA r: row j = jr_, rows t tp + 128 r .. + 127
+        tp = ((int)m_tile - jr_ * ka.tb_per_row) * (2 * BM);
+        jrow = ka.row_begin + jr_;
+        abase = jrow * ka.Lc * (2 * (int64_t)ka.N) + tp + (int)crank * BM;
+      }
       const uint64_t km = kblock_mask(ka, tp);
       int i = 0, kk = 0;
       for (int kb = 0; kb < ka.k_blocks; kb++) {
@@ -630,7 +649,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
             const uint32_t fb = smem_u32(&full[s]) & PEER_MASK;
             const int64_t arow = abase + (int64_t)i * (2 * (int64_t)ka.N) + kk * BK;
             if (kdbg(ka) != 5) tma_load_2d_2sm(smem_u32(sA + s * 4096), &map_a, 0, (int)arow, fb);
-            if (kdbg(ka) != 6) tma_load_2d_2sm(smem_u32(sB + s * B_HALF_MAX), &map_b, kb * BK, brow, fb);
+            if (kdbg(ka) != 6) tma_load_2d_2sm(smem_u32(sB + s * B_HALF_MAX), mbp, kb * BK, brow, fb);
           }
           __syncwarp();
           if (++s == S) { s = 0; ph ^= 1; }
@@ -642,16 +661,17 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
   } else if (warp == W_MMA) {
     // ===== MMA issuer (leader CTA only; warp-wide loop, elected lane issues + commits) =====
     if (leader) {
-      const uint32_t idesc = idesc_i8(2 * BM, n_mma);
+      const uint32_t idesc_full = idesc_i8(2 * BM, n_mma), idesc_tail = idesc_i8(2 * BM, ka.n_mma_tail);
       int s = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
       long long t_start = kdbg(ka) == 4 ? clock64() : 0, wt = 0, wf = 0;
       for (TileIter it(cid, ncl, ka.n_tiles); it.tile < total; it.next(ncl, ka.n_tiles)) {
+        const uint32_t idesc = it.n == ka.n_tiles - 1 ? idesc_tail : idesc_full;
         long long w0 = kdbg(ka) == 4 ? clock64() : 0;
         mbar_wait(&tempty[acc], aph ^ 1);
         if (kdbg(ka) == 4) wt += clock64() - w0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        const int tp = (int)((uint32_t)it.m % (uint32_t)ka.tb_per_row) * (2 * BM);
+        const int tp = (int)((uint32_t)it.m % (uint32_t)ka.tb_per_row) * (ka.jpair ? BM : 2 * BM);
         const uint64_t km = kblock_mask(ka, tp);
         uint32_t acc_flag = 0;  // first issued MMA of the tile overwrites the accumulator
         for (int kb = 0; kb < ka.k_blocks; kb++) {
@@ -697,8 +717,10 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       const int n_tile = it.n;
       const int tau0 = n_tile * ka.tpt;
       const int ntok = (int)min((int64_t)ka.tpt, ka.T - tau0);
-      const int jr = (int)((uint32_t)it.m / (uint32_t)ka.tb_per_row);
-      const int tb = ((int)it.m - jr * ka.tb_per_row) * (2 * BM) + (int)crank * BM;
+      const int jq = (int)((uint32_t)it.m / (uint32_t)ka.tb_per_row);
+      const int jr = ka.jpair ? 2 * jq + (int)crank : jq;
+      const int tb = ka.jpair ? ((int)it.m - jq * ka.tb_per_row) * BM
+                              : ((int)it.m - jq * ka.tb_per_row) * (2 * BM) + (int)crank * BM;
       const int nchunks = (ntok + EPI_TOK - 1) / EPI_TOK;
       const int first = (grp + (int)(iter & 1)) & 1;
       long long e0 = (kdbg(ka) == 4 && warp == 0 && lane == 0) ? clock64() : 0;
@@ -1075,7 +1097,7 @@ static int dispatch_ell(int ell, const CUtensorMap &ma, const CUtensorMap &mb, c
 
 
 template <int ELL, int MODE, int SH>
-static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo,
+static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbt, const CUtensorMap &mo,
                       const CUtensorMap &mot, const KArgs &ka, cudaStream_t st) {
   auto kern = limb_gemm_2sm_kernel<ELL, MODE, SH>;
   constexpr int smem = Cfg2<MODE>::SMEM;
@@ -1097,21 +1119,22 @@ static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtens
   attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mo, mot, ka) != cudaSuccess) return phe_set_cuda_error(cudaGetLastError());
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mbt, mo, mot, ka) != cudaSuccess)
+    return phe_set_cuda_error(cudaGetLastError());
   PHE_CUDA_CHECK_LAUNCH();
   return PHE_OK;
 }
 
 template <int MODE>
-static int dispatch_2sm(int ell, const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo,
+static int dispatch_2sm(int ell, const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbt, const CUtensorMap &mo,
                         const CUtensorMap &mot, const KArgs &ka, cudaStream_t st) {
   const int sh = ka.q_in - ka.out_bits;
-  if (MODE != OUT_U64 && ell == 5 && sh == 13) return launch_2sm<5, MODE, 13>(ma, mb, mo, mot, ka, st);  // Table 1
-  if (MODE != OUT_U64 && ell == 5 && sh == 7) return launch_2sm<5, MODE, 7>(ma, mb, mo, mot, ka, st);  // digits, q=39
-  if (MODE != OUT_U64 && ell == 4 && sh == 4) return launch_2sm<4, MODE, 4>(ma, mb, mo, mot, ka, st);    // toy
+  if (MODE != OUT_U64 && ell == 5 && sh == 13) return launch_2sm<5, MODE, 13>(ma, mb, mbt, mo, mot, ka, st);  // Table 1
+  if (MODE != OUT_U64 && ell == 5 && sh == 7) return launch_2sm<5, MODE, 7>(ma, mb, mbt, mo, mot, ka, st);  // digits, q=39
+  if (MODE != OUT_U64 && ell == 4 && sh == 4) return launch_2sm<4, MODE, 4>(ma, mb, mbt, mo, mot, ka, st);    // toy
   switch (ell) {
-    case 4: return launch_2sm<4, MODE, 0>(ma, mb, mo, mot, ka, st);
-    case 5: return launch_2sm<5, MODE, 0>(ma, mb, mo, mot, ka, st);
+    case 4: return launch_2sm<4, MODE, 0>(ma, mb, mbt, mo, mot, ka, st);
+    case 5: return launch_2sm<5, MODE, 0>(ma, mb, mbt, mo, mot, ka, st);
   }
   return PHE_EUNSUPPORTED;
 }
@@ -1205,15 +1228,27 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
     KArgs km = ka;
     if (two_sm) km.tpt = choose_tpt(a.T, ell, &km.n_mma);
     km.n_tiles = (int)((a.T + km.tpt - 1) / km.tpt);
-    CUtensorMap ma, mb, mo;
+    {  // the last token tile holds T - (n_tiles - 1) tpt tokens: MMA N = round16 of their limb columns
+      const int tail_tok = (int)(a.T - (int64_t)(km.n_tiles - 1) * km.tpt);
+      int nt = ((tail_tok * ell + 15) / 16) * 16;
+      if (nt < 32) nt = 32;
+      km.n_mma_tail = nt < km.n_mma ? nt : km.n_mma;
+    }
+    CUtensorMap ma, mb, mbt, mo;
     int rc = make_map_2d(&ma, a.wexp, 16, (uint64_t)(a.rows * a.Lc * 2 * N), 16, 16, A_ROWS_HANKEL,
                          CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
     rc = make_map_2d(&mb, a.mplanes, (uint64_t)K, brows, (uint64_t)K, BK, two_sm ? km.n_mma / 2 : BN,
                      CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
-    km.tb_per_row = N / (two_sm ? 2 * BM : BM);
-    km.m_tiles = R * km.tb_per_row;
+    rc = make_map_2d(&mbt, a.mplanes, (uint64_t)K, brows, (uint64_t)K, BK, two_sm ? km.n_mma_tail / 2 : BN,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    // pairs over (j, j+1) when the last block is partial (a K-window V + 127 instead of V + 255
+    // wide: k/v^T at d_in = 512 issue 5 of 16 K-blocks per tile instead of 7)
+    km.jpair = two_sm && !ka.full_k && R >= 2 && !(PHE_KERNEL_EXPERIMENTS && getenv("PHE_NO_JPAIR"));
+    km.tb_per_row = N / (two_sm && !km.jpair ? 2 * BM : BM);
+    km.m_tiles = (km.jpair ? (R + 1) / 2 : R) * km.tb_per_row;
     km.total_tiles = km.m_tiles * km.n_tiles;
     km.out = a.out_mask;
     if (a.digits && !two_sm) return PHE_EUNSUPPORTED;
@@ -1232,9 +1267,10 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
       if (km.dbg == 4) cudaMemcpyToSymbolAsync(g_dbg_cnt, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
       if (a.digits) {
         km.out_bits = KS_BITS;  // digits keep the top 32 bits (q_in >= 32)
-        rc = dispatch_2sm<OUT_DIG>(ell, ma, mb, mo, mot, km, st);
+        rc = dispatch_2sm<OUT_DIG>(ell, ma, mb, mbt, mo, mot, km, st);
       } else {
-        rc = sw ? dispatch_2sm<OUT_U32>(ell, ma, mb, mo, mot, km, st) : dispatch_2sm<OUT_U64>(ell, ma, mb, mo, mot, km, st);
+        rc = sw ? dispatch_2sm<OUT_U32>(ell, ma, mb, mbt, mo, mot, km, st)
+                : dispatch_2sm<OUT_U64>(ell, ma, mb, mbt, mo, mot, km, st);
       }
       if (km.dbg == 4) {
         unsigned long long c[8];

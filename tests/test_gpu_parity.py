@@ -122,6 +122,21 @@ def test_row_sharding_equals_slices(phe):
         assert torch.equal(ms, m[:, r0:r1]) and torch.equal(bs, b[:, r0:r1])
 
 
+def test_row_ranges_partial_block_vs_oracle(phe, coracle):
+    """A partial last block (d_in = 700 < N) runs the mask GEMM with CTA pairs over rows (j, j+1):
+    odd row counts and row ranges that end inside a pair (the partner row is computed but its
+    stores fall outside the range) give exactly the oracle's rows."""
+    p = phe.params(phe.PRESET_PAPER)
+    W = synth.weights_int8(301, 700, seed=4)
+    x = synth.activations_int8(9, 700, seed=5)
+    S, seeds, body, w, opnd, (m, b) = run_gpu(phe, p, W, x, out_bits=p.q_in)
+    _, _, _, mask_o, body_o = oracle_expect(coracle, p, W, x, 7, 12345)
+    assert np.array_equal(u64(m), mask_o) and np.array_equal(u64(b), body_o)
+    for r0, r1 in [(17, 18), (5, 128), (0, 301), (299, 301), (100, 233)]:
+        ms, bs = phe.matmul_clear(p, w, opnd, 9, out_bits=p.q_in, row_begin=r0, row_end=r1)
+        assert np.array_equal(u64(ms), mask_o[:, r0:r1]) and np.array_equal(u64(bs), body_o[:, r0:r1])
+
+
 def test_multiblock_L4_and_noise(phe, coracle):
     """d_in = 8192 (down_proj, L = 4) with CBD(21) noise in the encryption."""
     p = phe.params(phe.PRESET_PAPER, noise_eta=21)
