@@ -56,6 +56,12 @@ int phe_last_cuda_error(void);
  * beta   plaintext bits, t = 2^beta (R4).          gamma <= beta <= q_in.
  * gamma  MSBs guaranteed noise-free; informational (decrypt contract).
  * noise_eta  0 = E == 0 ("SPEC" reading of sigma, R5); else CBD(eta), eta <= 32.
+ *
+ * SECURITY NOTE: both presets set noise_eta = 0, the reading under which Table 1's sigma rounds
+ * to zero at q = 2^39 (R5).  With E == 0 every input ciphertext satisfies B - A S == Delta x
+ * exactly, so anyone who expands A from the public seed can solve for the binary key S: the
+ * presets give NO confidentiality and exist for bit-exact parity and benchmarks (the server-side
+ * cost does not depend on E).  Encrypt real data with noise, e.g. noise_eta = 21 (sigma ~ 3.2).
  */
 typedef struct phe_params {
   int32_t N;

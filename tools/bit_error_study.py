@@ -21,12 +21,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def run(d_ins=(768, 2048, 8192), trials=65536, eta=21, seed=4, beta_bits=27):
+def run(d_ins=(768, 2048, 8192), trials=65536, eta=21, seed=4, beta_bits=27, sigma=0.0):
+    """sigma > 0: the input ciphertexts carry a rounded-Gaussian noise E of that standard deviation
+    (in Z_Q units) instead of CBD(eta) -- added to the E = 0 bodies on the client side of the study
+    (B = A S + Delta x + E), outside the server path.  DESIGN.md R25: Fig. 4's d_in trend
+     needs sigma ||w|| / Delta comparable to the modulus-switch error, which Table 1's
+    sigma (R5) and the CBD(eta <= 32) sampler are far below."""
     import torch
 
     import paper_2505_07329_b200 as phe
     import synth
 
+    if sigma > 0:
+        eta = 0
     p = phe.params(phe.PRESET_PAPER, noise_eta=eta)
     p_ksk = phe.params(phe.PRESET_PAPER, noise_eta=0)   # sigma_ksk rounds to 0 (R5)
     S = phe.keygen(p, seed)
@@ -38,6 +45,11 @@ def run(d_ins=(768, 2048, 8192), trials=65536, eta=21, seed=4, beta_bits=27):
         W = torch.from_numpy(synth.uniform_int8((d_out, d_in), seed + d_in)).cuda()
         x = torch.from_numpy(synth.uniform_int8((T, d_in), seed + 2 * d_in)).cuda()
         seeds, body = phe.encrypt_pack(p, S, x, 1000 + d_in, 7 + d_in)
+        if sigma > 0:
+            g = torch.Generator(device="cuda")
+            g.manual_seed(seed * 7919 + d_in)
+            E = torch.round(torch.randn(body.shape, generator=g, device="cuda", dtype=torch.float64) * sigma)
+            body = (body + E.to(torch.int64)) & ((1 << p.q_in) - 1)
         w = phe.Weights(p, W)
         op = phe.ct_prepare(p, seeds, body)
         packed = phe.matmul_clear_packed(p, w, op, T, K)
@@ -46,7 +58,7 @@ def run(d_ins=(768, 2048, 8192), trials=65536, eta=21, seed=4, beta_bits=27):
         diff = (y ^ truth) & ((1 << beta_bits) - 1)
         n = diff.size
         for b in range(beta_bits):
-            rows.append((d_in, b, float(((diff >> b) & 1).sum()) / n, n))
+            rows.append((d_in, b, float(((diff >> b) & 1).sum()) / n, n, sigma if sigma > 0 else f"cbd{eta}"))
         del w, op, packed
     return rows
 
@@ -54,17 +66,22 @@ def run(d_ins=(768, 2048, 8192), trials=65536, eta=21, seed=4, beta_bits=27):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--trials", type=int, default=65536)
+    ap.add_argument("--sigma", type=float, nargs="*", default=[0.0],
+                    help="input-noise standard deviations to sweep (0 = CBD(21), the round-1 setting)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_fig4_bit_errors.csv"))
     a = ap.parse_args()
-    rows = run(trials=a.trials)
+    rows = []
+    for sg in a.sigma:
+        rows += run(trials=a.trials, sigma=sg)
     with open(a.out, "w", newline="") as f:
         wr = csv.writer(f)
-        wr.writerow(["d_in", "bit_position", "error_rate", "trials"])
+        wr.writerow(["d_in", "bit_position", "error_rate", "trials", "input_noise"])
         wr.writerows(rows)
-    for d_in in sorted({r[0] for r in rows}):
-        rr = [r for r in rows if r[0] == d_in]
-        print(d_in, " ".join(f"{r[1]}:{r[2]:.4f}" for r in rr if r[1] in (0, 4, 6, 8, 10, 11, 12, 13, 14, 16, 20)),
-              "max>=12:", max(r[2] for r in rr if r[1] >= 12))
+    for nz in dict.fromkeys(r[4] for r in rows):
+        for d_in in sorted({r[0] for r in rows}):
+            rr = [r for r in rows if r[0] == d_in and r[4] == nz]
+            print(nz, d_in, " ".join(f"{r[1]}:{r[2]:.4f}" for r in rr if r[1] in (0, 4, 6, 8, 10, 11, 12, 13, 14, 16, 20)),
+                  "max>=12:", max(r[2] for r in rr if r[1] >= 12))
 
 
 if __name__ == "__main__":

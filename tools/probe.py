@@ -12,6 +12,9 @@ import torch  # noqa: E402
 
 import paper_2505_07329_b200 as phe  # noqa: E402
 import synth  # noqa: E402
+
+if os.environ.get("PHE_LIB"):  # experiment builds (tools/build_variant.sh)
+    phe.load(os.environ["PHE_LIB"])
 from bench import ClockSampler  # noqa: E402
 
 
