@@ -71,12 +71,13 @@ def parse():
     ap.add_argument("--shard", choices=["tokens", "rows"], default=None,
                     help="N>1: rows = W rows split, same tokens (strong; default for LWE workloads); "
                          "tokens = each rank its own batch (weak; default for packed workloads)")
-    ap.add_argument("--gather", choices=["none", "nccl", "p2p"], default=None,
-                    help="rows mode: nccl (default) = a separately timed pass in which every (chunk, linear)'s "
-                         "row shards are serialized to the 26-bit wire form and sent to rank 0 over NCCL P2P on a "
-                         "side stream, overlapped with the next GEMMs; p2p (q_proj) = fused gather: every rank's "
-                         "kernels store their row block straight into rank 0's buffer (CUDA IPC / NVLink) inside "
-                         "the timed step; none")
+    ap.add_argument("--gather", choices=["none", "both", "fused", "nccl", "p2p"], default=None,
+                    help="rows mode, gather of the output ciphertexts to rank 0, in separately timed passes: "
+                         "fused = every rank's GEMM epilogue TMA-stores its row block straight into one of two "
+                         "IPC-mapped slots on rank 0 (NVLink peer stores, tile by tile), a 4-byte all-reduce per "
+                         "call orders the slot reuse; nccl = row shards serialized to the 26-bit wire form and sent "
+                         "with NCCL P2P on a side stream, overlapped with the next call's GEMMs; both (default); "
+                         "p2p (q_proj) = the fused form over the whole [T][R][N] output inside the timed step; none")
     args = ap.parse_args()
     if args.tokens is None:  # B*C = 8*256; the paper's training step is B = 1, C = 16
         args.tokens = 16 if args.workload == "stack_packed" else 2048
@@ -219,7 +220,7 @@ def run_ours(args):
         args.shard = "tokens" if packed else "rows"
     rows_mode = args.shard == "rows" and world > 1
     if args.gather is None:
-        args.gather = "nccl" if rows_mode and not packed else "none"
+        args.gather = "both" if rows_mode and not packed else "none"
     lins = linears(args.workload, args.layers)
     # ---------------- untimed setup: weights (server registration) and client encryption
     from paper_2505_07329_b200.dist import PeerGather, gather_wire_shards, shard_range
@@ -299,9 +300,10 @@ def run_ours(args):
     parts_ms = {"ct_prepare": [], "body_gemm": [], "mask_gemm": []}
     launches = [0]
 
-    def step(chunk_=chunk, after=None):
+    def step(chunk_=chunk, after=None, into=None):
         """One pass over all calls.  `after(name, w, t0, n, mask_view, body_view)` runs after each
-        (chunk, linear)'s GEMMs on the compute stream (the gather pass hooks in here)."""
+        (chunk, linear)'s GEMMs on the compute stream; `into(name, w, t0, n, r0, r1)` may return
+        (mask_block, body_block) row-block views the GEMMs write instead (the gather passes)."""
         evs = []
         for t0 in range(0, T, chunk_):
             n = min(chunk_, T - t0)
@@ -341,13 +343,16 @@ def run_ours(args):
                     f, opnd = (phe.matmul_clear_T if w.transpose else phe.matmul_clear), operand
                 r0, r1 = rr[name]
                 nr = r1 - r0
-                if peer is not None:  # fused gather: a5 + a6 stores land in rank 0's buffer
+                blocks = ((peer.mask[t0:t0 + n, r0:r1], peer.body[t0:t0 + n, r0:r1]) if peer is not None
+                          else into(name, w, t0, n, r0, r1) if into is not None else None)
+                if blocks is not None:  # fused gather: a5 + a6 stores land in rank 0's buffer
                     e[2].record(stream)
-                    phe.matmul_clear_into(p, w, opnd, n, peer.mask[t0:t0 + n, r0:r1], peer.body[t0:t0 + n, r0:r1],
-                                          r0, r1)
+                    phe.matmul_clear_into(p, w, opnd, n, blocks[0], blocks[1], r0, r1)
                     launches[0] += phe.last_launch_count()
                     e[3].record(stream)
                     evs.append((name, e))
+                    if after is not None:
+                        after(name, w, t0, n, None, None)
                     continue
                 mview = out_mask.view(-1)[: n * nr * p.N].view(n, nr, p.N)
                 bview = out_body.view(-1)[: n * nr].view(n, nr)
@@ -423,9 +428,14 @@ def run_ours(args):
         gather = {"mode": "p2p: fused into the kernels' stores (dist.PeerGather, phe_matmul_clear_into); "
                           "included in ms_per_step",
                   "bytes": int(T * regs[0][1].rows * (p.N + 1) * 4)}
-    if rows_mode and args.gather == "nccl" and not args.profile:
-        gather = gather_pass(args, p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, shared,
-                             gather_wire_shards, shard_range, ms_max)
+    gather_nccl = None
+    if rows_mode and args.gather in ("both", "fused") and not args.profile:
+        gather = gather_pass_fused(p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, ms_max)
+    if rows_mode and args.gather in ("both", "nccl") and not args.profile:
+        gather_nccl = gather_pass(args, p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, shared,
+                                  gather_wire_shards, shard_range, ms_max)
+        if gather is None:
+            gather, gather_nccl = gather_nccl, None
 
     # ---------------- roofline of the dominant kernel (mask limb GEMM, or the NTT kernel if the
     # NTT-domain contraction takes more of the step)
@@ -530,9 +540,69 @@ def run_ours(args):
                 "frac_of_peak": round(o_ops / (o_ms / 1e3) / 1e12 / peak, 4)}}
         if gather is not None:
             line["gather"] = gather
+        if gather_nccl is not None:
+            line["gather_nccl"] = gather_nccl
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def gather_pass_fused(p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, ms_compute):
+    """The gather fused into the contraction (one kernel does the GEMM and the
+    transfer): rank 0 allocates two output slots sized for the widest linear and maps them into
+    every rank (CUDA IPC, dist.PeerGather); for call k every rank's GEMMs (phe_matmul_clear_into)
+    write their row block of slot k % 2 directly -- the mask epilogue's TMA stores and the body
+    GEMM's stores go over NVLink into rank 0's HBM tile by tile as the tiles finish.  A 4-byte
+    all-reduce on the compute stream after each call is the ordering fence: call k+1 (which
+    reuses the slot of k-1) starts on any rank only after every rank finished call k, so slot
+    (k-1) % 2 holds call k-1's complete outputs while call k runs (rank 0 may consume it then)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_07329_b200.dist import PeerGather
+    R_max = max(w.rows for _, w, _ in regs)
+    gchunk = min(T, tile_round(14_000_000_000 // (R_max * (p.N + 1) * 4), tpt))
+    pg = PeerGather(2 * gchunk, R_max, p.N, dtype=torch.int32, root=0)
+    mslots, bslots = pg.mask.view(2, -1), pg.body.view(2, -1)
+    fence = torch.zeros(1, dtype=torch.int32, device=dev)
+    count = [0]
+    sent = [0]
+
+    def into(name, w, t0, n, r0, r1):
+        s = count[0] % 2
+        count[0] += 1
+        R = w.rows
+        for k in range(1, world):  # bytes other ranks store into rank 0's slot
+            a, b = rr_of(w.rows, k)
+            sent[0] += n * (b - a) * (p.N + 1) * 4
+        return (mslots[s][: n * R * p.N].view(n, R, p.N)[:, r0:r1], bslots[s][: n * R].view(n, R)[:, r0:r1])
+
+    def after(*_):
+        dist.all_reduce(fence)  # stream-ordered fence: every rank finished this call
+
+    from paper_2505_07329_b200.dist import shard_range
+
+    def rr_of(R, k):
+        return shard_range(R, world, k)
+    dist.all_reduce(fence)
+    torch.cuda.synchronize()
+    dist.barrier()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    step(gchunk, after, into)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    pg.complete()
+    tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+    ms_g = float(tg.item())
+    del pg
+    return {"mode": "fused: GEMM epilogue stores into 2 IPC-mapped slots on rank 0 (NVLink peer stores, "
+                    "phe_matmul_clear_into + dist.PeerGather), 4-byte all-reduce per call as the slot-reuse "
+                    "fence; uint32 words; separate pass, not in ms_per_step",
+            "ms_step_with_gather": round(ms_g, 2), "ms_step_compute_only": round(ms_compute, 2),
+            "exposed_ms": round(ms_g - ms_compute, 2), "bytes_to_rank0": int(sent[0]),
+            "rank0_ingress_GBps": round(sent[0] / (ms_g / 1e3) / 1e9, 1), "chunk_tokens": gchunk}
 
 
 def gather_pass(args, p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, shared, gather_wire_shards,

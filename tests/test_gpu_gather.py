@@ -28,7 +28,7 @@ def _port():
     return port
 
 
-def _worker(rank, world, port, backend, q):
+def _worker(rank, world, port, backend, q, fused=False):
     import torch.distributed as dist
 
     import paper_2505_07329_b200 as phe
@@ -52,6 +52,21 @@ def _worker(rank, world, port, backend, q):
         w = phe.Weights(p, torch.from_numpy(W).to(dev))
         opnd = phe.ct_prepare(p, seeds, body)
         r0, r1 = shard_range(D_OUT, world, rank)
+        if fused:
+            # bench.py's fused gather: every rank's GEMMs store their row block straight into
+            # rank 0's IPC-mapped slot (NVLink peer stores), a 4-byte all-reduce is the fence
+            from paper_2505_07329_b200.dist import PeerGather
+            pg = PeerGather(T, D_OUT, p.N, dtype=torch.int32, root=0)
+            phe.matmul_clear_into(p, w, opnd, T, pg.mask[:, r0:r1], pg.body[:, r0:r1], r0, r1)
+            fence = torch.zeros(1, dtype=torch.int32, device=dev)
+            dist.all_reduce(fence)
+            pg.complete()
+            if rank == 0:
+                q.put((pg.mask.cpu().numpy().astype(np.uint32).astype(np.uint64),
+                       pg.body.cpu().numpy().astype(np.uint32).astype(np.uint64),
+                       seeds.cpu().numpy().view(np.uint64), body.cpu().numpy().view(np.uint64)))
+            dist.barrier()
+            return
         m, b = phe.matmul_clear(p, w, opnd, T, row_begin=r0, row_end=r1)
         shard = phe.wire_serialize_lwe(p, m, b)
         blocks = None
@@ -73,11 +88,11 @@ def _worker(rank, world, port, backend, q):
         dist.destroy_process_group()
 
 
-def _run(backend, world=2):
+def _run(backend, world=2, fused=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, q, fused)) for r in range(world)]
     for pr in procs:
         pr.start()
     out = q.get(timeout=600)
@@ -114,3 +129,15 @@ def test_gather_nccl_two_gpus(phe, coracle):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs (NCCL P2P); the one-GPU variant above runs the same logic over gloo")
     _check_against_oracle(coracle, *_run("nccl"))
+
+
+def test_fused_gather_two_ranks_one_gpu(phe, coracle):
+    """The fused form (bench.py --gather fused): rank 1's GEMM epilogue writes its rows into rank 0's
+    IPC-mapped buffer; rank 0's buffer then holds every row, checked against the oracle."""
+    _check_against_oracle(coracle, *_run("gloo", fused=True))
+
+
+def test_fused_gather_nccl_two_gpus(phe, coracle):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (peer stores over NVLink); the one-GPU variant above runs the same code")
+    _check_against_oracle(coracle, *_run("nccl", fused=True))

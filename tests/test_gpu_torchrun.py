@@ -53,16 +53,20 @@ def test_bench_two_ranks_one_gpu(extra, tokens_total):
     if "--layers" in extra:
         # default N > 1 stack line: row-sharded (strong) with the separately timed gather pass
         assert d["scaling"] == "strong" and d["config"]["parallelism"] == "row-sharded x2"
-        g = d["gather"]
-        assert g["ms_step_with_gather"] > 0 and g["chunk_tokens"] >= 1
-        # rank 1's wire bytes of every call: its half of each linear's rows at 26 bits per word
+        # the fused pass (GEMM epilogue stores into rank 0's IPC-mapped slots) and the NCCL pass
+        g, gn = d["gather"], d["gather_nccl"]
+        assert g["mode"].startswith("fused") and gn["mode"].startswith("nccl")
+        assert g["ms_step_with_gather"] > 0 and gn["ms_step_with_gather"] > 0 and gn["chunk_tokens"] >= 1
+        # rank 1's bytes of every call: its half of each linear's rows, uint32 words (fused) and
+        # 26-bit wire words (nccl)
         import paper_2505_07329_b200 as phe
         import bench
         from paper_2505_07329_b200.dist import shard_range
         p = phe.params(phe.PRESET_PAPER)
-        exp = 0
+        exp_wire = exp_u32 = 0
         for _, d_out, d_in, tr, _ in bench.linears("stack", 1):
             rows = d_in if tr else d_out
             a, b = shard_range(rows, 2, 1)
-            exp += 8 * phe.wire_lwe_bytes(p, b - a)
-        assert g["bytes_to_rank0"] == exp
+            exp_wire += 8 * phe.wire_lwe_bytes(p, b - a)
+            exp_u32 += 8 * (b - a) * (p.N + 1) * 4
+        assert gn["bytes_to_rank0"] == exp_wire and g["bytes_to_rank0"] == exp_u32
