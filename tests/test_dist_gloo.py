@@ -78,3 +78,43 @@ def test_sharded_equals_unsharded_world2(mode):
         p.join(timeout=180)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5) is True
+
+
+def _wire_worker(rank, world, port, staged, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2505_07329_b200.dist import gather_wire_shards
+        R, n = 23, 3
+        # each rank's "wire shard": n tokens x bytes of its rows (here 7 bytes per row)
+        sizes = [(b - a) * 7 for a, b in (shard_range(R, world, k) for k in range(world))]
+        shard = torch.full((n, sizes[rank]), rank + 1, dtype=torch.uint8)
+        shard[:, 0] = torch.arange(n, dtype=torch.uint8)
+        recv = [torch.zeros((n, s_), dtype=torch.uint8) for s_ in sizes] if rank == 0 else None
+        if rank == 0:
+            recv[0].copy_(shard)
+        for wk in gather_wire_shards(shard, recv, world, rank, 0, staged=staged):
+            wk.wait()
+        if rank == 0:
+            ok = all(bool((r[:, 1:] == k + 1).all()) and r[:, 0].tolist() == list(range(n))
+                     for k, r in enumerate(recv))
+            q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("staged", [False, True])
+def test_gather_wire_shards_world3(staged):
+    """dist.gather_wire_shards (bench.py's NCCL gather, here over gloo on CPU tensors): rank 0 ends
+    with every rank's shard in its own destination block, batched P2P or staged send/recv."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_wire_worker, args=(r, 3, port, staged, q)) for r in range(3)]
+    for p_ in procs:
+        p_.start()
+    for p_ in procs:
+        p_.join(timeout=180)
+    assert all(p_.exitcode == 0 for p_ in procs)
+    assert q.get(timeout=5) is True
