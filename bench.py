@@ -429,13 +429,21 @@ def run_ours(args):
                           "included in ms_per_step",
                   "bytes": int(T * regs[0][1].rows * (p.N + 1) * 4)}
     gather_nccl = None
-    if rows_mode and args.gather in ("both", "fused") and not args.profile:
-        gather = gather_pass_fused(p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, ms_max)
+    # NCCL pass first (library transport), then the fused pass (our kernels' stores into peer
+    # memory); a Python-level failure of either is recorded in its record instead of losing the line
     if rows_mode and args.gather in ("both", "nccl") and not args.profile:
-        gather_nccl = gather_pass(args, p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, shared,
-                                  gather_wire_shards, shard_range, ms_max)
-        if gather is None:
-            gather, gather_nccl = gather_nccl, None
+        try:
+            gather_nccl = gather_pass(args, p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, shared,
+                                      gather_wire_shards, shard_range, ms_max)
+        except Exception as ex:  # noqa: BLE001
+            gather_nccl = {"mode": "nccl", "error": repr(ex)[:300]}
+    if rows_mode and args.gather in ("both", "fused") and not args.profile:
+        try:
+            gather = gather_pass_fused(p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, ms_max)
+        except Exception as ex:  # noqa: BLE001
+            gather = {"mode": "fused", "error": repr(ex)[:300]}
+    if gather is None and gather_nccl is not None:
+        gather, gather_nccl = gather_nccl, None
 
     # ---------------- roofline of the dominant kernel (mask limb GEMM, or the NTT kernel if the
     # NTT-domain contraction takes more of the step)
