@@ -570,7 +570,16 @@ def gather_pass_fused(p, phe, regs, rr, world, rank, T, tpt, step, stream, dev, 
     from paper_2505_07329_b200.dist import PeerGather
     R_max = max(w.rows for _, w, _ in regs)
     gchunk = min(T, tile_round(14_000_000_000 // (R_max * (p.N + 1) * 4), tpt))
-    pg = PeerGather(2 * gchunk, R_max, p.N, dtype=torch.int32, root=0)
+    ok = torch.ones(1, dtype=torch.int32, device=dev)
+    err = None
+    try:  # every rank maps rank 0's slots (CUDA IPC); agree on success before any fence runs
+        pg = PeerGather(2 * gchunk, R_max, p.N, dtype=torch.int32, root=0)
+    except Exception as ex:  # noqa: BLE001
+        pg, err = None, ex
+        ok.zero_()
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if int(ok.item()) == 0:
+        raise RuntimeError(f"fused gather unavailable: {err!r}" if err else "fused gather unavailable on a peer rank")
     mslots, bslots = pg.mask.view(2, -1), pg.body.view(2, -1)
     fence = torch.zeros(1, dtype=torch.int32, device=dev)
     count = [0]
