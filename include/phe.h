@@ -360,9 +360,23 @@ int phe_wire_serialize_lwe(const phe_params *p, const uint32_t *d_mask, const ui
                            int64_t R, uint8_t *d_wire, void *stream);
 int phe_wire_deserialize_lwe(const phe_params *p, const uint8_t *d_wire, int64_t T, int64_t R,
                              uint32_t *d_mask, uint32_t *d_body, void *stream);
+/* phe_matmul_clear_wire: matmul_clear(_T) (by `transpose`) with the fused switch, writing the wire
+ * records directly: the mask GEMM's epilogue packs each 128-coefficient block of a row at q_out
+ * bits (2 q_out 64-bit words) and TMA-stores it into d_wire [T][phe_wire_lwe_bytes(p, R)], R =
+ * row_end - row_begin; the bodies go through d_ws (uint32 [T][R], phe_matmul_clear_wire_ws_bytes)
+ * into each record's tail.  Byte-identical to phe_wire_serialize_lwe of phe_matmul_clear's
+ * uint32 outputs, with 0.8125 of their HBM writes.  EUNSUPPORTED unless
+ * phe_wire_lwe_direct_supported(p, R) (ell in {4, 5}, N a multiple of 256, 16 <= q_out <= 26 < q_in,
+ * 16-byte record stride) and d_wire is 16-byte aligned.                                        */
+size_t phe_matmul_clear_wire_ws_bytes(const phe_params *p, int64_t T, int64_t R);
+int phe_wire_lwe_direct_supported(const phe_params *p, int64_t R);
+int phe_matmul_clear_wire(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
+                          int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T, uint8_t *d_wire,
+                          void *d_ws, size_t ws_bytes, void *stream);
 /* The LWE server step as the network sees it: h_wire_in [T][L] wire input blocks (9992 B each)
  * -> h_wire_out [T][phe_wire_lwe_bytes(p, R)], R = row_end - row_begin; chunked H2D, deserialize,
- * ct_prepare, matmul_clear(_T) with the fused switch, serialize, D2H on two internal streams
+ * ct_prepare, matmul_clear(_T) with the fused switch (phe_matmul_clear_wire where supported, else
+ * uint32 outputs + serialize), D2H on two per-call streams
  * (caller workspace of phe_server_matvec_wire_host_ws_bytes bytes).  Synchronous.           */
 size_t phe_server_matvec_wire_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose,
                                             int64_t row_begin, int64_t row_end, int64_t T, int64_t chunk_tokens);

@@ -45,7 +45,8 @@ EXPORTS = [
     "phe_matmul_clear_digits_ntt", "phe_matmul_clear_into", "phe_matmul_clear_ntt_into",
     "phe_server_matvec_host_ws_bytes", "phe_server_matvec_packed_host_ws_bytes", "phe_server_wire_host_ws_bytes",
     "phe_server_wire_host_ntt_ws_bytes", "phe_server_wire_host_nttw_ws_bytes",
-    "phe_server_matvec_wire_host_ws_bytes",
+    "phe_server_matvec_wire_host_ws_bytes", "phe_matmul_clear_wire_ws_bytes", "phe_wire_lwe_direct_supported",
+    "phe_matmul_clear_wire",
 ]
 
 
@@ -105,6 +106,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "phe_server_matvec_host": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _vp, _i64,
                                     _i64, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
         "phe_server_matvec_host_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64, _i64, _i64], _sz),
+        "phe_matmul_clear_wire_ws_bytes": ([_P, _i64, _i64], _sz),
+        "phe_wire_lwe_direct_supported": ([_P, _i64], ctypes.c_int),
+        "phe_matmul_clear_wire": ([_P, _vp, _i64, _i64, ctypes.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _sz, _vp],
+                                  ctypes.c_int),
         "phe_server_matvec_wire_host_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64, _i64, _i64], _sz),
         "phe_server_matvec_packed_host_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64], _sz),
         "phe_server_wire_host_ws_bytes": ([_P, _i64, _i64, ctypes.c_int, _i64, _i64], _sz),
@@ -766,6 +771,32 @@ def wire_serialize_lwe(p: Params, mask: torch.Tensor, body: torch.Tensor, out: t
         raise PheError(f"out must be a contiguous, 8-byte aligned uint8 CUDA tensor of shape {(T, nb)}")
     _check(load().phe_wire_serialize_lwe(ctypes.byref(p), _ptr(mask), _ptr(body), T, R, _ptr(out), _stream()),
            "phe_wire_serialize_lwe")
+    return out
+
+
+def wire_lwe_direct_supported(p: Params, R: int) -> bool:
+    return bool(load().phe_wire_lwe_direct_supported(ctypes.byref(p), R))
+
+
+def matmul_clear_wire(p: Params, w, operand: torch.Tensor, T: int, row_begin: int = 0, row_end: int | None = None,
+                      out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """matmul_clear / matmul_clear_T (by w.transpose) writing the switched LWE outputs straight into
+    wire records uint8 [T][wire_lwe_bytes(p, R)] (the mask epilogue bit-packs at q_out;
+    phe_matmul_clear_wire).  Byte-identical to wire_serialize_lwe(matmul_clear(...))."""
+    row_end = w.rows if row_end is None else row_end
+    R = row_end - row_begin
+    _need_bytes(operand, load().phe_ct_operand_bytes(ctypes.byref(p), T, p.L(w.cols)), "operand")
+    nb = wire_lwe_bytes(p, R) if R > 0 else 0
+    if out is None:
+        out = torch.empty((T, nb), dtype=torch.uint8, device=operand.device)
+    _need(out, torch.uint8, (T, nb), "out")
+    need = load().phe_matmul_clear_wire_ws_bytes(ctypes.byref(p), T, max(R, 1))
+    if ws is None:
+        ws = torch.empty(need, dtype=torch.uint8, device=operand.device)
+    _need_bytes(ws, need, "ws")
+    _check(load().phe_matmul_clear_wire(ctypes.byref(p), _ptr(w.buf), w.d_out, w.d_in, int(w.transpose), row_begin,
+                                        row_end, _ptr(operand), T, _ptr(out), _ptr(ws), ws.numel(), _stream()),
+           "phe_matmul_clear_wire")
     return out
 
 

@@ -443,12 +443,16 @@ constexpr int EPI_TOK = 16;                   // tokens per epilogue chunk
 constexpr int OUT_U64 = 0;  // raw LWE masks mod 2^q_in (uint64)
 constexpr int OUT_U32 = 1;  // modulus-switched to q_out (uint32), the hot-path product
 constexpr int OUT_DIG = 2;  // Decomp(A_LWE) digits for KeySwitch packing (Eq. 8): 3 int8 planes
+constexpr int OUT_WIRE = 3; // switched to q_out and packed into the wire bitstream (R22): a CTA's
+                            // 128 coefficients of one row are 2 q_out consecutive 64-bit words
+constexpr int WIRE_QMAX = 26;  // q_out bound of OUT_WIRE (shared-memory budget)
 template <int MODE> struct Cfg2 {
   using OutT = typename std::conditional<MODE == OUT_U64, unsigned long long,
-               typename std::conditional<MODE == OUT_U32, uint32_t, uint8_t>::type>::type;
+               typename std::conditional<MODE == OUT_U32 || MODE == OUT_WIRE, uint32_t, uint8_t>::type>::type;
   static constexpr int STAGES = MODE == OUT_U64 ? 6 : 8;
   static constexpr int OUT_BUF = EPI_TOK * BM * (MODE == OUT_DIG ? KS_LEVELS : (int)sizeof(OutT));  // 8/16/8 KB
-  static constexpr int SMEM = 1024 + STAGES * (B_HALF_MAX + 4096) + 4 * OUT_BUF + 256;
+  static constexpr int WIRE_BUF = MODE == OUT_WIRE ? EPI_TOK * 2 * WIRE_QMAX * 8 : 0;              // 6.5 KB
+  static constexpr int SMEM = 1024 + STAGES * (B_HALF_MAX + 4096) + 4 * OUT_BUF + 4 * WIRE_BUF + 256;
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -491,6 +495,13 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t sr
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(src), "r"(x), "r"(y), "r"(z)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -577,7 +588,8 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
   uint8_t *sB = smem;                                // S x 16 KB (1024-aligned)
   uint8_t *sA = smem + S * B_HALF_MAX;               // S x 4 KB
   uint8_t *sO = sA + S * 4096;                       // 2 groups x 2 buffers x OUT_BUF
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sO + 4 * C2::OUT_BUF);
+  uint64_t *sW = reinterpret_cast<uint64_t *>(sO + 4 * C2::OUT_BUF);  // OUT_WIRE: 2 x 2 x WIRE_BUF
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sO + 4 * C2::OUT_BUF + 4 * C2::WIRE_BUF);
   uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
 
@@ -746,7 +758,27 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         }
         OutT *ob = obuf + nbuf * OB_ELEMS;
         named_bar(1 + grp, 128);  // the store that last read buffer nbuf has drained
-        if (kdbg(ka) != 1) {
+        if constexpr (MODE == OUT_WIRE) {
+          // the warp's 32 consecutive coefficients (t = 32 q4 + lane) of one token are 32 q bits =
+          // q 32-bit words of the wire bitstream (R22): lane k < q assembles word k from the (up
+          // to three) coefficients it overlaps, taken from their lanes by shuffles, and stores it
+          // at u32 word 4 q tk + q q4 + k of the chunk's [16 tokens][128 coefficients] block
+          const int qb = ka.out_bits;
+          const int c0 = (32 * lane) / qb, s0 = 32 * lane - qb * c0;
+          const int l0 = min(c0, 31), l1 = min(c0 + 1, 31), l2 = min(c0 + 2, 31);
+          uint32_t *wb32 = reinterpret_cast<uint32_t *>(sW + (grp * 2 + nbuf) * (C2::WIRE_BUF / 8));
+#pragma unroll
+          for (int tk = 0; tk < EPI_TOK; tk++) {
+            uint32_t val;
+            if constexpr (SH > 0) val = finish_sw<ELL, SH>(&v[tk * ELL], (uint32_t)omask);
+            else val = (uint32_t)finish<ELL, true, uint32_t>(&v[tk * ELL], half, shift, omask);
+            const uint64_t a0 = __shfl_sync(0xffffffffu, val, l0);
+            const uint64_t a1 = __shfl_sync(0xffffffffu, val, l1);
+            const uint64_t a2 = __shfl_sync(0xffffffffu, val, l2);
+            const uint64_t cat = a0 | (a1 << qb) | (a2 << (2 * qb));
+            if (lane < qb && tk < nt) wb32[tk * 4 * qb + q4 * qb + lane] = (uint32_t)(cat >> s0);
+          }
+        } else if (kdbg(ka) != 1) {
           if constexpr (MODE == OUT_DIG) {
             // r = top 32 bits of v after rounding the q_in - 32 bit tail half up; signed base-2^8
             // digits, least significant first with carry (Decomp, Eq. 4 / S:59-67; R18);
@@ -779,7 +811,15 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         }
         fence_proxy_async_smem();
         named_bar(1 + grp, 128);  // chunk staged
-        if (issuer) {
+        if (MODE == OUT_WIRE && issuer && jr < ka.R) {
+          // [tokens][words] box: the row's segment word jr * N q / 64 + the block's first word
+          const CUtensorMap *mo = (c0 + EPI_TOK <= ka.tpt) ? &map_out : &map_out_tail;
+          const int qw = 2 * ka.out_bits;
+          uint64_t *wb = sW + (grp * 2 + nbuf) * (C2::WIRE_BUF / 8);
+          if (kdbg(ka) == 0 || kdbg(ka) == 4)
+            tma_store_2d(mo, smem_u32(wb), (int)((int64_t)jr * (ka.N / BM) * qw + (tb / BM) * qw), tau0 + c0);
+          bulk_wait_read_1();
+        } else if (MODE != OUT_WIRE && issuer) {
           // a full 16-token box, or the tpt % 16 tail box of this tile (never past the tile)
           const CUtensorMap *mo = (c0 + EPI_TOK <= ka.tpt) ? &map_out : &map_out_tail;
           if (kdbg(ka) == 0 || kdbg(ka) == 4) {
@@ -1163,6 +1203,19 @@ static int make_map_digits(CUtensorMap *m, void *base, int64_t N, int64_t Rpad, 
   return r == CUDA_SUCCESS ? PHE_OK : PHE_EINVAL;
 }
 
+// LWE wire records [T][tw] uint64 words; box = one row's 128-coefficient block (2 q words) x tokens
+static int make_map_wire(CUtensorMap *m, void *base, int64_t tw, int64_t T, int qw, int box_tok) {
+  auto enc = get_encode();
+  if (!enc) return PHE_ECUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)tw, (cuuint64_t)T};
+  cuuint64_t strides[1] = {(cuuint64_t)(tw * 8)};
+  cuuint32_t box[2] = {(cuuint32_t)qw, (cuuint32_t)box_tok};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? PHE_OK : PHE_EINVAL;
+}
+
 static int make_map_out(CUtensorMap *m, void *base, bool sw, int64_t N, int64_t R, int64_t T, int box_tok,
                         int64_t out_rows) {
   auto enc = get_encode();
@@ -1252,12 +1305,18 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
     km.total_tiles = km.m_tiles * km.n_tiles;
     km.out = a.out_mask;
     if (a.digits && !two_sm) return PHE_EUNSUPPORTED;
+    if (a.wire_words > 0 && (!two_sm || !sw || a.out_bits > WIRE_QMAX || (a.wire_words & 1) ||
+                             (reinterpret_cast<uintptr_t>(a.out_mask) & 15)))
+      return PHE_EUNSUPPORTED;
     if (two_sm) {
       const int tail = km.tpt % EPI_TOK ? km.tpt % EPI_TOK : EPI_TOK;
       CUtensorMap mot;
       if (a.digits) {
         rc = make_map_digits(&mo, a.out_mask, N, a.digit_rows, a.T, EPI_TOK);
         if (!rc) rc = make_map_digits(&mot, a.out_mask, N, a.digit_rows, a.T, tail);
+      } else if (a.wire_words > 0) {
+        rc = make_map_wire(&mo, a.out_mask, a.wire_words, a.T, 2 * a.out_bits, EPI_TOK);
+        if (!rc) rc = make_map_wire(&mot, a.out_mask, a.wire_words, a.T, 2 * a.out_bits, tail);
       } else {
         rc = make_map_out(&mo, a.out_mask, sw, N, R, a.T, EPI_TOK, ka.out_rows);
         if (!rc) rc = make_map_out(&mot, a.out_mask, sw, N, R, a.T, tail, ka.out_rows);
@@ -1268,6 +1327,8 @@ int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches) {
       if (a.digits) {
         km.out_bits = KS_BITS;  // digits keep the top 32 bits (q_in >= 32)
         rc = dispatch_2sm<OUT_DIG>(ell, ma, mb, mbt, mo, mot, km, st);
+      } else if (a.wire_words > 0) {
+        rc = dispatch_2sm<OUT_WIRE>(ell, ma, mb, mbt, mo, mot, km, st);
       } else {
         rc = sw ? dispatch_2sm<OUT_U32>(ell, ma, mb, mbt, mo, mot, km, st)
                 : dispatch_2sm<OUT_U64>(ell, ma, mb, mbt, mo, mot, km, st);

@@ -848,16 +848,80 @@ int phe_wire_deserialize_lwe(const phe_params *p, const uint8_t *d_wire, int64_t
   return phe::launch_wire_u32(d_body, T, (int)R, p->q_out, w, lwe_body_words(p, R), 1, tw, R * sw, 1, S(stream));
 }
 
+size_t phe_matmul_clear_wire_ws_bytes(const phe_params *p, int64_t T, int64_t R) {
+  if (!p || T < 0 || R < 1) return 0;
+  return (size_t)round_up(T * R * 4, 256);
+}
+
+// the fused wire form is supported iff the 2-CTA mask kernel runs (ell 4/5, N a multiple of 256),
+// q_out <= 26 and the per-token record is a whole number of 16-byte units (TMA row stride)
+static bool wire_direct_ok(const phe_params *p, int64_t R) {
+  const int ell = (p->q_in + 7) / 8;
+  if ((ell != 4 && ell != 5) || p->N % 256 || p->q_out > 26 || p->q_out < 16 || p->q_out == p->q_in) return false;
+  return (phe_wire_lwe_bytes(p, R) % 16) == 0;
+}
+int phe_wire_lwe_direct_supported(const phe_params *p, int64_t R) {
+  if (!p || phe_params_validate(p) || R < 1 || p->N % 64) return 0;
+  return wire_direct_ok(p, R) ? 1 : 0;
+}
+
+int phe_matmul_clear_wire(const phe_params *p, const void *d_wprep, int64_t d_out, int64_t d_in, int transpose,
+                          int64_t row_begin, int64_t row_end, const void *d_operand, int64_t T, uint8_t *d_wire,
+                          void *d_ws, size_t ws_bytes, void *stream) {
+  g_last_launches = 0;
+  KParams kp;
+  int rc = check_wire(p, &kp);
+  if (rc) return rc;
+  if (transpose != 0 && transpose != 1) return PHE_EINVAL;
+  const int64_t rows = transpose ? d_in : d_out, cols = transpose ? d_out : d_in;
+  if (rows < 1 || cols < 1 || T < 0) return PHE_EINVAL;
+  if (row_begin < 0 || row_end > rows || row_begin > row_end) return PHE_EINVAL;
+  const int64_t R = row_end - row_begin;
+  if (T == 0 || R == 0) return PHE_OK;
+  if (!d_wprep || !d_operand || !d_wire || !d_ws) return PHE_EINVAL;
+  if (!wire_direct_ok(p, R) || ((uintptr_t)d_wire & 15)) return PHE_EUNSUPPORTED;
+  if (ws_bytes < phe_matmul_clear_wire_ws_bytes(p, T, R)) return PHE_ENOMEM;
+  const int64_t N = p->N, Lc = phe_num_blocks(p, cols);
+  phe::GemmArgs a{};
+  a.kp = kp;
+  a.wexp = static_cast<const uint8_t *>(d_wprep);
+  a.wplain = reinterpret_cast<const int8_t *>(a.wexp + rows * Lc * 2 * N * 16);
+  a.rows = rows;
+  a.wplain_rows = round_up(rows, 128);
+  a.op_rows = op_rows(T, kp.ell);
+  a.Lc = Lc;
+  a.cols = cols;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  a.mplanes = static_cast<const uint8_t *>(d_operand);
+  a.bplanes = a.mplanes + a.op_rows * Lc * N;
+  a.T = T;
+  a.out_bits = p->q_out;
+  a.out_mask = d_wire;
+  a.out_body = d_ws;  // uint32 bodies [T][R], then packed into each record's tail
+  a.wire_words = (int64_t)phe_wire_lwe_bytes(p, R) / 8;
+  int n = 0;
+  rc = phe::launch_limb_gemm(a, S(stream), &n);
+  if (rc) return rc;
+  rc = phe::launch_wire_u32(static_cast<uint32_t *>(d_ws), T, (int)R, p->q_out, d_wire, lwe_body_words(p, R), 1,
+                            a.wire_words, R * lwe_seg_words(p), 0, S(stream));
+  g_last_launches = n + 1;
+  return rc;
+}
+
 // slot of phe_server_matvec_wire_host: wire inputs, seeds, bodies, operand, uint32 outputs, wire outputs
 struct LweWireSlot {
   size_t win, seeds, body, op, om, ob, wout;
   size_t total() const { return win + seeds + body + op + om + ob + wout; }
 };
+// (with the fused wire epilogue -- phe_matmul_clear_wire -- no uint32 mask buffer is needed)
 static LweWireSlot lwe_wire_slot(const phe_params *p, int64_t L, int64_t R, int64_t C) {
   const int64_t N = p->N, bin = (int64_t)phe_wire_input_bytes(p), bout = (int64_t)phe_wire_lwe_bytes(p, R);
+  const bool direct = wire_direct_ok(p, R);
   return {(size_t)round_up(C * L * bin, 256), (size_t)round_up(C * L * 8, 256), (size_t)round_up(C * L * N * 8, 256),
-          (size_t)round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256), (size_t)round_up(C * R * N * 4, 256),
-          (size_t)round_up(C * R * 4, 256), (size_t)round_up(C * bout, 256)};
+          (size_t)round_up((int64_t)phe_ct_operand_bytes(p, C, L), 256),
+          direct ? (size_t)0 : (size_t)round_up(C * R * N * 4, 256), (size_t)round_up(C * R * 4, 256),
+          (size_t)round_up(C * bout, 256)};
 }
 
 size_t phe_server_matvec_wire_host_ws_bytes(const phe_params *p, int64_t d_out, int64_t d_in, int transpose,
@@ -903,8 +967,13 @@ int phe_server_matvec_wire_host(const phe_params *p, const void *d_wprep, int64_
     cudaMemcpyAsync(d_win, h_wire_in + t0 * L * bin, n * L * bin, cudaMemcpyHostToDevice, st);
     rc = phe_wire_deserialize_inputs(p, d_win, n, L, d_seeds, d_bod, st);
     if (!rc) rc = phe_ct_prepare(p, d_seeds, d_bod, n, L, d_op, sl.op, st);
-    if (!rc) rc = matmul_common(p, d_wprep, rows, cols, row_begin, row_end, d_op, n, p->q_out, d_om, d_ob, st);
-    if (!rc) rc = phe_wire_serialize_lwe(p, d_om, d_ob, n, R, d_wout, st);
+    if (sl.om == 0) {  // the mask GEMM writes the wire record itself
+      if (!rc) rc = phe_matmul_clear_wire(p, d_wprep, d_out, d_in, transpose, row_begin, row_end, d_op, n, d_wout, d_ob,
+                                          sl.ob, st);
+    } else {
+      if (!rc) rc = matmul_common(p, d_wprep, rows, cols, row_begin, row_end, d_op, n, p->q_out, d_om, d_ob, st);
+      if (!rc) rc = phe_wire_serialize_lwe(p, d_om, d_ob, n, R, d_wout, st);
+    }
     if (rc) break;
     cudaMemcpyAsync(h_wire_out + t0 * bout, d_wout, n * bout, cudaMemcpyDeviceToHost, st);
   }

@@ -88,6 +88,9 @@ struct GemmArgs {
   int64_t out_rows;       // row stride of out_mask/out_body ([T][out_rows][N] / [T][out_rows]); 0 = R
   int digits;             // 1: out_mask receives Decomp digits int8 [T][digit_rows][3][N] (Eq. 8)
   int64_t digit_rows;     // row stride of the digit tensor (>= row_end - row_begin)
+  int64_t wire_words;     // > 0: out_mask is the LWE wire record [T][wire_words] (uint64 words, R22):
+                          // the mask GEMM writes the switched words bit-packed at q_out; out_body
+                          // receives uint32 bodies (packed into the record by the caller)
 };
 int launch_limb_gemm(const GemmArgs &a, cudaStream_t st, int *n_launches);
 

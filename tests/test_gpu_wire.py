@@ -89,3 +89,68 @@ def test_server_matvec_wire_host_matches_device(phe):
     m2, b2 = phe.wire_deserialize_lwe(p, ho.cuda(), 247)
     assert torch.equal(m2, m) and torch.equal(b2, b)
 
+
+
+@pytest.mark.parametrize("d_out,d_in,T,transpose,rows", [
+    (300, 2048, 53, False, None),       # R = 300 (even record), ragged token tiles
+    (2048, 2048, 60, False, (0, 2048)),  # q_proj shape, 51 + 9 tokens (narrow tail MMA)
+    (512, 2048, 9, True, None),         # k^T: d_in = 512 < N, (j, j+1) CTA pairs
+    (301, 700, 17, False, (5, 261)),     # partial block, a row range with R = 256
+    (301, 700, 1, False, (0, 300)),      # odd rows in the last (j, j+1) pair
+    (8192, 2048, 4, True, None),        # gate^T: L = 4
+])
+def test_matmul_clear_wire_equals_serialized(phe, d_out, d_in, T, transpose, rows):
+    """phe_matmul_clear_wire (the mask epilogue bit-packs the switched words into the wire record,
+    R22) is byte-identical to wire_serialize_lwe of matmul_clear's uint32 outputs, whose bytes are
+    pinned to the oracle's serializer above."""
+    p = phe.params(phe.PRESET_PAPER)
+    W = synth.weights_int8(d_out, d_in, seed=d_out + d_in)
+    cols = d_out if transpose else d_in
+    x = synth.activations_int8(T, cols, seed=T)
+    S = phe.keygen(p, 7)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).cuda(), 93)
+    w = phe.Weights(p, torch.from_numpy(W).cuda(), transpose=transpose)
+    opnd = phe.ct_prepare(p, seeds, body)
+    r0, r1 = rows if rows else (0, w.rows)
+    assert phe.wire_lwe_direct_supported(p, r1 - r0)
+    f = phe.matmul_clear_T if transpose else phe.matmul_clear
+    m, b = f(p, w, opnd, T, row_begin=r0, row_end=r1)
+    ref = phe.wire_serialize_lwe(p, m, b)
+    got = phe.matmul_clear_wire(p, w, opnd, T, row_begin=r0, row_end=r1)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+
+
+def test_matmul_clear_wire_unsupported_record_stride(phe):
+    """R = 301 gives an odd number of 64-bit words per record (no 16-byte TMA row stride): the fused
+    form refuses (EUNSUPPORTED) and the host pipeline falls back to uint32 outputs + serialize."""
+    p = phe.params(phe.PRESET_PAPER)
+    assert not phe.wire_lwe_direct_supported(p, 301)
+    W = synth.weights_int8(301, 2048, seed=3)
+    x = synth.activations_int8(5, 2048, seed=4)
+    S = phe.keygen(p, 8)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).cuda(), 94)
+    w = phe.Weights(p, torch.from_numpy(W).cuda())
+    with pytest.raises(phe.PheError):
+        phe.matmul_clear_wire(p, w, phe.ct_prepare(p, seeds, body), 5)
+    m, b = phe.matmul_clear(p, w, phe.ct_prepare(p, seeds, body), 5)
+    hi = phe.wire_serialize_inputs(p, seeds, body).cpu().pin_memory()
+    ho = torch.empty((5, phe.wire_lwe_bytes(p, 301)), dtype=torch.uint8, pin_memory=True)
+    phe.server_matvec_wire_host(p, w, hi, ho, chunk_tokens=2)
+    assert torch.equal(ho.cuda(), phe.wire_serialize_lwe(p, m, b))
+
+
+def test_server_matvec_wire_host_fused_epilogue(phe):
+    """The host pipeline with a supported R runs phe_matmul_clear_wire inside: same bytes."""
+    p = phe.params(phe.PRESET_PAPER)
+    W = synth.weights_int8(256, 2048, seed=5)
+    x = synth.activations_int8(70, 2048, seed=6)
+    S = phe.keygen(p, 9)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).cuda(), 95)
+    w = phe.Weights(p, torch.from_numpy(W).cuda())
+    assert phe.wire_lwe_direct_supported(p, 256)
+    m, b = phe.matmul_clear(p, w, phe.ct_prepare(p, seeds, body), 70)
+    hi = phe.wire_serialize_inputs(p, seeds, body).cpu().pin_memory()
+    ho = torch.empty((70, phe.wire_lwe_bytes(p, 256)), dtype=torch.uint8, pin_memory=True)
+    phe.server_matvec_wire_host(p, w, hi, ho, chunk_tokens=32)
+    assert torch.equal(ho.cuda(), phe.wire_serialize_lwe(p, m, b))

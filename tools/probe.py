@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--T", type=int, default=2048)
     ap.add_argument("--transpose", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--wire", action="store_true", help="phe_matmul_clear_wire (bit-packed outputs)")
     a = ap.parse_args()
     p = phe.params(phe.PRESET_PAPER)
     W = torch.from_numpy(synth.weights_int8(a.d_out, a.d_in)).cuda()
@@ -35,6 +36,13 @@ def main():
     op = phe.ct_prepare(p, seeds, body)
     out = torch.empty((a.T, w.rows, p.N), dtype=torch.int32, device="cuda")
     f = phe.matmul_clear_T if a.transpose else phe.matmul_clear
+    if a.wire:
+        del out
+        wout = torch.empty((a.T, phe.wire_lwe_bytes(p, w.rows)), dtype=torch.uint8, device="cuda")
+        wws = torch.empty(phe.load().phe_matmul_clear_wire_ws_bytes(__import__("ctypes").byref(p), a.T, w.rows),
+                          dtype=torch.uint8, device="cuda")
+        f = lambda p_, w_, op_, T_, out_mask=None, out_body=None: phe.matmul_clear_wire(p_, w_, op_, T_, out=wout, ws=wws)  # noqa: E731
+        out = None
     for _ in range(2):
         f(p, w, op, a.T, out_mask=out, out_body=phe.SKIP)
     torch.cuda.synchronize()
