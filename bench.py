@@ -50,6 +50,11 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["stack", "q_proj", "ffn", "q_proj_packed", "stack_packed"],
                     default="stack")
+    ap.add_argument("--bwd", choices=["per-matrix", "fused"], default="per-matrix",
+                    help="stack backward: per-matrix = one W^T call per weight matrix on its own gradient "
+                         "(q, k, v, o, gate, up, down; R26, the default); fused = dx of the fused projections, "
+                         "W_qkv^T [g_q; g_k; g_v] and W_gate_up^T [g_gate; g_up] (the input gradient a training "
+                         "step needs: one output per input coordinate instead of one per matrix)")
     ap.add_argument("--layers", type=int, default=16,
                     help="stack workloads: transformer layers (Llama-3.2-1B has 16; fewer only for tests)")
     ap.add_argument("--pack", choices=["tc", "ntt"], default="ntt",
@@ -141,7 +146,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workloads
-def linears(workload: str, layers: int = 16):
+def linears(workload: str, layers: int = 16, bwd: str = "per-matrix"):
     """Calls one step makes: (name, d_out, d_in, transpose, input_key).  Llama-3.2-1B:
     d = 2048, m = 8192, GQA k/v 512x2048, 16 layers.  Linears that share an input ciphertext
     are registered fused (qkv 3072x2048, gate_up 16384x2048), so the input is expanded once and
@@ -154,6 +159,15 @@ def linears(workload: str, layers: int = 16):
                 ("gate_T", 8192, 2048, True, "g_gate"), ("up_T", 8192, 2048, True, "g_up"),
                 ("down_T", 2048, 8192, True, "g_down")]
     calls = []                # configs[3]: the full 16-layer stack, forward + backward
+    if bwd == "fused":        # dx = W_qkv^T [g_q; g_k; g_v], W_gate_up^T [g_gate; g_up] (same MACs)
+        for l in range(layers):
+            calls += [(f"L{l}.qkv", 3072, 2048, False, f"L{l}.x"), (f"L{l}.o", 2048, 2048, False, f"L{l}.a"),
+                      (f"L{l}.gate_up", 16384, 2048, False, f"L{l}.h"),
+                      (f"L{l}.down", 2048, 8192, False, f"L{l}.m"),
+                      (f"L{l}.qkv_T", 3072, 2048, True, f"L{l}.gqkv"), (f"L{l}.o_T", 2048, 2048, True, f"L{l}.go"),
+                      (f"L{l}.gate_up_T", 16384, 2048, True, f"L{l}.ggu"),
+                      (f"L{l}.down_T", 2048, 8192, True, f"L{l}.gd")]
+        return calls
     for l in range(layers):
         calls += [(f"L{l}.qkv", 3072, 2048, False, f"L{l}.x"), (f"L{l}.o", 2048, 2048, False, f"L{l}.a"),
                   (f"L{l}.gate_up", 16384, 2048, False, f"L{l}.h"), (f"L{l}.down", 2048, 8192, False, f"L{l}.m"),
@@ -221,7 +235,7 @@ def run_ours(args):
     rows_mode = args.shard == "rows" and world > 1
     if args.gather is None:
         args.gather = "both" if rows_mode and not packed else "none"
-    lins = linears(args.workload, args.layers)
+    lins = linears(args.workload, args.layers, args.bwd)
     # ---------------- untimed setup: weights (server registration) and client encryption
     from paper_2505_07329_b200.dist import PeerGather, gather_wire_shards, shard_range
     regs = []   # (name, Weights | NttWeights, input_key)
@@ -826,7 +840,10 @@ def config_dict(args, world, T, rows_mode=False):
                       "LWE ciphertexts, uint32 per coefficient after 39->26 modulus switch")}
     if args.workload.startswith("stack"):
         cfg["layers"] = args.layers
-        cfg["calls_per_step"] = 11 * args.layers
+        cfg["calls_per_step"] = (11 if args.bwd == "per-matrix" else 8) * args.layers
+        if args.bwd == "fused":
+            cfg["workload"] += ("; backward as dx of the fused projections (W_qkv^T [g_q; g_k; g_v], "
+                                "W_gate_up^T [g_gate; g_up]), same MACs")
     return cfg
 
 
@@ -905,7 +922,7 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return  # rank 0 alone runs the CPU oracle; other ranks exit 0 without work
-    lins = linears(args.workload, args.layers)
+    lins = linears(args.workload, args.layers, args.bwd)
     cores = os.cpu_count() or 1
     budget = 2.0 if len({rows_cols(d, e, t)[1] for _, d, e, t, _ in lins}) > 1 else 1.0
     for _ in range(args.warmup):
