@@ -30,6 +30,7 @@
 //                       mod 2^q_in -> the uint64 accumulator of pack_finalize_kernel
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "phe_common.cuh"
 #include "side_kernels.cuh"
@@ -610,6 +611,9 @@ int launch_ntt_ks_prepare(const KParams &kp, const uint64_t *ksk, void *buf, cud
 // best fill down to 4 tiles per CTA.
 int ntt_ks_splits(const KParams &kp, int64_t T, int64_t G) {
   constexpr int64_t SMS = 148;
+#if defined(PHE_KERNEL_EXPERIMENTS) && PHE_KERNEL_EXPERIMENTS
+  if (const char *e = getenv("PHE_KS_SPLITS")) return atoi(e);
+#endif
   const int64_t tiles = (int64_t)KS_LEVELS * kp.N / nks::ks_tile(kp.log2N);
   int64_t best = 1;
   double best_eff = 0.0;
