@@ -2,7 +2,7 @@
 T = 2048 (throughput).  Table 3 times the paper's whole primitive (Eq. 6 + KeySwitch packing
 Eq. 7/8 + switch) for one token on an RTX 4060 Laptop; the like-for-like computation here is
 matmul_clear_packed (NEXT #1).  The LWE hot path (north_star) is timed through both
-contractions too.  Context only (different GPU).  Writes gpurun_out/r1_table3.json."""
+contractions too.  Context only (different GPU).  Writes gpurun_out/r2_table3.json."""
 import json
 import os
 import statistics
@@ -80,7 +80,7 @@ def main():
             torch.cuda.empty_cache()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     json.dump({"what": __doc__.split("\n")[0], "results": out},
-              open(os.path.join(ROOT, "gpurun_out", "r1_table3.json"), "w"), indent=1)
+              open(os.path.join(ROOT, "gpurun_out", "r2_table3.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
