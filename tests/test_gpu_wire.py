@@ -154,3 +154,27 @@ def test_server_matvec_wire_host_fused_epilogue(phe):
     ho = torch.empty((70, phe.wire_lwe_bytes(p, 256)), dtype=torch.uint8, pin_memory=True)
     phe.server_matvec_wire_host(p, w, hi, ho, chunk_tokens=32)
     assert torch.equal(ho.cuda(), phe.wire_serialize_lwe(p, m, b))
+
+
+@pytest.mark.parametrize("over,d_out,d_in,T", [
+    (dict(N=512, q_in=39, q_out=26, beta=27), 64, 1100, 9),    # P1-like ring, L = 3
+    (dict(N=4096, q_in=39, q_out=26, beta=27), 64, 4096, 3),   # P3 ring
+    (dict(N=2048, q_in=32, q_out=24, beta=27), 64, 2048, 70),  # P2: ell = 4, q_out = 24 (generic epilogue)
+    (dict(N=2048, q_in=39, q_out=20, beta=27), 64, 2048, 20),  # q_out = 20: 3-coefficient words
+    (dict(N=2048, q_in=39, q_out=16, beta=16, gamma=8), 64, 2048, 5),  # q_out = 16 (lower bound)
+])
+def test_matmul_clear_wire_parameter_sets(phe, over, d_out, d_in, T):
+    """The wire-record epilogue on other rings and output widths (16 <= q_out <= 26): byte-identical
+    to wire_serialize_lwe(matmul_clear)."""
+    p = phe.params(phe.PRESET_PAPER, **over)
+    assert phe.wire_lwe_direct_supported(p, d_out)
+    W = synth.weights_int8(d_out, d_in, seed=d_out + d_in + p.N)
+    x = synth.activations_int8(T, d_in, seed=T + p.N)
+    S = phe.keygen(p, 3)
+    seeds, body = phe.encrypt_pack(p, S, torch.from_numpy(x).cuda(), 96)
+    w = phe.Weights(p, torch.from_numpy(W).cuda())
+    opnd = phe.ct_prepare(p, seeds, body)
+    m, b = phe.matmul_clear(p, w, opnd, T)
+    got = phe.matmul_clear_wire(p, w, opnd, T)
+    torch.cuda.synchronize()
+    assert torch.equal(got, phe.wire_serialize_lwe(p, m, b))
