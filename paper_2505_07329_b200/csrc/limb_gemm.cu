@@ -1092,13 +1092,15 @@ static int make_map_2d(CUtensorMap *m, const void *base, uint64_t dim0, uint64_t
   return r == CUDA_SUCCESS ? PHE_OK : PHE_EINVAL;
 }
 
-static int num_sms() {
-  static int n = 0;
+static int num_sms() {  // per device (a process may drive several GPUs)
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &n = cache[dev & 63];
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n = v > 0 ? v : 148;
   }
   return n;
 }
@@ -1107,11 +1109,11 @@ template <int ELL, bool HANKEL, bool SW>
 static int launch_one(const CUtensorMap &ma, const CUtensorMap &mb, const KArgs &ka, cudaStream_t st) {
   auto kern = limb_gemm_kernel<ELL, HANKEL, SW>;
   constexpr int smem = smem_bytes<HANKEL>();
-  static thread_local bool set = false;
-  if (!set) {
+  static thread_local uint64_t set = 0;  // devices this thread configured the kernel on
+  if (!(set & phe_device_bit())) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return phe_set_cuda_error(cudaGetLastError());
-    set = true;
+    set |= phe_device_bit();
   }
   int64_t grid = ka.total_tiles < num_sms() ? ka.total_tiles : num_sms();
   kern<<<(unsigned)grid, NUM_THREADS, smem, st>>>(ma, mb, ka);
@@ -1141,11 +1143,11 @@ static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtens
                       const CUtensorMap &mot, const KArgs &ka, cudaStream_t st) {
   auto kern = limb_gemm_2sm_kernel<ELL, MODE, SH>;
   constexpr int smem = Cfg2<MODE>::SMEM;
-  static thread_local bool set = false;
-  if (!set) {
+  static thread_local uint64_t set = 0;  // devices this thread configured the kernel on
+  if (!(set & phe_device_bit())) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return phe_set_cuda_error(cudaGetLastError());
-    set = true;
+    set |= phe_device_bit();
   }
   int64_t pairs = num_sms() / 2;
   if (ka.total_tiles < pairs) pairs = ka.total_tiles;
@@ -1388,12 +1390,12 @@ int launch_pack_gemm(const PackArgs &a, cudaStream_t st) {
                    CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   auto kern = ell == 5 ? pack_gemm_2sm_kernel<5> : pack_gemm_2sm_kernel<4>;
-  static thread_local bool set5 = false, set4 = false;
-  bool &set = ell == 5 ? set5 : set4;
-  if (!set) {
+  static thread_local uint64_t set5 = 0, set4 = 0;  // devices configured, per instantiation
+  uint64_t &set = ell == 5 ? set5 : set4;
+  if (!(set & phe_device_bit())) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PK_SMEM) != cudaSuccess)
       return phe_set_cuda_error(cudaGetLastError());
-    set = true;
+    set |= phe_device_bit();
   }
   int64_t pairs = num_sms() / 2;
   if (pa.total_tiles < pairs) pairs = pa.total_tiles;

@@ -83,6 +83,15 @@ __device__ __forceinline__ void chacha20_u64x8(uint64_t seed, uint32_t blk, Nonc
 
 // thread-local error plumbing (phe_api.cu)
 int phe_set_cuda_error(cudaError_t e);
+// Bit of the calling thread's current device, for "once per device" caches of per-device
+// settings (cudaFuncSetAttribute is a per-device property: a per-thread flag alone would skip it
+// when one thread drives a second GPU).
+inline uint64_t phe_device_bit() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return 1ull << (dev & 63);
+}
+
 #define PHE_CUDA_CHECK_LAUNCH()                                   \
   do {                                                            \
     cudaError_t e__ = cudaGetLastError();                         \

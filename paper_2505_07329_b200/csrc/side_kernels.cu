@@ -321,10 +321,10 @@ int launch_encrypt(const KParams &kp, const uint8_t *S, const int8_t *x, int64_t
                    uint64_t *body, cudaStream_t st) {
   if (T == 0) return PHE_OK;
   size_t smem = sizeof(uint64_t) * kp.N + kp.N;
-  static thread_local int configured = 0;
-  if (!configured) {
+  static thread_local uint64_t configured = 0;  // per device (a per-device attribute)
+  if (!(configured & phe_device_bit())) {
     cudaFuncSetAttribute(encrypt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = 1;
+    configured |= phe_device_bit();
   }
   encrypt_kernel<<<(unsigned)(T * L), ENC_THREADS, smem, st>>>(kp, S, x, T, d_in, L, seed_base,
                                                               noise_seed, seeds, body);
@@ -553,10 +553,10 @@ decrypt_packed_kernel(KParams kp, const uint8_t *__restrict__ S, const uint32_t 
 int launch_ksk_gen(const KParams &kp, const uint8_t *S, uint64_t seed, uint64_t *KA, uint64_t *KB,
                    cudaStream_t st) {
   size_t smem = sizeof(uint64_t) * kp.N + kp.N;
-  static thread_local int configured = 0;
-  if (!configured) {
+  static thread_local uint64_t configured = 0;  // per device (a per-device attribute)
+  if (!(configured & phe_device_bit())) {
     cudaFuncSetAttribute(ksk_gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = 1;
+    configured |= phe_device_bit();
   }
   ksk_gen_kernel<<<(unsigned)(KS_LEVELS * kp.N), ENC_THREADS, smem, st>>>(kp, S, seed, KA, KB);
   PHE_CUDA_CHECK_LAUNCH();
