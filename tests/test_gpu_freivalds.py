@@ -40,7 +40,9 @@ DEV = "cuda:0"
 # (qkv / gate_up fused forward; q/o share 2048x2048, k/v 512x2048, gate/up 8192x2048 backward)
 CASES = [("qkv", 3072, 2048, False), ("o", 2048, 2048, False), ("gate_up", 16384, 2048, False),
          ("down", 2048, 8192, False), ("q_T", 2048, 2048, True), ("k_T", 512, 2048, True),
-         ("gate_T", 8192, 2048, True), ("down_T", 2048, 8192, True)]
+         ("gate_T", 8192, 2048, True), ("down_T", 2048, 8192, True),
+         # bench.py --bwd fused: dx of the fused projections (L = 2 with a half block; L = 8)
+         ("qkv_T", 3072, 2048, True), ("gate_up_T", 16384, 2048, True)]
 
 
 def _u64(t):
@@ -103,7 +105,10 @@ def test_all_outputs_vs_oracle(phe, coracle, name, d_out, d_in, transpose, T):
                           O.modswitch(_u64(b39), op.q_in, op.q_out))
     del m26, b26
 
-    # NEXT #4: the NTT-domain contraction on the same inputs, identical q_in words
+    # NEXT #4: the NTT-domain contraction on the same inputs, identical q_in words (within its
+    # CRT range: L <= phe_ntt_max_blocks, R23)
+    if L > phe.ntt_max_blocks(p):
+        return
     tabs = phe.NttTables(p)
     wn = phe.NttWeights(p, tabs, torch.from_numpy(W).to(DEV), transpose=transpose)
     mn, bn = phe.matmul_clear_ntt(p, wn, phe.ntt_ct_prepare(p, tabs, sd, bd), T, out_bits=p.q_in)
