@@ -50,6 +50,15 @@ constexpr int UK = 32;    // K of one tcgen05.mma kind::i8
 constexpr int NUM_THREADS = 384;  // 8 epilogue warps (0-7) + producer 8, MMA 9, TMEM 10, spare 11
 constexpr int W_PROD = 8, W_MMA = 9, W_TMEM = 10;
 constexpr int NUM_EPI = 256;
+// The 2-CTA mask kernel's epilogue groups (4 warps each, one per TMEM lane quarter): EG = 3 gives
+// 12 epilogue warps (0-11) + producer 12, MMA 13, TMEM 14, spare 15 (512 threads).
+#ifndef PHE_EPI_GROUPS
+#define PHE_EPI_GROUPS 2
+#endif
+constexpr int EG = PHE_EPI_GROUPS;
+constexpr int NT2 = (4 * EG + 4) * 32;
+constexpr int W2_PROD = 4 * EG, W2_MMA = 4 * EG + 1, W2_TMEM = 4 * EG + 2;
+constexpr int NUM_EPI2 = 128 * EG;
 constexpr int A_ROWS_HANKEL = BM + BK - 16;            // 240 compact rows
 constexpr int A_BYTES_HANKEL = A_ROWS_HANKEL * 16;     // 3840
 constexpr int A_BYTES_PLAIN = BM * BK;                 // 16384
@@ -449,10 +458,10 @@ constexpr int WIRE_QMAX = 26;  // q_out bound of OUT_WIRE (shared-memory budget)
 template <int MODE> struct Cfg2 {
   using OutT = typename std::conditional<MODE == OUT_U64, unsigned long long,
                typename std::conditional<MODE == OUT_U32 || MODE == OUT_WIRE, uint32_t, uint8_t>::type>::type;
-  static constexpr int STAGES = MODE == OUT_U64 ? 6 : 8;
+  static constexpr int STAGES = MODE == OUT_U64 ? 6 : (EG > 2 && MODE == OUT_WIRE) ? 7 : 8;
   static constexpr int OUT_BUF = EPI_TOK * BM * (MODE == OUT_DIG ? KS_LEVELS : (int)sizeof(OutT));  // 8/16/8 KB
   static constexpr int WIRE_BUF = MODE == OUT_WIRE ? EPI_TOK * 2 * WIRE_QMAX * 8 : 0;              // 6.5 KB
-  static constexpr int SMEM = 1024 + STAGES * (B_HALF_MAX + 4096) + 4 * OUT_BUF + 4 * WIRE_BUF + 256;
+  static constexpr int SMEM = 1024 + STAGES * (B_HALF_MAX + 4096) + 2 * EG * (OUT_BUF + WIRE_BUF) + 256;
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -574,7 +583,7 @@ __device__ __forceinline__ uint64_t kblock_mask(const KArgs &ka, int tp) {
 __device__ __forceinline__ bool kb_issue(uint64_t m, int kb) { return kb >= 64 || ((m >> kb) & 1ull); }
 
 template <int ELL, int MODE, int SH>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(NT2, 1)
 limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const __grid_constant__ CUtensorMap map_b_tail, const __grid_constant__ CUtensorMap map_out,
                      const __grid_constant__ CUtensorMap map_out_tail, KArgs ka) {
@@ -587,9 +596,9 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
                                               ~uintptr_t(1023));
   uint8_t *sB = smem;                                // S x 16 KB (1024-aligned)
   uint8_t *sA = smem + S * B_HALF_MAX;               // S x 4 KB
-  uint8_t *sO = sA + S * 4096;                       // 2 groups x 2 buffers x OUT_BUF
-  uint64_t *sW = reinterpret_cast<uint64_t *>(sO + 4 * C2::OUT_BUF);  // OUT_WIRE: 2 x 2 x WIRE_BUF
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sO + 4 * C2::OUT_BUF + 4 * C2::WIRE_BUF);
+  uint8_t *sO = sA + S * 4096;                       // EG groups x 2 buffers x OUT_BUF
+  uint64_t *sW = reinterpret_cast<uint64_t *>(sO + 2 * EG * C2::OUT_BUF);  // OUT_WIRE: EG x 2 x WIRE_BUF
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sO + 2 * EG * C2::OUT_BUF + 2 * EG * C2::WIRE_BUF);
   uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
 
@@ -601,15 +610,15 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * NUM_EPI); }
+    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * NUM_EPI2); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == W_PROD && lane == 0) {
+  if (warp == W2_PROD && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_out)) : "memory");
   }
-  if (warp == W_TMEM) {
+  if (warp == W2_TMEM) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_holder))
                  : "memory");
@@ -622,7 +631,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
 
   const int64_t total = ka.total_tiles;
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  if (warp == W_PROD) {
+  if (warp == W2_PROD) {
     // ===== TMA producer (both CTAs, warp-wide loop, elected lane issues): own Hankel rows +
     // own half of B, bytes land on CTA 0's barrier =====
     int s = 0; uint32_t ph = 0;
@@ -670,7 +679,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       }
     }
     if (kdbg(ka) == 4 && lane == 0) dbg_add(5, pw);
-  } else if (warp == W_MMA) {
+  } else if (warp == W2_MMA) {
     // ===== MMA issuer (leader CTA only; warp-wide loop, elected lane issues + commits) =====
     if (leader) {
       const uint32_t idesc_full = idesc_i8(2 * BM, n_mma), idesc_tail = idesc_i8(2 * BM, ka.n_mma_tail);
@@ -711,7 +720,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       }
       if (kdbg(ka) == 4 && lane == 0) { dbg_add(0, wt); dbg_add(1, wf); dbg_add(2, clock64() - t_start); }
     }
-  } else if (warp < 8) {
+  } else if (warp < 4 * EG) {
     // ===== epilogue (both CTAs): own 128 TMEM lanes = own 128 rows t =====
     // Group g (warps 0-3 / 4-7) takes every other 16-token chunk (alternating per tile).
     const int q4 = warp & 3;
@@ -722,7 +731,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
     const int64_t half = SW ? (1ll << (shift - 1)) : 0;
     const uint64_t omask = mask_bits(ka.out_bits);
     const uint32_t tempty_c0 = smem_u32(&tempty[0]) & PEER_MASK;
-    OutT *const obuf = reinterpret_cast<OutT *>(sO + grp * 2 * C2::OUT_BUF);
+    OutT *const obuf = reinterpret_cast<OutT *>(sO + grp * 2 * C2::OUT_BUF);  // grp < EG
     constexpr int OB_ELEMS = C2::OUT_BUF / (int)sizeof(OutT);
     int acc = 0; uint32_t aph = 0; int nbuf = 0; int64_t iter = 0;
     for (TileIter it(cid, ncl, ka.n_tiles); it.tile < total; it.next(ncl, ka.n_tiles), iter++) {
@@ -734,7 +743,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       const int tb = ka.jpair ? ((int)it.m - jq * ka.tb_per_row) * BM
                               : ((int)it.m - jq * ka.tb_per_row) * (2 * BM) + (int)crank * BM;
       const int nchunks = (ntok + EPI_TOK - 1) / EPI_TOK;
-      const int first = (grp + (int)(iter & 1)) & 1;
+      const int first = (grp + (int)(iter % EG)) % EG;
       long long e0 = (kdbg(ka) == 4 && warp == 0 && lane == 0) ? clock64() : 0;
       mbar_wait(&tfull[acc], aph);
       long long e1 = (kdbg(ka) == 4 && warp == 0 && lane == 0) ? clock64() : 0;
@@ -742,7 +751,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN);
       bool arrived = false;
-      for (int c = first; c < nchunks; c += 2) {
+      for (int c = first; c < nchunks; c += EG) {
         const int c0 = c * EPI_TOK;
         const int nt = min(EPI_TOK, ntok - c0);
         const int nloads = (nt * ELL + 15) / 16;
@@ -751,7 +760,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
         for (int q = 0; q < ELL; q++)
           if (q < nloads) tmem_ld16(tbase + (uint32_t)(c0 * ELL + 16 * q), &v[16 * q]);
         tmem_wait_ld();
-        if (c + 2 >= nchunks) {  // last TMEM read of this tile by this thread: release the buffer
+        if (c + EG >= nchunks) {  // last TMEM read of this tile by this thread: release the buffer
           tc_fence_before();
           mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)acc);
           arrived = true;
@@ -842,7 +851,7 @@ limb_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_con
   tc_fence_before();
   __syncthreads();
   cluster_sync();
-  if (warp == W_TMEM) {
+  if (warp == W2_TMEM) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
@@ -1153,7 +1162,7 @@ static int launch_2sm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtens
   if (ka.total_tiles < pairs) pairs = ka.total_tiles;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(2 * pairs));
-  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.blockDim = dim3(NT2);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
